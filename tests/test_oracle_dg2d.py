@@ -1,0 +1,308 @@
+"""Pins of the oracle's 2D quadtree mesh, fluxes and flux-differencing DGSEM,
+and of the re-mesh transfer (O5), against mathematics the paper and the method fix:
+entropy conservation of the two-point flux, brute-force face enumeration, face-slot
+accounting, free-stream preservation with mortars, discrete conservation, semi-discrete
+entropy conservation, isentropic vortex translation, polynomial exactness of the transfer."""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import oracle as O
+from oracle import tableau as T
+
+G = 1.4
+
+
+def _prim(u):
+    rho, v1, v2 = u[0], u[1] / u[0], u[2] / u[0]
+    p = (G - 1) * (u[3] - 0.5 * rho * (v1 * v1 + v2 * v2))
+    return rho, v1, v2, p
+
+
+def _cons(rho, v1, v2, p):
+    return np.array([rho, rho * v1, rho * v2, p / (G - 1) + 0.5 * rho * (v1 * v1 + v2 * v2)])
+
+
+def _entropy_vars(u):
+    rho, v1, v2, p = _prim(u)
+    s = np.log(p) - G * np.log(rho)
+    return np.array([(G - s) / (G - 1) - 0.5 * rho * (v1 * v1 + v2 * v2) / p, rho * v1 / p, rho * v2 / p, -rho / p])
+
+
+def _euler_flux(u, o):
+    rho, v1, v2, p = _prim(u)
+    vn = v1 if o == 0 else v2
+    return np.array([rho * vn, rho * v1 * vn + (p if o == 0 else 0), rho * v2 * vn + (p if o == 1 else 0),
+                     (u[3] + p) * vn])
+
+
+def _rand_state(rng, near=None, eps=1.0):
+    if near is None:
+        return _cons(0.5 + rng.random(), rng.standard_normal(), rng.standard_normal(), 0.5 + rng.random())
+    rho, v1, v2, p = _prim(near)
+    d = eps * rng.standard_normal(4)
+    return _cons(rho * (1 + 0.1 * d[0]), v1 + d[1], v2 + d[2], p * (1 + 0.1 * d[3]))
+
+
+def test_ranocha_flux_entropy_conservative_and_consistent():
+    rng = np.random.default_rng(0)
+    for k in range(2000):
+        uL = _rand_state(rng)
+        uR = _rand_state(rng, uL, eps=[1.0, 1e-3, 1e-6][k % 3])   # exercise both ln-mean branches
+        for o in (0, 1):
+            f = O.flux_ranocha(uL, uR, o)
+            psiL = uL[1 + o]
+            psiR = uR[1 + o]   # psi_n = rho v_n
+            lhs = (_entropy_vars(uR) - _entropy_vars(uL)) @ f
+            scale = np.abs(_entropy_vars(uR)).max() * np.abs(f).max() + 1.0
+            assert abs(lhs - (psiR - psiL)) <= 1e-13 * scale
+            assert np.allclose(f, O.flux_ranocha(uR, uL, o), rtol=1e-14, atol=1e-14)   # symmetric
+        for o in (0, 1):
+            assert np.allclose(O.flux_ranocha(uL, uL, o), _euler_flux(uL, o), rtol=1e-13, atol=1e-13)
+
+
+def test_ln_mean():
+    rng = np.random.default_rng(1)
+    for _ in range(1000):
+        a = rng.random() + 0.1
+        b = a * (1 + 10 ** rng.uniform(-9, 0.5))
+        exact = (b - a) / np.log1p((b - a) / a)
+        got = O.ln_mean(a, b)
+        if exact is not None:
+            assert abs(got - exact) <= 1e-13 * exact
+        assert min(a, b) <= got * (1 + 1e-15) and got <= max(a, b) * (1 + 1e-15)
+        assert abs(got - np.sqrt(a * b)) <= abs(b - a)   # between geometric and arithmetic means
+    assert O.ln_mean(2.0, 2.0) == 2.0
+
+
+def _prob(nb=4, L=2, dom=1.0, surface="hll", periodic=(1, 1)):
+    return W.configs._problem(2, "euler", "fluxdiff", surface, nb, L, 0.0, dom, periodic=periodic)
+
+
+def _random_map(rng, nb, L):
+    T_ = rng.integers(0, L + 1, size=(nb * 2 ** L, nb * 2 ** L))
+    # smooth the target a bit so that several levels survive balancing
+    T_ = (T_ * (rng.random(T_.shape) < 0.15)).astype(np.int32)
+    return W.balance(T_, L, (True, True))
+
+
+def _brute_adjacency(lv, nfx, nfy, L):
+    """all (a, b, orient) such that b touches a's +orient face, by rectangle geometry (periodic)."""
+    n = len(lv["fx"])
+    s = [1 << (L - int(l)) for l in lv["level"]]
+    adj = set()
+    for a in range(n):
+        for b in range(n):
+            # +x face of a
+            if (lv["fx"][a] + s[a]) % nfx == lv["fx"][b]:
+                lo = max(lv["fy"][a], lv["fy"][b])
+                hi = min(lv["fy"][a] + s[a], lv["fy"][b] + s[b])
+                if hi > lo:
+                    adj.add((a, b, 0))
+            if (lv["fy"][a] + s[a]) % nfy == lv["fy"][b]:
+                lo = max(lv["fx"][a], lv["fx"][b])
+                hi = min(lv["fx"][a] + s[a], lv["fx"][b] + s[b])
+                if hi > lo:
+                    adj.add((a, b, 1))
+    return adj
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_mesh_bruteforce(seed):
+    rng = np.random.default_rng(seed)
+    nb, L = 4, 2
+    lm = _random_map(rng, nb, L)
+    fam = T.family(16, [4, 8, 16], "taylor")
+    m = O.OracleMesh(_prob(nb, L), lm, fam)
+    lv = m.leaves()
+    n = m.n
+    # Morton order of leaf origins, and area
+    codes = []
+    for x, y in zip(lv["fx"], lv["fy"]):
+        c = 0
+        for bit in range(16):
+            c |= ((int(x) >> bit) & 1) << (2 * bit) | ((int(y) >> bit) & 1) << (2 * bit + 1)
+        codes.append(c)
+    assert codes == sorted(codes)
+    assert abs(sum(4.0 ** -int(l) for l in lv["level"]) - nb * nb) < 1e-12
+    ifc, ifm = m.faces("interfaces")
+    mor, mom = m.faces("mortars")
+    # face-slot accounting: each interface covers 2 element faces, each mortar 3
+    assert 2 * len(ifc) + 3 * len(mor) == 4 * n
+    # brute-force adjacency equals what interfaces + mortars describe
+    adj = _brute_adjacency(lv, nb << L, nb << L, L)
+    got = set()
+    for a, b, o in ifc:
+        got.add((a, b, o))
+    for large, s0, s1, o, side in mor:
+        for s_ in (s0, s1):
+            got.add((large, s_, o) if side == 0 else (s_, large, o))
+        # small elements ordered along the face, both one level finer
+        t = 1 - o
+        key = "fy" if o == 0 else "fx"
+        assert lv[key][s0] < lv[key][s1]
+        assert lv["level"][s0] == lv["level"][s1] == lv["level"][large] + 1
+        del t
+    assert got == adj
+    # conforming interfaces join equal levels; members per P:l.1253-1256 and l.1276-1279
+    mem = lv["member"]
+    for (a, b, o), mm in zip(ifc, ifm):
+        assert lv["level"][a] == lv["level"][b] and mm == mem[a]
+    for (large, s0, s1, o, side), mm in zip(mor, mom):
+        assert mm == mem[s0]
+    # per-member lists: stable, descending member, partition of all items
+    for kind, items_mem in (("elements", mem), ("interfaces", ifm), ("mortars", mom)):
+        lst, seg = m.list(kind)
+        assert sorted(lst.tolist()) == list(range(len(items_mem)))
+        for sgi in range(fam["R"]):
+            part = lst[seg[sgi]:seg[sgi + 1]]
+            assert all(items_mem[k] == fam["R"] - 1 - sgi for k in part)
+            assert list(part) == sorted(part)
+        ca = m.count_active(kind)
+        for i in range(1, 17):
+            want = sum(1 for mm in items_mem if T.active(16, fam["E"][mm], i))
+            assert ca[i - 1] == want
+
+
+def test_unbalanced_map_rejected():
+    lm = np.zeros((8, 8), np.uint8)
+    lm[0:2, 0:2] = 2
+    lm = W.leafify(lm, 2).astype(np.uint8)
+    fam = T.family(16, [4, 8, 16], "taylor")
+    with pytest.raises(ValueError):
+        O.OracleMesh(_prob(2, 2), lm, fam)
+    bad = np.zeros((8, 8), np.uint8)
+    bad[0, 1] = 1    # not block aligned
+    with pytest.raises(ValueError):
+        O.OracleMesh(_prob(2, 2), bad, fam)
+
+
+@pytest.fixture(scope="module")
+def nc_mesh():
+    rng = np.random.default_rng(11)
+    lm = _random_map(rng, 4, 2)
+    fam = T.family(16, [4, 8, 16], "taylor")
+    m = O.OracleMesh(_prob(4, 2, dom=2.0), lm, fam)
+    assert m.face_counts()["mortars"] > 0
+    return m
+
+
+def _weights2d(m):
+    w = O.basis()["w"]
+    lev = m.leaves()["level"].astype(float)
+    h = 2.0 / (4 * 2.0 ** lev)
+    return (h / 2) ** 2, np.outer(w, w).ravel()
+
+
+def test_free_stream_with_mortars(nc_mesh):
+    m = nc_mesh
+    u = _cons(1.3, 0.7, -0.4, 2.1)
+    U = np.broadcast_to(u[None, :, None], m.shape).copy()
+    dU = m.rhs(U)
+    f = max(np.abs(_euler_flux(u, 0)).max(), np.abs(_euler_flux(u, 1)).max())
+    hmin = 2.0 / (4 * 4)
+    assert np.abs(dU).max() <= 1e-13 * (2 / hmin) * f
+
+
+def test_conservation_with_mortars(nc_mesh):
+    m = nc_mesh
+    xy = m.node_coords()
+    X, Y = xy[:, 0], xy[:, 1]
+    U = np.stack([1 + 0.3 * np.sin(np.pi * X) * np.cos(np.pi * Y), 0.5 + 0.2 * np.cos(np.pi * Y),
+                  -0.3 + 0.1 * np.sin(np.pi * X), 3 + 0.5 * np.cos(np.pi * (X + Y))], axis=1)
+    U += 0.01 * np.random.default_rng(2).standard_normal(U.shape)    # discontinuous traces
+    dU = m.rhs(U)
+    J, wq = _weights2d(m)
+    tot = np.einsum("e,evq,q->v", J, dU, wq)
+    mag = np.einsum("e,evq,q->v", J, np.abs(dU), wq)
+    assert np.all(np.abs(tot) <= 1e-14 * mag)
+
+
+def test_semidiscrete_entropy_conservation():
+    """EC volume + EC surface flux on a conforming periodic mesh: sum J w v(u) . du = 0; HLL: <= 0."""
+    lm = np.zeros((6, 6), np.uint8)
+    fam = T.family(16, [16], "taylor")
+    rng = np.random.default_rng(4)
+    out = {}
+    for surf in ("ec", "hll"):
+        p = W.configs._problem(2, "euler", "fluxdiff", surf, 6, 0, 0.0, 2.0)
+        m = O.OracleMesh(p, lm, fam)
+        xy = m.node_coords()
+        X, Y = xy[:, 0], xy[:, 1]
+        rho = 1 + 0.2 * np.sin(np.pi * X)
+        v1 = 0.3 * np.cos(np.pi * Y)
+        v2 = 0.2 * np.sin(np.pi * (X - Y))
+        pr = 1 + 0.2 * np.cos(np.pi * X)
+        U = np.stack([rho, rho * v1, rho * v2, pr / (G - 1) + 0.5 * rho * (v1 ** 2 + v2 ** 2)], axis=1)
+        U *= 1 + 0.02 * rng.standard_normal(U.shape[0])[:, None, None]   # jumps across elements
+        dU = m.rhs(U)
+        V = np.stack([_entropy_vars(U[e]) for e in range(m.n)])
+        wq = np.outer(O.basis()["w"], O.basis()["w"]).ravel()
+        J = (2.0 / 6 / 2) ** 2
+        s = J * np.einsum("evq,evq,q->", V, dU, wq)
+        mag = J * np.einsum("evq,evq,q->", np.abs(V), np.abs(dU), wq)
+        out[surf] = (s, mag)
+    s, mag = out["ec"]
+    assert abs(s) <= 1e-13 * mag
+    s, mag = out["hll"]
+    assert s < -1e-6 * mag
+
+
+def test_isentropic_vortex_translation():
+    """single vortex on a uniform periodic mesh advects with (1, 1): the error is spatial only and
+    converges at high order under h-refinement (16^2 -> 32^2 cells, N = 3)."""
+    errs = []
+    for nb in (16, 32):
+        p = W.configs._problem(2, "euler", "fluxdiff", "hll", nb, 0, 0.0, 10.0)
+        lm = np.zeros((nb, nb), np.uint8)
+        fam = T.family(8, [8], "taylor")
+        m = O.OracleMesh(p, lm, fam)
+        ic = W.configs._isentropic_vortices([(5.0, 5.0)], per=10.0)
+        U = m.initial_state(ic)
+        m.step(U, 0.025, 40)                       # T = 1
+        xy = m.node_coords()
+        ex = ic(xy[:, 0] - 1.0, xy[:, 1] - 1.0)
+        errs.append(np.abs(U[:, 0] - ex[0]).max())
+    assert errs[0] < 5e-3 and errs[1] < errs[0] / 6, errs   # observed order ~3 (>= 2.5)
+
+
+def test_reference_equals_restricted_2d(nc_mesh):
+    m = nc_mesh
+    xy = m.node_coords()
+    U = m.initial_state(W.configs._isentropic_vortices([(1.0, 1.0)], per=2.0, eps=1.0))
+    for mask in (1, 2, 4, 5, 7):
+        assert np.array_equal(m.rhs(U, mask, 0), m.rhs(U, mask, 1))
+    a, b = U.copy(), U.copy()
+    m.step(a, 1e-3, 2, mode=0)
+    m.step(b, 1e-3, 2, mode=1)
+    assert np.array_equal(a, b)
+    del xy
+
+
+def test_transfer_polynomial_exact_and_conservative():
+    fam = T.family(16, [4, 8, 16], "taylor")
+    p = _prob(4, 2, dom=2.0)
+    rng = np.random.default_rng(7)
+    lm0 = _random_map(rng, 4, 2)
+    lm1 = lm0.copy()
+    # refine one level-0 block fully and coarsen one level-1 group where possible
+    lm1 = W.balance(np.maximum(lm1, (rng.random(lm1.shape) < 0.05).astype(np.uint8)), 2, (True, True))
+    assert np.abs(lm1.astype(int) - lm0.astype(int)).max() <= 1
+    m0 = O.OracleMesh(p, lm0, fam)
+    m1 = O.OracleMesh(p, lm1, fam)
+
+    def poly(x, y):   # degree <= 3 per direction, one per conserved variable
+        return np.stack([1 + x ** 3 - 2 * x * y, y ** 2 * x, 0.5 + y ** 3 * x ** 2, x * x * y * y * y + 2])
+
+    U0 = m0.initial_state(poly)
+    U1 = O.transfer(m0, m1, U0)
+    assert np.abs(U1 - m1.initial_state(poly)).max() < 1e-12       # refinement + copy exact
+    # coarsen back: projection is exact on the polynomial space too, and conservative
+    U2 = O.transfer(m1, m0, U1)
+    assert np.abs(U2 - U0).max() < 1e-12
+    rnd = rng.standard_normal(m1.shape)
+    back = O.transfer(m1, m0, rnd)
+    J1, wq = _weights2d(m1)
+    J0, _ = _weights2d(m0)
+    assert np.allclose(np.einsum("e,evq,q->v", J1, rnd, wq), np.einsum("e,evq,q->v", J0, back, wq),
+                       rtol=0, atol=1e-13 * np.abs(rnd).sum())
