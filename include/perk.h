@@ -1,0 +1,172 @@
+/*
+ * perk.h -- C ABI of libperk_b200.so: one Paired-Explicit Runge-Kutta (P-ERK) multirate step
+ * on a DGSEM (N = 3) semidiscretisation partitioned by AMR refinement level, on one B200.
+ *
+ * Source of every operation: /root/reference/PAPER.md ("P:l.N" = line N), readings in
+ * SURVEY.md §8(c) and DESIGN.md §2.
+ *   - problem U'(t) = F(t, U), DOFs partitioned by cell level into R partitions
+ *     (P:l.192-205, eq. PartitionedODESys; mask matrices I^(r), P:l.289-301)
+ *   - stage update K_i^(r) = F^(r)(U_n + dt sum_j sum_k a_ij^(k) K_j^(k)), U_{n+1} = U_n + dt sum b_i K_i
+ *     (P:l.209-218, eq. PartitionedRKSystem) with the P-ERK2 pattern: shared c, b = e_S, two nonzeros
+ *     a_{i,1}, a_{i,i-1} per row, member E evaluates stages {1} u {S-E+2..S}
+ *     (P:l.407-436, eq. PERK_ButcherTableauClassic; a_{i,1} = c_i - a_{i,i-1}, P:l.533)
+ *   - coefficients a_{i,i-1} from the stability polynomial (P:l.1048-1064, eqs. PERK2_StabPnom,
+ *     PERKCoeffsConstruction)
+ *   - per-level element / boundary / interface / mortar index lists; interfaces by common level,
+ *     mortars by the fine side (P:l.1243-1256); level -> member fill rule (P:l.1276-1279)
+ *
+ * Conventions (all calls):
+ *   - return 0 (PERK_OK) or a negative PERK_E* code; no exception crosses the ABI;
+ *     perk_last_error(ctx) gives a text for the last failure.
+ *   - pointers named *_dev are CUDA device pointers (e.g. torch.Tensor.data_ptr() of a cuda tensor),
+ *     pointers named *_host are host pointers; the library never frees caller memory and never
+ *     retains a caller pointer past the call, except U_dev inside the captured step graph, which is
+ *     re-captured whenever perk_step sees a different U_dev or dt.
+ *   - all device work is ordered on the context stream (perk_set_stream; default: the legacy
+ *     stream 0).  Calls documented "asynchronous" do not synchronise; device-side errors
+ *     (capacity overflow, unbalanced level map) latch a device flag reported by the next
+ *     synchronising call (perk_sync and every introspection call).
+ *   - one context per host thread at a time; contexts are independent.
+ */
+#ifndef PERK_B200_PERK_H
+#define PERK_B200_PERK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    PERK_OK = 0,
+    PERK_EINVAL = -1,       /* invalid argument (null pointer, bad enum, S/R/E out of range, ...) */
+    PERK_EUNBALANCED = -2,  /* level map not block-aligned, or 2:1 face balance violated */
+    PERK_ECAPACITY = -3,    /* more cells / faces than the capacity given at perk_init */
+    PERK_ECUDA = -4,        /* a CUDA runtime call failed */
+    PERK_ENOTINIT = -5,     /* context null or destroyed */
+    PERK_EUNSUPPORTED = -6  /* combination not implemented (e.g. Navier-Stokes BR1 this round) */
+};
+
+enum { PERK_EQ_ADVECTION = 0, PERK_EQ_EULER = 1, PERK_EQ_NAVIER_STOKES = 2 };
+enum { PERK_VOL_WEAK = 0, PERK_VOL_FLUXDIFF = 1 };               /* weak form (1D), Ranocha flux differencing (2D) */
+enum { PERK_FLUX_UPWIND = 0, PERK_FLUX_RUSANOV = 1, PERK_FLUX_HLL = 2 };
+enum { PERK_KIND_ELEMENTS = 0, PERK_KIND_INTERFACES = 1, PERK_KIND_MORTARS = 2, PERK_KIND_BOUNDARIES = 3 };
+
+#define PERK_MAX_STAGES 64
+#define PERK_MAX_MEMBERS 8
+#define PERK_NUM_KERNEL_KINDS 4   /* profile slots: 0 surface flux, 1 volume+stage, 2 mesh rebuild, 3 transfer */
+
+/* Problem description.  DG degree N = 3 (LGL nodes) is fixed.
+ *   dim            1 or 2
+ *   n_base[2]      base cells per direction (n_base[1] ignored in 1D); square cells required in 2D
+ *   max_level      maximum allowed refinement level L (finest grid = n_base << L per direction)
+ *   periodic[2]    1 = periodic, 0 = weakly imposed Dirichlet state bc_state on that direction's faces
+ *   domain_lo/hi   physical box ([lo, hi] per direction)
+ *   gamma          ratio of specific heats (Euler / NS)
+ *   prandtl, mu    Navier-Stokes parameters (equation 2; not supported in this build -> EUNSUPPORTED)
+ *   adv_velocity   1D linear advection speed a (equation 0)
+ *   bc_state[4]    conserved ghost state for non-periodic faces
+ *   max_cells      capacity (cells) for all buffers; the caller's U_dev must hold max_cells rows */
+typedef struct perk_problem {
+    int32_t dim;
+    int32_t equation;
+    int32_t volume;
+    int32_t surface;
+    int32_t n_base[2];
+    int32_t max_level;
+    int32_t periodic[2];
+    int32_t _pad;
+    double domain_lo[2];
+    double domain_hi[2];
+    double gamma;
+    double prandtl;
+    double mu;
+    double adv_velocity;
+    double bc_state[4];
+    int64_t max_cells;
+} perk_problem;
+
+/* P-ERK2 family.  S stages, R members with E[0] < ... < E[R-1] <= S (E[r] >= 2).
+ * c[i-1] = c_i, a_sub[r][i-1] = a_{i,i-1} of member r; a_{i,1} = c_i - a_{i,i-1} is derived.
+ * b = e_S (P:l.423).  Member r is assigned to level l by r = clamp(R-1-(L-l), 0, R-1). */
+typedef struct perk_tableau {
+    int32_t S;
+    int32_t R;
+    int32_t E[PERK_MAX_MEMBERS];
+    double c[PERK_MAX_STAGES];
+    double a_sub[PERK_MAX_MEMBERS][PERK_MAX_STAGES];
+} perk_tableau;
+
+typedef struct perk_ctx perk_ctx;
+
+/* Host only.  Taylor rule of BASELINE.json cfg 1: alpha[k] = 1/k!, k = 0..E (alpha has E+1 entries). */
+int perk_alpha_taylor(int32_t E, double *alpha_host);
+
+/* Host only.  Build a P-ERK2 family from stability-polynomial coefficients:
+ * alpha_host is R rows of (S+1) doubles, row r = alpha_0..alpha_S of member r (entries above E[r]
+ * ignored).  c_i = (i-1)/(2(S-1)) (P:l.439-442); a_{i,i-1} by the recursion of P:l.1062 for
+ * i = 0..E-3, all other a_{i,i-1} = 0.  EINVAL on bad sizes or a zero pivot. */
+int perk_tableau_p2(int32_t S, int32_t R, const int32_t *E_host, const double *alpha_host, perk_tableau *out);
+
+/* Create a context: validates prob/tab (EINVAL, EUNSUPPORTED), uploads the tableau, allocates
+ * capacity-sized device buffers and builds the mesh and per-member lists on the device from the
+ * finest-grid level map level_map_dev (uint8, (n_base[0] << L) x (n_base[1] << L) entries, x
+ * fastest; not retained).  Synchronises once at the end: EUNBALANCED / ECAPACITY are reported here.
+ * stream: a cudaStream_t (NULL = legacy stream). */
+int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t *level_map_dev, const perk_tableau *tab,
+              void *stream);
+int perk_destroy(perk_ctx *ctx);
+int perk_set_stream(perk_ctx *ctx, void *stream);
+
+/* One P-ERK step in place, asynchronous.  U_dev: fp64 [max_cells][nv][(N+1)^dim], cells in the
+ * canonical (Morton) order of perk_get_leaves, variables conserved, nodes x fastest.  The step is
+ * a CUDA graph captured on first use (and re-captured when U_dev or dt change). */
+int perk_step(perk_ctx *ctx, double *U_dev, double dt);
+
+/* Same step with HOST buffers: copies U_host (n_cells rows) to the device, runs nsteps steps,
+ * copies the result back and synchronises.  End-to-end API used by bench.py's e2e number. */
+int perk_run_host(perk_ctx *ctx, double *U_host, double dt, int64_t nsteps);
+
+/* Re-mesh, asynchronous: rebuild leaves, faces, per-member lists and stage prefix tables from a new
+ * level map on the device (no host round trip), and transfer U_dev in place (refine: interpolation,
+ * coarsen: exact L2 projection; |level change| <= 1 per finest cell required). */
+int perk_repartition(perk_ctx *ctx, const uint8_t *level_map_dev, double *U_dev);
+
+/* dU = sum_{r in mask} I^(r) F(U) (P:l.289-301): zero on cells of unmasked members.  Asynchronous.
+ * U_dev read only; dU_dev caller-owned, same layout as U. */
+int rhs_eval(perk_ctx *ctx, const double *U_dev, uint32_t partition_mask, double *dU_dev);
+
+/* ---- introspection (synchronising) ---- */
+int perk_num_cells(perk_ctx *ctx, int64_t *n_cells);
+int perk_num_faces(perk_ctx *ctx, int64_t *counts3);            /* interfaces, mortars, boundaries */
+/* physical node coordinates, device array [n_cells][dim][(N+1)^dim] (asynchronous) */
+int perk_node_coords(perk_ctx *ctx, double *xy_dev);
+/* leaf origins on the finest grid, level and member, host arrays of >= n_cells entries */
+int perk_get_leaves(perk_ctx *ctx, int32_t *fx_host, int32_t *fy_host, uint8_t *level_host, int32_t *member_host,
+                    int64_t cap);
+/* face records (host): interfaces [n][3] = low elem, high elem, orientation; mortars [n][5] = large,
+ * small_lo, small_hi, orientation, large_side (0: large element on the low side); boundaries [n][2] =
+ * elem, face (0 +x, 1 -x, 2 +y, 3 -y); member_host[n] = the partition of each record. */
+int perk_get_faces(perk_ctx *ctx, int32_t kind, int32_t *rec_host, int32_t *member_host, int64_t cap, int64_t *len);
+/* per-member compacted list of `kind` (item indices), segments by descending member; seg_host[R+1] */
+int perk_get_list(perk_ctx *ctx, int32_t kind, int32_t *list_host, int64_t cap, int64_t *seg_host);
+/* count_active_host[i-1] = number of `kind` items evaluated at stage i, i = 1..S */
+int perk_get_count_active(perk_ctx *ctx, int32_t kind, int32_t *count_active_host);
+/* element-RHS evaluations (sum over steps of sum_r E_r N_C(r), P:l.1282-1289) and steps taken */
+int perk_get_counters(perk_ctx *ctx, int64_t *elem_rhs_evals, int64_t *steps);
+int perk_sync(perk_ctx *ctx);
+const char *perk_last_error(perk_ctx *ctx);
+
+/* Profiling (synchronising): run one step eagerly (no graph) with CUDA events around every launch
+ * on the context stream; ms_host[k] += device time of kernel kind k, launches_host[k] += launches. */
+int perk_profile_step(perk_ctx *ctx, double *U_dev, double dt, float *ms_host, int32_t *launches_host);
+/* Same for one repartition (kinds 2 and 3). */
+int perk_profile_repartition(perk_ctx *ctx, const uint8_t *level_map_dev, double *U_dev, float *ms_host,
+                             int32_t *launches_host);
+/* Number of kernel launches one perk_step performs (graph nodes). */
+int perk_launches_per_step(perk_ctx *ctx, int32_t *launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PERK_B200_PERK_H */

@@ -1,0 +1,362 @@
+// dg2d.cuh -- 2D compressible Euler DGSEM (N = 3) kernels of one P-ERK stage.
+//
+// k_surf2d : one launch per stage over the active prefixes of the interface, mortar and boundary
+//            lists (4 threads per face, one per face node): gathers the two traces of the stage-i
+//            state (U_n, the stage buffer, or U_n + dt c_i K_1 formed on the fly), HLL flux,
+//            writes the per-element face-flux slots Fs.  Mortars interpolate the large trace to the
+//            two halves (P_lower/P_upper) and project the two half fluxes back (exact-L2 R), with
+//            the 4-node exchanges done by warp shuffles inside the 4-lane group.
+// k_vol2d  : one launch per stage over the active element prefix, 8 threads per element (4 x-lines
+//            + 4 y-lines): primitives and logarithms per node once (shared memory), 48 symmetric
+//            Ranocha two-point fluxes (6 per line), surface lift (1/w) and Jacobian (-2/h), then the
+//            stage epilogue in registers: K_1 (stage 1), the next stage state
+//            U^(i+1) = U_n + dt (a_{i+1,1} K_1 + a_{i+1,i} K_i) (1 < i < S), or U_{n+1} = U_n + dt K_S.
+#pragma once
+#include "common.cuh"
+
+namespace perk {
+
+// ---------------------------------------------------------------------------------------------
+// fluxes
+// ---------------------------------------------------------------------------------------------
+struct Prim {
+    double rho, v1, v2, p, lrho, beta, lbeta;
+};
+
+// logarithmic mean as a quotient N / D (no division here): (b - a) / (ln b - ln a), or near a = b
+// the series (a + b) / (2 + u (2/3 + u (2/5 + u 2/7))), u = ((b - a)/(b + a))^2 < 1e-4
+// (SURVEY §8(c) D3), multiplied through by (a + b)^6.
+__device__ __forceinline__ void ln_mean_nd(double a, double b, double la, double lb, double &N, double &D)
+{
+    const double s = a + b, d = b - a;
+    const double s2 = s * s, d2 = d * d;
+    const bool series = d2 < 1e-4 * s2;
+    const double s4 = s2 * s2, s6 = s4 * s2;
+    const double Ds = fma(2.0, s6, d2 * fma(2.0 / 3.0, s4, d2 * fma(2.0 / 5.0, s2, d2 * (2.0 / 7.0))));
+    N = series ? s6 * s : d;
+    D = series ? Ds : lb - la;
+}
+
+// Ranocha entropy-conserving two-point flux in direction o:
+// f_rho = rho_hat vbar_n, f_m = f_rho vbar + pbar n, f_E = f_rho (1/2 vL.vR + 1/((g-1) beta_hat)) + 1/2 (pL vnR + pR vnL)
+__device__ __forceinline__ void flux_ranocha(const Prim &L, const Prim &R, int o, double inv_gm1, double f[4])
+{
+    double Nr, Dr, Nb, Db;
+    ln_mean_nd(L.rho, R.rho, L.lrho, R.lrho, Nr, Dr);
+    ln_mean_nd(L.beta, R.beta, L.lbeta, R.lbeta, Nb, Db);
+    const double q = rcp64(Dr * Nb);
+    const double rho_hat = Nr * Nb * q;          // Nr / Dr
+    const double inv_beta_hat = Db * Dr * q;     // Db / Nb
+    const double v1a = 0.5 * (L.v1 + R.v1), v2a = 0.5 * (L.v2 + R.v2), pa = 0.5 * (L.p + R.p);
+    const double vnL = o == 0 ? L.v1 : L.v2, vnR = o == 0 ? R.v1 : R.v2;
+    const double frho = rho_hat * 0.5 * (vnL + vnR);
+    f[0] = frho;
+    f[1] = fma(frho, v1a, o == 0 ? pa : 0.0);
+    f[2] = fma(frho, v2a, o == 1 ? pa : 0.0);
+    f[3] = fma(frho, fma(0.5, fma(L.v1, R.v1, L.v2 * R.v2), inv_beta_hat * inv_gm1), 0.5 * fma(L.p, vnR, R.p * vnL));
+}
+
+__device__ __forceinline__ void euler_flux2d(const double u[4], double p, double vn, int o, double f[4])
+{
+    f[0] = u[0] * vn;
+    f[1] = u[1] * vn + (o == 0 ? p : 0.0);
+    f[2] = u[2] * vn + (o == 1 ? p : 0.0);
+    f[3] = (u[3] + p) * vn;
+}
+
+// HLL with Davis wave-speed estimates; Rusanov as the alternative
+__device__ __forceinline__ void numflux2d(const double uL[4], const double uR[4], int o, double g, int surface,
+                                          double f[4])
+{
+    const double gm1 = g - 1.0;
+    const double v1L = uL[1] / uL[0], v2L = uL[2] / uL[0];
+    const double v1R = uR[1] / uR[0], v2R = uR[2] / uR[0];
+    const double pL = gm1 * (uL[3] - 0.5 * (uL[1] * v1L + uL[2] * v2L));
+    const double pR = gm1 * (uR[3] - 0.5 * (uR[1] * v1R + uR[2] * v2R));
+    const double cL = sqrt(g * pL / uL[0]), cR = sqrt(g * pR / uR[0]);
+    const double vnL = o == 0 ? v1L : v2L, vnR = o == 0 ? v1R : v2R;
+    double fL[4], fR[4];
+    euler_flux2d(uL, pL, vnL, o, fL);
+    euler_flux2d(uR, pR, vnR, o, fR);
+    if (surface == 1) {
+        const double lam = fmax(fabs(vnL) + cL, fabs(vnR) + cR);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) f[v] = 0.5 * (fL[v] + fR[v]) - 0.5 * lam * (uR[v] - uL[v]);
+        return;
+    }
+    const double sL = fmin(vnL - cL, vnR - cR), sR = fmax(vnL + cL, vnR + cR);
+    if (sL >= 0.0) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) f[v] = fL[v];
+    } else if (sR <= 0.0) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) f[v] = fR[v];
+    } else {
+        const double inv = 1.0 / (sR - sL);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) f[v] = (sR * fL[v] - sL * fR[v] + sL * sR * (uR[v] - uL[v])) * inv;
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// surface kernel
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void trace2d(const StateBufs &sb, int src, double dtc, int e, int face, int k, double u[4])
+{
+    const size_t b = (size_t)e * 64 + face_node2d(face, k);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) u[v] = load_state(sb, src, dtc, b + v * 16);
+}
+
+__device__ __forceinline__ void store_face2d(double *Fs, int e, int face, int k, const double f[4])
+{
+    const size_t b = ((size_t)e * 4 + face) * 16 + k;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) Fs[b + v * 4] = f[v];
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_surf2d(MeshDev md, StageParams sp, const double *__restrict__ Un,
+                                               const double *__restrict__ Ubuf, const double *__restrict__ K1,
+                                               const double *__restrict__ Uin, double *__restrict__ Fs)
+{
+    int nif, nmo, nbd;
+    if (MODE == MODE_STAGE) {
+        nif = md.count_active[KIND_IF * MAXS + sp.stage - 1];
+        nmo = md.count_active[KIND_MO * MAXS + sp.stage - 1];
+        nbd = md.count_active[KIND_BD * MAXS + sp.stage - 1];
+    } else {
+        nif = md.n[1]; nmo = md.n[2]; nbd = md.n[3];
+    }
+    const int total = 4 * (nif + nmo + nbd);
+    const StateBufs sb{Un, Ubuf, K1, Uin};
+    const double dtc = sp.dt * sp.c_stage;
+    const double g = md.gamma;
+    const int lane = threadIdx.x & 31;
+    const unsigned gmask = 0xFu << (lane & ~3);
+    for (int gt = blockIdx.x * blockDim.x + threadIdx.x; gt < total; gt += gridDim.x * blockDim.x) {
+        const int item = gt >> 2, k = gt & 3;
+        if (item < nif) {
+            const int f = MODE == MODE_STAGE ? md.list[KIND_IF][item] : item;
+            const int4 I = md.ifc[f];
+            const int o = I.z;
+            const int src = state_src(sp, I.w);    // conforming: both sides share the member
+            double uL[4], uR[4], fl[4];
+            trace2d(sb, src, dtc, I.x, 2 * o, k, uL);
+            trace2d(sb, src, dtc, I.y, 2 * o + 1, k, uR);
+            numflux2d(uL, uR, o, g, md.surface, fl);
+            store_face2d(Fs, I.x, 2 * o, k, fl);
+            store_face2d(Fs, I.y, 2 * o + 1, k, fl);
+        } else if (item < nif + nmo) {
+            const int q = item - nif;
+            const int mo = MODE == MODE_STAGE ? md.list[KIND_MO][q] : q;
+            const int4 M = md.mor[mo];
+            const int o = M.w & 1, side = (M.w >> 1) & 1, mfine = M.w >> 8;
+            const int lf = 2 * o + side, sf = 2 * o + 1 - side;
+            const int srcL = state_src(sp, md.mem[M.x]);
+            const int srcS = state_src(sp, mfine);
+            double ul[4];
+            trace2d(sb, srcL, dtc, M.x, lf, k, ul);
+            double uil[4] = {0, 0, 0, 0}, uih[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int j = 0; j < NP; ++j) {
+                const double plo = cB.Plo[k][j], pup = cB.Pup[k][j];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const double uj = __shfl_sync(gmask, ul[v], j, 4);
+                    uil[v] = fma(plo, uj, uil[v]);
+                    uih[v] = fma(pup, uj, uih[v]);
+                }
+            }
+            double us0[4], us1[4], flo[4], fhi[4];
+            trace2d(sb, srcS, dtc, M.y, sf, k, us0);
+            trace2d(sb, srcS, dtc, M.z, sf, k, us1);
+            if (side == 0) {
+                numflux2d(uil, us0, o, g, md.surface, flo);
+                numflux2d(uih, us1, o, g, md.surface, fhi);
+            } else {
+                numflux2d(us0, uil, o, g, md.surface, flo);
+                numflux2d(us1, uih, o, g, md.surface, fhi);
+            }
+            store_face2d(Fs, M.y, sf, k, flo);
+            store_face2d(Fs, M.z, sf, k, fhi);
+            double fl[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int j = 0; j < NP; ++j) {
+                const double rlo = cB.Rlo[k][j], rup = cB.Rup[k][j];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const double a = __shfl_sync(gmask, flo[v], j, 4);
+                    const double b = __shfl_sync(gmask, fhi[v], j, 4);
+                    fl[v] = fma(rup, b, fma(rlo, a, fl[v]));
+                }
+            }
+            store_face2d(Fs, M.x, lf, k, fl);
+        } else {
+            const int q = item - nif - nmo;
+            const int bi = MODE == MODE_STAGE ? md.list[KIND_BD][q] : q;
+            const int2 B = md.bnd[bi];
+            const int face = B.y & 7, o = face >> 1;
+            const int src = state_src(sp, B.y >> 8);
+            double u[4], fl[4];
+            trace2d(sb, src, dtc, B.x, face, k, u);
+            if ((face & 1) == 0) numflux2d(u, md.bc, o, g, md.surface, fl);
+            else numflux2d(md.bc, u, o, g, md.surface, fl);
+            store_face2d(Fs, B.x, face, k, fl);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// volume + surface lift + Jacobian + stage epilogue
+// ---------------------------------------------------------------------------------------------
+constexpr int VOL2D_EPB = 16;   // elements per 128-thread block
+
+__device__ __forceinline__ double2 load_state2(const StateBufs &sb, int src, double dtc, size_t idx)
+{
+    switch (src) {
+    case SRC_UN: return __ldg(reinterpret_cast<const double2 *>(sb.Un + idx));
+    case SRC_BUF: return __ldg(reinterpret_cast<const double2 *>(sb.Ubuf + idx));
+    case SRC_LAZY: {
+        const double2 a = __ldg(reinterpret_cast<const double2 *>(sb.Un + idx));
+        const double2 k = __ldg(reinterpret_cast<const double2 *>(sb.K1 + idx));
+        return make_double2(fma(dtc, k.x, a.x), fma(dtc, k.y, a.y));
+    }
+    default: return __ldg(reinterpret_cast<const double2 *>(sb.Uin + idx));
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(128) k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
+                                              double *__restrict__ Ubuf, double *__restrict__ K1,
+                                              const double *__restrict__ Fs, const double *__restrict__ Uin,
+                                              double *__restrict__ dU)
+{
+    __shared__ double sprim[VOL2D_EPB][16][8];
+    __shared__ double sacc[VOL2D_EPB][4][16];
+    const int t8 = threadIdx.x & 7, le = threadIdx.x >> 3;
+    const int n_act = MODE == MODE_STAGE ? md.count_active[KIND_EL * MAXS + sp.stage - 1] : md.n[0];
+    const double g = md.gamma, gm1 = g - 1.0, inv_gm1 = 1.0 / gm1;
+    const StateBufs sb{Un, Ubuf, K1, Uin};
+    const double dtc = sp.dt * sp.c_stage;
+    const int q0 = 2 * t8;
+    const int o = t8 >> 2, ln = t8 & 3;
+
+    if (MODE == MODE_STAGE && sp.stage == sp.S && blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long tot = 0;
+        for (int i = 0; i < sp.S; ++i) tot += (unsigned long long)md.count_active[KIND_EL * MAXS + i];
+        atomicAdd(md.evals, tot);
+        atomicAdd(md.evals + 1, 1ull);
+    }
+
+    for (int base = blockIdx.x * VOL2D_EPB; base < n_act; base += gridDim.x * VOL2D_EPB) {
+        const int t = base + le;
+        const bool valid = t < n_act;
+        const int tt = valid ? t : base;
+        const int e = MODE == MODE_STAGE ? md.list[KIND_EL][tt] : tt;
+        const int m = md.mem[e];
+        const int src = state_src(sp, m);
+        const size_t eb = (size_t)e * 64;
+
+        // phase 1: nodes q0, q0+1 -> primitives + logs in shared memory
+        {
+            double2 u[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) u[v] = load_state2(sb, src, dtc, eb + v * 16 + q0);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const double r = h ? u[0].y : u[0].x;
+                const double m1 = h ? u[1].y : u[1].x, m2 = h ? u[2].y : u[2].x, E = h ? u[3].y : u[3].x;
+                const double ir = rcp64(r);
+                const double v1 = m1 * ir, v2 = m2 * ir;
+                const double p = gm1 * (E - 0.5 * fma(m1, v1, m2 * v2));
+                const double beta = r * rcp64(p);
+                double *P = sprim[le][q0 + h];
+                P[0] = r; P[1] = v1; P[2] = v2; P[3] = p;
+                P[4] = log(r); P[5] = beta; P[6] = log(beta);
+            }
+        }
+        __syncwarp();
+
+        // phase 2: 6 symmetric two-point fluxes along this thread's line
+        double acc[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[a][v] = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const int qa = o == 0 ? ln * 4 + a : a * 4 + ln;
+            const double *PA = sprim[le][qa];
+            const Prim A{PA[0], PA[1], PA[2], PA[3], PA[4], PA[5], PA[6]};
+#pragma unroll
+            for (int b = a + 1; b < 4; ++b) {
+                const int qb = o == 0 ? ln * 4 + b : b * 4 + ln;
+                const double *PB = sprim[le][qb];
+                const Prim Bp{PB[0], PB[1], PB[2], PB[3], PB[4], PB[5], PB[6]};
+                double f[4];
+                flux_ranocha(A, Bp, o, inv_gm1, f);
+                const double dab = cB.Dsplit[a][b], dba = cB.Dsplit[b][a];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    acc[a][v] = fma(dab, f[v], acc[a][v]);
+                    acc[b][v] = fma(dba, f[v], acc[b][v]);
+                }
+            }
+        }
+        // surface lift: + f*_hi / w_N at the last node, - f*_lo / w_0 at the first node
+        {
+            const double *Fhi = Fs + ((size_t)e * 4 + 2 * o) * 16 + ln;
+            const double *Flo = Fs + ((size_t)e * 4 + 2 * o + 1) * 16 + ln;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                acc[3][v] = fma(__ldg(Fhi + v * 4), cB.invw[3], acc[3][v]);
+                acc[0][v] = fma(-__ldg(Flo + v * 4), cB.invw[0], acc[0][v]);
+            }
+        }
+        // combine the x-line and y-line contributions of every node
+        if (o == 0) {
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) sacc[le][v][ln * 4 + a] = acc[a][v];
+        }
+        __syncwarp();
+        if (o == 1) {
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) sacc[le][v][a * 4 + ln] += acc[a][v];
+        }
+        __syncwarp();
+
+        // phase 3: K = -(2/h) acc, stage epilogue for nodes q0, q0+1
+        if (valid) {
+            const double J = -2.0 / (md.hf * (double)(1 << (md.max_level - md.lev[e])));
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const size_t idx = eb + v * 16 + q0;
+                const double2 s = *reinterpret_cast<const double2 *>(&sacc[le][v][q0]);
+                const double2 K = make_double2(J * s.x, J * s.y);
+                if (MODE == MODE_RHS) {
+                    const bool on = (sp.mask >> m) & 1u;
+                    *reinterpret_cast<double2 *>(dU + idx) = on ? K : make_double2(0.0, 0.0);
+                } else if (sp.stage == 1) {
+                    *reinterpret_cast<double2 *>(K1 + idx) = K;
+                } else if (sp.stage == sp.S) {
+                    const double2 un = *reinterpret_cast<const double2 *>(Un + idx);
+                    *reinterpret_cast<double2 *>(Un + idx) = make_double2(fma(sp.dt, K.x, un.x), fma(sp.dt, K.y, un.y));
+                } else {
+                    const double2 un = __ldg(reinterpret_cast<const double2 *>(Un + idx));
+                    const double2 k1 = __ldg(reinterpret_cast<const double2 *>(K1 + idx));
+                    const double a1 = sp.a1_next[m], as = sp.asub_next[m];
+                    *reinterpret_cast<double2 *>(Ubuf + idx) =
+                        make_double2(fma(sp.dt, fma(a1, k1.x, as * K.x), un.x), fma(sp.dt, fma(a1, k1.y, as * K.y), un.y));
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace perk

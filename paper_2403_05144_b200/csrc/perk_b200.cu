@@ -1,0 +1,703 @@
+// perk_b200.cu -- libperk_b200.so: the C ABI of include/perk.h (host side) + all device kernels.
+//
+// Host-side responsibilities: argument validation, tableau construction (P:l.1062), capacity-sized
+// allocations, launching the device mesh pipeline (mesh.cuh), capturing one CUDA graph per P-ERK
+// step (2 launches per stage: k_surf*, k_vol*), profiling hooks.  No step of the method runs on
+// the host: after perk_init the host never reads mesh data except in introspection calls.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "perk.h"
+#include "common.cuh"
+#include "basis.cuh"
+#include "partition.cuh"
+#include "mesh.cuh"
+#include "dg1d.cuh"
+#include "dg2d.cuh"
+#include "transfer.cuh"
+
+using namespace perk;
+
+struct Prof {
+    float ms[PERK_NUM_KERNEL_KINDS];
+    int launches[PERK_NUM_KERNEL_KINDS];
+    std::vector<cudaEvent_t> ev;
+    std::vector<int> kind;
+};
+
+struct perk_ctx {
+    perk_problem prob;
+    perk_tableau tab;
+    MeshDev md;
+    int nv = 0, npe = 0, nd = 0;
+    long long nmorton = 0;
+    size_t nf = 0;
+    int cap = 0, cap_faces = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t cap_stream = nullptr;
+    double *K1 = nullptr, *Ubuf = nullptr, *Fs = nullptr, *Utmp = nullptr, *Uhost_dev = nullptr;
+    uint8_t *lmap = nullptr, *keys = nullptr;
+    int *items = nullptr, *rank = nullptr, *blockcnt = nullptr, *blockoff = nullptr, *segtmp = nullptr;
+    int *dconst = nullptr;     // [0] = nmorton
+    int *n_old = nullptr, *cell_of_old = nullptr, *fx_old = nullptr, *fy_old = nullptr;
+    uint8_t *lev_old = nullptr;
+    int vol_blocks = 0, surf_blocks = 0;
+    cudaGraphExec_t gexec = nullptr;
+    double *gU = nullptr;
+    double gdt = 0.0;
+    std::vector<void *> allocs;
+    std::string err;
+};
+
+static bool g_basis_uploaded = false;
+
+static int set_err(perk_ctx *c, int code, const std::string &msg)
+{
+    if (c) c->err = msg;
+    return code;
+}
+
+#define CU(call)                                                                                     \
+    do {                                                                                             \
+        cudaError_t e_ = (call);                                                                     \
+        if (e_ != cudaSuccess)                                                                       \
+            return set_err(c, PERK_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
+    } while (0)
+
+template <class T>
+static cudaError_t dalloc(perk_ctx *c, T **p, size_t n)
+{
+    cudaError_t e = cudaMalloc((void **)p, sizeof(T) * (n ? n : 1));
+    if (e == cudaSuccess) {
+        c->allocs.push_back((void *)*p);
+        cudaMemset(*p, 0, sizeof(T) * (n ? n : 1));
+    }
+    return e;
+}
+
+// ----------------------------------------------------------------------------------------------
+// tableau
+// ----------------------------------------------------------------------------------------------
+extern "C" int perk_alpha_taylor(int32_t E, double *alpha)
+{
+    if (!alpha || E < 0 || E >= PERK_MAX_STAGES) return PERK_EINVAL;
+    double f = 1.0;
+    alpha[0] = 1.0;
+    for (int k = 1; k <= E; ++k) {
+        f *= k;
+        alpha[k] = 1.0 / f;
+    }
+    return PERK_OK;
+}
+
+extern "C" int perk_tableau_p2(int32_t S, int32_t R, const int32_t *E, const double *alpha, perk_tableau *out)
+{
+    if (!E || !alpha || !out || S < 2 || S > PERK_MAX_STAGES || R < 1 || R > PERK_MAX_MEMBERS) return PERK_EINVAL;
+    for (int r = 0; r < R; ++r) {
+        if (E[r] < 2 || E[r] > S) return PERK_EINVAL;
+        if (r > 0 && E[r] <= E[r - 1]) return PERK_EINVAL;
+    }
+    memset(out, 0, sizeof(*out));
+    out->S = S;
+    out->R = R;
+    for (int i = 1; i <= S; ++i) out->c[i - 1] = (double)(i - 1) / (double)(2 * (S - 1));
+    for (int r = 0; r < R; ++r) {
+        out->E[r] = E[r];
+        const double *al = alpha + (size_t)r * (S + 1);
+        double a[PERK_MAX_STAGES + 1] = {0};
+        // a_{S-i} = alpha_{3+i} / (c_{S-i-1} prod_{j<i} a_{S-j}),  i = 0..E-3   (P:l.1058-1064)
+        for (int i = 0; i <= E[r] - 3; ++i) {
+            double prod = 1.0;
+            for (int j = 0; j < i; ++j) prod *= a[S - j];
+            const double den = out->c[S - i - 2] * prod;
+            if (den == 0.0) return PERK_EINVAL;
+            a[S - i] = al[3 + i] / den;
+        }
+        for (int m = 1; m <= S; ++m) out->a_sub[r][m - 1] = a[m];
+    }
+    return PERK_OK;
+}
+
+// ----------------------------------------------------------------------------------------------
+// partition launcher
+// ----------------------------------------------------------------------------------------------
+static ActiveDesc active_desc(const perk_ctx *c)
+{
+    ActiveDesc ad;
+    ad.S = c->tab.S;
+    ad.R = c->tab.R;
+    for (int r = 0; r < MAXR; ++r) ad.E[r] = r < c->tab.R ? c->tab.E[r] : 0;
+    return ad;
+}
+
+static void prof_mark(Prof *p, cudaStream_t s, int kind)
+{
+    if (!p) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    p->ev.push_back(e);
+    p->kind.push_back(kind);
+}
+
+template <class KeyFn>
+static void partition(perk_ctx *c, cudaStream_t s, KeyFn kf, const int *n_ptr, int mult, long long max_items, int R,
+                      int *out, int *rank, int *seg, int *total_out, int *count_active)
+{
+    int nb = (int)((max_items + PART_T - 1) / PART_T);
+    if (nb < 1) nb = 1;
+    k_part_count<<<nb, PART_T, 0, s>>>(kf, n_ptr, mult, R, c->blockcnt);
+    k_part_offsets<<<1, PART_T, 0, s>>>(c->blockcnt, nb, R, c->blockoff, seg, total_out, active_desc(c), count_active);
+    k_part_scatter<<<nb, PART_T, 0, s>>>(kf, n_ptr, mult, R, c->blockoff, out, rank);
+}
+
+__global__ void k_set_count(int *dst, const int *seg, int idx) { *dst = seg[idx + 1] - seg[idx]; }
+
+static int blocks_for(long long n, int t)
+{
+    long long b = (n + t - 1) / t;
+    return (int)(b < 1 ? 1 : b);
+}
+
+// level map (device) -> leaves, faces, per-member lists, stage prefix tables; all asynchronous
+static void build_mesh(perk_ctx *c, cudaStream_t s, const uint8_t *lmap)
+{
+    MeshDev &md = c->md;
+    const int R = c->tab.R;
+    k_leaf_flags<<<blocks_for(c->nmorton, 256), 256, 0, s>>>(md, lmap, c->nmorton, c->keys);
+    partition(c, s, KeyU8{c->keys}, c->dconst, 1, c->nmorton, 2, c->items, c->rank, c->segtmp, nullptr, nullptr);
+    k_set_count<<<1, 1, 0, s>>>(md.n, c->segtmp, 0);
+    k_check_capacity<<<1, 1, 0, s>>>(md);
+    k_leaf_fill<<<blocks_for(c->cap, 256), 256, 0, s>>>(md, lmap, c->items, R);
+    k_cell_of<<<blocks_for((long long)c->nf, 256), 256, 0, s>>>(md, lmap, c->rank);
+    k_classify<<<blocks_for((long long)c->nd * c->cap, 256), 256, 0, s>>>(md, c->keys);
+    partition(c, s, KeyU8{c->keys}, md.n, c->nd, (long long)c->nd * c->cap, 4, c->items, nullptr, c->segtmp, nullptr,
+              nullptr);
+    k_face_counts<<<1, 1, 0, s>>>(md, c->segtmp, c->cap_faces);
+    k_face_records<<<blocks_for((long long)c->nd * c->cap, 256), 256, 0, s>>>(md, c->items, c->segtmp, R);
+    partition(c, s, KeyU8{md.mem}, md.n + 0, 1, c->cap, R, md.list[KIND_EL], nullptr, md.seg + 0 * (MAXR + 1), nullptr,
+              md.count_active + KIND_EL * MAXS);
+    partition(c, s, KeyIfc{md.ifc}, md.n + 1, 1, c->cap_faces, R, md.list[KIND_IF], nullptr, md.seg + 1 * (MAXR + 1),
+              nullptr, md.count_active + KIND_IF * MAXS);
+    partition(c, s, KeyMor{md.mor}, md.n + 2, 1, c->cap_faces, R, md.list[KIND_MO], nullptr, md.seg + 2 * (MAXR + 1),
+              nullptr, md.count_active + KIND_MO * MAXS);
+    partition(c, s, KeyBnd{md.bnd}, md.n + 3, 1, c->cap_faces, R, md.list[KIND_BD], nullptr, md.seg + 3 * (MAXR + 1),
+              nullptr, md.count_active + KIND_BD * MAXS);
+}
+
+// ----------------------------------------------------------------------------------------------
+// stage launches
+// ----------------------------------------------------------------------------------------------
+static StageParams stage_params(const perk_ctx *c, int i, double dt, int mode, unsigned mask)
+{
+    StageParams sp;
+    memset(&sp, 0, sizeof(sp));
+    sp.stage = i;
+    sp.S = c->tab.S;
+    sp.R = c->tab.R;
+    sp.mode = mode;
+    sp.mask = mask;
+    sp.dt = dt;
+    sp.c_stage = c->tab.c[i - 1];
+    for (int r = 0; r < c->tab.R; ++r) {
+        sp.first[r] = c->tab.S - c->tab.E[r] + 2;
+        if (i < c->tab.S) {
+            sp.asub_next[r] = c->tab.a_sub[r][i];                  // a_{i+1,i}
+            sp.a1_next[r] = c->tab.c[i] - c->tab.a_sub[r][i];       // a_{i+1,1} = c_{i+1} - a_{i+1,i}
+        }
+    }
+    return sp;
+}
+
+static void launch_surface(perk_ctx *c, cudaStream_t s, const StageParams &sp, const double *Un, const double *Uin)
+{
+    const MeshDev &md = c->md;
+    if (c->prob.dim == 2) {
+        if (sp.mode == MODE_STAGE)
+            k_surf2d<MODE_STAGE><<<c->surf_blocks, 256, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs);
+        else
+            k_surf2d<MODE_RHS><<<c->surf_blocks, 256, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs);
+    } else if (c->nv == 1) {
+        if (sp.mode == MODE_STAGE)
+            k_surf1d<1, MODE_STAGE><<<c->surf_blocks, 256, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs);
+        else
+            k_surf1d<1, MODE_RHS><<<c->surf_blocks, 256, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs);
+    } else {
+        if (sp.mode == MODE_STAGE)
+            k_surf1d<3, MODE_STAGE><<<c->surf_blocks, 256, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs);
+        else
+            k_surf1d<3, MODE_RHS><<<c->surf_blocks, 256, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs);
+    }
+}
+
+static void launch_volume(perk_ctx *c, cudaStream_t s, const StageParams &sp, double *Un, const double *Uin, double *dU)
+{
+    const MeshDev &md = c->md;
+    if (c->prob.dim == 2) {
+        if (sp.mode == MODE_STAGE)
+            k_vol2d<MODE_STAGE><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU);
+        else
+            k_vol2d<MODE_RHS><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU);
+    } else if (c->nv == 1) {
+        if (sp.mode == MODE_STAGE)
+            k_vol1d<1, MODE_STAGE><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU);
+        else
+            k_vol1d<1, MODE_RHS><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU);
+    } else {
+        if (sp.mode == MODE_STAGE)
+            k_vol1d<3, MODE_STAGE><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU);
+        else
+            k_vol1d<3, MODE_RHS><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU);
+    }
+}
+
+static void launch_step(perk_ctx *c, cudaStream_t s, double *U, double dt, Prof *p)
+{
+    for (int i = 1; i <= c->tab.S; ++i) {
+        const StageParams sp = stage_params(c, i, dt, MODE_STAGE, 0u);
+        prof_mark(p, s, 0);
+        launch_surface(c, s, sp, U, nullptr);
+        prof_mark(p, s, 1);
+        launch_volume(c, s, sp, U, nullptr, nullptr);
+        prof_mark(p, s, -1);
+    }
+}
+
+static int check_device_err(perk_ctx *c)
+{
+    CU(cudaStreamSynchronize(c->stream));
+    int e = 0;
+    CU(cudaMemcpy(&e, c->md.err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (e) {
+        int z = 0;
+        CU(cudaMemcpy(c->md.err, &z, sizeof(int), cudaMemcpyHostToDevice));
+        if (e & ERR_UNBALANCED) return set_err(c, PERK_EUNBALANCED, "level map not block-aligned or not 2:1 face balanced");
+        if (e & ERR_CAPACITY) return set_err(c, PERK_ECAPACITY, "cell / face capacity exceeded");
+        if (e & ERR_TRANSFER) return set_err(c, PERK_EUNBALANCED, "re-mesh changed a level by more than one");
+    }
+    return PERK_OK;
+}
+
+// ----------------------------------------------------------------------------------------------
+// C ABI
+// ----------------------------------------------------------------------------------------------
+static int validate(perk_ctx *c, const perk_problem *p, const perk_tableau *t)
+{
+    if (p->dim != 1 && p->dim != 2) return set_err(c, PERK_EINVAL, "dim must be 1 or 2");
+    if (p->n_base[0] < 1 || (p->dim == 2 && p->n_base[1] < 1)) return set_err(c, PERK_EINVAL, "n_base");
+    if (p->max_level < 0 || p->max_level > 12) return set_err(c, PERK_EINVAL, "max_level");
+    if (p->max_cells < 1 || p->max_cells > (1ll << 28)) return set_err(c, PERK_EINVAL, "max_cells");
+    if (p->dim == 1) {
+        if (p->equation == PERK_EQ_ADVECTION) {
+            if (p->surface != PERK_FLUX_UPWIND) return set_err(c, PERK_EUNSUPPORTED, "1D advection uses the upwind flux");
+        } else if (p->equation == PERK_EQ_EULER) {
+            if (p->surface != PERK_FLUX_RUSANOV) return set_err(c, PERK_EUNSUPPORTED, "1D Euler uses the Rusanov flux");
+        } else {
+            return set_err(c, PERK_EUNSUPPORTED, "1D supports advection and Euler");
+        }
+        if (p->volume != PERK_VOL_WEAK) return set_err(c, PERK_EUNSUPPORTED, "1D uses the weak form");
+    } else {
+        if (p->equation == PERK_EQ_NAVIER_STOKES) return set_err(c, PERK_EUNSUPPORTED, "Navier-Stokes (BR1) not in this build");
+        if (p->equation != PERK_EQ_EULER) return set_err(c, PERK_EUNSUPPORTED, "2D supports Euler");
+        if (p->volume != PERK_VOL_FLUXDIFF) return set_err(c, PERK_EUNSUPPORTED, "2D uses flux differencing");
+        if (p->surface != PERK_FLUX_HLL && p->surface != PERK_FLUX_RUSANOV) return set_err(c, PERK_EUNSUPPORTED, "2D surface flux");
+        const double hx = (p->domain_hi[0] - p->domain_lo[0]) / p->n_base[0];
+        const double hy = (p->domain_hi[1] - p->domain_lo[1]) / p->n_base[1];
+        if (!(hx > 0) || std::fabs(hx - hy) > 1e-12 * hx) return set_err(c, PERK_EINVAL, "2D cells must be square");
+    }
+    if (!(p->domain_hi[0] > p->domain_lo[0])) return set_err(c, PERK_EINVAL, "domain");
+    if (t->S < 2 || t->S > PERK_MAX_STAGES || t->R < 1 || t->R > PERK_MAX_MEMBERS) return set_err(c, PERK_EINVAL, "S/R");
+    for (int r = 0; r < t->R; ++r) {
+        if (t->E[r] < 2 || t->E[r] > t->S || (r > 0 && t->E[r] <= t->E[r - 1]))
+            return set_err(c, PERK_EINVAL, "E must be ascending in [2, S]");
+    }
+    return PERK_OK;
+}
+
+extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t *level_map_dev, const perk_tableau *tab,
+                         void *stream)
+{
+    if (!out || !prob || !level_map_dev || !tab) return PERK_EINVAL;
+    *out = nullptr;
+    perk_ctx *c = new perk_ctx();
+    int rc = validate(c, prob, tab);
+    if (rc) { *out = c; return rc; }
+    c->prob = *prob;
+    c->tab = *tab;
+    c->stream = (cudaStream_t)stream;
+    const int dim = prob->dim, L = prob->max_level;
+    c->nv = prob->equation == PERK_EQ_ADVECTION ? 1 : (dim == 1 ? 3 : 4);
+    c->npe = dim == 1 ? NP : NP * NP;
+    c->nd = dim == 1 ? 2 : 4;
+    c->cap = (int)prob->max_cells;
+    c->cap_faces = c->nd * c->cap;
+    MeshDev &md = c->md;
+    memset(&md, 0, sizeof(md));
+    md.dim = dim;
+    md.nv = c->nv;
+    md.npe = c->npe;
+    md.max_level = L;
+    md.nfx = prob->n_base[0] << L;
+    md.nfy = dim == 1 ? 1 : (prob->n_base[1] << L);
+    md.periodic[0] = prob->periodic[0];
+    md.periodic[1] = dim == 1 ? 1 : prob->periodic[1];
+    md.equation = prob->equation;
+    md.surface = prob->surface;
+    md.lo[0] = prob->domain_lo[0];
+    md.lo[1] = prob->domain_lo[1];
+    md.hf = (prob->domain_hi[0] - prob->domain_lo[0]) / md.nfx;
+    md.gamma = prob->gamma;
+    md.adv = prob->adv_velocity;
+    for (int v = 0; v < MAXV; ++v) md.bc[v] = prob->bc_state[v];
+    md.cap = c->cap;
+    c->nf = (size_t)md.nfx * md.nfy;
+    if (dim == 1) {
+        c->nmorton = md.nfx;
+    } else {
+        long long P = 1;
+        while (P < md.nfx || P < md.nfy) P <<= 1;
+        c->nmorton = P * P;
+    }
+    if (c->nmorton > (1ll << 30)) { *out = c; return set_err(c, PERK_EINVAL, "finest grid too large"); }
+
+    CU(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+    if (!g_basis_uploaded) {
+        BasisTables B;
+        build_basis(B);
+        CU(cudaMemcpyToSymbol(cB, &B, sizeof(B)));
+        g_basis_uploaded = true;
+    }
+    const size_t rowd = (size_t)c->nv * c->npe;
+    const long long max_items = c->nmorton > (long long)c->nd * c->cap ? c->nmorton : (long long)c->nd * c->cap;
+    const int nb_max = (int)((max_items + PART_T - 1) / PART_T) + 1;
+    CU(dalloc(c, &md.n, 4));
+    CU(dalloc(c, &md.count_active, 4 * MAXS));
+    CU(dalloc(c, &md.seg, 4 * (MAXR + 1)));
+    CU(dalloc(c, &md.err, 1));
+    CU(dalloc(c, &md.evals, 2));
+    CU(dalloc(c, &md.list[KIND_EL], c->cap));
+    for (int k = 1; k < 4; ++k) CU(dalloc(c, &md.list[k], c->cap_faces));
+    CU(dalloc(c, &md.fx, c->cap));
+    CU(dalloc(c, &md.fy, c->cap));
+    CU(dalloc(c, &md.lev, c->cap));
+    CU(dalloc(c, &md.mem, c->cap));
+    CU(dalloc(c, &md.cell_of, c->nf));
+    CU(dalloc(c, &md.ifc, c->cap_faces));
+    CU(dalloc(c, &md.mor, c->cap_faces));
+    CU(dalloc(c, &md.bnd, c->cap_faces));
+    CU(dalloc(c, &c->K1, (size_t)c->cap * rowd));
+    CU(dalloc(c, &c->Ubuf, (size_t)c->cap * rowd));
+    CU(dalloc(c, &c->Fs, (size_t)c->cap * (dim == 1 ? 2 * c->nv : 4 * c->nv * NP)));
+    CU(dalloc(c, &c->lmap, c->nf));
+    CU(dalloc(c, &c->keys, (size_t)max_items));
+    CU(dalloc(c, &c->items, (size_t)max_items));
+    CU(dalloc(c, &c->rank, (size_t)c->nmorton));
+    CU(dalloc(c, &c->blockcnt, (size_t)nb_max * MAXR));
+    CU(dalloc(c, &c->blockoff, (size_t)nb_max * MAXR));
+    CU(dalloc(c, &c->segtmp, 16));
+    CU(dalloc(c, &c->dconst, 4));
+    int h_const[4] = {(int)c->nmorton, 0, 0, 0};
+    CU(cudaMemcpy(c->dconst, h_const, sizeof(h_const), cudaMemcpyHostToDevice));
+
+    int occ = 0;
+    if (dim == 2) {
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vol2d<MODE_STAGE>, 128, 0));
+        const int want = (c->cap + VOL2D_EPB - 1) / VOL2D_EPB;
+        c->vol_blocks = std::min(want, SM_COUNT_B200 * std::max(occ, 1));
+        c->surf_blocks = std::min(blocks_for(4ll * c->cap_faces, 256), SM_COUNT_B200 * 8);
+    } else {
+        c->vol_blocks = std::min(blocks_for(c->cap, 128), SM_COUNT_B200 * 8);
+        c->surf_blocks = std::min(blocks_for(c->cap_faces, 256), SM_COUNT_B200 * 8);
+    }
+    CU(cudaMemcpyAsync(c->lmap, level_map_dev, c->nf, cudaMemcpyDeviceToDevice, c->stream));
+    build_mesh(c, c->stream, c->lmap);
+    CU(cudaGetLastError());
+    rc = check_device_err(c);
+    *out = c;
+    return rc;
+}
+
+extern "C" int perk_destroy(perk_ctx *c)
+{
+    if (!c) return PERK_ENOTINIT;
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    cudaDeviceSynchronize();
+    for (void *p : c->allocs) cudaFree(p);
+    if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+    delete c;
+    return PERK_OK;
+}
+
+extern "C" int perk_set_stream(perk_ctx *c, void *stream)
+{
+    if (!c) return PERK_ENOTINIT;
+    c->stream = (cudaStream_t)stream;
+    return PERK_OK;
+}
+
+static int ensure_graph(perk_ctx *c, double *U, double dt)
+{
+    if (c->gexec && c->gU == U && c->gdt == dt) return PERK_OK;
+    if (c->gexec) {
+        cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+    }
+    cudaGraph_t g;
+    CU(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+    launch_step(c, c->cap_stream, U, dt, nullptr);
+    CU(cudaStreamEndCapture(c->cap_stream, &g));
+    CU(cudaGraphInstantiate(&c->gexec, g, 0));
+    cudaGraphDestroy(g);
+    c->gU = U;
+    c->gdt = dt;
+    return PERK_OK;
+}
+
+extern "C" int perk_step(perk_ctx *c, double *U, double dt)
+{
+    if (!c) return PERK_ENOTINIT;
+    if (!U) return set_err(c, PERK_EINVAL, "U_dev is null");
+    int rc = ensure_graph(c, U, dt);
+    if (rc) return rc;
+    CU(cudaGraphLaunch(c->gexec, c->stream));
+    return PERK_OK;
+}
+
+extern "C" int perk_launches_per_step(perk_ctx *c, int32_t *launches)
+{
+    if (!c) return PERK_ENOTINIT;
+    if (!launches) return PERK_EINVAL;
+    *launches = 2 * c->tab.S;
+    return PERK_OK;
+}
+
+extern "C" int perk_num_cells(perk_ctx *c, int64_t *n)
+{
+    if (!c) return PERK_ENOTINIT;
+    if (!n) return PERK_EINVAL;
+    int rc = check_device_err(c);
+    if (rc) return rc;
+    int h = 0;
+    CU(cudaMemcpy(&h, c->md.n, sizeof(int), cudaMemcpyDeviceToHost));
+    *n = h;
+    return PERK_OK;
+}
+
+extern "C" int perk_num_faces(perk_ctx *c, int64_t *counts3)
+{
+    if (!c) return PERK_ENOTINIT;
+    if (!counts3) return PERK_EINVAL;
+    int rc = check_device_err(c);
+    if (rc) return rc;
+    int h[4];
+    CU(cudaMemcpy(h, c->md.n, sizeof(h), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < 3; ++k) counts3[k] = h[k + 1];
+    return PERK_OK;
+}
+
+extern "C" int perk_run_host(perk_ctx *c, double *U_host, double dt, int64_t nsteps)
+{
+    if (!c) return PERK_ENOTINIT;
+    if (!U_host || nsteps < 0) return set_err(c, PERK_EINVAL, "U_host / nsteps");
+    int64_t n = 0;
+    int rc = perk_num_cells(c, &n);
+    if (rc) return rc;
+    const size_t bytes = (size_t)n * c->nv * c->npe * sizeof(double);
+    if (!c->Uhost_dev) CU(dalloc(c, &c->Uhost_dev, (size_t)c->cap * c->nv * c->npe));
+    CU(cudaMemcpyAsync(c->Uhost_dev, U_host, bytes, cudaMemcpyHostToDevice, c->stream));
+    for (int64_t s = 0; s < nsteps; ++s) {
+        rc = perk_step(c, c->Uhost_dev, dt);
+        if (rc) return rc;
+    }
+    CU(cudaMemcpyAsync(U_host, c->Uhost_dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return PERK_OK;
+}
+
+static int do_repartition(perk_ctx *c, const uint8_t *lmap, double *U, Prof *p)
+{
+    if (c->prob.dim != 2) return set_err(c, PERK_EUNSUPPORTED, "repartition with solution transfer is 2D only");
+    cudaStream_t s = c->stream;
+    if (!c->Utmp) {
+        CU(dalloc(c, &c->Utmp, (size_t)c->cap * c->nv * c->npe));
+        CU(dalloc(c, &c->n_old, 1));
+        CU(dalloc(c, &c->cell_of_old, c->nf));
+        CU(dalloc(c, &c->lev_old, c->cap));
+        CU(dalloc(c, &c->fx_old, c->cap));
+        CU(dalloc(c, &c->fy_old, c->cap));
+    }
+    prof_mark(p, s, 2);
+    CU(cudaMemcpyAsync(c->lmap, lmap, c->nf, cudaMemcpyDeviceToDevice, s));
+    k_save_old<<<SM_COUNT_B200 * 4, 256, 0, s>>>(c->md, c->n_old, c->cell_of_old, c->lev_old, c->fx_old, c->fy_old);
+    k_copy_rows<<<SM_COUNT_B200 * 4, 256, 0, s>>>(c->md.n, c->nv * c->npe, U, c->Utmp);
+    build_mesh(c, s, c->lmap);
+    prof_mark(p, s, 3);
+    OldMesh om{c->n_old, c->cell_of_old, c->lev_old, c->fx_old, c->fy_old};
+    k_transfer2d<<<SM_COUNT_B200 * 8, 256, 0, s>>>(c->md, om, c->nv, c->Utmp, U);
+    prof_mark(p, s, -1);
+    CU(cudaGetLastError());
+    return PERK_OK;
+}
+
+extern "C" int perk_repartition(perk_ctx *c, const uint8_t *lmap, double *U)
+{
+    if (!c) return PERK_ENOTINIT;
+    if (!lmap || !U) return set_err(c, PERK_EINVAL, "null pointer");
+    return do_repartition(c, lmap, U, nullptr);
+}
+
+extern "C" int rhs_eval(perk_ctx *c, const double *U, uint32_t mask, double *dU)
+{
+    if (!c) return PERK_ENOTINIT;
+    if (!U || !dU) return set_err(c, PERK_EINVAL, "null pointer");
+    const StageParams sp = stage_params(c, 1, 0.0, MODE_RHS, mask);
+    launch_surface(c, c->stream, sp, nullptr, U);
+    launch_volume(c, c->stream, sp, nullptr, U, dU);
+    CU(cudaGetLastError());
+    return PERK_OK;
+}
+
+extern "C" int perk_node_coords(perk_ctx *c, double *xy)
+{
+    if (!c) return PERK_ENOTINIT;
+    if (!xy) return PERK_EINVAL;
+    k_node_coords<<<blocks_for(c->cap, 128), 128, 0, c->stream>>>(c->md, xy);
+    CU(cudaGetLastError());
+    return PERK_OK;
+}
+
+extern "C" int perk_get_leaves(perk_ctx *c, int32_t *fx, int32_t *fy, uint8_t *lev, int32_t *mem, int64_t cap)
+{
+    int64_t n = 0;
+    int rc = perk_num_cells(c, &n);
+    if (rc) return rc;
+    if (cap < n || !fx || !fy || !lev || !mem) return set_err(c, PERK_EINVAL, "host arrays too small");
+    std::vector<uint8_t> m8(n);
+    CU(cudaMemcpy(fx, c->md.fx, n * sizeof(int), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(fy, c->md.fy, n * sizeof(int), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(lev, c->md.lev, n, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(m8.data(), c->md.mem, n, cudaMemcpyDeviceToHost));
+    for (int64_t k = 0; k < n; ++k) mem[k] = m8[k];
+    return PERK_OK;
+}
+
+extern "C" int perk_get_faces(perk_ctx *c, int32_t kind, int32_t *rec, int32_t *mem, int64_t cap, int64_t *len)
+{
+    if (!c) return PERK_ENOTINIT;
+    if (kind < 1 || kind > 3 || !len) return set_err(c, PERK_EINVAL, "kind");
+    int64_t cnt[3];
+    int rc = perk_num_faces(c, cnt);
+    if (rc) return rc;
+    const int64_t n = cnt[kind - 1];
+    *len = n;
+    if (!rec || !mem || cap < n) return set_err(c, PERK_EINVAL, "host arrays too small");
+    if (kind == 1) {
+        std::vector<int4> h(n);
+        CU(cudaMemcpy(h.data(), c->md.ifc, n * sizeof(int4), cudaMemcpyDeviceToHost));
+        for (int64_t k = 0; k < n; ++k) {
+            rec[3 * k] = h[k].x; rec[3 * k + 1] = h[k].y; rec[3 * k + 2] = h[k].z; mem[k] = h[k].w;
+        }
+    } else if (kind == 2) {
+        std::vector<int4> h(n);
+        CU(cudaMemcpy(h.data(), c->md.mor, n * sizeof(int4), cudaMemcpyDeviceToHost));
+        for (int64_t k = 0; k < n; ++k) {
+            rec[5 * k] = h[k].x; rec[5 * k + 1] = h[k].y; rec[5 * k + 2] = h[k].z;
+            rec[5 * k + 3] = h[k].w & 1; rec[5 * k + 4] = (h[k].w >> 1) & 1; mem[k] = h[k].w >> 8;
+        }
+    } else {
+        std::vector<int2> h(n);
+        CU(cudaMemcpy(h.data(), c->md.bnd, n * sizeof(int2), cudaMemcpyDeviceToHost));
+        for (int64_t k = 0; k < n; ++k) {
+            rec[2 * k] = h[k].x; rec[2 * k + 1] = h[k].y & 7; mem[k] = h[k].y >> 8;
+        }
+    }
+    return PERK_OK;
+}
+
+extern "C" int perk_get_list(perk_ctx *c, int32_t kind, int32_t *list, int64_t cap, int64_t *seg)
+{
+    if (!c) return PERK_ENOTINIT;
+    if (kind < 0 || kind > 3 || !seg) return set_err(c, PERK_EINVAL, "kind");
+    int rc = check_device_err(c);
+    if (rc) return rc;
+    int hs[MAXR + 1];
+    CU(cudaMemcpy(hs, c->md.seg + kind * (MAXR + 1), sizeof(hs), cudaMemcpyDeviceToHost));
+    const int R = c->tab.R;
+    for (int s = 0; s <= R; ++s) seg[s] = hs[s];
+    const int64_t n = hs[R];
+    if (!list || cap < n) return set_err(c, PERK_EINVAL, "host array too small");
+    CU(cudaMemcpy(list, c->md.list[kind], n * sizeof(int), cudaMemcpyDeviceToHost));
+    return PERK_OK;
+}
+
+extern "C" int perk_get_count_active(perk_ctx *c, int32_t kind, int32_t *out)
+{
+    if (!c) return PERK_ENOTINIT;
+    if (kind < 0 || kind > 3 || !out) return set_err(c, PERK_EINVAL, "kind");
+    int rc = check_device_err(c);
+    if (rc) return rc;
+    CU(cudaMemcpy(out, c->md.count_active + kind * MAXS, c->tab.S * sizeof(int), cudaMemcpyDeviceToHost));
+    return PERK_OK;
+}
+
+extern "C" int perk_get_counters(perk_ctx *c, int64_t *evals, int64_t *steps)
+{
+    if (!c) return PERK_ENOTINIT;
+    int rc = check_device_err(c);
+    if (rc) return rc;
+    unsigned long long h[2];
+    CU(cudaMemcpy(h, c->md.evals, sizeof(h), cudaMemcpyDeviceToHost));
+    if (evals) *evals = (int64_t)h[0];
+    if (steps) *steps = (int64_t)h[1];
+    return PERK_OK;
+}
+
+extern "C" int perk_sync(perk_ctx *c)
+{
+    if (!c) return PERK_ENOTINIT;
+    return check_device_err(c);
+}
+
+extern "C" const char *perk_last_error(perk_ctx *c)
+{
+    if (!c) return "null context";
+    return c->err.c_str();
+}
+
+static int finish_prof(perk_ctx *c, Prof &p, float *ms, int32_t *launches)
+{
+    CU(cudaStreamSynchronize(c->stream));
+    for (size_t k = 0; k + 1 < p.ev.size(); ++k) {
+        const int kind = p.kind[k];
+        if (kind >= 0) {
+            float t = 0.f;
+            cudaEventElapsedTime(&t, p.ev[k], p.ev[k + 1]);
+            if (ms) ms[kind] += t;
+            if (launches) launches[kind] += 1;
+        }
+    }
+    for (auto e : p.ev) cudaEventDestroy(e);
+    return PERK_OK;
+}
+
+extern "C" int perk_profile_step(perk_ctx *c, double *U, double dt, float *ms, int32_t *launches)
+{
+    if (!c) return PERK_ENOTINIT;
+    if (!U) return set_err(c, PERK_EINVAL, "U_dev is null");
+    Prof p;
+    launch_step(c, c->stream, U, dt, &p);
+    CU(cudaGetLastError());
+    return finish_prof(c, p, ms, launches);
+}
+
+extern "C" int perk_profile_repartition(perk_ctx *c, const uint8_t *lmap, double *U, float *ms, int32_t *launches)
+{
+    if (!c) return PERK_ENOTINIT;
+    if (!lmap || !U) return set_err(c, PERK_EINVAL, "null pointer");
+    Prof p;
+    int rc = do_repartition(c, lmap, U, &p);
+    if (rc) return rc;
+    return finish_prof(c, p, ms, launches);
+}

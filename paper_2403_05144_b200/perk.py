@@ -1,0 +1,304 @@
+"""Thin ctypes binding of libperk_b200.so (include/perk.h) -- argument marshalling only.
+
+Every step of the P-ERK hot path (mesh/list rebuild, fluxes, volume integral, stage
+combination, re-mesh transfer) runs in the CUDA kernels behind the C ABI.  PyTorch is used for
+device memory and the current CUDA stream.  There is no CPU fallback: if the shared library is
+missing or CUDA is unavailable, constructing a `Perk` raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libperk_b200.so")
+
+EQ = {"advection": 0, "euler": 1, "navier_stokes": 2}
+VOL = {"weak": 0, "fluxdiff": 1}
+SURF = {"upwind": 0, "rusanov": 1, "hll": 2}
+KIND = {"elements": 0, "interfaces": 1, "mortars": 2, "boundaries": 3}
+ERRORS = {-1: "EINVAL", -2: "EUNBALANCED", -3: "ECAPACITY", -4: "ECUDA", -5: "ENOTINIT", -6: "EUNSUPPORTED"}
+NP = 4
+
+
+class PerkError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class perk_problem(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("equation", C.c_int32), ("volume", C.c_int32), ("surface", C.c_int32),
+                ("n_base", C.c_int32 * 2), ("max_level", C.c_int32), ("periodic", C.c_int32 * 2), ("_pad", C.c_int32),
+                ("domain_lo", C.c_double * 2), ("domain_hi", C.c_double * 2), ("gamma", C.c_double),
+                ("prandtl", C.c_double), ("mu", C.c_double), ("adv_velocity", C.c_double),
+                ("bc_state", C.c_double * 4), ("max_cells", C.c_int64)]
+
+
+class perk_tableau(C.Structure):
+    _fields_ = [("S", C.c_int32), ("R", C.c_int32), ("E", C.c_int32 * 8), ("c", C.c_double * 64),
+                ("a_sub", (C.c_double * 64) * 8)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not built: run __graft_entry__.build() (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        P = C.c_void_p
+        i32, i64, dbl = C.c_int32, C.c_int64, C.c_double
+        L.perk_alpha_taylor.argtypes = [i32, C.POINTER(dbl)]
+        L.perk_tableau_p2.argtypes = [i32, i32, C.POINTER(i32), C.POINTER(dbl), C.POINTER(perk_tableau)]
+        L.perk_init.argtypes = [C.POINTER(P), C.POINTER(perk_problem), P, C.POINTER(perk_tableau), P]
+        L.perk_destroy.argtypes = [P]
+        L.perk_set_stream.argtypes = [P, P]
+        L.perk_step.argtypes = [P, P, dbl]
+        L.perk_run_host.argtypes = [P, P, dbl, i64]
+        L.perk_repartition.argtypes = [P, P, P]
+        L.rhs_eval.argtypes = [P, P, C.c_uint32, P]
+        L.perk_num_cells.argtypes = [P, C.POINTER(i64)]
+        L.perk_num_faces.argtypes = [P, C.POINTER(i64)]
+        L.perk_node_coords.argtypes = [P, P]
+        L.perk_get_leaves.argtypes = [P, P, P, P, P, i64]
+        L.perk_get_faces.argtypes = [P, i32, P, P, i64, C.POINTER(i64)]
+        L.perk_get_list.argtypes = [P, i32, P, i64, P]
+        L.perk_get_count_active.argtypes = [P, i32, P]
+        L.perk_get_counters.argtypes = [P, C.POINTER(i64), C.POINTER(i64)]
+        L.perk_sync.argtypes = [P]
+        L.perk_last_error.argtypes = [P]
+        L.perk_last_error.restype = C.c_char_p
+        L.perk_profile_step.argtypes = [P, P, dbl, P, P]
+        L.perk_profile_repartition.argtypes = [P, P, P, P, P]
+        L.perk_launches_per_step.argtypes = [P, C.POINTER(i32)]
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return ["perk_alpha_taylor", "perk_tableau_p2", "perk_init", "perk_destroy", "perk_set_stream", "perk_step",
+            "perk_run_host", "perk_repartition", "rhs_eval", "perk_num_cells", "perk_num_faces", "perk_node_coords",
+            "perk_get_leaves", "perk_get_faces", "perk_get_list", "perk_get_count_active", "perk_get_counters",
+            "perk_sync", "perk_last_error", "perk_profile_step", "perk_profile_repartition", "perk_launches_per_step"]
+
+
+def tableau_p2(S: int, E, alpha_rows=None) -> perk_tableau:
+    """P-ERK2 family via the library (C recursion).  alpha_rows: R rows of S+1 coefficients; default
+    the Taylor rule alpha_k = 1/k! (BASELINE.json cfg 1), also built by the library."""
+    E = [int(e) for e in E]
+    R = len(E)
+    al = np.zeros((R, S + 1))
+    for r, e in enumerate(E):
+        ek = max(0, min(e, S))          # out-of-range E is rejected by the library below
+        if alpha_rows is None:
+            row = (C.c_double * (ek + 1))()
+            _check(None, lib().perk_alpha_taylor(ek, row))
+            al[r, : ek + 1] = np.frombuffer(row, dtype=np.float64)
+        else:
+            n = min(len(alpha_rows[r]), S + 1)
+            al[r, :n] = alpha_rows[r][:n]
+    al = np.ascontiguousarray(al)
+    t = perk_tableau()
+    Ea = (C.c_int32 * R)(*E)
+    _check(None, lib().perk_tableau_p2(S, R, Ea, al.ctypes.data_as(C.POINTER(C.c_double)), C.byref(t)))
+    return t
+
+
+def _check(h, rc):
+    if rc != 0:
+        msg = lib().perk_last_error(h).decode() if h else ""
+        raise PerkError(rc, msg)
+
+
+def _problem_struct(p: dict, max_cells: int) -> perk_problem:
+    s = perk_problem()
+    s.dim = p["dim"]
+    s.equation = EQ[p["equation"]]
+    s.volume = VOL[p["volume"]]
+    s.surface = SURF[p["surface"]]
+    s.n_base[0], s.n_base[1] = p["n_base"]
+    s.max_level = p["max_level"]
+    s.periodic[0], s.periodic[1] = [int(x) for x in p["periodic"]]
+    s.domain_lo[0], s.domain_lo[1] = p["domain_lo"]
+    s.domain_hi[0], s.domain_hi[1] = p["domain_hi"]
+    s.gamma, s.prandtl, s.mu, s.adv_velocity = p["gamma"], p["prandtl"], p["mu"], p["adv_velocity"]
+    for k, v in enumerate(p["bc_state"]):
+        s.bc_state[k] = v
+    s.max_cells = int(max_cells)
+    return s
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr())
+
+
+class Perk:
+    """One P-ERK multirate DGSEM context on the current CUDA device (all work on the current stream)."""
+
+    def __init__(self, problem: dict, level_map, S: int, E, alpha_rows=None, max_cells=None, stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("CUDA device required: libperk_b200 has no CPU path")
+        self.torch = torch
+        self.problem = problem
+        self.dim = problem["dim"]
+        self.nv = problem["nv"]
+        self.npe = NP ** self.dim
+        self.S = S
+        self.E = list(E)
+        self.R = len(self.E)
+        self.max_cells = int(max_cells or problem["max_cells"])
+        self._tab = tableau_p2(S, self.E, alpha_rows)
+        self._prob = _problem_struct(problem, self.max_cells)
+        lm = self._to_dev_u8(level_map)
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        h = C.c_void_p()
+        rc = lib().perk_init(C.byref(h), C.byref(self._prob), _ptr(lm), C.byref(self._tab),
+                             C.c_void_p(self.stream.cuda_stream))
+        self.h = h
+        if rc != 0:
+            msg = lib().perk_last_error(h).decode() if h else ""
+            if h:
+                lib().perk_destroy(h)
+                self.h = None
+            raise PerkError(rc, msg)
+
+    def _to_dev_u8(self, level_map):
+        torch = self.torch
+        if isinstance(level_map, torch.Tensor):
+            return level_map.to(device="cuda", dtype=torch.uint8).contiguous()
+        return torch.from_numpy(np.ascontiguousarray(np.asarray(level_map, dtype=np.uint8))).cuda()
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().perk_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- state ----
+    @property
+    def n_cells(self) -> int:
+        n = C.c_int64()
+        _check(self.h, lib().perk_num_cells(self.h, C.byref(n)))
+        return n.value
+
+    def face_counts(self) -> dict:
+        a = (C.c_int64 * 3)()
+        _check(self.h, lib().perk_num_faces(self.h, a))
+        return {"interfaces": a[0], "mortars": a[1], "boundaries": a[2]}
+
+    def alloc_state(self):
+        return self.torch.zeros((self.max_cells, self.nv, self.npe), dtype=self.torch.float64, device="cuda")
+
+    def node_coords(self):
+        torch = self.torch
+        xy = torch.zeros((self.max_cells, self.dim, self.npe), dtype=torch.float64, device="cuda")
+        _check(self.h, lib().perk_node_coords(self.h, _ptr(xy)))
+        n = self.n_cells
+        return xy[:n, 0] if self.dim == 1 else xy[:n]
+
+    def initial_state(self, ic):
+        """U (capacity rows) with the first n_cells rows = ic evaluated at this mesh's nodes."""
+        xy = self.node_coords().cpu().numpy()
+        U0 = ic(xy) if self.dim == 1 else ic(xy[:, 0, :], xy[:, 1, :])
+        U0 = np.ascontiguousarray(np.moveaxis(np.asarray(U0, np.float64), 0, 1))
+        U = self.alloc_state()
+        U[: U0.shape[0]] = self.torch.from_numpy(U0).cuda()
+        return U
+
+    # ---- the hot path ----
+    def step(self, U, dt: float, nsteps: int = 1):
+        assert U.is_cuda and U.dtype == self.torch.float64 and U.is_contiguous()
+        for _ in range(nsteps):
+            _check(self.h, lib().perk_step(self.h, _ptr(U), float(dt)))
+
+    def run_host(self, U_host, dt: float, nsteps: int = 1):
+        """End-to-end call with a host (ideally pinned) float64 tensor of n_cells rows."""
+        assert not U_host.is_cuda and U_host.dtype == self.torch.float64 and U_host.is_contiguous()
+        _check(self.h, lib().perk_run_host(self.h, C.c_void_p(U_host.data_ptr()), float(dt), int(nsteps)))
+
+    def repartition(self, level_map, U):
+        lm = self._to_dev_u8(level_map)
+        _check(self.h, lib().perk_repartition(self.h, _ptr(lm), _ptr(U)))
+        self._keep = lm   # keep the map alive until the stream has consumed it
+
+    def rhs(self, U, mask=None):
+        mask = (1 << self.R) - 1 if mask is None else int(mask)
+        dU = self.torch.zeros_like(U)
+        _check(self.h, lib().rhs_eval(self.h, _ptr(U), mask, _ptr(dU)))
+        return dU
+
+    def sync(self):
+        _check(self.h, lib().perk_sync(self.h))
+
+    # ---- introspection ----
+    def leaves(self) -> dict:
+        n = self.n_cells
+        fx = np.zeros(n, np.int32)
+        fy = np.zeros(n, np.int32)
+        lev = np.zeros(n, np.uint8)
+        mem = np.zeros(n, np.int32)
+        _check(self.h, lib().perk_get_leaves(self.h, fx.ctypes.data, fy.ctypes.data, lev.ctypes.data, mem.ctypes.data, n))
+        return dict(fx=fx, fy=fy, level=lev, member=mem)
+
+    def faces(self, kind: str):
+        k = KIND[kind]
+        width = {1: 3, 2: 5, 3: 2}[k]
+        n = self.face_counts()[kind]
+        rec = np.zeros(max(n, 1) * width, np.int32)
+        mem = np.zeros(max(n, 1), np.int32)
+        ln = C.c_int64()
+        _check(self.h, lib().perk_get_faces(self.h, k, rec.ctypes.data, mem.ctypes.data, max(n, 1), C.byref(ln)))
+        return rec[: n * width].reshape(n, width), mem[:n]
+
+    def list(self, kind: str):
+        k = KIND[kind]
+        n = self.n_cells if k == 0 else self.face_counts()[kind]
+        lst = np.zeros(max(n, 1), np.int32)
+        seg = np.zeros(self.R + 1, np.int64)
+        _check(self.h, lib().perk_get_list(self.h, k, lst.ctypes.data, max(n, 1), seg.ctypes.data))
+        return lst[:n], seg
+
+    def count_active(self, kind: str):
+        out = np.zeros(self.S, np.int32)
+        _check(self.h, lib().perk_get_count_active(self.h, KIND[kind], out.ctypes.data))
+        return out
+
+    def counters(self):
+        ev, st = C.c_int64(), C.c_int64()
+        _check(self.h, lib().perk_get_counters(self.h, C.byref(ev), C.byref(st)))
+        return ev.value, st.value
+
+    def launches_per_step(self) -> int:
+        n = C.c_int32()
+        _check(self.h, lib().perk_launches_per_step(self.h, C.byref(n)))
+        return n.value
+
+    def profile_step(self, U, dt):
+        ms = (C.c_float * 4)()
+        nl = (C.c_int32 * 4)()
+        _check(self.h, lib().perk_profile_step(self.h, _ptr(U), float(dt), ms, nl))
+        return list(ms), list(nl)
+
+    def profile_repartition(self, level_map, U):
+        lm = self._to_dev_u8(level_map)
+        ms = (C.c_float * 4)()
+        nl = (C.c_int32 * 4)()
+        _check(self.h, lib().perk_profile_repartition(self.h, _ptr(lm), _ptr(U), ms, nl))
+        return list(ms), list(nl)
+
+    @property
+    def tableau(self) -> dict:
+        t = self._tab
+        return dict(S=t.S, R=t.R, E=list(t.E[: t.R]), c=list(t.c[: t.S]),
+                    a_sub=[list(t.a_sub[r][: t.S]) for r in range(t.R)])

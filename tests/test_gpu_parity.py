@@ -1,0 +1,231 @@
+"""GPU parity: the CUDA path (libperk_b200.so through its C ABI) against the oracle on identical
+seeded inputs.  Index lists bit-exact; states <= 1e-10 max relative error per conserved variable
+(BASELINE.json north_star).  Sizes: every BASELINE config's full mesh (lists, one RHS, a few steps
+at full size), full step counts where the oracle finishes in seconds, plus small ragged meshes,
+boundaries, re-meshing and degenerate cases."""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import oracle as O
+from oracle import tableau as T
+from gpu_util import TOL, build_pair, compare_mesh, gpu_state_numpy, rel_err_per_var
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+
+def _run_both(w, steps, ora, gpu, mode=1):
+    Uo = ora.initial_state(w.ic)
+    Ug = gpu.initial_state(w.ic)
+    assert np.abs(gpu_state_numpy(gpu, Ug) - Uo).max() < 1e-13 * max(1.0, np.abs(Uo).max())
+    ora.step(Uo, w.dt, steps, mode=mode)
+    gpu.step(Ug, w.dt, steps)
+    torch.cuda.synchronize()
+    gpu.sync()
+    return Uo, gpu_state_numpy(gpu, Ug)
+
+
+# ----------------------------------------------------------------------------------------------
+# lists (a1-a3): bit-exact
+# ----------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_lists_full_size(cfg):
+    w = W.make(cfg)
+    ora, gpu = build_pair(w)
+    assert ora.n == gpu.n_cells
+    compare_mesh(ora, gpu)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_lists_random_small_2d(seed):
+    rng = np.random.default_rng(100 + seed)
+    nb, L = int(rng.choice([3, 4, 5, 8])), int(rng.integers(1, 4))
+    T_ = (rng.integers(0, L + 1, size=(nb << L, nb << L)) * (rng.random((nb << L, nb << L)) < 0.1)).astype(np.int32)
+    lm = W.balance(T_, L, (True, True))
+    w = W.make(3, n_base=nb)
+    p = W.configs._problem(2, "euler", "fluxdiff", "hll", nb, L, 0.0, 10.0)
+    R = min(L + 1, 3)
+    w.S, w.E = 16, [4, 8, 16][3 - R:]
+    ora, gpu = build_pair(w, problem=p, level_map=lm)
+    compare_mesh(ora, gpu)
+
+
+def test_lists_nonperiodic_boundaries():
+    w = W.make(3, n_base=8)
+    p = dict(w.problem, periodic=(0, 1), bc_state=(1.0, 0.1, 0.0, 2.5))
+    ora, gpu = build_pair(w, problem=p)
+    assert ora.face_counts()["boundaries"] > 0
+    compare_mesh(ora, gpu)
+
+
+def test_unbalanced_rejected():
+    from paper_2403_05144_b200 import PerkError
+    lm = np.zeros((8, 8), np.uint8)
+    lm[0:2, 0:2] = 2
+    lm = W.leafify(lm, 2).astype(np.uint8)
+    p = W.configs._problem(2, "euler", "fluxdiff", "hll", 2, 2, 0.0, 1.0)
+    from paper_2403_05144_b200 import Perk
+    with pytest.raises(PerkError) as ei:
+        Perk(p, lm, 16, [4, 8, 16])
+    assert ei.value.code == -2
+
+
+def test_capacity_rejected():
+    from paper_2403_05144_b200 import Perk, PerkError
+    w = W.make(3, n_base=8)
+    with pytest.raises(PerkError) as ei:
+        Perk(w.problem, w.level_map, w.S, w.E, max_cells=10)
+    assert ei.value.code == -3
+
+
+# ----------------------------------------------------------------------------------------------
+# one RHS per partition mask (a5-a10 without the stage combination)
+# ----------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+def test_rhs_eval_masks_full_size(cfg):
+    w = W.make(cfg)
+    ora, gpu = build_pair(w)
+    Uo = ora.initial_state(w.ic)
+    Ug = gpu.initial_state(w.ic)
+    R = len(w.E)
+    for mask in sorted({(1 << R) - 1, 1, 1 << (R - 1), (1 << R) - 2}):
+        dUo = ora.rhs(Uo, mask, mode=1)
+        dUg = gpu_state_numpy(gpu, gpu.rhs(Ug, mask))
+        for v in range(dUo.shape[1]):
+            den = max(np.abs(ora.rhs(Uo, (1 << R) - 1, 1)[:, v]).max(), 1e-300)
+            assert np.abs(dUg[:, v] - dUo[:, v]).max() / den < 1e-12, (mask, v)
+        # unmasked partitions are exactly zero
+        mem = ora.leaves()["member"]
+        off = ~np.isin(mem, [r for r in range(R) if (mask >> r) & 1])
+        assert np.all(dUg[off] == 0.0)
+
+
+# ----------------------------------------------------------------------------------------------
+# full runs: the P-ERK step (a5-a13)
+# ----------------------------------------------------------------------------------------------
+def test_cfg1_full_run():
+    w = W.make(1)
+    ora, gpu = build_pair(w)
+    Uo, Ug = _run_both(w, w.steps, ora, gpu)
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
+    ev, st = gpu.counters()
+    assert st == w.steps and ev == 320 * w.steps
+
+
+def test_cfg2_full_run():
+    w = W.make(2)
+    ora, gpu = build_pair(w)
+    Uo, Ug = _run_both(w, w.steps, ora, gpu)
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
+    ev, st = gpu.counters()
+    assert ev == 2560 * w.steps
+
+
+def test_cfg3_small_full_steps():
+    """cfg-3 structure on a 16^2 base (several tiles + ragged tails), the full 500 steps."""
+    w = W.make(3, n_base=16)
+    ora, gpu = build_pair(w)
+    assert ora.face_counts()["mortars"] > 0
+    Uo, Ug = _run_both(w, w.steps, ora, gpu)
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
+
+
+def test_cfg3_full_size_steps():
+    """BASELINE cfg 3 mesh (62,932 cells) in the bench launch configuration, 2 steps."""
+    w = W.make(3)
+    ora, gpu = build_pair(w)
+    Uo, Ug = _run_both(w, 2, ora, gpu)
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
+    ev, st = gpu.counters()
+    assert ev == 2 * 713596
+
+
+def test_cfg4_initial_mesh_steps():
+    w = W.make(4, n_base=16, max_level=3, widths=(0.3, 0.15, 0.06))
+    w.S, w.E = 16, [4, 6, 10, 16]
+    ora, gpu = build_pair(w)
+    Uo, Ug = _run_both(w, 20, ora, gpu)
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
+
+
+def test_boundary_variant_2d():
+    """weakly imposed Dirichlet faces (a8) on a non-periodic x direction."""
+    w = W.make(3, n_base=8)
+    p = dict(w.problem, periodic=(0, 1), bc_state=(1.0, 1.0, 1.0, 1.0 / 0.4 + 1.0))
+    ora, gpu = build_pair(w, problem=p)
+    Uo, Ug = _run_both(w, 30, ora, gpu)
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
+
+
+def test_boundary_variant_1d():
+    w = W.make(2, n_base=64, w1=16, w2=4, steps=200)
+    p = dict(w.problem, periodic=(0, 1), bc_state=(1.0, 1.0, 1.0 / 0.4 + 0.5))
+    ora, gpu = build_pair(w, problem=p)
+    assert ora.face_counts()["boundaries"] == 2
+    Uo, Ug = _run_both(w, w.steps, ora, gpu)
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
+
+
+def test_single_level_reduction():
+    """uniform mesh at the finest level: GPU multirate == oracle single-rate S-stage P-ERK."""
+    w = W.make(3, n_base=8, steps=10)
+    lm = np.full_like(w.level_map, w.problem["max_level"])
+    from paper_2403_05144_b200 import Perk
+    ora = O.OracleMesh(w.problem, lm, T.family(16, [16], "taylor"))
+    gpu = Perk(w.problem, lm, 16, [4, 8, 16])
+    Uo, Ug = _run_both(w, w.steps, ora, gpu)
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
+
+
+def test_cfg1_coarse_only_mesh():
+    """degenerate: no cell at the finest level (all cells in the lowest member)."""
+    w = W.make(1)
+    lm = np.zeros_like(w.level_map)
+    ora, gpu = build_pair(w, level_map=lm)
+    compare_mesh(ora, gpu)
+    Uo, Ug = _run_both(w, 50, ora, gpu)
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
+
+
+def test_e2e_host_buffers_match_device_path():
+    w = W.make(3, n_base=16)
+    from paper_2403_05144_b200 import Perk
+    gpu = Perk(w.problem, w.level_map, w.S, w.E)
+    U = gpu.initial_state(w.ic)
+    n = gpu.n_cells
+    Uh = U[:n].cpu().pin_memory()
+    gpu.step(U, w.dt, 3)
+    gpu.run_host(Uh, w.dt, 3)
+    torch.cuda.synchronize()
+    assert torch.equal(Uh, U[:n].cpu())
+
+
+# ----------------------------------------------------------------------------------------------
+# dynamic re-mesh (a1-a4 on the device)
+# ----------------------------------------------------------------------------------------------
+def test_repartition_lists_and_transfer():
+    w = W.make(4, n_base=16, max_level=3, widths=(0.3, 0.15, 0.06))
+    w.S, w.E = 16, [4, 6, 10, 16]
+    fam = T.family(w.S, w.E, "taylor")
+    ora, gpu = build_pair(w, max_cells=4 * W.configs.count_leaves(w))
+    Uo = ora.initial_state(w.ic)
+    Ug = gpu.initial_state(w.ic)
+    for k in range(1, 5):
+        ora.step(Uo, w.dt, 5)
+        gpu.step(Ug, w.dt, 5)
+        lm = w.level_map_seq(k)
+        ora_new = O.OracleMesh(w.problem, lm, fam)
+        Uo = O.transfer(ora, ora_new, Uo)
+        ora = ora_new
+        gpu.repartition(lm, Ug)
+        gpu.sync()
+        compare_mesh(ora, gpu)
+        assert rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo).max() <= TOL
+    ora.step(Uo, w.dt, 5)
+    gpu.step(Ug, w.dt, 5)
+    torch.cuda.synchronize()
+    assert rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo).max() <= TOL
