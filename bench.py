@@ -285,6 +285,20 @@ def cpu_baseline(w, budget_s=20.0):
             "seconds": round(total_t, 2)}
 
 
+def run_profile_only(args):
+    import torch
+    from paper_2403_05144_b200 import Perk
+    w = W.make(args.config)
+    perk = Perk(w.problem, w.level_map, w.S, w.E)
+    U = perk.initial_state(w.ic)
+    for _ in range(args.warmup + args.steps):
+        perk.step(U, w.dt)
+    torch.cuda.synchronize()
+    perk.sync()
+    print(json.dumps({"profile_only": w.name, "steps": args.warmup + args.steps,
+                      "launches_per_step": perk.launches_per_step()}))
+
+
 def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
@@ -324,11 +338,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-only", action="store_true",
+                    help="build the workload and run warmup+steps P-ERK steps only (short ncu target)")
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per step of the dominant kernel from an ncu --set full capture")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
-    if args.impl == "reference":
+    if args.profile_only:
+        run_profile_only(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

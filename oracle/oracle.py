@@ -67,6 +67,7 @@ def lib():
         L.ora_get_list.argtypes = [P, C.c_int, ip, lp]
         L.ora_count_active.argtypes = [P, C.c_int, ip]
         L.ora_node_coords.argtypes = [P, dp]
+        L.ora_rhs.restype = C.c_int
         L.ora_rhs.argtypes = [P, dp, C.c_uint32, dp, C.c_int]
         L.ora_step.restype = C.c_int64
         L.ora_step.argtypes = [P, dp, C.c_double, C.c_int]
@@ -216,10 +217,13 @@ class OracleMesh:
         return np.ascontiguousarray(np.moveaxis(np.asarray(U, np.float64), 0, 1))  # (n, nv, npe)
 
     def rhs(self, U, mask=None, mode=0):
+        """dU = sum_{r in mask} I^(r) F(U).  mode 0 (default) is the definition (full F, then mask);
+        mode 1 loops over the member lists and requires an upward-closed mask."""
         mask = (1 << self.fam["R"]) - 1 if mask is None else mask
         U = np.ascontiguousarray(U, np.float64)
         dU = np.zeros_like(U)
-        lib().ora_rhs(self.h, U.ravel(), mask, dU.ravel(), mode)
+        if lib().ora_rhs(self.h, U.ravel(), mask, dU.ravel(), mode) != 0:
+            raise ValueError("restricted mode needs an upward-closed partition mask")
         return dU
 
     def step(self, U, dt, nsteps=1, mode=1):

@@ -720,10 +720,18 @@ static void element_rhs(Ora *o, const double *U, int e, double *dU)
    mode 0 "reference": evaluate every face and element, then zero the unmasked elements.
    mode 1 "restricted": loop over the members in mask only, through the per-member lists;
    a mortar is evaluated whenever its (fine-side) member is in the mask (P:l.1256). */
-void ora_rhs(void *p, const double *U, uint32_t mask, double *dU, int mode)
+int ora_rhs(void *p, const double *U, uint32_t mask, double *dU, int mode)
 {
     Ora *o = (Ora *)p;
     int R = o->tab.R;
+    if (mode == 1) {
+        /* the restricted loops are only equivalent to I^(r)F for upward-closed masks (every member
+           finer than a masked one is masked too), which is what every P-ERK stage uses (P:l.428):
+           a coarse element's mortar faces belong to the finer member (P:l.1256). */
+        for (int r = 0; r + 1 < R; ++r)
+            if (((mask >> r) & 1u) && !((mask >> (r + 1)) & 1u)) return -1;
+        memset(o->Fs, 0, sizeof(double) * (size_t)o->n * 4 * o->nv * NP);
+    }
     if (mode == 0) {
         for (int f = 0; f < o->n_if; ++f) interface_flux(o, U, f);
         for (int m = 0; m < o->n_mo; ++m) mortar_flux(o, U, m);
@@ -733,7 +741,7 @@ void ora_rhs(void *p, const double *U, uint32_t mask, double *dU, int mode)
             if (!((mask >> o->member[e]) & 1u))
                 for (int v = 0; v < o->nv; ++v)
                     for (int q = 0; q < o->npe; ++q) dU[UIDX(o, e, v, q)] = 0.0;
-        return;
+        return 0;
     }
     memset(dU, 0, sizeof(double) * (size_t)o->n * o->nv * o->npe);
     for (int s = 0; s < R; ++s) {
@@ -748,6 +756,7 @@ void ora_rhs(void *p, const double *U, uint32_t mask, double *dU, int mode)
         if (!((mask >> r) & 1u)) continue;
         for (int64_t t = o->seg[0][s]; t < o->seg[0][s + 1]; ++t) element_rhs(o, U, o->list[0][t], dU);
     }
+    return 0;
 }
 
 /* ------------------------------------------------------------------------- */
@@ -798,7 +807,7 @@ static int64_t perk_step_generic(const OraTableau *t, int nunits, int usize, con
 }
 
 static int g_rhs_mode;
-static void dg_rhs_cb(void *ctx, const double *U, uint32_t mask, double *dU) { ora_rhs(ctx, U, mask, dU, g_rhs_mode); }
+static void dg_rhs_cb(void *ctx, const double *U, uint32_t mask, double *dU) { (void)ora_rhs(ctx, U, mask, dU, g_rhs_mode); }
 
 /* one P-ERK step of the DG system; returns element-RHS evaluations of this step */
 int64_t ora_step(void *p, double *U, double dt, int mode)

@@ -35,7 +35,9 @@ def _run_both(w, steps, ora, gpu, mode=1):
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
 def test_lists_full_size(cfg):
     w = W.make(cfg)
-    ora, gpu = build_pair(w)
+    # the lists do not depend on the equation; cfg 5's BR1 operator is not built this round
+    p = dict(w.problem, equation="euler") if cfg == 5 else w.problem
+    ora, gpu = build_pair(w, problem=p)
     assert ora.n == gpu.n_cells
     compare_mesh(ora, gpu)
 
@@ -93,10 +95,10 @@ def test_rhs_eval_masks_full_size(cfg):
     Ug = gpu.initial_state(w.ic)
     R = len(w.E)
     for mask in sorted({(1 << R) - 1, 1, 1 << (R - 1), (1 << R) - 2}):
-        dUo = ora.rhs(Uo, mask, mode=1)
+        dUo = ora.rhs(Uo, mask, mode=0)       # the definition: full F, then the mask I^(r)
         dUg = gpu_state_numpy(gpu, gpu.rhs(Ug, mask))
         for v in range(dUo.shape[1]):
-            den = max(np.abs(ora.rhs(Uo, (1 << R) - 1, 1)[:, v]).max(), 1e-300)
+            den = max(np.abs(ora.rhs(Uo, (1 << R) - 1, 0)[:, v]).max(), 1e-300)
             assert np.abs(dUg[:, v] - dUo[:, v]).max() / den < 1e-12, (mask, v)
         # unmasked partitions are exactly zero
         mem = ora.leaves()["member"]

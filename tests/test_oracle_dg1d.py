@@ -110,8 +110,10 @@ def test_reference_equals_restricted(cfg1):
     m.step(a, w.dt, 3, mode=0)
     m.step(b, w.dt, 3, mode=1)
     assert np.array_equal(a, b)
-    for mask in (1, 2, 3):
+    for mask in (2, 3):      # upward-closed masks (the ones P-ERK stages use)
         assert np.array_equal(m.rhs(U0, mask, 0), m.rhs(U0, mask, 1))
+    with pytest.raises(ValueError):
+        m.rhs(U0, 1, 1)
 
 
 def test_single_level_reduction_dg():

@@ -270,7 +270,7 @@ def test_reference_equals_restricted_2d(nc_mesh):
     m = nc_mesh
     xy = m.node_coords()
     U = m.initial_state(W.configs._isentropic_vortices([(1.0, 1.0)], per=2.0, eps=1.0))
-    for mask in (1, 2, 4, 5, 7):
+    for mask in (4, 6, 7):   # upward-closed masks
         assert np.array_equal(m.rhs(U, mask, 0), m.rhs(U, mask, 1))
     a, b = U.copy(), U.copy()
     m.step(a, 1e-3, 2, mode=0)
