@@ -123,4 +123,15 @@ __device__ __forceinline__ double rcp64(double x)
     return fma(y, e, y);
 }
 
+// fast fp64 square root: MUFU reciprocal-sqrt approximation + Newton steps (<= 1 ulp off IEEE)
+__device__ __forceinline__ double sqrt64(double x)
+{
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    r = r * fma(-0.5 * x * r, r, 1.5);
+    r = r * fma(-0.5 * x * r, r, 1.5);
+    double s = x * r;
+    return fma(0.5 * r, fma(-s, s, x), s);
+}
+
 }  // namespace perk

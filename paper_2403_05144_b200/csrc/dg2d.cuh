@@ -69,21 +69,23 @@ __device__ __forceinline__ void numflux2d(const double uL[4], const double uR[4]
                                           double f[4])
 {
     const double gm1 = g - 1.0;
-    const double v1L = uL[1] / uL[0], v2L = uL[2] / uL[0];
-    const double v1R = uR[1] / uR[0], v2R = uR[2] / uR[0];
+    const double irL = rcp64(uL[0]), irR = rcp64(uR[0]);
+    const double v1L = uL[1] * irL, v2L = uL[2] * irL;
+    const double v1R = uR[1] * irR, v2R = uR[2] * irR;
     const double pL = gm1 * (uL[3] - 0.5 * (uL[1] * v1L + uL[2] * v2L));
     const double pR = gm1 * (uR[3] - 0.5 * (uR[1] * v1R + uR[2] * v2R));
-    const double cL = sqrt(g * pL / uL[0]), cR = sqrt(g * pR / uR[0]);
+    const double cL = sqrt64(g * pL * irL), cR = sqrt64(g * pR * irR);
     const double vnL = o == 0 ? v1L : v2L, vnR = o == 0 ? v1R : v2R;
     double fL[4], fR[4];
     euler_flux2d(uL, pL, vnL, o, fL);
     euler_flux2d(uR, pR, vnR, o, fR);
-    if (surface == 1) {
+    if (surface == 1) {   // Rusanov
         const double lam = fmax(fabs(vnL) + cL, fabs(vnR) + cR);
 #pragma unroll
         for (int v = 0; v < 4; ++v) f[v] = 0.5 * (fL[v] + fR[v]) - 0.5 * lam * (uR[v] - uL[v]);
         return;
     }
+    // HLL with Davis wave-speed estimates
     const double sL = fmin(vnL - cL, vnR - cR), sR = fmax(vnL + cL, vnR + cR);
     if (sL >= 0.0) {
 #pragma unroll
@@ -92,7 +94,7 @@ __device__ __forceinline__ void numflux2d(const double uL[4], const double uR[4]
 #pragma unroll
         for (int v = 0; v < 4; ++v) f[v] = fR[v];
     } else {
-        const double inv = 1.0 / (sR - sL);
+        const double inv = rcp64(sR - sL);
 #pragma unroll
         for (int v = 0; v < 4; ++v) f[v] = (sR * fL[v] - sL * fR[v] + sL * sR * (uR[v] - uL[v])) * inv;
     }
@@ -101,11 +103,26 @@ __device__ __forceinline__ void numflux2d(const double uL[4], const double uR[4]
 // ---------------------------------------------------------------------------------------------
 // surface kernel
 // ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ const double *state_base(const StateBufs &sb, int src)
+{
+    return src == SRC_BUF ? sb.Ubuf : (src == SRC_IN ? sb.Uin : sb.Un);
+}
+
+// the 4 conserved variables of face node k of element e in the stage state given by src; all loads
+// are issued before any use (the K_1 loads only when the state is formed lazily)
 __device__ __forceinline__ void trace2d(const StateBufs &sb, int src, double dtc, int e, int face, int k, double u[4])
 {
     const size_t b = (size_t)e * 64 + face_node2d(face, k);
+    const double *P = state_base(sb, src);
 #pragma unroll
-    for (int v = 0; v < 4; ++v) u[v] = load_state(sb, src, dtc, b + v * 16);
+    for (int v = 0; v < 4; ++v) u[v] = __ldg(P + b + v * 16);
+    if (src == SRC_LAZY) {
+        double kk[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) kk[v] = __ldg(sb.K1 + b + v * 16);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) u[v] = fma(dtc, kk[v], u[v]);
+    }
 }
 
 __device__ __forceinline__ void store_face2d(double *Fs, int e, int face, int k, const double f[4])
@@ -116,7 +133,7 @@ __device__ __forceinline__ void store_face2d(double *Fs, int e, int face, int k,
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(256) k_surf2d(MeshDev md, StageParams sp, const double *__restrict__ Un,
+__global__ void __launch_bounds__(256, 3) k_surf2d(MeshDev md, StageParams sp, const double *__restrict__ Un,
                                                const double *__restrict__ Ubuf, const double *__restrict__ K1,
                                                const double *__restrict__ Uin, double *__restrict__ Fs)
 {
@@ -168,18 +185,21 @@ __global__ void __launch_bounds__(256) k_surf2d(MeshDev md, StageParams sp, cons
                     uih[v] = fma(pup, uj, uih[v]);
                 }
             }
-            double us0[4], us1[4], flo[4], fhi[4];
-            trace2d(sb, srcS, dtc, M.y, sf, k, us0);
-            trace2d(sb, srcS, dtc, M.z, sf, k, us1);
-            if (side == 0) {
-                numflux2d(uil, us0, o, g, md.surface, flo);
-                numflux2d(uih, us1, o, g, md.surface, fhi);
-            } else {
-                numflux2d(us0, uil, o, g, md.surface, flo);
-                numflux2d(us1, uih, o, g, md.surface, fhi);
+            double flo[4], fhi[4];
+            {
+                double us[4];
+                trace2d(sb, srcS, dtc, M.y, sf, k, us);
+                if (side == 0) numflux2d(uil, us, o, g, md.surface, flo);
+                else numflux2d(us, uil, o, g, md.surface, flo);
+                store_face2d(Fs, M.y, sf, k, flo);
             }
-            store_face2d(Fs, M.y, sf, k, flo);
-            store_face2d(Fs, M.z, sf, k, fhi);
+            {
+                double us[4];
+                trace2d(sb, srcS, dtc, M.z, sf, k, us);
+                if (side == 0) numflux2d(uih, us, o, g, md.surface, fhi);
+                else numflux2d(us, uih, o, g, md.surface, fhi);
+                store_face2d(Fs, M.z, sf, k, fhi);
+            }
             double fl[4] = {0, 0, 0, 0};
 #pragma unroll
             for (int j = 0; j < NP; ++j) {
@@ -210,7 +230,13 @@ __global__ void __launch_bounds__(256) k_surf2d(MeshDev md, StageParams sp, cons
 // ---------------------------------------------------------------------------------------------
 // volume + surface lift + Jacobian + stage epilogue
 // ---------------------------------------------------------------------------------------------
-constexpr int VOL2D_EPB = 16;   // elements per 128-thread block
+constexpr int VOL2D_EPB = 16;   // elements per 128-thread block (8 threads per element)
+// Shared-memory layout (bank-conflict free for the line loops): every field is
+// stored twice, once in x-line order (index le*17 + 4j + i) and once in y-line order
+// (index le*17 + 4i + j), the y copy offset by 2 doubles so that the 16 x-threads and 16 y-threads
+// of a warp hit 32 distinct banks.  The accumulators alias the first 8 field arrays.
+constexpr int VOL2D_LS = 288;   // doubles per field array: >= 16*17 + 2, and == 0 mod 16 so the +2 y offset shifts banks
+constexpr int VOL2D_NF = 7;                    // rho, v1, v2, p, ln rho, beta, ln beta
 
 __device__ __forceinline__ double2 load_state2(const StateBufs &sb, int src, double dtc, size_t idx)
 {
@@ -227,13 +253,12 @@ __device__ __forceinline__ double2 load_state2(const StateBufs &sb, int src, dou
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(128) k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
-                                              double *__restrict__ Ubuf, double *__restrict__ K1,
-                                              const double *__restrict__ Fs, const double *__restrict__ Uin,
-                                              double *__restrict__ dU)
+__global__ void __launch_bounds__(128, 5) k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
+                                                 double *__restrict__ Ubuf, double *__restrict__ K1,
+                                                 const double *__restrict__ Fs, const double *__restrict__ Uin,
+                                                 double *__restrict__ dU)
 {
-    __shared__ double sprim[VOL2D_EPB][16][8];
-    __shared__ double sacc[VOL2D_EPB][4][16];
+    __shared__ double sm[VOL2D_NF][2][VOL2D_LS];
     const int t8 = threadIdx.x & 7, le = threadIdx.x >> 3;
     const int n_act = MODE == MODE_STAGE ? md.count_active[KIND_EL * MAXS + sp.stage - 1] : md.n[0];
     const double g = md.gamma, gm1 = g - 1.0, inv_gm1 = 1.0 / gm1;
@@ -241,6 +266,8 @@ __global__ void __launch_bounds__(128) k_vol2d(MeshDev md, StageParams sp, doubl
     const double dtc = sp.dt * sp.c_stage;
     const int q0 = 2 * t8;
     const int o = t8 >> 2, ln = t8 & 3;
+    const int eo = le * 17;                 // element offset inside a field array
+    const int yo = 2;                       // y-layout offset
 
     if (MODE == MODE_STAGE && sp.stage == sp.S && blockIdx.x == 0 && threadIdx.x == 0) {
         unsigned long long tot = 0;
@@ -258,27 +285,32 @@ __global__ void __launch_bounds__(128) k_vol2d(MeshDev md, StageParams sp, doubl
         const int src = state_src(sp, m);
         const size_t eb = (size_t)e * 64;
 
-        // phase 1: nodes q0, q0+1 -> primitives + logs in shared memory
+        // phase 1: nodes q0, q0+1 -> primitives + logs, stored in x-line and y-line layouts
         {
             double2 u[4];
 #pragma unroll
             for (int v = 0; v < 4; ++v) u[v] = load_state2(sb, src, dtc, eb + v * 16 + q0);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
+                const int q = q0 + h, i = q & 3, j = q >> 2;
                 const double r = h ? u[0].y : u[0].x;
                 const double m1 = h ? u[1].y : u[1].x, m2 = h ? u[2].y : u[2].x, E = h ? u[3].y : u[3].x;
                 const double ir = rcp64(r);
                 const double v1 = m1 * ir, v2 = m2 * ir;
                 const double p = gm1 * (E - 0.5 * fma(m1, v1, m2 * v2));
                 const double beta = r * rcp64(p);
-                double *P = sprim[le][q0 + h];
-                P[0] = r; P[1] = v1; P[2] = v2; P[3] = p;
-                P[4] = log(r); P[5] = beta; P[6] = log(beta);
+                const double f[VOL2D_NF] = {r, v1, v2, p, log(r), beta, log(beta)};
+#pragma unroll
+                for (int k = 0; k < VOL2D_NF; ++k) {
+                    sm[k][0][eo + 4 * j + i] = f[k];
+                    sm[k][1][yo + eo + 4 * i + j] = f[k];
+                }
             }
         }
         __syncwarp();
 
-        // phase 2: 6 symmetric two-point fluxes along this thread's line
+        // phase 2: 6 symmetric two-point fluxes along this thread's line (x-line j = ln, or y-line i = ln)
+        const int lo = o == 0 ? eo + 4 * ln : yo + eo + 4 * ln;   // line start in layout o
         double acc[4][4];
 #pragma unroll
         for (int a = 0; a < 4; ++a)
@@ -286,14 +318,12 @@ __global__ void __launch_bounds__(128) k_vol2d(MeshDev md, StageParams sp, doubl
             for (int v = 0; v < 4; ++v) acc[a][v] = 0.0;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            const int qa = o == 0 ? ln * 4 + a : a * 4 + ln;
-            const double *PA = sprim[le][qa];
-            const Prim A{PA[0], PA[1], PA[2], PA[3], PA[4], PA[5], PA[6]};
+            const Prim A{sm[0][o][lo + a], sm[1][o][lo + a], sm[2][o][lo + a], sm[3][o][lo + a],
+                         sm[4][o][lo + a], sm[5][o][lo + a], sm[6][o][lo + a]};
 #pragma unroll
             for (int b = a + 1; b < 4; ++b) {
-                const int qb = o == 0 ? ln * 4 + b : b * 4 + ln;
-                const double *PB = sprim[le][qb];
-                const Prim Bp{PB[0], PB[1], PB[2], PB[3], PB[4], PB[5], PB[6]};
+                const Prim Bp{sm[0][o][lo + b], sm[1][o][lo + b], sm[2][o][lo + b], sm[3][o][lo + b],
+                              sm[4][o][lo + b], sm[5][o][lo + b], sm[6][o][lo + b]};
                 double f[4];
                 flux_ranocha(A, Bp, o, inv_gm1, f);
                 const double dab = cB.Dsplit[a][b], dba = cB.Dsplit[b][a];
@@ -314,30 +344,23 @@ __global__ void __launch_bounds__(128) k_vol2d(MeshDev md, StageParams sp, doubl
                 acc[0][v] = fma(-__ldg(Flo + v * 4), cB.invw[0], acc[0][v]);
             }
         }
-        // combine the x-line and y-line contributions of every node
-        if (o == 0) {
+        __syncwarp();   // all primitives consumed: reuse sm[v][o] as the accumulator arrays
 #pragma unroll
-            for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < 4; ++a)
 #pragma unroll
-                for (int v = 0; v < 4; ++v) sacc[le][v][ln * 4 + a] = acc[a][v];
-        }
-        __syncwarp();
-        if (o == 1) {
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-                for (int v = 0; v < 4; ++v) sacc[le][v][a * 4 + ln] += acc[a][v];
-        }
+            for (int v = 0; v < 4; ++v) sm[v][o][lo + a] = acc[a][v];
         __syncwarp();
 
-        // phase 3: K = -(2/h) acc, stage epilogue for nodes q0, q0+1
+        // phase 3: K = -(2/h) (x + y contributions), stage epilogue for nodes q0, q0+1
         if (valid) {
             const double J = -2.0 / (md.hf * (double)(1 << (md.max_level - md.lev[e])));
+            const int i0 = q0 & 3, j0 = q0 >> 2;   // q0 + 1 has i0 + 1
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
                 const size_t idx = eb + v * 16 + q0;
-                const double2 s = *reinterpret_cast<const double2 *>(&sacc[le][v][q0]);
-                const double2 K = make_double2(J * s.x, J * s.y);
+                const double s0 = sm[v][0][eo + q0] + sm[v][1][yo + eo + 4 * i0 + j0];
+                const double s1 = sm[v][0][eo + q0 + 1] + sm[v][1][yo + eo + 4 * (i0 + 1) + j0];
+                const double2 K = make_double2(J * s0, J * s1);
                 if (MODE == MODE_RHS) {
                     const bool on = (sp.mask >> m) & 1u;
                     *reinterpret_cast<double2 *>(dU + idx) = on ? K : make_double2(0.0, 0.0);

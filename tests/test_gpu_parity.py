@@ -97,9 +97,12 @@ def test_rhs_eval_masks_full_size(cfg):
     for mask in sorted({(1 << R) - 1, 1, 1 << (R - 1), (1 << R) - 2}):
         dUo = ora.rhs(Uo, mask, mode=0)       # the definition: full F, then the mask I^(r)
         dUg = gpu_state_numpy(gpu, gpu.rhs(Ug, mask))
+        # a single RHS is a difference of O((2/h) |f|) terms: rounding-order differences scale with
+        # (2/h_min) max|U|, not with |dU| (the 1e-10 state criterion applies to the full runs below)
+        scale = 2.0 / w.problem["h_min"] * np.abs(Uo).max()   # magnitude of the summed flux terms
         for v in range(dUo.shape[1]):
-            den = max(np.abs(ora.rhs(Uo, (1 << R) - 1, 0)[:, v]).max(), 1e-300)
-            assert np.abs(dUg[:, v] - dUo[:, v]).max() / den < 1e-12, (mask, v)
+            tol = 1e-12 * np.abs(dUo[:, v]).max() + 4e-14 * scale
+            assert np.abs(dUg[:, v] - dUo[:, v]).max() <= tol, (mask, v)
         # unmasked partitions are exactly zero
         mem = ora.leaves()["member"]
         off = ~np.isin(mem, [r for r in range(R) if (mask >> r) & 1])
