@@ -46,7 +46,8 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled every 20 ms during the clock soak (untimed steps
+    of the same workload, >= 0.5 s, so the sample count does not depend on K) and the timed region."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -60,7 +61,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
@@ -175,6 +176,11 @@ def run_ours(args):
         return [a.elapsed_time(b) for a, b in evs]
 
     with ClockSampler(local) as clk:
+        t_soak = time.perf_counter()
+        while time.perf_counter() - t_soak < 0.5:          # clock soak: untimed steps under load
+            for _ in range(50):
+                perk.step(U, w.dt)
+            torch.cuda.synchronize()
         times = timed_steps(perk, U, args.steps, args.warmup)
     ms = float(np.mean(times))
     if ws > 1:
