@@ -16,14 +16,16 @@
  *   2. Mesh from a finest-grid level map: Morton leaves, 2:1 check, faces,
  *      partition (member) assignment, per-member lists   P:l.1243-1256, l.1276-1279
  *   3. Numerical fluxes (upwind, Rusanov, HLL, Ranocha EC two-point flux)
- *   4. RHS F(U) (weak form 1D, flux differencing 2D), "reference" (full F then
+ *   4. RHS F(U) (weak form 1D, flux differencing 2D; 4b: BR1 viscous terms for
+ *      Navier-Stokes), "reference" (full F then
  *      mask I^(r), P:l.299) and "restricted" (active lists only) modes
  *   5. Partitioned P-ERK step, materialised stage states   P:l.209-218, l.407-436
  *   6. Re-mesh solution transfer (refine = interpolation, coarsen = exact L2)
  *   7. FV Godunov testbed (linear advection / Burgers)     P:l.479-520
  *
- * Parity status: every function here is pinned by tests/test_oracle_*.py
- * except the Navier-Stokes BR1 operator, which is not implemented in this round.
+ * Parity status: every function here is pinned by tests/test_oracle_*.py; the
+ * Navier-Stokes BR1 operator (section 4b) by tests/test_oracle_ns.py (free stream,
+ * conservation, manufactured viscous terms term by term, restricted == reference).
  */
 #include <math.h>
 #include <stdint.h>
@@ -41,7 +43,7 @@
 /* ------------------------------------------------------------------------- */
 typedef struct {
     int32_t dim;          /* 1 or 2 */
-    int32_t equation;     /* 0 advection, 1 euler, 2 navier-stokes (not implemented) */
+    int32_t equation;     /* 0 advection, 1 euler, 2 navier-stokes (2D, BR1) */
     int32_t volume;       /* 0 weak form, 1 flux differencing (Ranocha) */
     int32_t surface;      /* 0 upwind, 1 Rusanov, 2 HLL, 3 Ranocha EC (2D Euler; entropy pin only) */
     int32_t nbx, nby;     /* base cells per direction (nby = 1 in 1D) */
@@ -209,6 +211,9 @@ typedef struct {
     int32_t *list[4]; int64_t seg[4][MAXR + 1];
     /* scratch */
     double *Fs;               /* surface flux per element face: [n][4][nv][NP] */
+    double *Gs;               /* BR1: central gradient-variable trace w* per element face, [n][4][4][NP] */
+    double *Q;                /* BR1: gradients of w = (rho, v1, v2, T), [n][2 (x, y)][4][NP*NP] */
+    double *Fv;               /* BR1: central viscous face flux per element face, [n][4][4][NP] */
     int64_t elem_rhs_count;   /* element-RHS evaluations (counter, P:l.1282-1289) */
 } Ora;
 
@@ -277,7 +282,7 @@ void ora_destroy(void *p)
     free(o->ifc); free(o->mor); free(o->bnd);
     free(o->if_member); free(o->mo_member); free(o->bd_member);
     for (int k = 0; k < 4; ++k) free(o->list[k]);
-    free(o->Fs);
+    free(o->Fs); free(o->Gs); free(o->Q); free(o->Fv);
     free(o);
 }
 
@@ -416,6 +421,19 @@ void *ora_create(const OraProblem *prob, const uint8_t *lmap, const OraTableau *
     build_lists(o, 2, o->n_mo, o->mo_member);
     build_lists(o, 3, o->n_bd, o->bd_member);
     o->Fs = (double *)calloc((size_t)o->n * 4 * o->nv * NP, sizeof(double));
+    if (prob->equation == 2) {
+        if (dim != 2 || prob->volume != 1) {
+            snprintf(err, errlen, "Navier-Stokes (BR1) is implemented for 2D flux differencing only");
+            ora_destroy(o); return NULL;
+        }
+        if (o->n_bd > 0) {
+            snprintf(err, errlen, "Navier-Stokes (BR1) needs a periodic domain (no viscous boundary fluxes)");
+            ora_destroy(o); return NULL;
+        }
+        o->Gs = (double *)calloc((size_t)o->n * 4 * 4 * NP, sizeof(double));
+        o->Q = (double *)calloc((size_t)o->n * 2 * 4 * NP * NP, sizeof(double));
+        o->Fv = (double *)calloc((size_t)o->n * 4 * 4 * NP, sizeof(double));
+    }
     return o;
 }
 
@@ -716,6 +734,181 @@ static void element_rhs(Ora *o, const double *U, int e, double *dU)
         }
 }
 
+
+/* ------------------------------------------------------------------------- */
+/* 4b. Navier-Stokes viscous terms, BR1 (P:l.1419-1420 cites Bassi-Rebay 1;  */
+/*     the paper does not define it: SURVEY §8(c) O3 "BR1", D5; D7) */
+/*   U_t + div F^a(U) = div F^v(U, grad w),  w = (rho, v1, v2, T = p/rho)     */
+/*   1. q = grad w by the weak-form DG derivative with the central trace      */
+/*      w* = (w_L + w_R)/2 (mortars: halves (P w_large + w_small)/2, large    */
+/*      side = R_lower w*_lo + R_upper w*_hi)                                 */
+/*   2. F^v(u, q) at the nodes: tau = mu (grad v + grad v^T - 2/3 div v I),   */
+/*      heat flux kappa grad T, kappa = mu gamma / ((gamma - 1) Pr)           */
+/*   3. central viscous face flux (F^v_L + F^v_R)/2 (mortars as in step 1,    */
+/*      applied to the normal viscous flux traces)                            */
+/*   4. du += (2/h) [ -Dhat F^v_x - Dhat F^v_y + surface lift ]  (weak form)  */
+/* ------------------------------------------------------------------------- */
+#define GIDX(o, e, face, v, k) ((((size_t)(e) * 4 + (face)) * 4 + (v)) * NP + (k))
+#define QIDX(o, e, d, v, q) ((((size_t)(e) * 2 + (d)) * 4 + (v)) * (NP * NP) + (q))
+
+/* gradient variables w = (rho, v1, v2, T), T = p / rho */
+static void prim_w(const Ora *o, const double *u, double *w)
+{
+    double g = o->prob.gamma;
+    double rho = u[0], v1 = u[1] / rho, v2 = u[2] / rho;
+    double p = (g - 1.0) * (u[3] - 0.5 * rho * (v1 * v1 + v2 * v2));
+    w[0] = rho; w[1] = v1; w[2] = v2; w[3] = p / rho;
+}
+
+/* viscous flux F^v_orient(u, q), q = (dw/dx, dw/dy) */
+static void visc_flux(const Ora *o, const double *u, const double *qx, const double *qy, int orient, double *f)
+{
+    double mu = o->prob.mu, g = o->prob.gamma;
+    double kappa = mu * g / ((g - 1.0) * o->prob.prandtl);
+    double v1 = u[1] / u[0], v2 = u[2] / u[0];
+    double v1x = qx[1], v2x = qx[2], Tx = qx[3];
+    double v1y = qy[1], v2y = qy[2], Ty = qy[3];
+    double t11 = mu * (4.0 / 3.0 * v1x - 2.0 / 3.0 * v2y);
+    double t22 = mu * (4.0 / 3.0 * v2y - 2.0 / 3.0 * v1x);
+    double t12 = mu * (v1y + v2x);
+    f[0] = 0.0;
+    if (orient == 0) {
+        f[1] = t11; f[2] = t12; f[3] = v1 * t11 + v2 * t12 + kappa * Tx;
+    } else {
+        f[1] = t12; f[2] = t22; f[3] = v1 * t12 + v2 * t22 + kappa * Ty;
+    }
+}
+
+static void trace_w(const Ora *o, const double *U, int e, int face, int k, double *w)
+{
+    double u[MAXV];
+    trace(o, U, e, face, k, u);
+    prim_w(o, u, w);
+}
+
+/* normal viscous flux at face node k of element e (orientation of the face) */
+static void trace_fv(const Ora *o, const double *U, int e, int face, int k, double *f)
+{
+    int q = face_node(o, face, k);
+    double u[MAXV], qx[4], qy[4];
+    for (int v = 0; v < 4; ++v) {
+        u[v] = U[UIDX(o, e, v, q)];
+        qx[v] = o->Q[QIDX(o, e, 0, v, q)];
+        qy[v] = o->Q[QIDX(o, e, 1, v, q)];
+    }
+    visc_flux(o, u, qx, qy, face / 2, f);
+}
+
+typedef void (*trace_fn)(const Ora *o, const double *U, int e, int face, int k, double *val);
+
+/* central face value of a BR1 quantity (w for the gradient, F^v_n for the viscous flux) into the
+   per-element face slots `out` ([n][4][4][NP]) */
+static void central_interface(Ora *o, const double *U, int f, trace_fn tr, double *out)
+{
+    int eL = o->ifc[3 * f], eR = o->ifc[3 * f + 1], orient = o->ifc[3 * f + 2];
+    for (int k = 0; k < NP; ++k) {
+        double a[4], b[4];
+        tr(o, U, eL, 2 * orient, k, a);
+        tr(o, U, eR, 2 * orient + 1, k, b);
+        for (int v = 0; v < 4; ++v) {
+            double c = 0.5 * (a[v] + b[v]);
+            out[GIDX(o, eL, 2 * orient, v, k)] = c;
+            out[GIDX(o, eR, 2 * orient + 1, v, k)] = c;
+        }
+    }
+}
+
+static void central_mortar(Ora *o, const double *U, int m, trace_fn tr, double *out)
+{
+    const int32_t *M = o->mor + 5 * m;
+    int eL = M[0], orient = M[3], side = M[4];
+    int large_face = 2 * orient + (side == 0 ? 0 : 1);
+    int small_face = 2 * orient + (side == 0 ? 1 : 0);
+    double al[NP][4], ch[2][NP][4];
+    for (int k = 0; k < NP; ++k) tr(o, U, eL, large_face, k, al[k]);
+    for (int h = 0; h < 2; ++h) {
+        int es = M[1 + h];
+        for (int k = 0; k < NP; ++k) {
+            double ai[4], as[4];
+            for (int v = 0; v < 4; ++v) {
+                double s = 0.0;
+                for (int j = 0; j < NP; ++j) s += (h == 0 ? o->B.Plo[k][j] : o->B.Pup[k][j]) * al[j][v];
+                ai[v] = s;
+            }
+            tr(o, U, es, small_face, k, as);
+            for (int v = 0; v < 4; ++v) {
+                ch[h][k][v] = 0.5 * (ai[v] + as[v]);
+                out[GIDX(o, es, small_face, v, k)] = ch[h][k][v];
+            }
+        }
+    }
+    for (int k = 0; k < NP; ++k)
+        for (int v = 0; v < 4; ++v) {
+            double s = 0.0;
+            for (int j = 0; j < NP; ++j) s += o->B.Rlo[k][j] * ch[0][j][v] + o->B.Rup[k][j] * ch[1][j][v];
+            out[GIDX(o, eL, large_face, v, k)] = s;
+        }
+}
+
+/* q = grad w of element e (weak form with the central traces in Gs):
+     q_x[i,j] = (2/h) [ -sum_k Dhat_ik w[k,j] + (delta_iN w*_{+x}[j] - delta_i0 w*_{-x}[j]) / w_i ] */
+static void element_grad(Ora *o, const double *U, int e)
+{
+    double J = 2.0 / cell_h(o, e);
+    double w[NP * NP][4];
+    for (int q = 0; q < NP * NP; ++q) {
+        double u[MAXV];
+        for (int v = 0; v < 4; ++v) u[v] = U[UIDX(o, e, v, q)];
+        prim_w(o, u, w[q]);
+    }
+    for (int j = 0; j < NP; ++j)
+        for (int i = 0; i < NP; ++i)
+            for (int v = 0; v < 4; ++v) {
+                double sx = 0.0, sy = 0.0;
+                for (int k = 0; k < NP; ++k) {
+                    sx -= o->B.Dhat[i][k] * w[j * NP + k][v];
+                    sy -= o->B.Dhat[j][k] * w[k * NP + i][v];
+                }
+                if (i == NP - 1) sx += o->Gs[GIDX(o, e, 0, v, j)] / o->B.w[NP - 1];
+                if (i == 0) sx -= o->Gs[GIDX(o, e, 1, v, j)] / o->B.w[0];
+                if (j == NP - 1) sy += o->Gs[GIDX(o, e, 2, v, i)] / o->B.w[NP - 1];
+                if (j == 0) sy -= o->Gs[GIDX(o, e, 3, v, i)] / o->B.w[0];
+                o->Q[QIDX(o, e, 0, v, j * NP + i)] = J * sx;
+                o->Q[QIDX(o, e, 1, v, j * NP + i)] = J * sy;
+            }
+}
+
+/* du += (2/h) [ -sum_k Dhat_ik F^v_x[k,j] - sum_k Dhat_jk F^v_y[i,k] + viscous surface lift ] */
+static void element_visc(Ora *o, const double *U, int e, double *dU)
+{
+    double J = 2.0 / cell_h(o, e);
+    double fx[NP * NP][4], fy[NP * NP][4];
+    for (int q = 0; q < NP * NP; ++q) {
+        double u[MAXV], qx[4], qy[4];
+        for (int v = 0; v < 4; ++v) {
+            u[v] = U[UIDX(o, e, v, q)];
+            qx[v] = o->Q[QIDX(o, e, 0, v, q)];
+            qy[v] = o->Q[QIDX(o, e, 1, v, q)];
+        }
+        visc_flux(o, u, qx, qy, 0, fx[q]);
+        visc_flux(o, u, qx, qy, 1, fy[q]);
+    }
+    for (int j = 0; j < NP; ++j)
+        for (int i = 0; i < NP; ++i)
+            for (int v = 0; v < 4; ++v) {
+                double s = 0.0;
+                for (int k = 0; k < NP; ++k) {
+                    s -= o->B.Dhat[i][k] * fx[j * NP + k][v];
+                    s -= o->B.Dhat[j][k] * fy[k * NP + i][v];
+                }
+                if (i == NP - 1) s += o->Fv[GIDX(o, e, 0, v, j)] / o->B.w[NP - 1];
+                if (i == 0) s -= o->Fv[GIDX(o, e, 1, v, j)] / o->B.w[0];
+                if (j == NP - 1) s += o->Fv[GIDX(o, e, 2, v, i)] / o->B.w[NP - 1];
+                if (j == 0) s -= o->Fv[GIDX(o, e, 3, v, i)] / o->B.w[0];
+                dU[UIDX(o, e, v, j * NP + i)] += J * s;
+            }
+}
+
 /* dU = sum_{r in mask} I^(r) F(U) (P:l.289-301).
    mode 0 "reference": evaluate every face and element, then zero the unmasked elements.
    mode 1 "restricted": loop over the members in mask only, through the per-member lists;
@@ -724,6 +917,7 @@ int ora_rhs(void *p, const double *U, uint32_t mask, double *dU, int mode)
 {
     Ora *o = (Ora *)p;
     int R = o->tab.R;
+    int ns = o->prob.equation == 2;
     if (mode == 1) {
         /* the restricted loops are only equivalent to I^(r)F for upward-closed masks (every member
            finer than a masked one is masked too), which is what every P-ERK stage uses (P:l.428):
@@ -733,10 +927,22 @@ int ora_rhs(void *p, const double *U, uint32_t mask, double *dU, int mode)
         memset(o->Fs, 0, sizeof(double) * (size_t)o->n * 4 * o->nv * NP);
     }
     if (mode == 0) {
+        if (ns) {   /* BR1 step 1: gradients everywhere */
+            for (int f = 0; f < o->n_if; ++f) central_interface(o, U, f, trace_w, o->Gs);
+            for (int m = 0; m < o->n_mo; ++m) central_mortar(o, U, m, trace_w, o->Gs);
+            for (int e = 0; e < o->n; ++e) element_grad(o, U, e);
+        }
         for (int f = 0; f < o->n_if; ++f) interface_flux(o, U, f);
         for (int m = 0; m < o->n_mo; ++m) mortar_flux(o, U, m);
         for (int b = 0; b < o->n_bd; ++b) boundary_flux(o, U, b);
-        for (int e = 0; e < o->n; ++e) element_rhs(o, U, e, dU);
+        if (ns) {
+            for (int f = 0; f < o->n_if; ++f) central_interface(o, U, f, trace_fv, o->Fv);
+            for (int m = 0; m < o->n_mo; ++m) central_mortar(o, U, m, trace_fv, o->Fv);
+        }
+        for (int e = 0; e < o->n; ++e) {
+            element_rhs(o, U, e, dU);
+            if (ns) element_visc(o, U, e, dU);
+        }
         for (int e = 0; e < o->n; ++e)
             if (!((mask >> o->member[e]) & 1u))
                 for (int v = 0; v < o->nv; ++v)
@@ -744,17 +950,42 @@ int ora_rhs(void *p, const double *U, uint32_t mask, double *dU, int mode)
         return 0;
     }
     memset(dU, 0, sizeof(double) * (size_t)o->n * o->nv * o->npe);
+    if (ns) {
+        /* BR1 gradients are needed on the active elements and on their face neighbours across
+           active mortars, which belong to the next coarser member: evaluate them over the members
+           of mask | (mask >> 1).  Every face of such an element has a member in that set (a face
+           belongs to its finer side, P:l.1256), so these gradients equal the full-F ones. */
+        uint32_t ext = mask | (mask >> 1);
+        for (int s = 0; s < R; ++s) {
+            int r = R - 1 - s;
+            if (!((ext >> r) & 1u)) continue;
+            for (int64_t t = o->seg[1][s]; t < o->seg[1][s + 1]; ++t) central_interface(o, U, o->list[1][t], trace_w, o->Gs);
+            for (int64_t t = o->seg[2][s]; t < o->seg[2][s + 1]; ++t) central_mortar(o, U, o->list[2][t], trace_w, o->Gs);
+        }
+        for (int s = 0; s < R; ++s) {
+            int r = R - 1 - s;
+            if (!((ext >> r) & 1u)) continue;
+            for (int64_t t = o->seg[0][s]; t < o->seg[0][s + 1]; ++t) element_grad(o, U, o->list[0][t]);
+        }
+    }
     for (int s = 0; s < R; ++s) {
         int r = R - 1 - s;
         if (!((mask >> r) & 1u)) continue;
         for (int64_t t = o->seg[1][s]; t < o->seg[1][s + 1]; ++t) interface_flux(o, U, o->list[1][t]);
         for (int64_t t = o->seg[2][s]; t < o->seg[2][s + 1]; ++t) mortar_flux(o, U, o->list[2][t]);
         for (int64_t t = o->seg[3][s]; t < o->seg[3][s + 1]; ++t) boundary_flux(o, U, o->list[3][t]);
+        if (ns) {
+            for (int64_t t = o->seg[1][s]; t < o->seg[1][s + 1]; ++t) central_interface(o, U, o->list[1][t], trace_fv, o->Fv);
+            for (int64_t t = o->seg[2][s]; t < o->seg[2][s + 1]; ++t) central_mortar(o, U, o->list[2][t], trace_fv, o->Fv);
+        }
     }
     for (int s = 0; s < R; ++s) {
         int r = R - 1 - s;
         if (!((mask >> r) & 1u)) continue;
-        for (int64_t t = o->seg[0][s]; t < o->seg[0][s + 1]; ++t) element_rhs(o, U, o->list[0][t], dU);
+        for (int64_t t = o->seg[0][s]; t < o->seg[0][s + 1]; ++t) {
+            element_rhs(o, U, o->list[0][t], dU);
+            if (ns) element_visc(o, U, o->list[0][t], dU);
+        }
     }
     return 0;
 }
