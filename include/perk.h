@@ -44,7 +44,7 @@ enum {
     PERK_ECAPACITY = -3,    /* more cells / faces than the capacity given at perk_init */
     PERK_ECUDA = -4,        /* a CUDA runtime call failed */
     PERK_ENOTINIT = -5,     /* context null or destroyed */
-    PERK_EUNSUPPORTED = -6  /* combination not implemented (e.g. Navier-Stokes BR1 this round) */
+    PERK_EUNSUPPORTED = -6  /* combination not implemented (e.g. Navier-Stokes with non-periodic faces) */
 };
 
 enum { PERK_EQ_ADVECTION = 0, PERK_EQ_EULER = 1, PERK_EQ_NAVIER_STOKES = 2 };
@@ -54,7 +54,8 @@ enum { PERK_KIND_ELEMENTS = 0, PERK_KIND_INTERFACES = 1, PERK_KIND_MORTARS = 2, 
 
 #define PERK_MAX_STAGES 64
 #define PERK_MAX_MEMBERS 8
-#define PERK_NUM_KERNEL_KINDS 4   /* profile slots: 0 surface flux, 1 volume+stage, 2 mesh rebuild, 3 transfer */
+#define PERK_NUM_KERNEL_KINDS 6   /* profile slots: 0 surface flux, 1 volume+stage, 2 mesh rebuild, 3 transfer,
+                                    4 BR1 gradient traces, 5 BR1 gradients + viscous-flux traces */
 
 /* Problem description.  DG degree N = 3 (LGL nodes) is fixed.
  *   dim            1 or 2
@@ -63,7 +64,9 @@ enum { PERK_KIND_ELEMENTS = 0, PERK_KIND_INTERFACES = 1, PERK_KIND_MORTARS = 2, 
  *   periodic[2]    1 = periodic, 0 = weakly imposed Dirichlet state bc_state on that direction's faces
  *   domain_lo/hi   physical box ([lo, hi] per direction)
  *   gamma          ratio of specific heats (Euler / NS)
- *   prandtl, mu    Navier-Stokes parameters (equation 2; not supported in this build -> EUNSUPPORTED)
+ *   prandtl, mu    Navier-Stokes parameters (equation 2, 2D only, periodic only): viscosity mu, Prandtl
+ *                  number; heat conductivity kappa = mu gamma / ((gamma - 1) Pr), T = p / rho.  The
+ *                  viscous terms are BR1 (P:l.1419-1420; D7)
  *   adv_velocity   1D linear advection speed a (equation 0)
  *   bc_state[4]    conserved ghost state for non-periodic faces
  *   max_cells      capacity (cells) for all buffers; the caller's U_dev must hold max_cells rows */

@@ -19,6 +19,9 @@ constexpr int MAXR = 8;
 constexpr int SM_COUNT_B200 = 148;
 
 enum Kind { KIND_EL = 0, KIND_IF = 1, KIND_MO = 2, KIND_BD = 3 };
+// count_active[EXT_OFF + kind * MAXS + i - 1]: items of the active members at stage i plus the next
+// coarser member (BR1 gradients are needed one element beyond the active set across mortars)
+constexpr int EXT_OFF = 4 * MAXS;
 enum Mode { MODE_STAGE = 0, MODE_RHS = 1 };
 enum ErrBits { ERR_UNBALANCED = 1, ERR_CAPACITY = 2, ERR_TRANSFER = 4 };
 
@@ -40,11 +43,12 @@ struct MeshDev {
     int equation, surface;
     double lo[2], hf;            // domain origin, finest cell size
     double gamma, adv;
+    double mu, kappa;            // Navier-Stokes: viscosity, heat conductivity mu gamma / ((gamma - 1) Pr)
     double bc[MAXV];
     int cap;                     // cell capacity
     // device pointers
     int *n;                      // [4]: cells, interfaces, mortars, boundaries
-    int *count_active;           // [4][MAXS]
+    int *count_active;           // [4][MAXS] stage prefix counts, then [4][MAXS] BR1 gradient prefixes (EXT_OFF)
     int *seg;                    // [4][MAXR+1]
     int *err;                    // error flag bits
     unsigned long long *evals;   // element-RHS evaluation counter

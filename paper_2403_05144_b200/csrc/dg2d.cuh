@@ -101,6 +101,46 @@ __device__ __forceinline__ void numflux2d(const double uL[4], const double uR[4]
 }
 
 // ---------------------------------------------------------------------------------------------
+// Navier-Stokes BR1 helpers (D7): gradient variables w = (rho, v1, v2,
+// T = p/rho); the gradient, viscous-flux and face arrays hold the 3 components (v1, v2, T) /
+// (momentum x, momentum y, energy) -- the density gradient and the viscous mass flux are unused / 0.
+// ---------------------------------------------------------------------------------------------
+constexpr int GV = 3;
+
+__device__ __forceinline__ void prim_vT(const double u[4], double gm1, double w[GV])
+{
+    const double ir = rcp64(u[0]);
+    const double v1 = u[1] * ir, v2 = u[2] * ir;
+    const double p = gm1 * (u[3] - 0.5 * fma(u[1], v1, u[2] * v2));
+    w[0] = v1;
+    w[1] = v2;
+    w[2] = p * ir;
+}
+
+// viscous flux in direction o from the velocities and q_x = (v1_x, v2_x, T_x), q_y = (...)_y:
+// tau = mu (grad v + grad v^T - 2/3 div v I), heat flux kappa grad T; returns the momentum-x,
+// momentum-y and energy components
+__device__ __forceinline__ void visc_flux2d(double v1, double v2, const double qx[GV], const double qy[GV], int o,
+                                            double mu, double kappa, double f[GV])
+{
+    const double t11 = mu * ((4.0 / 3.0) * qx[0] - (2.0 / 3.0) * qy[1]);
+    const double t22 = mu * ((4.0 / 3.0) * qy[1] - (2.0 / 3.0) * qx[0]);
+    const double t12 = mu * (qy[0] + qx[1]);
+    if (o == 0) {
+        f[0] = t11;
+        f[1] = t12;
+        f[2] = fma(v1, t11, fma(v2, t12, kappa * qx[2]));
+    } else {
+        f[0] = t12;
+        f[1] = t22;
+        f[2] = fma(v1, t12, fma(v2, t22, kappa * qy[2]));
+    }
+}
+
+// BR1 face arrays Gs (central w*), Vt (normal viscous flux trace): [cell][face][GV][k]
+__device__ __forceinline__ size_t gidx2d(int e, int face, int c, int k) { return (((size_t)e * 4 + face) * GV + c) * NP + k; }
+
+// ---------------------------------------------------------------------------------------------
 // surface kernel
 // ---------------------------------------------------------------------------------------------
 __device__ __forceinline__ const double *state_base(const StateBufs &sb, int src)
@@ -132,10 +172,13 @@ __device__ __forceinline__ void store_face2d(double *Fs, int e, int face, int k,
     for (int v = 0; v < 4; ++v) Fs[b + v * 4] = f[v];
 }
 
-template <int MODE>
+// NS: the face flux is HLL(u_L, u_R) - (F^v_L + F^v_R)/2 (central BR1 viscous flux from the
+// normal viscous-flux traces Vt of k_grad2d), so the volume kernel lifts one combined flux.
+template <int MODE, bool NS>
 __global__ void __launch_bounds__(256, 3) k_surf2d(MeshDev md, StageParams sp, const double *__restrict__ Un,
                                                const double *__restrict__ Ubuf, const double *__restrict__ K1,
-                                               const double *__restrict__ Uin, double *__restrict__ Fs)
+                                               const double *__restrict__ Uin, double *__restrict__ Fs,
+                                               const double *__restrict__ Vt)
 {
     int nif, nmo, nbd;
     if (MODE == MODE_STAGE) {
@@ -162,6 +205,11 @@ __global__ void __launch_bounds__(256, 3) k_surf2d(MeshDev md, StageParams sp, c
             trace2d(sb, src, dtc, I.x, 2 * o, k, uL);
             trace2d(sb, src, dtc, I.y, 2 * o + 1, k, uR);
             numflux2d(uL, uR, o, g, md.surface, fl);
+            if (NS) {
+#pragma unroll
+                for (int c = 0; c < GV; ++c)
+                    fl[1 + c] -= 0.5 * (__ldg(Vt + gidx2d(I.x, 2 * o, c, k)) + __ldg(Vt + gidx2d(I.y, 2 * o + 1, c, k)));
+            }
             store_face2d(Fs, I.x, 2 * o, k, fl);
             store_face2d(Fs, I.y, 2 * o + 1, k, fl);
         } else if (item < nif + nmo) {
@@ -191,15 +239,32 @@ __global__ void __launch_bounds__(256, 3) k_surf2d(MeshDev md, StageParams sp, c
                 trace2d(sb, srcS, dtc, M.y, sf, k, us);
                 if (side == 0) numflux2d(uil, us, o, g, md.surface, flo);
                 else numflux2d(us, uil, o, g, md.surface, flo);
-                store_face2d(Fs, M.y, sf, k, flo);
             }
             {
                 double us[4];
                 trace2d(sb, srcS, dtc, M.z, sf, k, us);
                 if (side == 0) numflux2d(uih, us, o, g, md.surface, fhi);
                 else numflux2d(us, uih, o, g, md.surface, fhi);
-                store_face2d(Fs, M.z, sf, k, fhi);
             }
+            if (NS) {   // central viscous flux on each half: (P F^v_large + F^v_small) / 2
+                double vl[GV];
+#pragma unroll
+                for (int c = 0; c < GV; ++c) vl[c] = __ldg(Vt + gidx2d(M.x, lf, c, k));
+#pragma unroll
+                for (int c = 0; c < GV; ++c) {
+                    double il = 0.0, ih = 0.0;
+#pragma unroll
+                    for (int j = 0; j < NP; ++j) {
+                        const double vj = __shfl_sync(gmask, vl[c], j, 4);
+                        il = fma(cB.Plo[k][j], vj, il);
+                        ih = fma(cB.Pup[k][j], vj, ih);
+                    }
+                    flo[1 + c] -= 0.5 * (il + __ldg(Vt + gidx2d(M.y, sf, c, k)));
+                    fhi[1 + c] -= 0.5 * (ih + __ldg(Vt + gidx2d(M.z, sf, c, k)));
+                }
+            }
+            store_face2d(Fs, M.y, sf, k, flo);
+            store_face2d(Fs, M.z, sf, k, fhi);
             double fl[4] = {0, 0, 0, 0};
 #pragma unroll
             for (int j = 0; j < NP; ++j) {
@@ -234,9 +299,10 @@ constexpr int VOL2D_EPB = 16;   // elements per 128-thread block (8 threads per 
 // Shared-memory layout (bank-conflict free for the line loops): every field is
 // stored twice, once in x-line order (index le*17 + 4j + i) and once in y-line order
 // (index le*17 + 4i + j), the y copy offset by 2 doubles so that the 16 x-threads and 16 y-threads
-// of a warp hit 32 distinct banks.  The accumulators alias the first 8 field arrays.
+// of a warp hit 32 distinct banks.  The accumulators alias the first 4 field arrays; the BR1
+// gradients (NS) alias fields 4..6 once the two-point fluxes have consumed them.
 constexpr int VOL2D_LS = 288;   // doubles per field array: >= 16*17 + 2, and == 0 mod 16 so the +2 y offset shifts banks
-constexpr int VOL2D_NF = 7;                    // rho, v1, v2, p, ln rho, beta, ln beta
+constexpr int F_RHO = 0, F_V1 = 1, F_V2 = 2, F_P = 3, F_LRHO = 4, F_BETA = 5, F_LBETA = 6, F_T = 7;
 
 __device__ __forceinline__ double2 load_state2(const StateBufs &sb, int src, double dtc, size_t idx)
 {
@@ -252,13 +318,80 @@ __device__ __forceinline__ double2 load_state2(const StateBufs &sb, int src, dou
     }
 }
 
-template <int MODE>
+// BR1 gradient of (v1, v2, T) along this thread's line (direction o, line ln), weak form with the
+// central traces Gs:  q[c][a] = (2/h) [ -sum_k Dhat_ak w_c[k] + (delta_a3 w*_{+o} - delta_a0 w*_{-o}) / w_a ]
+template <int LS>
+__device__ __forceinline__ void line_gradient(const double (*sm)[2][LS], int o, int lo, int e, int ln,
+                                              const double *__restrict__ Gs, double Jq, double q[GV][NP])
+{
+    const int fld[GV] = {F_V1, F_V2, F_T};
+#pragma unroll
+    for (int c = 0; c < GV; ++c) {
+        double w[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) w[k] = sm[fld[c]][o][lo + k];
+        const double ghi = __ldg(Gs + gidx2d(e, 2 * o, c, ln));
+        const double glo = __ldg(Gs + gidx2d(e, 2 * o + 1, c, ln));
+#pragma unroll
+        for (int a = 0; a < NP; ++a) {
+            double t = 0.0;
+#pragma unroll
+            for (int k = 0; k < NP; ++k) t = fma(-cB.Dhat[a][k], w[k], t);
+            if (a == NP - 1) t = fma(ghi, cB.invw[NP - 1], t);
+            if (a == 0) t = fma(-glo, cB.invw[0], t);
+            q[c][a] = Jq * t;
+        }
+    }
+}
+
+// NS volume contribution (MODE_STAGE and MODE_RHS): adds sum_a Dhat_ia F^v_o(node a) to acc, i.e.
+// -(2/h)(...) of the weak-form viscous divergence after the common -2/h scaling.  sm must hold the
+// primitive fields; fields 4..6 are overwritten with the gradients.
+template <int LS>
+__device__ __forceinline__ void visc_volume(double (*sm)[2][LS], int o, int lo, int eo, int yo, int ln, int e,
+                                            const double *__restrict__ Gs, double Jq, double mu, double kappa,
+                                            double acc[NP][4])
+{
+    double q[GV][NP];
+    line_gradient<LS>(sm, o, lo, e, ln, Gs, Jq, q);
+    __syncwarp();   // every thread of the element is done with fields 4..6 (two-point fluxes)
+#pragma unroll
+    for (int c = 0; c < GV; ++c)
+#pragma unroll
+        for (int a = 0; a < NP; ++a) sm[4 + c][o][lo + a] = q[c][a];
+    __syncwarp();
+    double fv[NP][GV];
+#pragma unroll
+    for (int a = 0; a < NP; ++a) {
+        // the other direction's gradient at this node: node (a, ln) of an x-line lives at y-layout
+        // index yo + eo + 4a + ln; node (ln, a) of a y-line at x-layout index eo + 4a + ln
+        const int oi = o == 0 ? yo + eo + 4 * a + ln : eo + 4 * a + ln;
+        double qo[GV], qs[GV];
+#pragma unroll
+        for (int c = 0; c < GV; ++c) {
+            qs[c] = q[c][a];
+            qo[c] = sm[4 + c][1 - o][oi];
+        }
+        const double v1 = sm[F_V1][o][lo + a], v2 = sm[F_V2][o][lo + a];
+        if (o == 0) visc_flux2d(v1, v2, qs, qo, 0, mu, kappa, fv[a]);
+        else visc_flux2d(v1, v2, qo, qs, 1, mu, kappa, fv[a]);
+    }
+#pragma unroll
+    for (int i = 0; i < NP; ++i)
+#pragma unroll
+        for (int a = 0; a < NP; ++a)
+#pragma unroll
+            for (int c = 0; c < GV; ++c) acc[i][1 + c] = fma(cB.Dhat[i][a], fv[a][c], acc[i][1 + c]);
+}
+
+template <int MODE, bool NS>
 __global__ void __launch_bounds__(128, 5) k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                                                  double *__restrict__ Ubuf, double *__restrict__ K1,
                                                  const double *__restrict__ Fs, const double *__restrict__ Uin,
-                                                 double *__restrict__ dU)
+                                                 double *__restrict__ dU, const double *__restrict__ Gs)
 {
-    __shared__ double sm[VOL2D_NF][2][VOL2D_LS];
+    constexpr int NF = NS ? 8 : 7;          // rho, v1, v2, p, ln rho, beta, ln beta (+ T)
+    __shared__ double sm[NF][2][VOL2D_LS];
     const int t8 = threadIdx.x & 7, le = threadIdx.x >> 3;
     const int n_act = MODE == MODE_STAGE ? md.count_active[KIND_EL * MAXS + sp.stage - 1] : md.n[0];
     const double g = md.gamma, gm1 = g - 1.0, inv_gm1 = 1.0 / gm1;
@@ -284,6 +417,7 @@ __global__ void __launch_bounds__(128, 5) k_vol2d(MeshDev md, StageParams sp, do
         const int m = md.mem[e];
         const int src = state_src(sp, m);
         const size_t eb = (size_t)e * 64;
+        const double hcell = md.hf * (double)(1 << (md.max_level - md.lev[e]));
 
         // phase 1: nodes q0, q0+1 -> primitives + logs, stored in x-line and y-line layouts
         {
@@ -299,9 +433,9 @@ __global__ void __launch_bounds__(128, 5) k_vol2d(MeshDev md, StageParams sp, do
                 const double v1 = m1 * ir, v2 = m2 * ir;
                 const double p = gm1 * (E - 0.5 * fma(m1, v1, m2 * v2));
                 const double beta = r * rcp64(p);
-                const double f[VOL2D_NF] = {r, v1, v2, p, log(r), beta, log(beta)};
+                const double f[8] = {r, v1, v2, p, log(r), beta, log(beta), p * ir};
 #pragma unroll
-                for (int k = 0; k < VOL2D_NF; ++k) {
+                for (int k = 0; k < NF; ++k) {
                     sm[k][0][eo + 4 * j + i] = f[k];
                     sm[k][1][yo + eo + 4 * i + j] = f[k];
                 }
@@ -334,6 +468,8 @@ __global__ void __launch_bounds__(128, 5) k_vol2d(MeshDev md, StageParams sp, do
                 }
             }
         }
+        // NS: + sum_a Dhat_ia F^v(node a) along the line (BR1 gradients recomputed from Gs)
+        if (NS) visc_volume<VOL2D_LS>(sm, o, lo, eo, yo, ln, e, Gs, 2.0 / hcell, md.mu, md.kappa, acc);
         // surface lift: + f*_hi / w_N at the last node, - f*_lo / w_0 at the first node
         {
             const double *Fhi = Fs + ((size_t)e * 4 + 2 * o) * 16 + ln;
@@ -353,7 +489,7 @@ __global__ void __launch_bounds__(128, 5) k_vol2d(MeshDev md, StageParams sp, do
 
         // phase 3: K = -(2/h) (x + y contributions), stage epilogue for nodes q0, q0+1
         if (valid) {
-            const double J = -2.0 / (md.hf * (double)(1 << (md.max_level - md.lev[e])));
+            const double J = -2.0 / hcell;
             const int i0 = q0 & 3, j0 = q0 >> 2;   // q0 + 1 has i0 + 1
 #pragma unroll
             for (int v = 0; v < 4; ++v) {

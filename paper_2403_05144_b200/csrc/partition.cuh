@@ -83,7 +83,8 @@ __device__ __forceinline__ int block_incl_scan(int v, int *wsum, int &total)
 
 // One block.  blockoff[b][r] = start of block b's bucket-r items; seg[s] = start of segment s
 // (key R-1-s), seg[R] = total.  Optionally: *total_out = total, and count_active[i-1] for the
-// member partitions (active members are the top ones, i.e. a prefix of the segments).
+// member partitions (active members are the top ones, i.e. a prefix of the segments), and
+// count_active[EXT_OFF + i-1] for the prefix extended by the next coarser member (BR1 gradients).
 __global__ void __launch_bounds__(PART_T) k_part_offsets(const int *blockcnt, int nblocks, int R, int *blockoff, int *seg,
                                                         int *total_out, ActiveDesc ad, int *count_active)
 {
@@ -112,6 +113,7 @@ __global__ void __launch_bounds__(PART_T) k_part_offsets(const int *blockcnt, in
         for (int r = 0; r < ad.R; ++r)
             if (i == 1 || ad.E[r] >= ad.S - i + 2) ++k;
         count_active[i - 1] = seg[k];
+        count_active[EXT_OFF + i - 1] = seg[k < ad.R ? k + 1 : ad.R];
     }
 }
 

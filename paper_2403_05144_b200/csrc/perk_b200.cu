@@ -16,6 +16,7 @@
 #include "mesh.cuh"
 #include "dg1d.cuh"
 #include "dg2d.cuh"
+#include "br1.cuh"
 #include "transfer.cuh"
 
 using namespace perk;
@@ -38,12 +39,14 @@ struct perk_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t cap_stream = nullptr;
     double *K1 = nullptr, *Ubuf = nullptr, *Fs = nullptr, *Utmp = nullptr, *Uhost_dev = nullptr;
+    double *Gs = nullptr, *Vt = nullptr;   // BR1 (Navier-Stokes): central w* and viscous-flux traces
+    bool ns = false;
     uint8_t *lmap = nullptr, *keys = nullptr;
     int *items = nullptr, *rank = nullptr, *blockcnt = nullptr, *blockoff = nullptr, *segtmp = nullptr;
     int *dconst = nullptr;     // [0] = nmorton
     int *n_old = nullptr, *cell_of_old = nullptr, *fx_old = nullptr, *fy_old = nullptr;
     uint8_t *lev_old = nullptr;
-    int vol_blocks = 0, surf_blocks = 0;
+    int vol_blocks = 0, surf_blocks = 0, grad_blocks = 0;
     cudaGraphExec_t gexec = nullptr;
     double *gU = nullptr;
     double gdt = 0.0;
@@ -215,10 +218,17 @@ static void launch_surface(perk_ctx *c, cudaStream_t s, const StageParams &sp, c
 {
     const MeshDev &md = c->md;
     if (c->prob.dim == 2) {
-        if (sp.mode == MODE_STAGE)
-            k_surf2d<MODE_STAGE><<<c->surf_blocks, 256, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs);
-        else
-            k_surf2d<MODE_RHS><<<c->surf_blocks, 256, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs);
+        if (c->ns) {
+            if (sp.mode == MODE_STAGE)
+                k_surf2d<MODE_STAGE, true><<<c->surf_blocks, 256, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs, c->Vt);
+            else
+                k_surf2d<MODE_RHS, true><<<c->surf_blocks, 256, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs, c->Vt);
+        } else {
+            if (sp.mode == MODE_STAGE)
+                k_surf2d<MODE_STAGE, false><<<c->surf_blocks, 256, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs, nullptr);
+            else
+                k_surf2d<MODE_RHS, false><<<c->surf_blocks, 256, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs, nullptr);
+        }
     } else if (c->nv == 1) {
         if (sp.mode == MODE_STAGE)
             k_surf1d<1, MODE_STAGE><<<c->surf_blocks, 256, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs);
@@ -236,10 +246,17 @@ static void launch_volume(perk_ctx *c, cudaStream_t s, const StageParams &sp, do
 {
     const MeshDev &md = c->md;
     if (c->prob.dim == 2) {
-        if (sp.mode == MODE_STAGE)
-            k_vol2d<MODE_STAGE><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU);
-        else
-            k_vol2d<MODE_RHS><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU);
+        if (c->ns) {
+            if (sp.mode == MODE_STAGE)
+                k_vol2d<MODE_STAGE, true><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Gs);
+            else
+                k_vol2d<MODE_RHS, true><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Gs);
+        } else {
+            if (sp.mode == MODE_STAGE)
+                k_vol2d<MODE_STAGE, false><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, nullptr);
+            else
+                k_vol2d<MODE_RHS, false><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, nullptr);
+        }
     } else if (c->nv == 1) {
         if (sp.mode == MODE_STAGE)
             k_vol1d<1, MODE_STAGE><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU);
@@ -253,10 +270,27 @@ static void launch_volume(perk_ctx *c, cudaStream_t s, const StageParams &sp, do
     }
 }
 
+// BR1 passes (Navier-Stokes): central gradient traces, then gradients + viscous-flux traces
+static void launch_br1(perk_ctx *c, cudaStream_t s, const StageParams &sp, const double *Un, const double *Uin, Prof *p)
+{
+    const MeshDev &md = c->md;
+    prof_mark(p, s, 4);
+    if (sp.mode == MODE_STAGE)
+        k_gsurf2d<MODE_STAGE><<<c->surf_blocks, 256, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs);
+    else
+        k_gsurf2d<MODE_RHS><<<c->surf_blocks, 256, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs);
+    prof_mark(p, s, 5);
+    if (sp.mode == MODE_STAGE)
+        k_grad2d<MODE_STAGE><<<c->grad_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs, c->Vt);
+    else
+        k_grad2d<MODE_RHS><<<c->grad_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs, c->Vt);
+}
+
 static void launch_step(perk_ctx *c, cudaStream_t s, double *U, double dt, Prof *p)
 {
     for (int i = 1; i <= c->tab.S; ++i) {
         const StageParams sp = stage_params(c, i, dt, MODE_STAGE, 0u);
+        if (c->ns) launch_br1(c, s, sp, U, nullptr, p);
         prof_mark(p, s, 0);
         launch_surface(c, s, sp, U, nullptr);
         prof_mark(p, s, 1);
@@ -299,8 +333,13 @@ static int validate(perk_ctx *c, const perk_problem *p, const perk_tableau *t)
         }
         if (p->volume != PERK_VOL_WEAK) return set_err(c, PERK_EUNSUPPORTED, "1D uses the weak form");
     } else {
-        if (p->equation == PERK_EQ_NAVIER_STOKES) return set_err(c, PERK_EUNSUPPORTED, "Navier-Stokes (BR1) not in this build");
-        if (p->equation != PERK_EQ_EULER) return set_err(c, PERK_EUNSUPPORTED, "2D supports Euler");
+        if (p->equation == PERK_EQ_NAVIER_STOKES) {
+            if (!p->periodic[0] || !p->periodic[1])
+                return set_err(c, PERK_EUNSUPPORTED, "Navier-Stokes (BR1) needs a periodic domain (no viscous boundary fluxes)");
+            if (!(p->mu >= 0.0) || !(p->prandtl > 0.0)) return set_err(c, PERK_EINVAL, "mu >= 0 and prandtl > 0 required");
+        } else if (p->equation != PERK_EQ_EULER) {
+            return set_err(c, PERK_EUNSUPPORTED, "2D supports Euler and Navier-Stokes");
+        }
         if (p->volume != PERK_VOL_FLUXDIFF) return set_err(c, PERK_EUNSUPPORTED, "2D uses flux differencing");
         if (p->surface != PERK_FLUX_HLL && p->surface != PERK_FLUX_RUSANOV) return set_err(c, PERK_EUNSUPPORTED, "2D surface flux");
         const double hx = (p->domain_hi[0] - p->domain_lo[0]) / p->n_base[0];
@@ -350,6 +389,9 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
     md.hf = (prob->domain_hi[0] - prob->domain_lo[0]) / md.nfx;
     md.gamma = prob->gamma;
     md.adv = prob->adv_velocity;
+    c->ns = dim == 2 && prob->equation == PERK_EQ_NAVIER_STOKES;
+    md.mu = c->ns ? prob->mu : 0.0;
+    md.kappa = c->ns ? prob->mu * prob->gamma / ((prob->gamma - 1.0) * prob->prandtl) : 0.0;
     for (int v = 0; v < MAXV; ++v) md.bc[v] = prob->bc_state[v];
     md.cap = c->cap;
     c->nf = (size_t)md.nfx * md.nfy;
@@ -373,7 +415,7 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
     const long long max_items = c->nmorton > (long long)c->nd * c->cap ? c->nmorton : (long long)c->nd * c->cap;
     const int nb_max = (int)((max_items + PART_T - 1) / PART_T) + 1;
     CU(dalloc(c, &md.n, 4));
-    CU(dalloc(c, &md.count_active, 4 * MAXS));
+    CU(dalloc(c, &md.count_active, 2 * EXT_OFF));
     CU(dalloc(c, &md.seg, 4 * (MAXR + 1)));
     CU(dalloc(c, &md.err, 1));
     CU(dalloc(c, &md.evals, 2));
@@ -390,6 +432,10 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
     CU(dalloc(c, &c->K1, (size_t)c->cap * rowd));
     CU(dalloc(c, &c->Ubuf, (size_t)c->cap * rowd));
     CU(dalloc(c, &c->Fs, (size_t)c->cap * (dim == 1 ? 2 * c->nv : 4 * c->nv * NP)));
+    if (c->ns) {
+        CU(dalloc(c, &c->Gs, (size_t)c->cap * 4 * GV * NP));
+        CU(dalloc(c, &c->Vt, (size_t)c->cap * 4 * GV * NP));
+    }
     CU(dalloc(c, &c->lmap, c->nf));
     CU(dalloc(c, &c->keys, (size_t)max_items));
     CU(dalloc(c, &c->items, (size_t)max_items));
@@ -403,9 +449,13 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
 
     int occ = 0;
     if (dim == 2) {
-        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vol2d<MODE_STAGE>, 128, 0));
+        if (c->ns) CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vol2d<MODE_STAGE, true>, 128, 0));
+        else CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vol2d<MODE_STAGE, false>, 128, 0));
         const int want = (c->cap + VOL2D_EPB - 1) / VOL2D_EPB;
         c->vol_blocks = std::min(want, SM_COUNT_B200 * std::max(occ, 1));
+        int occg = 0;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occg, k_grad2d<MODE_STAGE>, 128, 0));
+        c->grad_blocks = std::min(want, SM_COUNT_B200 * std::max(occg, 1));
         c->surf_blocks = std::min(blocks_for(4ll * c->cap_faces, 256), SM_COUNT_B200 * 8);
     } else {
         c->vol_blocks = std::min(blocks_for(c->cap, 128), SM_COUNT_B200 * 8);
@@ -469,7 +519,7 @@ extern "C" int perk_launches_per_step(perk_ctx *c, int32_t *launches)
 {
     if (!c) return PERK_ENOTINIT;
     if (!launches) return PERK_EINVAL;
-    *launches = 2 * c->tab.S;
+    *launches = (c->ns ? 4 : 2) * c->tab.S;
     return PERK_OK;
 }
 
@@ -553,6 +603,7 @@ extern "C" int rhs_eval(perk_ctx *c, const double *U, uint32_t mask, double *dU)
     if (!c) return PERK_ENOTINIT;
     if (!U || !dU) return set_err(c, PERK_EINVAL, "null pointer");
     const StageParams sp = stage_params(c, 1, 0.0, MODE_RHS, mask);
+    if (c->ns) launch_br1(c, c->stream, sp, nullptr, U, nullptr);
     launch_surface(c, c->stream, sp, nullptr, U);
     launch_volume(c, c->stream, sp, nullptr, U, dU);
     CU(cudaGetLastError());

@@ -21,6 +21,7 @@ SURF = {"upwind": 0, "rusanov": 1, "hll": 2}
 KIND = {"elements": 0, "interfaces": 1, "mortars": 2, "boundaries": 3}
 ERRORS = {-1: "EINVAL", -2: "EUNBALANCED", -3: "ECAPACITY", -4: "ECUDA", -5: "ENOTINIT", -6: "EUNSUPPORTED"}
 NP = 4
+NKINDS = 6   # PERK_NUM_KERNEL_KINDS: surface, volume+stage, mesh, transfer, BR1 traces, BR1 gradients
 
 
 class PerkError(RuntimeError):
@@ -285,15 +286,15 @@ class Perk:
         return n.value
 
     def profile_step(self, U, dt):
-        ms = (C.c_float * 4)()
-        nl = (C.c_int32 * 4)()
+        ms = (C.c_float * NKINDS)()
+        nl = (C.c_int32 * NKINDS)()
         _check(self.h, lib().perk_profile_step(self.h, _ptr(U), float(dt), ms, nl))
         return list(ms), list(nl)
 
     def profile_repartition(self, level_map, U):
         lm = self._to_dev_u8(level_map)
-        ms = (C.c_float * 4)()
-        nl = (C.c_int32 * 4)()
+        ms = (C.c_float * NKINDS)()
+        nl = (C.c_int32 * NKINDS)()
         _check(self.h, lib().perk_profile_repartition(self.h, _ptr(lm), _ptr(U), ms, nl))
         return list(ms), list(nl)
 

@@ -35,9 +35,7 @@ def _run_both(w, steps, ora, gpu, mode=1):
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
 def test_lists_full_size(cfg):
     w = W.make(cfg)
-    # the lists do not depend on the equation; cfg 5's BR1 operator is not built this round
-    p = dict(w.problem, equation="euler") if cfg == 5 else w.problem
-    ora, gpu = build_pair(w, problem=p)
+    ora, gpu = build_pair(w)
     assert ora.n == gpu.n_cells
     compare_mesh(ora, gpu)
 
@@ -234,3 +232,79 @@ def test_repartition_lists_and_transfer():
     gpu.step(Ug, w.dt, 5)
     torch.cuda.synchronize()
     assert rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo).max() <= TOL
+
+
+# ----------------------------------------------------------------------------------------------
+# Navier-Stokes, BR1 (a10): cfg 5 structure
+# ----------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("n_base", [8, 256])
+def test_ns_rhs_eval_masks(n_base):
+    """one RHS per upward-closed mask and the full mask; 256 = the BASELINE cfg-5 mesh (305,827 cells)"""
+    w = W.make(5, n_base=n_base)
+    ora, gpu = build_pair(w)
+    assert ora.face_counts()["mortars"] > 0
+    Uo = ora.initial_state(w.ic)
+    Ug = gpu.initial_state(w.ic)
+    R = len(w.E)
+    masks = [(1 << R) - 1, 1 << (R - 1), ((1 << R) - 1) & ~1]
+    for mask in masks:
+        dUo = ora.rhs(Uo, mask, mode=0)
+        dUg = gpu_state_numpy(gpu, gpu.rhs(Ug, mask))
+        scale = 2.0 / w.problem["h_min"] * np.abs(Uo).max()
+        for v in range(4):
+            tol = 1e-12 * np.abs(dUo[:, v]).max() + 4e-14 * scale
+            assert np.abs(dUg[:, v] - dUo[:, v]).max() <= tol, (mask, v)
+
+
+def test_cfg5_small_full_run():
+    """cfg-5 structure (4 levels, {4, 8, 16, 32}, BR1) on an 8^2 base, the full 200 steps"""
+    w = W.make(5, n_base=8)
+    ora, gpu = build_pair(w)
+    Uo, Ug = _run_both(w, w.steps, ora, gpu)
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
+    ev, st = gpu.counters()
+    cnt = ora.count_active("elements")
+    assert st == w.steps and ev == int(cnt.sum()) * w.steps
+
+
+def test_cfg5_medium_steps():
+    w = W.make(5, n_base=32)
+    ora, gpu = build_pair(w)
+    Uo, Ug = _run_both(w, 5, ora, gpu)
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
+
+
+def test_cfg5_full_size_step():
+    """BASELINE cfg 5 mesh (305,827 cells) in the bench launch configuration, 1 step (~50 s oracle)"""
+    w = W.make(5)
+    ora, gpu = build_pair(w)
+    Uo, Ug = _run_both(w, 1, ora, gpu)
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
+
+
+def test_ns_single_level_reduction():
+    w = W.make(5, n_base=8, steps=10)
+    lm = np.full_like(w.level_map, w.problem["max_level"])
+    from paper_2403_05144_b200 import Perk
+    ora = O.OracleMesh(w.problem, lm, T.family(32, [32], "taylor"))
+    gpu = Perk(w.problem, lm, 32, [4, 8, 16, 32])
+    Uo, Ug = _run_both(w, w.steps, ora, gpu)
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
+
+
+def test_ns_free_stream_gpu():
+    w = W.make(5, n_base=8)
+    from paper_2403_05144_b200 import Perk
+    gpu = Perk(w.problem, w.level_map, w.S, w.E)
+    U = gpu.initial_state(lambda x, y: np.stack([1.2 + 0 * x, 0.36 + 0 * x, -0.6 + 0 * x, 60.0 + 0 * x]))
+    dU = gpu_state_numpy(gpu, gpu.rhs(U))
+    assert np.abs(dU).max() <= 1e-13 * (2.0 / w.problem["h_min"]) * 60.0
+
+
+def test_ns_nonperiodic_rejected():
+    from paper_2403_05144_b200 import Perk, PerkError
+    w = W.make(5, n_base=8)
+    p = dict(w.problem, periodic=(0, 1))
+    with pytest.raises(PerkError) as ei:
+        Perk(p, w.level_map, w.S, w.E)
+    assert ei.value.code == -6
