@@ -142,7 +142,9 @@ __global__ void __launch_bounds__(128) k_grad2d(MeshDev md, StageParams sp, cons
         __syncwarp();
         const int lo = o == 0 ? eo + 4 * ln : yo + eo + 4 * ln;
         double q[GV][NP];
-        line_gradient<GRAD2D_LS>(sm, o, lo, e, ln, Gs, 2.0 / hcell, q);
+        const int fld[GV] = {F_V1, F_V2, F_T};
+        const double sc[GV] = {1.0, 1.0, 1.0};
+        line_gradient<GRAD2D_LS>(sm, o, lo, e, ln, Gs, 2.0 / hcell, fld, sc, q);
 #pragma unroll
         for (int c = 0; c < GV; ++c)
 #pragma unroll

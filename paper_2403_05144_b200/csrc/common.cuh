@@ -57,7 +57,16 @@ struct MeshDev {
     uint8_t *lev, *mem;          // leaf level, member
     int *cell_of;                // finest cell -> leaf
     int4 *ifc; int4 *mor; int2 *bnd;
+    // hot-path copies in list (member-sorted) order, so a stage kernel reaches its item with one load:
+    int *elpk;                   // elements: e | member << 24 | level << 27 (PK_* below)
+    int4 *ifcs; int4 *mors;      // interface / mortar records in list order
 };
+
+// packed element entry of md.elpk (cells < 2^24, members < 8, levels < 16)
+constexpr int PK_EBITS = 24;
+__device__ __forceinline__ int pk_elem(int pk) { return pk & ((1 << PK_EBITS) - 1); }
+__device__ __forceinline__ int pk_member(int pk) { return (pk >> PK_EBITS) & 7; }
+__device__ __forceinline__ int pk_level(int pk) { return (pk >> (PK_EBITS + 3)) & 15; }
 
 // Per-launch stage parameters (kernel argument, graph-captured).
 struct StageParams {
@@ -119,12 +128,37 @@ __device__ __forceinline__ double rcp64(double x)
 {
     double y;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    double e = fma(-x, y, 1.0);
-    y = fma(y, e, y);
-    e = fma(-x, y, 1.0);
+    double e = fma(-x, y, 1.0);      // |e| <~ 2^-22 from the MUFU seed; two Newton steps reach 2^-88
     y = fma(y, e, y);
     e = fma(-x, y, 1.0);
     return fma(y, e, y);
+}
+
+// natural logarithm of a positive, finite, normal double without branches (the libm log has
+// special-case control flow that serialises the hot loop): x = 2^k m, m in [sqrt(1/2), sqrt(2)),
+// log m = 2 atanh(t) = 2 t (1 + t^2/3 + ... + t^20/21), t = (m-1)/(m+1), |t| <= 0.1716 (truncation
+// < 1e-17 relative); <= 3 ulp against the correctly rounded result in a 40k-sample host check.
+__device__ __forceinline__ double log_pos(double x)
+{
+    const long long ix = __double_as_longlong(x);
+    const long long k = (ix - 0x3FE6A09E667F3BCDll) >> 52;          // sqrt(1/2) = 0x3FE6A09E667F3BCD
+    const double m = __longlong_as_double(ix - (k << 52));
+    const double f = m - 1.0;
+    const double t = f * rcp64(2.0 + f);
+    const double t2 = t * t;
+    double q = 1.0 / 21.0;
+    q = fma(q, t2, 1.0 / 19.0);
+    q = fma(q, t2, 1.0 / 17.0);
+    q = fma(q, t2, 1.0 / 15.0);
+    q = fma(q, t2, 1.0 / 13.0);
+    q = fma(q, t2, 1.0 / 11.0);
+    q = fma(q, t2, 1.0 / 9.0);
+    q = fma(q, t2, 1.0 / 7.0);
+    q = fma(q, t2, 1.0 / 5.0);
+    q = fma(q, t2, 1.0 / 3.0);
+    q = fma(q, t2, 1.0);
+    const double kd = (double)k;
+    return fma(kd, 6.93147180369123816490e-01, fma(2.0 * t, q, kd * 1.90821492927058770002e-10));
 }
 
 // fast fp64 square root: MUFU reciprocal-sqrt approximation + Newton steps (<= 1 ulp off IEEE)
@@ -136,6 +170,54 @@ __device__ __forceinline__ double sqrt64(double x)
     r = r * fma(-0.5 * x * r, r, 1.5);
     double s = x * r;
     return fma(0.5 * r, fma(-s, s, x), s);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Blackwell bulk-copy (TMA engine, SASS UBLKCP) + mbarrier helpers: a 512 B element block is one
+// cp.async.bulk global -> shared copy whose completion is counted in bytes on an mbarrier.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init()
+{
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// order this thread's earlier generic-proxy shared-memory accesses before later async-proxy ones
+__device__ __forceinline__ void fence_proxy_async_smem()
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long *bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
 }
 
 }  // namespace perk

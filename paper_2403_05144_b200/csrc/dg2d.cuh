@@ -56,6 +56,32 @@ __device__ __forceinline__ void flux_ranocha(const Prim &L, const Prim &R, int o
     f[3] = fma(frho, fma(0.5, fma(L.v1, R.v1, L.v2 * R.v2), inv_beta_hat * inv_gm1), 0.5 * fma(L.p, vnR, R.p * vnL));
 }
 
+// The same flux in line coordinates, as the volume kernel evaluates it: per node the layout of the
+// line's direction stores rho, hvn = v_n / 2, hvt = v_t / 2, hp = p / 2 (n = the line direction, t
+// the other one), so the flux needs no orientation selects and the averages are single additions:
+// f = (rho_hat vbar_n, rho_hat vbar_n^2 + pbar, rho_hat vbar_n vbar_t,
+//      rho_hat vbar_n (2 (hvn_L hvn_R + hvt_L hvt_R) + 1/((g-1) beta_hat)) + 2 (hp_L hvn_R + hp_R hvn_L))
+struct LinePrim {
+    double rho, hvn, hvt, hp, lrho, beta, lbeta;
+};
+
+__device__ __forceinline__ void flux_ranocha_line(const LinePrim &L, const LinePrim &R, double inv_gm1, double f[4])
+{
+    double Nr, Dr, Nb, Db;
+    ln_mean_nd(L.rho, R.rho, L.lrho, R.lrho, Nr, Dr);
+    ln_mean_nd(L.beta, R.beta, L.lbeta, R.lbeta, Nb, Db);
+    const double q = rcp64(Dr * Nb);
+    const double rho_hat = Nr * Nb * q;          // Nr / Dr
+    const double inv_beta_hat = Db * Dr * q;     // Db / Nb
+    const double vna = L.hvn + R.hvn, vta = L.hvt + R.hvt, pa = L.hp + R.hp;
+    const double frho = rho_hat * vna;
+    f[0] = frho;
+    f[1] = fma(frho, vna, pa);
+    f[2] = frho * vta;
+    f[3] = fma(frho, fma(2.0, fma(L.hvn, R.hvn, L.hvt * R.hvt), inv_beta_hat * inv_gm1),
+               2.0 * fma(L.hp, R.hvn, R.hp * L.hvn));
+}
+
 __device__ __forceinline__ void euler_flux2d(const double u[4], double p, double vn, int o, double f[4])
 {
     f[0] = u[0] * vn;
@@ -197,8 +223,7 @@ __global__ void __launch_bounds__(256, 3) k_surf2d(MeshDev md, StageParams sp, c
     for (int gt = blockIdx.x * blockDim.x + threadIdx.x; gt < total; gt += gridDim.x * blockDim.x) {
         const int item = gt >> 2, k = gt & 3;
         if (item < nif) {
-            const int f = MODE == MODE_STAGE ? md.list[KIND_IF][item] : item;
-            const int4 I = md.ifc[f];
+            const int4 I = MODE == MODE_STAGE ? md.ifcs[item] : md.ifc[item];
             const int o = I.z;
             const int src = state_src(sp, I.w);    // conforming: both sides share the member
             double uL[4], uR[4], fl[4];
@@ -214,8 +239,7 @@ __global__ void __launch_bounds__(256, 3) k_surf2d(MeshDev md, StageParams sp, c
             store_face2d(Fs, I.y, 2 * o + 1, k, fl);
         } else if (item < nif + nmo) {
             const int q = item - nif;
-            const int mo = MODE == MODE_STAGE ? md.list[KIND_MO][q] : q;
-            const int4 M = md.mor[mo];
+            const int4 M = MODE == MODE_STAGE ? md.mors[q] : md.mor[q];
             const int o = M.w & 1, side = (M.w >> 1) & 1, mfine = M.w >> 8;
             const int lf = 2 * o + side, sf = 2 * o + 1 - side;
             const int srcL = state_src(sp, md.mem[M.x]);
@@ -302,7 +326,10 @@ constexpr int VOL2D_EPB = 16;   // elements per 128-thread block (8 threads per 
 // of a warp hit 32 distinct banks.  The accumulators alias the first 4 field arrays; the BR1
 // gradients (NS) alias fields 4..6 once the two-point fluxes have consumed them.
 constexpr int VOL2D_LS = 288;   // doubles per field array: >= 16*17 + 2, and == 0 mod 16 so the +2 y offset shifts banks
-constexpr int F_RHO = 0, F_V1 = 1, F_V2 = 2, F_P = 3, F_LRHO = 4, F_BETA = 5, F_LBETA = 6, F_T = 7;
+// k_vol2d fields (layout o = line direction): rho, v_n/2, v_t/2, p/2, ln rho, beta = rho/p, ln beta (+ T)
+constexpr int F_RHO = 0, F_HVN = 1, F_HVT = 2, F_HP = 3, F_LRHO = 4, F_BETA = 5, F_LBETA = 6, F_T = 7;
+// k_grad2d fields (both layouts): v1, v2, T
+constexpr int F_V1 = 1, F_V2 = 2;
 
 __device__ __forceinline__ double2 load_state2(const StateBufs &sb, int src, double dtc, size_t idx)
 {
@@ -319,19 +346,22 @@ __device__ __forceinline__ double2 load_state2(const StateBufs &sb, int src, dou
 }
 
 // BR1 gradient of (v1, v2, T) along this thread's line (direction o, line ln), weak form with the
-// central traces Gs:  q[c][a] = (2/h) [ -sum_k Dhat_ak w_c[k] + (delta_a3 w*_{+o} - delta_a0 w*_{-o}) / w_a ]
+// central traces Gs:  q[c][a] = (2/h) [ -sum_k Dhat_ak w_c[k] + (delta_a3 w*_{+o} - delta_a0 w*_{-o}) / w_a ].
+// Component c is read from field fld[c] of layout o, which holds w_c / sc[c] (sc = 1 or 2: the volume
+// kernel stores half velocities; scaling by 2 is exact, so q is bitwise the unscaled result).
 template <int LS>
 __device__ __forceinline__ void line_gradient(const double (*sm)[2][LS], int o, int lo, int e, int ln,
-                                              const double *__restrict__ Gs, double Jq, double q[GV][NP])
+                                              const double *__restrict__ Gs, double Jq, const int fld[GV],
+                                              const double sc[GV], double q[GV][NP])
 {
-    const int fld[GV] = {F_V1, F_V2, F_T};
 #pragma unroll
     for (int c = 0; c < GV; ++c) {
         double w[NP];
 #pragma unroll
         for (int k = 0; k < NP; ++k) w[k] = sm[fld[c]][o][lo + k];
-        const double ghi = __ldg(Gs + gidx2d(e, 2 * o, c, ln));
-        const double glo = __ldg(Gs + gidx2d(e, 2 * o + 1, c, ln));
+        const double isc = 1.0 / sc[c];
+        const double ghi = __ldg(Gs + gidx2d(e, 2 * o, c, ln)) * isc;
+        const double glo = __ldg(Gs + gidx2d(e, 2 * o + 1, c, ln)) * isc;
 #pragma unroll
         for (int a = 0; a < NP; ++a) {
             double t = 0.0;
@@ -339,21 +369,23 @@ __device__ __forceinline__ void line_gradient(const double (*sm)[2][LS], int o, 
             for (int k = 0; k < NP; ++k) t = fma(-cB.Dhat[a][k], w[k], t);
             if (a == NP - 1) t = fma(ghi, cB.invw[NP - 1], t);
             if (a == 0) t = fma(-glo, cB.invw[0], t);
-            q[c][a] = Jq * t;
+            q[c][a] = (Jq * sc[c]) * t;
         }
     }
 }
 
-// NS volume contribution (MODE_STAGE and MODE_RHS): adds sum_a Dhat_ia F^v_o(node a) to acc, i.e.
-// -(2/h)(...) of the weak-form viscous divergence after the common -2/h scaling.  sm must hold the
-// primitive fields; fields 4..6 are overwritten with the gradients.
+// NS volume contribution (MODE_STAGE and MODE_RHS): adds sum_a Dhat_ia F^v_o(node a) to acc (in line
+// coordinates: acc[.][1] normal, acc[.][2] tangential momentum), i.e. -(2/h)(...) of the weak-form
+// viscous divergence after the common -2/h scaling.  Fields 4..6 are overwritten with the gradients.
 template <int LS>
 __device__ __forceinline__ void visc_volume(double (*sm)[2][LS], int o, int lo, int eo, int yo, int ln, int e,
                                             const double *__restrict__ Gs, double Jq, double mu, double kappa,
                                             double acc[NP][4])
 {
+    const int fld[GV] = {o == 0 ? F_HVN : F_HVT, o == 0 ? F_HVT : F_HVN, F_T};   // v1/2, v2/2, T
+    const double sc[GV] = {2.0, 2.0, 1.0};
     double q[GV][NP];
-    line_gradient<LS>(sm, o, lo, e, ln, Gs, Jq, q);
+    line_gradient<LS>(sm, o, lo, e, ln, Gs, Jq, fld, sc, q);
     __syncwarp();   // every thread of the element is done with fields 4..6 (two-point fluxes)
 #pragma unroll
     for (int c = 0; c < GV; ++c)
@@ -372,9 +404,14 @@ __device__ __forceinline__ void visc_volume(double (*sm)[2][LS], int o, int lo, 
             qs[c] = q[c][a];
             qo[c] = sm[4 + c][1 - o][oi];
         }
-        const double v1 = sm[F_V1][o][lo + a], v2 = sm[F_V2][o][lo + a];
-        if (o == 0) visc_flux2d(v1, v2, qs, qo, 0, mu, kappa, fv[a]);
-        else visc_flux2d(v1, v2, qo, qs, 1, mu, kappa, fv[a]);
+        const double v1 = 2.0 * sm[fld[0]][o][lo + a], v2 = 2.0 * sm[fld[1]][o][lo + a];
+        double f[GV];
+        if (o == 0) visc_flux2d(v1, v2, qs, qo, 0, mu, kappa, f);
+        else visc_flux2d(v1, v2, qo, qs, 1, mu, kappa, f);
+        // (momentum x, momentum y, energy) -> line coordinates (normal, tangential, energy)
+        fv[a][0] = o == 0 ? f[0] : f[1];
+        fv[a][1] = o == 0 ? f[1] : f[0];
+        fv[a][2] = f[2];
     }
 #pragma unroll
     for (int i = 0; i < NP; ++i)
@@ -384,23 +421,47 @@ __device__ __forceinline__ void visc_volume(double (*sm)[2][LS], int o, int lo, 
             for (int c = 0; c < GV; ++c) acc[i][1 + c] = fma(cB.Dhat[i][a], fv[a][c], acc[i][1 + c]);
 }
 
+// Dynamic shared memory of k_vol2d (bytes), see vol2d_smem_layout below.
+__host__ __device__ constexpr int vol2d_nf(bool ns) { return ns ? 8 : 7; }
+__host__ __device__ constexpr size_t vol2d_smem_bytes(bool ns)
+{
+    return sizeof(double) * ((size_t)vol2d_nf(ns) * 2 * VOL2D_LS + VOL2D_EPB * 2 * 64 + VOL2D_EPB * 3 * 64) +
+           sizeof(unsigned long long) * 2 * (VOL2D_EPB / 4);
+}
+
+// Volume + surface lift + Jacobian + stage epilogue.  Persistent grid-stride loop over groups of 16
+// active elements per 128-thread CTA; each element's 512 B blocks are staged into shared memory with
+// bulk copies (TMA engine), issued by lane 0 of each warp for the warp's 4 elements, completing on one
+// mbarrier per warp and buffer:
+//   stg[le][0..1] : the stage state of the NEXT group (U_n | stage buffer | U_in, or U_n and K_1 for a
+//                   lazy state), issued as soon as the current group's state has been read (phase 1)
+//   epi[le][0..2] : U_n, K_1 and the face fluxes Fs of the CURRENT group, issued before the two-point
+//                   flux loop and consumed after it (lift + epilogue)
+// so neither the state gather nor the epilogue reads expose DRAM latency (the ncu stall profile of the
+// unstaged kernel was dominated by long-scoreboard waits on exactly these loads).
 template <int MODE, bool NS>
-__global__ void __launch_bounds__(128, 5) k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
+__global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                                                  double *__restrict__ Ubuf, double *__restrict__ K1,
                                                  const double *__restrict__ Fs, const double *__restrict__ Uin,
                                                  double *__restrict__ dU, const double *__restrict__ Gs)
 {
-    constexpr int NF = NS ? 8 : 7;          // rho, v1, v2, p, ln rho, beta, ln beta (+ T)
-    __shared__ double sm[NF][2][VOL2D_LS];
+    constexpr int NF = vol2d_nf(NS);          // rho, v1, v2, p, ln rho, beta, ln beta (+ T)
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double (*sm)[2][VOL2D_LS] = reinterpret_cast<double (*)[2][VOL2D_LS]>(smraw);
+    double (*stg)[2][64] = reinterpret_cast<double (*)[2][64]>(smraw + sizeof(double) * NF * 2 * VOL2D_LS);
+    double (*epi)[3][64] = reinterpret_cast<double (*)[3][64]>(reinterpret_cast<unsigned char *>(stg) +
+                                                                sizeof(double) * VOL2D_EPB * 2 * 64);
+    unsigned long long *bar = reinterpret_cast<unsigned long long *>(reinterpret_cast<unsigned char *>(epi) +
+                                                                     sizeof(double) * VOL2D_EPB * 3 * 64);
     const int t8 = threadIdx.x & 7, le = threadIdx.x >> 3;
     const int n_act = MODE == MODE_STAGE ? md.count_active[KIND_EL * MAXS + sp.stage - 1] : md.n[0];
     const double g = md.gamma, gm1 = g - 1.0, inv_gm1 = 1.0 / gm1;
-    const StateBufs sb{Un, Ubuf, K1, Uin};
     const double dtc = sp.dt * sp.c_stage;
     const int q0 = 2 * t8;
     const int o = t8 >> 2, ln = t8 & 3;
     const int eo = le * 17;                 // element offset inside a field array
     const int yo = 2;                       // y-layout offset
+    const int stride = gridDim.x * VOL2D_EPB;
 
     if (MODE == MODE_STAGE && sp.stage == sp.S && blockIdx.x == 0 && threadIdx.x == 0) {
         unsigned long long tot = 0;
@@ -408,22 +469,71 @@ __global__ void __launch_bounds__(128, 5) k_vol2d(MeshDev md, StageParams sp, do
         atomicAdd(md.evals, tot);
         atomicAdd(md.evals + 1, 1ull);
     }
+    int base = blockIdx.x * VOL2D_EPB;
+    if (base >= n_act) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned long long *bar_st = bar + warp, *bar_ep = bar + VOL2D_EPB / 4 + warp;
+    if (threadIdx.x < 2 * (VOL2D_EPB / 4)) mbar_init(bar + threadIdx.x, 1);
+    fence_mbar_init();
+    __syncthreads();
 
-    for (int base = blockIdx.x * VOL2D_EPB; base < n_act; base += gridDim.x * VOL2D_EPB) {
-        const int t = base + le;
-        const bool valid = t < n_act;
-        const int tt = valid ? t : base;
-        const int e = MODE == MODE_STAGE ? md.list[KIND_EL][tt] : tt;
-        const int m = md.mem[e];
+    // packed entry (element | member | level) of this thread's slot in the group starting at b
+    auto entry_at = [&](int b) {
+        const int t = b + le;
+        const int tt = t < n_act ? t : b;
+        if (MODE == MODE_STAGE) return md.elpk[tt];
+        return tt | ((int)md.mem[tt] << PK_EBITS) | ((int)md.lev[tt] << (PK_EBITS + 3));
+    };
+    // lane 0 of the warp: stage the states of the warp's 4 elements (packed entries pk of lanes 0, 8,
+    // 16, 24) on the warp's state barrier
+    auto issue_states = [&](int pk) {
+        int pks[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) pks[j] = __shfl_sync(0xffffffffu, pk, 8 * j);
+        if (lane == 0) {
+            unsigned bytes = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bytes += state_src(sp, pk_member(pks[j])) == SRC_LAZY ? 1024 : 512;
+            mbar_arrive_expect_tx(bar_st, bytes);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int sl = 4 * warp + j;
+                const size_t off = (size_t)pk_elem(pks[j]) * 64;
+                const int srce = state_src(sp, pk_member(pks[j]));
+                if (srce == SRC_LAZY) {
+                    bulk_g2s(stg[sl][0], Un + off, 512, bar_st);
+                    bulk_g2s(stg[sl][1], K1 + off, 512, bar_st);
+                } else {
+                    bulk_g2s(stg[sl][0], (srce == SRC_UN ? Un : (srce == SRC_BUF ? Ubuf : Uin)) + off, 512, bar_st);
+                }
+            }
+        }
+    };
+    int pk = entry_at(base);
+    issue_states(pk);
+
+    for (unsigned ph = 0; base < n_act; base += stride, ph ^= 1u) {
+        const bool valid = base + le < n_act;
+        const bool has_next = base + stride < n_act;
+        const int pk_next = has_next ? entry_at(base + stride) : 0;   // consumed after phase 1
+        const int e = pk_elem(pk);
+        const int m = pk_member(pk);
         const int src = state_src(sp, m);
         const size_t eb = (size_t)e * 64;
-        const double hcell = md.hf * (double)(1 << (md.max_level - md.lev[e]));
+        const double hcell = md.hf * (double)(1 << (md.max_level - pk_level(pk)));
 
         // phase 1: nodes q0, q0+1 -> primitives + logs, stored in x-line and y-line layouts
+        mbar_wait(bar_st, ph);
         {
             double2 u[4];
 #pragma unroll
-            for (int v = 0; v < 4; ++v) u[v] = load_state2(sb, src, dtc, eb + v * 16 + q0);
+            for (int v = 0; v < 4; ++v) {
+                u[v] = *reinterpret_cast<const double2 *>(&stg[le][0][v * 16 + q0]);
+                if (src == SRC_LAZY) {
+                    const double2 k = *reinterpret_cast<const double2 *>(&stg[le][1][v * 16 + q0]);
+                    u[v] = make_double2(fma(dtc, k.x, u[v].x), fma(dtc, k.y, u[v].y));
+                }
+            }
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int q = q0 + h, i = q & 3, j = q >> 2;
@@ -433,15 +543,40 @@ __global__ void __launch_bounds__(128, 5) k_vol2d(MeshDev md, StageParams sp, do
                 const double v1 = m1 * ir, v2 = m2 * ir;
                 const double p = gm1 * (E - 0.5 * fma(m1, v1, m2 * v2));
                 const double beta = r * rcp64(p);
-                const double f[8] = {r, v1, v2, p, log(r), beta, log(beta), p * ir};
+                const double lr = log_pos(r), lb = lr - log_pos(p);   // ln beta = ln rho - ln p
+                const double hv1 = 0.5 * v1, hv2 = 0.5 * v2, hp = 0.5 * p;
+                // x layout: normal = x; y layout: normal = y
+                const double fx[8] = {r, hv1, hv2, hp, lr, beta, lb, p * ir};
+                const double fy[8] = {r, hv2, hv1, hp, lr, beta, lb, p * ir};
 #pragma unroll
                 for (int k = 0; k < NF; ++k) {
-                    sm[k][0][eo + 4 * j + i] = f[k];
-                    sm[k][1][yo + eo + 4 * i + j] = f[k];
+                    sm[k][0][eo + 4 * j + i] = fx[k];
+                    sm[k][1][yo + eo + 4 * i + j] = fy[k];
                 }
             }
         }
         __syncwarp();
+        fence_proxy_async_smem();
+        if (has_next) issue_states(pk_next);   // next group's states (the whole warp has read stg)
+        {
+            // this group's epilogue operands: Fs, and U_n / K_1 where the epilogue needs them
+            const bool need_un = MODE == MODE_STAGE && sp.stage > 1;
+            const bool need_k1 = MODE == MODE_STAGE && sp.stage > 1 && sp.stage < sp.S;
+            int es[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) es[j] = __shfl_sync(0xffffffffu, e, 8 * j);
+            if (lane == 0) {
+                mbar_arrive_expect_tx(bar_ep, 4u * (512u + (need_un ? 512u : 0u) + (need_k1 ? 512u : 0u)));
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int sl = 4 * warp + j;
+                    const size_t off = (size_t)es[j] * 64;
+                    bulk_g2s(epi[sl][2], Fs + off, 512, bar_ep);
+                    if (need_un) bulk_g2s(epi[sl][0], Un + off, 512, bar_ep);
+                    if (need_k1) bulk_g2s(epi[sl][1], K1 + off, 512, bar_ep);
+                }
+            }
+        }
 
         // phase 2: 6 symmetric two-point fluxes along this thread's line (x-line j = ln, or y-line i = ln)
         const int lo = o == 0 ? eo + 4 * ln : yo + eo + 4 * ln;   // line start in layout o
@@ -450,16 +585,17 @@ __global__ void __launch_bounds__(128, 5) k_vol2d(MeshDev md, StageParams sp, do
         for (int a = 0; a < 4; ++a)
 #pragma unroll
             for (int v = 0; v < 4; ++v) acc[a][v] = 0.0;
+        const double *L0 = &sm[0][o][lo];   // field k of line node a: L0[k * 2 * VOL2D_LS + a]
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            const Prim A{sm[0][o][lo + a], sm[1][o][lo + a], sm[2][o][lo + a], sm[3][o][lo + a],
-                         sm[4][o][lo + a], sm[5][o][lo + a], sm[6][o][lo + a]};
+            const LinePrim A{L0[a], L0[2 * VOL2D_LS + a], L0[4 * VOL2D_LS + a], L0[6 * VOL2D_LS + a],
+                             L0[8 * VOL2D_LS + a], L0[10 * VOL2D_LS + a], L0[12 * VOL2D_LS + a]};
 #pragma unroll
             for (int b = a + 1; b < 4; ++b) {
-                const Prim Bp{sm[0][o][lo + b], sm[1][o][lo + b], sm[2][o][lo + b], sm[3][o][lo + b],
-                              sm[4][o][lo + b], sm[5][o][lo + b], sm[6][o][lo + b]};
+                const LinePrim Bp{L0[b], L0[2 * VOL2D_LS + b], L0[4 * VOL2D_LS + b], L0[6 * VOL2D_LS + b],
+                                  L0[8 * VOL2D_LS + b], L0[10 * VOL2D_LS + b], L0[12 * VOL2D_LS + b]};
                 double f[4];
-                flux_ranocha(A, Bp, o, inv_gm1, f);
+                flux_ranocha_line(A, Bp, inv_gm1, f);
                 const double dab = cB.Dsplit[a][b], dba = cB.Dsplit[b][a];
 #pragma unroll
                 for (int v = 0; v < 4; ++v) {
@@ -471,13 +607,23 @@ __global__ void __launch_bounds__(128, 5) k_vol2d(MeshDev md, StageParams sp, do
         // NS: + sum_a Dhat_ia F^v(node a) along the line (BR1 gradients recomputed from Gs)
         if (NS) visc_volume<VOL2D_LS>(sm, o, lo, eo, yo, ln, e, Gs, 2.0 / hcell, md.mu, md.kappa, acc);
         // surface lift: + f*_hi / w_N at the last node, - f*_lo / w_0 at the first node
+        // line coordinates (normal, tangential) -> (momentum x, momentum y)
+        if (o == 1) {
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const double t = acc[a][1];
+                acc[a][1] = acc[a][2];
+                acc[a][2] = t;
+            }
+        }
+        mbar_wait(bar_ep, ph);
         {
-            const double *Fhi = Fs + ((size_t)e * 4 + 2 * o) * 16 + ln;
-            const double *Flo = Fs + ((size_t)e * 4 + 2 * o + 1) * 16 + ln;
+            const double *Fhi = &epi[le][2][(2 * o) * 16 + ln];
+            const double *Flo = &epi[le][2][(2 * o + 1) * 16 + ln];
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
-                acc[3][v] = fma(__ldg(Fhi + v * 4), cB.invw[3], acc[3][v]);
-                acc[0][v] = fma(-__ldg(Flo + v * 4), cB.invw[0], acc[0][v]);
+                acc[3][v] = fma(Fhi[v * 4], cB.invw[3], acc[3][v]);
+                acc[0][v] = fma(-Flo[v * 4], cB.invw[0], acc[0][v]);
             }
         }
         __syncwarp();   // all primitives consumed: reuse sm[v][o] as the accumulator arrays
@@ -503,11 +649,11 @@ __global__ void __launch_bounds__(128, 5) k_vol2d(MeshDev md, StageParams sp, do
                 } else if (sp.stage == 1) {
                     *reinterpret_cast<double2 *>(K1 + idx) = K;
                 } else if (sp.stage == sp.S) {
-                    const double2 un = *reinterpret_cast<const double2 *>(Un + idx);
+                    const double2 un = *reinterpret_cast<const double2 *>(&epi[le][0][v * 16 + q0]);
                     *reinterpret_cast<double2 *>(Un + idx) = make_double2(fma(sp.dt, K.x, un.x), fma(sp.dt, K.y, un.y));
                 } else {
-                    const double2 un = __ldg(reinterpret_cast<const double2 *>(Un + idx));
-                    const double2 k1 = __ldg(reinterpret_cast<const double2 *>(K1 + idx));
+                    const double2 un = *reinterpret_cast<const double2 *>(&epi[le][0][v * 16 + q0]);
+                    const double2 k1 = *reinterpret_cast<const double2 *>(&epi[le][1][v * 16 + q0]);
                     const double a1 = sp.a1_next[m], as = sp.asub_next[m];
                     *reinterpret_cast<double2 *>(Ubuf + idx) =
                         make_double2(fma(sp.dt, fma(a1, k1.x, as * K.x), un.x), fma(sp.dt, fma(a1, k1.y, as * K.y), un.y));
@@ -515,6 +661,7 @@ __global__ void __launch_bounds__(128, 5) k_vol2d(MeshDev md, StageParams sp, do
             }
         }
         __syncwarp();
+        pk = pk_next;
     }
 }
 

@@ -205,6 +205,18 @@ __global__ void k_face_records(MeshDev md, const int *__restrict__ slot_list, co
 }
 
 // physical node coordinates [n][dim][npe]
+// hot-path copies in list order: packed element entries, interface and mortar records
+__global__ void k_hot_lists(MeshDev md)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < md.n[0]) {
+        const int e = md.list[KIND_EL][t];
+        md.elpk[t] = e | ((int)md.mem[e] << PK_EBITS) | ((int)md.lev[e] << (PK_EBITS + 3));
+    }
+    if (t < md.n[1]) md.ifcs[t] = md.ifc[md.list[KIND_IF][t]];
+    if (t < md.n[2]) md.mors[t] = md.mor[md.list[KIND_MO][t]];
+}
+
 __global__ void k_node_coords(MeshDev md, double *xy)
 {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;

@@ -188,6 +188,7 @@ static void build_mesh(perk_ctx *c, cudaStream_t s, const uint8_t *lmap)
               nullptr, md.count_active + KIND_MO * MAXS);
     partition(c, s, KeyBnd{md.bnd}, md.n + 3, 1, c->cap_faces, R, md.list[KIND_BD], nullptr, md.seg + 3 * (MAXR + 1),
               nullptr, md.count_active + KIND_BD * MAXS);
+    k_hot_lists<<<blocks_for(c->cap_faces, 256), 256, 0, s>>>(md);
 }
 
 // ----------------------------------------------------------------------------------------------
@@ -248,14 +249,14 @@ static void launch_volume(perk_ctx *c, cudaStream_t s, const StageParams &sp, do
     if (c->prob.dim == 2) {
         if (c->ns) {
             if (sp.mode == MODE_STAGE)
-                k_vol2d<MODE_STAGE, true><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Gs);
+                k_vol2d<MODE_STAGE, true><<<c->vol_blocks, 128, vol2d_smem_bytes(true), s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Gs);
             else
-                k_vol2d<MODE_RHS, true><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Gs);
+                k_vol2d<MODE_RHS, true><<<c->vol_blocks, 128, vol2d_smem_bytes(true), s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Gs);
         } else {
             if (sp.mode == MODE_STAGE)
-                k_vol2d<MODE_STAGE, false><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, nullptr);
+                k_vol2d<MODE_STAGE, false><<<c->vol_blocks, 128, vol2d_smem_bytes(false), s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, nullptr);
             else
-                k_vol2d<MODE_RHS, false><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, nullptr);
+                k_vol2d<MODE_RHS, false><<<c->vol_blocks, 128, vol2d_smem_bytes(false), s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, nullptr);
         }
     } else if (c->nv == 1) {
         if (sp.mode == MODE_STAGE)
@@ -322,7 +323,7 @@ static int validate(perk_ctx *c, const perk_problem *p, const perk_tableau *t)
     if (p->dim != 1 && p->dim != 2) return set_err(c, PERK_EINVAL, "dim must be 1 or 2");
     if (p->n_base[0] < 1 || (p->dim == 2 && p->n_base[1] < 1)) return set_err(c, PERK_EINVAL, "n_base");
     if (p->max_level < 0 || p->max_level > 12) return set_err(c, PERK_EINVAL, "max_level");
-    if (p->max_cells < 1 || p->max_cells > (1ll << 28)) return set_err(c, PERK_EINVAL, "max_cells");
+    if (p->max_cells < 1 || p->max_cells > (1ll << 24)) return set_err(c, PERK_EINVAL, "max_cells must be in [1, 2^24]");
     if (p->dim == 1) {
         if (p->equation == PERK_EQ_ADVECTION) {
             if (p->surface != PERK_FLUX_UPWIND) return set_err(c, PERK_EUNSUPPORTED, "1D advection uses the upwind flux");
@@ -429,6 +430,9 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
     CU(dalloc(c, &md.ifc, c->cap_faces));
     CU(dalloc(c, &md.mor, c->cap_faces));
     CU(dalloc(c, &md.bnd, c->cap_faces));
+    CU(dalloc(c, &md.elpk, c->cap));
+    CU(dalloc(c, &md.ifcs, c->cap_faces));
+    CU(dalloc(c, &md.mors, c->cap_faces));
     CU(dalloc(c, &c->K1, (size_t)c->cap * rowd));
     CU(dalloc(c, &c->Ubuf, (size_t)c->cap * rowd));
     CU(dalloc(c, &c->Fs, (size_t)c->cap * (dim == 1 ? 2 * c->nv : 4 * c->nv * NP)));
@@ -449,8 +453,12 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
 
     int occ = 0;
     if (dim == 2) {
-        if (c->ns) CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vol2d<MODE_STAGE, true>, 128, 0));
-        else CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vol2d<MODE_STAGE, false>, 128, 0));
+        CU(cudaFuncSetAttribute(k_vol2d<MODE_STAGE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vol2d_smem_bytes(true)));
+        CU(cudaFuncSetAttribute(k_vol2d<MODE_RHS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vol2d_smem_bytes(true)));
+        CU(cudaFuncSetAttribute(k_vol2d<MODE_STAGE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vol2d_smem_bytes(false)));
+        CU(cudaFuncSetAttribute(k_vol2d<MODE_RHS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vol2d_smem_bytes(false)));
+        if (c->ns) CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vol2d<MODE_STAGE, true>, 128, vol2d_smem_bytes(true)));
+        else CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vol2d<MODE_STAGE, false>, 128, vol2d_smem_bytes(false)));
         const int want = (c->cap + VOL2D_EPB - 1) / VOL2D_EPB;
         c->vol_blocks = std::min(want, SM_COUNT_B200 * std::max(occ, 1));
         int occg = 0;
