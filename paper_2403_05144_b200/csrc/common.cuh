@@ -220,4 +220,13 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
         : "memory");
 }
 
+// Ampere-style asynchronous copies (SASS LDGSTS): no registers, per-thread commit groups
+__device__ __forceinline__ void cp_async16(void *dst, const void *src)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 }  // namespace perk

@@ -421,38 +421,35 @@ __device__ __forceinline__ void visc_volume(double (*sm)[2][LS], int o, int lo, 
             for (int c = 0; c < GV; ++c) acc[i][1 + c] = fma(cB.Dhat[i][a], fv[a][c], acc[i][1 + c]);
 }
 
-// Dynamic shared memory of k_vol2d (bytes), see vol2d_smem_layout below.
+// Dynamic shared memory of k_vol2d (bytes): field arrays, own-state staging, epilogue staging.
 __host__ __device__ constexpr int vol2d_nf(bool ns) { return ns ? 8 : 7; }
 __host__ __device__ constexpr size_t vol2d_smem_bytes(bool ns)
 {
-    return sizeof(double) * ((size_t)vol2d_nf(ns) * 2 * VOL2D_LS + VOL2D_EPB * 2 * 64 + VOL2D_EPB * 3 * 64) +
-           sizeof(unsigned long long) * 2 * (VOL2D_EPB / 4);
+    return sizeof(double) * ((size_t)vol2d_nf(ns) * 2 * VOL2D_LS + VOL2D_EPB * 2 * 64 + VOL2D_EPB * 3 * 64);
 }
 
 // Volume + surface lift + Jacobian + stage epilogue.  Persistent grid-stride loop over groups of 16
 // active elements per 128-thread CTA; each element's 512 B blocks are staged into shared memory with
-// bulk copies (TMA engine), issued by lane 0 of each warp for the warp's 4 elements, completing on one
-// mbarrier per warp and buffer:
+// cp.async (16 B per thread and copy, coalesced, no registers), in two commit groups per iteration:
 //   stg[le][0..1] : the stage state of the NEXT group (U_n | stage buffer | U_in, or U_n and K_1 for a
 //                   lazy state), issued as soon as the current group's state has been read (phase 1)
 //   epi[le][0..2] : U_n, K_1 and the face fluxes Fs of the CURRENT group, issued before the two-point
 //                   flux loop and consumed after it (lift + epilogue)
-// so neither the state gather nor the epilogue reads expose DRAM latency (the ncu stall profile of the
-// unstaged kernel was dominated by long-scoreboard waits on exactly these loads).
+// so neither the state gather nor the epilogue reads expose memory latency.  (A first version used
+// cp.async.bulk on mbarriers; issuing the per-element bulk copies through the uniform datapath cost
+// about a quarter of the kernel's issue slots.)
 template <int MODE, bool NS>
 __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                                                  double *__restrict__ Ubuf, double *__restrict__ K1,
                                                  const double *__restrict__ Fs, const double *__restrict__ Uin,
                                                  double *__restrict__ dU, const double *__restrict__ Gs)
 {
-    constexpr int NF = vol2d_nf(NS);          // rho, v1, v2, p, ln rho, beta, ln beta (+ T)
+    constexpr int NF = vol2d_nf(NS);          // rho, v_n/2, v_t/2, p/2, ln rho, beta, ln beta (+ T)
     extern __shared__ __align__(16) unsigned char smraw[];
     double (*sm)[2][VOL2D_LS] = reinterpret_cast<double (*)[2][VOL2D_LS]>(smraw);
     double (*stg)[2][64] = reinterpret_cast<double (*)[2][64]>(smraw + sizeof(double) * NF * 2 * VOL2D_LS);
     double (*epi)[3][64] = reinterpret_cast<double (*)[3][64]>(reinterpret_cast<unsigned char *>(stg) +
                                                                 sizeof(double) * VOL2D_EPB * 2 * 64);
-    unsigned long long *bar = reinterpret_cast<unsigned long long *>(reinterpret_cast<unsigned char *>(epi) +
-                                                                     sizeof(double) * VOL2D_EPB * 3 * 64);
     const int t8 = threadIdx.x & 7, le = threadIdx.x >> 3;
     const int n_act = MODE == MODE_STAGE ? md.count_active[KIND_EL * MAXS + sp.stage - 1] : md.n[0];
     const double g = md.gamma, gm1 = g - 1.0, inv_gm1 = 1.0 / gm1;
@@ -471,11 +468,6 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
     }
     int base = blockIdx.x * VOL2D_EPB;
     if (base >= n_act) return;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned long long *bar_st = bar + warp, *bar_ep = bar + VOL2D_EPB / 4 + warp;
-    if (threadIdx.x < 2 * (VOL2D_EPB / 4)) mbar_init(bar + threadIdx.x, 1);
-    fence_mbar_init();
-    __syncthreads();
 
     // packed entry (element | member | level) of this thread's slot in the group starting at b
     auto entry_at = [&](int b) {
@@ -484,37 +476,24 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
         if (MODE == MODE_STAGE) return md.elpk[tt];
         return tt | ((int)md.mem[tt] << PK_EBITS) | ((int)md.lev[tt] << (PK_EBITS + 3));
     };
-    // lane 0 of the warp: stage the states of the warp's 4 elements (packed entries pk of lanes 0, 8,
-    // 16, 24) on the warp's state barrier
-    auto issue_states = [&](int pk) {
-        int pks[4];
+    // the element's 8 threads copy a 512 B block: 16 B chunks t8, t8 + 8, t8 + 16, t8 + 24
+    auto copy_block = [&](double *dst, const double *src) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) pks[j] = __shfl_sync(0xffffffffu, pk, 8 * j);
-        if (lane == 0) {
-            unsigned bytes = 0;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) bytes += state_src(sp, pk_member(pks[j])) == SRC_LAZY ? 1024 : 512;
-            mbar_arrive_expect_tx(bar_st, bytes);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int sl = 4 * warp + j;
-                const size_t off = (size_t)pk_elem(pks[j]) * 64;
-                const int srce = state_src(sp, pk_member(pks[j]));
-                if (srce == SRC_LAZY) {
-                    bulk_g2s(stg[sl][0], Un + off, 512, bar_st);
-                    bulk_g2s(stg[sl][1], K1 + off, 512, bar_st);
-                } else {
-                    bulk_g2s(stg[sl][0], (srce == SRC_UN ? Un : (srce == SRC_BUF ? Ubuf : Uin)) + off, 512, bar_st);
-                }
-            }
-        }
+        for (int r = 0; r < 4; ++r) cp_async16(dst + 2 * (t8 + 8 * r), src + 2 * (t8 + 8 * r));
+    };
+    auto issue_state = [&](int pkx) {
+        const size_t off = (size_t)pk_elem(pkx) * 64;
+        const int srce = state_src(sp, pk_member(pkx));
+        copy_block(stg[le][0], (srce == SRC_UN || srce == SRC_LAZY ? Un : (srce == SRC_BUF ? Ubuf : Uin)) + off);
+        if (srce == SRC_LAZY) copy_block(stg[le][1], K1 + off);
+        cp_async_commit();
     };
     int pk = entry_at(base);
-    issue_states(pk);
+    issue_state(pk);
 
-    for (unsigned ph = 0; base < n_act; base += stride, ph ^= 1u) {
+    for (; base < n_act; base += stride) {
         const bool valid = base + le < n_act;
-        const bool has_next = base + stride < n_act;
+        const bool has_next = base + stride < n_act;     // uniform across the CTA
         const int pk_next = has_next ? entry_at(base + stride) : 0;   // consumed after phase 1
         const int e = pk_elem(pk);
         const int m = pk_member(pk);
@@ -523,7 +502,8 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
         const double hcell = md.hf * (double)(1 << (md.max_level - pk_level(pk)));
 
         // phase 1: nodes q0, q0+1 -> primitives + logs, stored in x-line and y-line layouts
-        mbar_wait(bar_st, ph);
+        cp_async_wait<0>();
+        __syncwarp();
         {
             double2 u[4];
 #pragma unroll
@@ -555,28 +535,16 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
                 }
             }
         }
-        __syncwarp();
-        fence_proxy_async_smem();
-        if (has_next) issue_states(pk_next);   // next group's states (the whole warp has read stg)
+        __syncwarp();   // the warp has read stg: refill it (next group) and stage this group's epilogue operands
         {
-            // this group's epilogue operands: Fs, and U_n / K_1 where the epilogue needs them
             const bool need_un = MODE == MODE_STAGE && sp.stage > 1;
             const bool need_k1 = MODE == MODE_STAGE && sp.stage > 1 && sp.stage < sp.S;
-            int es[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) es[j] = __shfl_sync(0xffffffffu, e, 8 * j);
-            if (lane == 0) {
-                mbar_arrive_expect_tx(bar_ep, 4u * (512u + (need_un ? 512u : 0u) + (need_k1 ? 512u : 0u)));
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int sl = 4 * warp + j;
-                    const size_t off = (size_t)es[j] * 64;
-                    bulk_g2s(epi[sl][2], Fs + off, 512, bar_ep);
-                    if (need_un) bulk_g2s(epi[sl][0], Un + off, 512, bar_ep);
-                    if (need_k1) bulk_g2s(epi[sl][1], K1 + off, 512, bar_ep);
-                }
-            }
+            copy_block(epi[le][2], Fs + eb);
+            if (need_un) copy_block(epi[le][0], Un + eb);
+            if (need_k1) copy_block(epi[le][1], K1 + eb);
+            cp_async_commit();
         }
+        if (has_next) issue_state(pk_next);
 
         // phase 2: 6 symmetric two-point fluxes along this thread's line (x-line j = ln, or y-line i = ln)
         const int lo = o == 0 ? eo + 4 * ln : yo + eo + 4 * ln;   // line start in layout o
@@ -616,7 +584,9 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
                 acc[a][2] = t;
             }
         }
-        mbar_wait(bar_ep, ph);
+        if (has_next) cp_async_wait<1>();    // this group's epilogue operands (the next state may still fly)
+        else cp_async_wait<0>();
+        __syncwarp();
         {
             const double *Fhi = &epi[le][2][(2 * o) * 16 + ln];
             const double *Flo = &epi[le][2][(2 * o + 1) * 16 + ln];

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libperk_b200.so")
+LIB_PATH = os.environ.get("PERK_LIB_PATH") or os.path.join(HERE, "lib", "libperk_b200.so")   # env: A/B builds
 
 EQ = {"advection": 0, "euler": 1, "navier_stokes": 2}
 VOL = {"weak": 0, "fluxdiff": 1}
