@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
     const double dtc = sp.dt * sp.c_stage;
     const int q0 = 2 * t8;
     const int o = t8 >> 2, ln = t8 & 3;
-    const int eo = le * 17;                 // element offset inside a field array
+    const int eo = le * 18;                 // element offset inside a field array (even: 16 B aligned pairs)
     const int yo = 2;                       // y-layout offset
     const int stride = gridDim.x * VOL2D_EPB;
 
@@ -514,9 +514,9 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
                     u[v] = make_double2(fma(dtc, k.x, u[v].x), fma(dtc, k.y, u[v].y));
                 }
             }
+            double fx[2][8], fy[2][8];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const int q = q0 + h, i = q & 3, j = q >> 2;
                 const double r = h ? u[0].y : u[0].x;
                 const double m1 = h ? u[1].y : u[1].x, m2 = h ? u[2].y : u[2].x, E = h ? u[3].y : u[3].x;
                 const double ir = rcp64(r);
@@ -526,13 +526,22 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
                 const double lr = log_pos(r), lb = lr - log_pos(p);   // ln beta = ln rho - ln p
                 const double hv1 = 0.5 * v1, hv2 = 0.5 * v2, hp = 0.5 * p;
                 // x layout: normal = x; y layout: normal = y
-                const double fx[8] = {r, hv1, hv2, hp, lr, beta, lb, p * ir};
-                const double fy[8] = {r, hv2, hv1, hp, lr, beta, lb, p * ir};
+                const double ax[8] = {r, hv1, hv2, hp, lr, beta, lb, p * ir};
+                const double ay[8] = {r, hv2, hv1, hp, lr, beta, lb, p * ir};
 #pragma unroll
-                for (int k = 0; k < NF; ++k) {
-                    sm[k][0][eo + 4 * j + i] = fx[k];
-                    sm[k][1][yo + eo + 4 * i + j] = fy[k];
+                for (int k = 0; k < 8; ++k) {
+                    fx[h][k] = ax[k];
+                    fy[h][k] = ay[k];
                 }
+            }
+            // nodes q0 = (i0, j0), q0 + 1 = (i0 + 1, j0): adjacent in the x layout (one 16 B store),
+            // 4 apart in the y layout
+            const int i0 = q0 & 3, j0 = q0 >> 2;
+#pragma unroll
+            for (int k = 0; k < NF; ++k) {
+                *reinterpret_cast<double2 *>(&sm[k][0][eo + 4 * j0 + i0]) = make_double2(fx[0][k], fx[1][k]);
+                sm[k][1][yo + eo + 4 * i0 + j0] = fy[0][k];
+                sm[k][1][yo + eo + 4 * (i0 + 1) + j0] = fy[1][k];
             }
         }
         __syncwarp();   // the warp has read stg: refill it (next group) and stage this group's epilogue operands
@@ -553,17 +562,29 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
         for (int a = 0; a < 4; ++a)
 #pragma unroll
             for (int v = 0; v < 4; ++v) acc[a][v] = 0.0;
-        const double *L0 = &sm[0][o][lo];   // field k of line node a: L0[k * 2 * VOL2D_LS + a]
+        // the line's 4 nodes x 7 fields, loaded once with 16 B shared loads (the line is contiguous)
+        LinePrim P[4];
+        {
+            const double *L0 = &sm[0][o][lo];   // field k of line node a: L0[k * 2 * VOL2D_LS + a]
+            double fv[7][4];
+#pragma unroll
+            for (int k = 0; k < 7; ++k) {
+                const double2 x01 = *reinterpret_cast<const double2 *>(L0 + k * 2 * VOL2D_LS);
+                const double2 x23 = *reinterpret_cast<const double2 *>(L0 + k * 2 * VOL2D_LS + 2);
+                fv[k][0] = x01.x;
+                fv[k][1] = x01.y;
+                fv[k][2] = x23.x;
+                fv[k][3] = x23.y;
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a) P[a] = LinePrim{fv[0][a], fv[1][a], fv[2][a], fv[3][a], fv[4][a], fv[5][a], fv[6][a]};
+        }
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            const LinePrim A{L0[a], L0[2 * VOL2D_LS + a], L0[4 * VOL2D_LS + a], L0[6 * VOL2D_LS + a],
-                             L0[8 * VOL2D_LS + a], L0[10 * VOL2D_LS + a], L0[12 * VOL2D_LS + a]};
 #pragma unroll
             for (int b = a + 1; b < 4; ++b) {
-                const LinePrim Bp{L0[b], L0[2 * VOL2D_LS + b], L0[4 * VOL2D_LS + b], L0[6 * VOL2D_LS + b],
-                                  L0[8 * VOL2D_LS + b], L0[10 * VOL2D_LS + b], L0[12 * VOL2D_LS + b]};
                 double f[4];
-                flux_ranocha_line(A, Bp, inv_gm1, f);
+                flux_ranocha_line(P[a], P[b], inv_gm1, f);
                 const double dab = cB.Dsplit[a][b], dba = cB.Dsplit[b][a];
 #pragma unroll
                 for (int v = 0; v < 4; ++v) {
@@ -598,9 +619,10 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
         }
         __syncwarp();   // all primitives consumed: reuse sm[v][o] as the accumulator arrays
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int v = 0; v < 4; ++v) sm[v][o][lo + a] = acc[a][v];
+        for (int v = 0; v < 4; ++v) {
+            *reinterpret_cast<double2 *>(&sm[v][o][lo]) = make_double2(acc[0][v], acc[1][v]);
+            *reinterpret_cast<double2 *>(&sm[v][o][lo + 2]) = make_double2(acc[2][v], acc[3][v]);
+        }
         __syncwarp();
 
         // phase 3: K = -(2/h) (x + y contributions), stage epilogue for nodes q0, q0+1
@@ -610,8 +632,9 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
                 const size_t idx = eb + v * 16 + q0;
-                const double s0 = sm[v][0][eo + q0] + sm[v][1][yo + eo + 4 * i0 + j0];
-                const double s1 = sm[v][0][eo + q0 + 1] + sm[v][1][yo + eo + 4 * (i0 + 1) + j0];
+                const double2 sx = *reinterpret_cast<const double2 *>(&sm[v][0][eo + q0]);
+                const double s0 = sx.x + sm[v][1][yo + eo + 4 * i0 + j0];
+                const double s1 = sx.y + sm[v][1][yo + eo + 4 * (i0 + 1) + j0];
                 const double2 K = make_double2(J * s0, J * s1);
                 if (MODE == MODE_RHS) {
                     const bool on = (sp.mask >> m) & 1u;
