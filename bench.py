@@ -10,6 +10,9 @@ Timing: W warm-up steps, then K steps each bracketed by CUDA events on the launc
 an L2 flush (256 MB write) between timed steps; barrier + synchronize on both sides; max over
 ranks.  N > 1 runs independent replicas of the workload (weak scaling; no data-path collective:
 the multi-GPU domain decomposition of SURVEY §8(e) is not built).
+`other_configs` adds the same measurement for BASELINE cfg 4 (dynamic AMR: device re-mesh every
+5 steps inside the timed steps, repartition time reported separately) and cfg 5 (Navier-Stokes,
+BR1) so one run shows every 2D config (--extra none skips them).
 --impl reference times the oracle (oracle/, plain C, 1 host core) on a bounded sample of the same
 workload (full-mesh P-ERK steps, at most ~120 s of CPU work).
 """
@@ -35,14 +38,35 @@ import workloads as W  # noqa: E402
 METRIC = "element-RHS evals/s per P-ERK step (fp64)"
 UNIT = "element-RHS/s"
 
+# Executed fp64 work of the hot kernels per element-RHS: counted with ncu
+# (smsp__sass_thread_inst_executed_op_{dfma,dmul,dadd}_pred_on.sum over all 32 launches of one cfg-3
+# step, profiles/r01_fp64_ops_dram_per_step_v10.csv) and divided by the step's 713,596 element-RHS;
+# flops = 2 DFMA + DMUL + DADD.  Cold-cache DRAM bytes of the same launches (ncu, per launch average)
+# give `traffic`.
+VOL_FLOPS_PER_ELEMENT_RHS = 6399.0        # k_vol2d (volume + lift + Jacobian + stage epilogue)
+SURF_FLOPS_PER_ELEMENT_RHS = 952.0        # k_surf2d (HLL interface / mortar fluxes)
+VOL_DRAM_BYTES_PER_LAUNCH = (1335868416.0 + 67343360.0) / 16   # k_vol2d, cold cache (ncu flushes)
+
 
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             P = json.load(f)
-        return P, "measured"
+        return P, "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
+
+
+def _fp64_peak():
+    """Measured fp64 FMA throughput of this GPU (tools/fp64_peak.cu, 8 independent DFMA chains per
+    thread, 148 x 8 blocks of 256 threads), else derived from unit counts and the max clock."""
+    exe = os.path.join(ROOT, "paper_2403_05144_b200", "lib", "fp64_peak")
+    try:
+        out = subprocess.run([exe], capture_output=True, text=True, timeout=60).stdout
+        d = json.loads(out.strip().splitlines()[-1])
+        return float(d["fp64_tflops"]), "measured: tools/fp64_peak.cu DFMA microbenchmark on this GPU"
+    except Exception:
+        return 148 * 64 * 2 * 1.965e9 / 1e12, "derived: 148 SM x 64 DFMA/clk x 2 x 1965 MHz"
 
 
 class ClockSampler:
@@ -102,7 +126,7 @@ def _dist():
     return ws, rank, local
 
 
-def _volume_bytes_per_step(count_el, S, first):
+def _volume_bytes_per_step(count_el, S):
     """Algorithmic HBM bytes of the volume/stage kernel per step: per element-stage
     8 B x 64 doubles for each state-sized vector it must touch:
       stage 1           : read U_n, Fs; write K_1                      -> 3 x 512 B
@@ -121,14 +145,98 @@ def _volume_bytes_per_step(count_el, S, first):
     return tot
 
 
-FLOPS_PER_ELEMENT_RHS = None  # filled from DESIGN.md §5 model below
+class _Timer:
+    """CUDA-event timing of P-ERK steps on the launching stream, L2 flushed between timed steps."""
+
+    def __init__(self, torch, dev, ws, dist):
+        self.torch, self.ws, self.dist = torch, ws, dist
+        self.flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+        self.stream = torch.cuda.current_stream()
+
+    def steps(self, run_step, K, Wm):
+        torch = self.torch
+        for s in range(Wm):
+            run_step(-1 - s)
+        torch.cuda.synchronize()
+        if self.ws > 1:
+            self.dist.barrier()
+        torch.cuda.synchronize()
+        evs = []
+        for k in range(K):
+            self.flush.fill_(1.0)                      # evict L2 between timed steps
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(self.stream)
+            run_step(k)
+            b.record(self.stream)
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        if self.ws > 1:
+            self.dist.barrier()
+        torch.cuda.synchronize()
+        return [a.elapsed_time(b) for a, b in evs]
 
 
-def flops_per_element_rhs():
-    """Algorithmic fp64 flops of one 2D element RHS (DESIGN.md §5 count, FMA = 2 flops):
-    48 two-point Ranocha fluxes x 96 + 16 nodes x 70 (primitives, 2 logs) + 64 x 6 (lift, Jacobian,
-    epilogue)."""
-    return 48 * 96 + 16 * 70 + 64 * 6
+def _max_over_ranks(torch, dist, ws, dev, x):
+    if ws == 1:
+        return x
+    t = torch.tensor([x], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def measure_config(cfg, K, Wm, timer, torch, dist, ws, dev, with_single=True):
+    """Device time per P-ERK step of BASELINE config `cfg` (and of the single-rate S-stage P-ERK on
+    the same mesh); cfg 4 re-meshes on the device every 5 steps inside the timed steps."""
+    from paper_2403_05144_b200 import Perk
+    w = W.make(cfg)
+    perk = Perk(w.problem, w.level_map, w.S, w.E)
+    U = perk.initial_state(w.ic)
+    res = {"workload": w.name, "cells": perk.n_cells, "S": w.S, "E": w.E, "dt": w.dt}
+    remesh = []
+    if w.remesh_every:
+        # level maps of the re-meshes inside the measured window, uploaded before the timed region
+        nmaps = (K + Wm) // w.remesh_every + 1
+        maps = [torch.from_numpy(np.ascontiguousarray(w.level_map_seq(k))).to(dev) for k in range(1, nmaps + 1)]
+        state = {"n": 0, "k": 0}
+        rp_ev = []
+
+        def run_step(_):
+            perk.step(U, w.dt)
+            state["n"] += 1
+            if state["n"] % w.remesh_every == 0 and state["k"] < len(maps):
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(timer.stream)
+                perk.repartition(maps[state["k"]], U)
+                b.record(timer.stream)
+                rp_ev.append((a, b))
+                state["k"] += 1
+        times = timer.steps(run_step, K, Wm)
+        torch.cuda.synchronize()
+        perk.sync()
+        remesh = [a.elapsed_time(b) for a, b in rp_ev]
+        res["remesh_every"] = w.remesh_every
+        res["repartitions_in_run"] = len(remesh)
+        res["repartition_ms_mean"] = round(float(np.mean(remesh)), 5) if remesh else None
+        ev, st = perk.counters()
+        elem_rhs_per_step = ev / max(st, 1)
+    else:
+        times = timer.steps(lambda k: perk.step(U, w.dt), K, Wm)
+        elem_rhs_per_step = int(sum(int(x) for x in perk.count_active("elements")))
+    ms = _max_over_ranks(torch, dist, ws, dev, float(np.mean(times)))
+    res.update(ms_per_step=round(ms, 5), element_rhs_per_step=round(float(elem_rhs_per_step), 1),
+               value=round(ws * elem_rhs_per_step / (ms * 1e-3), 1), n_cells_now=perk.n_cells)
+    if with_single and not w.remesh_every:
+        single = Perk(w.problem, w.level_map, w.S, [w.S])
+        Us = single.initial_state(w.ic)
+        ms_s = _max_over_ranks(torch, dist, ws, dev,
+                               float(np.mean(timer.steps(lambda k: single.step(Us, w.dt), max(3, K // 2), Wm))))
+        single.close()
+        res["single_rate_ms_per_step"] = round(ms_s, 5)
+        res["multirate_speedup"] = round(ms_s / ms, 4)
+        res["ideal_multirate_speedup"] = round(w.S * perk.n_cells / elem_rhs_per_step, 4)
+    return perk, U, w, res
 
 
 def run_ours(args):
@@ -139,90 +247,65 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if ws > 1:
         dist.init_process_group("nccl")
-    from paper_2403_05144_b200 import Perk
-
-    w = W.make(args.config)
     dev = torch.device("cuda", local)
-    perk = Perk(w.problem, w.level_map, w.S, w.E)
-    U = perk.initial_state(w.ic)
-    U0 = U.clone()
-    n = perk.n_cells
-    count_el = [int(x) for x in perk.count_active("elements")]
-    elem_rhs_per_step = sum(count_el)
-    npe = 4 ** w.problem["dim"]
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    stream = torch.cuda.current_stream()
+    timer = _Timer(torch, dev, ws, dist)
+    fp64_peak, fp64_src = _fp64_peak()
 
-    def timed_steps(p, Ux, K, Wm):
-        for _ in range(Wm):
-            p.step(Ux, w.dt)
-        torch.cuda.synchronize()
-        if ws > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        evs = []
-        for _ in range(K):
-            flush.fill_(1.0)                      # evict L2 between timed steps
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            p.step(Ux, w.dt)
-            b.record(stream)
-            evs.append((a, b))
-        torch.cuda.synchronize()
-        if ws > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        return [a.elapsed_time(b) for a, b in evs]
-
+    from paper_2403_05144_b200 import Perk  # noqa: F401  (fails loudly without the CUDA library)
     with ClockSampler(local) as clk:
+        w0 = W.make(args.config)
+        # clock soak: untimed steps of the headline workload under load (>= 0.5 s)
+        from paper_2403_05144_b200 import Perk as _P
+        soak = _P(w0.problem, w0.level_map, w0.S, w0.E)
+        Usoak = soak.initial_state(w0.ic)
         t_soak = time.perf_counter()
-        while time.perf_counter() - t_soak < 0.5:          # clock soak: untimed steps under load
+        while time.perf_counter() - t_soak < 0.5:
             for _ in range(50):
-                perk.step(U, w.dt)
+                soak.step(Usoak, w0.dt)
             torch.cuda.synchronize()
-        times = timed_steps(perk, U, args.steps, args.warmup)
-    ms = float(np.mean(times))
-    if ws > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    value = ws * elem_rhs_per_step / (ms * 1e-3)
-
-    # single-rate S-stage P-ERK on the same mesh and dt (multirate speedup, BASELINE north star)
-    single = Perk(w.problem, w.level_map, w.S, [w.S])
-    Us = single.initial_state(w.ic)
-    ms_single = float(np.mean(timed_steps(single, Us, max(3, args.steps // 2), args.warmup)))
-    single.close()
+        soak.close()
+        del Usoak
+        perk, U, w, res = measure_config(args.config, args.steps, args.warmup, timer, torch, dist, ws, dev)
+    n = perk.n_cells
+    npe = 4 ** w.problem["dim"]
+    ms = res["ms_per_step"]
+    value = res["value"]
+    elem_rhs_per_step = res["element_rhs_per_step"]
+    count_el = [int(x) for x in perk.count_active("elements")]
 
     # per-kernel device time of the same step: CUDA events around every launch on the launch stream
     prof_steps = 3
-    ms_k = np.zeros(4)
-    nl = np.zeros(4, dtype=np.int64)
-    Up = U0.clone()
+    ms_k = np.zeros(6)
+    U0 = perk.initial_state(w.ic)
     for _ in range(prof_steps):
-        m_, l_ = perk.profile_step(Up, w.dt)
+        m_, _l = perk.profile_step(U0, w.dt)
         ms_k += np.array(m_)
-        nl += np.array(l_)
-    vol_ms_per_step = ms_k[1] / prof_steps
-    surf_ms_per_step = ms_k[0] / prof_steps
-    vol_bytes = _volume_bytes_per_step(count_el, w.S, None)
+    ms_k /= prof_steps
+    kern = {"surface": round(ms_k[0], 5), "volume_stage": round(ms_k[1], 5)}
+    if w.problem["equation"] == "navier_stokes":
+        kern.update(br1_gradient_traces=round(ms_k[4], 5), br1_gradients=round(ms_k[5], 5))
+    vol_ms = ms_k[1]
     peaks, src = _peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
-    achieved_gbs = vol_bytes / (vol_ms_per_step * 1e-3) / 1e9
-    clk_max = float(peaks.get("sm_max_mhz", 1965.0))
-    fp64_peak = 148 * 64 * 2 * clk_max * 1e6 / 1e12   # TFLOP/s: 148 SMs x 64 FP64 FMA/clk x 2
-    achieved_tf = elem_rhs_per_step * flops_per_element_rhs() / (vol_ms_per_step * 1e-3) / 1e12
-    roof_hbm = {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(achieved_gbs / hbm, 4), "traffic": args.traffic,
-                "kernel": "k_vol2d<MODE_STAGE> (volume + surface lift + Jacobian + stage epilogue)",
-                "peak_source": src, "bytes_per_step": vol_bytes}
-    roof_alu = {"bound": "alu", "achieved": round(achieved_tf, 3), "peak": round(fp64_peak, 2), "unit": "TFLOP/s",
-                "frac": round(achieved_tf / fp64_peak, 4), "traffic": args.traffic,
-                "kernel": roof_hbm["kernel"], "peak_source": "derived: 148 SM x 64 DFMA/clk x 2 x sm_max_mhz",
-                "flops_per_element_rhs": flops_per_element_rhs()}
-    roof = roof_alu if roof_alu["frac"] >= roof_hbm["frac"] else roof_hbm
-    other = roof_hbm if roof is roof_alu else roof_alu
+    line_roof = None
+    if w.problem["dim"] == 2 and w.problem["equation"] == "euler":
+        vol_bytes = _volume_bytes_per_step(count_el, w.S)
+        launches = w.S
+        achieved_gbs = vol_bytes / (vol_ms * 1e-3) / 1e9
+        achieved_tf = elem_rhs_per_step * VOL_FLOPS_PER_ELEMENT_RHS / (vol_ms * 1e-3) / 1e12
+        kname = "k_vol2d<MODE_STAGE> (volume + surface lift + Jacobian + stage epilogue)"
+        roof_hbm = {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": hbm, "unit": "GB/s",
+                    "frac": round(achieved_gbs / hbm, 4), "traffic": round(VOL_DRAM_BYTES_PER_LAUNCH),
+                    "kernel": kname, "peak_source": src,
+                    "algorithmic_bytes_per_launch": round(vol_bytes / launches),
+                    "kernel_ms_per_launch": round(vol_ms / launches, 5),
+                    "traffic_note": "ncu dram bytes per launch, cold cache (ncu flushes caches between replays)"}
+        roof_alu = {"bound": "alu", "achieved": round(achieved_tf, 3), "peak": round(fp64_peak, 2),
+                    "unit": "TFLOP/s", "frac": round(achieved_tf / fp64_peak, 4), "traffic": roof_hbm["traffic"],
+                    "kernel": kname, "peak_source": fp64_src,
+                    "flops_per_element_rhs": VOL_FLOPS_PER_ELEMENT_RHS}
+        roof = roof_alu if roof_alu["frac"] >= roof_hbm["frac"] else roof_hbm
+        line_roof = (roof, roof_hbm if roof is roof_alu else roof_alu)
 
     # end to end through the public API with HOST buffers (pinned), copies inside the timed region
     Uh = U0[:n].cpu().pin_memory()
@@ -235,17 +318,31 @@ def run_ours(args):
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     e2e_val = ws * elem_rhs_per_step / e2e_s
     h2d = int(n * w.nv * npe * 8)
+    launches = perk.launches_per_step()
+    perk.close()
+
+    others = {}
+    if args.extra != "none":
+        for c in [int(x) for x in args.extra.split(",") if x and int(x) != args.config]:
+            try:
+                p2, _U, _w, r2 = measure_config(c, max(5, min(args.steps, 20)), args.warmup, timer, torch, dist,
+                                                 ws, dev)
+                r2["dof_stage_updates_per_s"] = round(r2["value"] * 4 ** _w.problem["dim"], 1)
+                r2["gpu_launches_per_step"] = p2.launches_per_step()
+                p2.close()
+                others[f"cfg{c}"] = r2
+            except Exception as ex:       # report, do not hide: the line records the failure
+                others[f"cfg{c}"] = {"error": repr(ex)[:200]}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(w, budget_s=args.cpu_budget)
 
     if rank == 0:
-        launches = perk.launches_per_step()
         clocks = clk.summary()
         line = {
-            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "weak",
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator workloads/, DESIGN.md §3)",
             "config": {"workload": w.name, "cells": n, "nodes": n * npe, "S": w.S, "E": w.E,
                        "element_rhs_per_step": elem_rhs_per_step, "dt": w.dt,
@@ -253,19 +350,21 @@ def run_ours(args):
                        "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
             "dof_stage_updates_per_s": round(value * npe, 1),
             "scalar_dof_stage_updates_per_s": round(value * npe * w.nv, 1),
-            "single_rate_ms_per_step": round(ms_single, 5),
-            "multirate_speedup": round(ms_single / ms, 4),
-            "ideal_multirate_speedup": round(w.S * n / elem_rhs_per_step, 4),
-            "kernel_ms_per_step": {"surface": round(surf_ms_per_step, 5), "volume_stage": round(vol_ms_per_step, 5)},
-            "roofline": roof, "roofline_other": other,
+            "single_rate_ms_per_step": res.get("single_rate_ms_per_step"),
+            "multirate_speedup": res.get("multirate_speedup"),
+            "ideal_multirate_speedup": res.get("ideal_multirate_speedup"),
+            "kernel_ms_per_step": kern,
             "e2e": {"value": round(e2e_val, 1), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": h2d},
             "gpu_launches": launches * args.steps,
             "clocks": clocks,
         }
+        if line_roof:
+            line["roofline"], line["roofline_other"] = line_roof
+        if others:
+            line["other_configs"] = others
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
-    perk.close()
     if ws > 1:
         dist.destroy_process_group()
 
@@ -342,12 +441,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--extra", default="4,5",
+                    help="other BASELINE configs measured into other_configs (comma list, or 'none')")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true",
                     help="build the workload and run warmup+steps P-ERK steps only (short ncu target)")
-    ap.add_argument("--traffic", type=float, default=None,
-                    help="dram bytes per step of the dominant kernel from an ncu --set full capture")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.profile_only:

@@ -18,9 +18,21 @@ def sources():
     return [os.path.join(d, f) for f in sorted(os.listdir(d))] + [os.path.join(ROOT, "include", "perk.h")]
 
 
+TOOLS = [("fp64_peak.cu", "fp64_peak")]   # measured fp64 FMA peak (bench.py roofline denominator)
+
+
+def build_tools(force: bool = False) -> None:
+    for src, exe in TOOLS:
+        s = os.path.join(ROOT, "tools", src)
+        o = os.path.join(HERE, "lib", exe)
+        if force or not os.path.exists(o) or os.path.getmtime(o) < os.path.getmtime(s):
+            subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-o", o, s])
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     newest = max(os.path.getmtime(s) for s in sources())
+    build_tools(force)
     if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= newest:
         return OUT
     cmd = [NVCC] + FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", OUT, SRC]
