@@ -178,11 +178,17 @@ class _Timer:
 
 
 def _max_over_ranks(torch, dist, ws, dev, x):
+    """max over ranks of a per-rank device time (the job takes as long as its slowest replica)"""
     if ws == 1:
         return x
     t = torch.tensor([x], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def replica_value(ws, elem_rhs_per_step, ms_max):
+    """whole-job throughput of ws independent replicas: all units processed / the slowest rank's time"""
+    return ws * elem_rhs_per_step / (ms_max * 1e-3)
 
 
 def measure_config(cfg, K, Wm, timer, torch, dist, ws, dev, with_single=True):
@@ -226,7 +232,7 @@ def measure_config(cfg, K, Wm, timer, torch, dist, ws, dev, with_single=True):
         elem_rhs_per_step = int(sum(int(x) for x in perk.count_active("elements")))
     ms = _max_over_ranks(torch, dist, ws, dev, float(np.mean(times)))
     res.update(ms_per_step=round(ms, 5), element_rhs_per_step=round(float(elem_rhs_per_step), 1),
-               value=round(ws * elem_rhs_per_step / (ms * 1e-3), 1), n_cells_now=perk.n_cells)
+               value=round(replica_value(ws, elem_rhs_per_step, ms), 1), n_cells_now=perk.n_cells)
     if with_single and not w.remesh_every:
         single = Perk(w.problem, w.level_map, w.S, [w.S])
         Us = single.initial_state(w.ic)
