@@ -19,6 +19,7 @@ __global__ void __launch_bounds__(256, 3) k_gsurf2d(MeshDev md, StageParams sp, 
                                                 const double *__restrict__ Ubuf, const double *__restrict__ K1,
                                                 const double *__restrict__ Uin, double *__restrict__ Gs)
 {
+    pdl_wait();
     int nif, nmo;
     if (MODE == MODE_STAGE) {
         nif = md.count_active[EXT_OFF + KIND_IF * MAXS + sp.stage - 1];
@@ -105,6 +106,7 @@ __global__ void __launch_bounds__(128) k_grad2d(MeshDev md, StageParams sp, cons
 {
     // field slots follow k_vol2d's numbering (F_V1, F_V2, F_T; gradients in 4..6)
     __shared__ double sm[8][2][GRAD2D_LS];
+    pdl_wait();
     const int t8 = threadIdx.x & 7, le = threadIdx.x >> 3;
     const int n_act = MODE == MODE_STAGE ? md.count_active[EXT_OFF + KIND_EL * MAXS + sp.stage - 1] : md.n[0];
     const double gm1 = md.gamma - 1.0;

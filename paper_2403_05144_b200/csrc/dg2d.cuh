@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(256, 3) k_surf2d(MeshDev md, StageParams sp, c
     const double g = md.gamma;
     const int lane = threadIdx.x & 31;
     const unsigned gmask = 0xFu << (lane & ~3);
+    pdl_wait();
     for (int gt = blockIdx.x * blockDim.x + threadIdx.x; gt < total; gt += gridDim.x * blockDim.x) {
         const int item = gt >> 2, k = gt & 3;
         if (item < nif) {
@@ -460,13 +461,17 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
     const int yo = 2;                       // y-layout offset
     const int stride = gridDim.x * VOL2D_EPB;
 
+    int base = blockIdx.x * VOL2D_EPB;
+    // prologue before the dependency wait: indices only (lists are rebuilt by the mesh pipeline,
+    // which completed before the step started)
+    const int pk0 = base < n_act ? (MODE == MODE_STAGE ? md.elpk[base + le < n_act ? base + le : base] : 0) : 0;
+    pdl_wait();
     if (MODE == MODE_STAGE && sp.stage == sp.S && blockIdx.x == 0 && threadIdx.x == 0) {
         unsigned long long tot = 0;
         for (int i = 0; i < sp.S; ++i) tot += (unsigned long long)md.count_active[KIND_EL * MAXS + i];
         atomicAdd(md.evals, tot);
         atomicAdd(md.evals + 1, 1ull);
     }
-    int base = blockIdx.x * VOL2D_EPB;
     if (base >= n_act) return;
 
     // packed entry (element | member | level) of this thread's slot in the group starting at b
@@ -488,7 +493,7 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
         if (srce == SRC_LAZY) copy_block(stg[le][1], K1 + off);
         cp_async_commit();
     };
-    int pk = entry_at(base);
+    int pk = MODE == MODE_STAGE ? pk0 : entry_at(base);
     issue_state(pk);
 
     for (; base < n_act; base += stride) {

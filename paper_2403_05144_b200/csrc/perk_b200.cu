@@ -158,6 +158,23 @@ static void partition(perk_ctx *c, cudaStream_t s, KeyFn kf, const int *n_ptr, i
 
 __global__ void k_set_count(int *dst, const int *seg, int idx) { *dst = seg[idx + 1] - seg[idx]; }
 
+// launch with programmatic stream serialisation (PDL): the kernels call pdl_trigger()/pdl_wait()
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*k)(KArgs...), int grid, int block, size_t smem, cudaStream_t s, Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 static int blocks_for(long long n, int t)
 {
     long long b = (n + t - 1) / t;
@@ -221,14 +238,14 @@ static void launch_surface(perk_ctx *c, cudaStream_t s, const StageParams &sp, c
     if (c->prob.dim == 2) {
         if (c->ns) {
             if (sp.mode == MODE_STAGE)
-                k_surf2d<MODE_STAGE, true><<<c->surf_blocks, 256, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs, c->Vt);
+                launch_pdl(k_surf2d<MODE_STAGE, true>, c->surf_blocks, 256, 0, s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs, c->Vt);
             else
-                k_surf2d<MODE_RHS, true><<<c->surf_blocks, 256, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs, c->Vt);
+                launch_pdl(k_surf2d<MODE_RHS, true>, c->surf_blocks, 256, 0, s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs, c->Vt);
         } else {
             if (sp.mode == MODE_STAGE)
-                k_surf2d<MODE_STAGE, false><<<c->surf_blocks, 256, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs, nullptr);
+                launch_pdl(k_surf2d<MODE_STAGE, false>, c->surf_blocks, 256, 0, s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs, nullptr);
             else
-                k_surf2d<MODE_RHS, false><<<c->surf_blocks, 256, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs, nullptr);
+                launch_pdl(k_surf2d<MODE_RHS, false>, c->surf_blocks, 256, 0, s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs, nullptr);
         }
     } else if (c->nv == 1) {
         if (sp.mode == MODE_STAGE)
@@ -249,14 +266,14 @@ static void launch_volume(perk_ctx *c, cudaStream_t s, const StageParams &sp, do
     if (c->prob.dim == 2) {
         if (c->ns) {
             if (sp.mode == MODE_STAGE)
-                k_vol2d<MODE_STAGE, true><<<c->vol_blocks, 128, vol2d_smem_bytes(true), s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Gs);
+                launch_pdl(k_vol2d<MODE_STAGE, true>, c->vol_blocks, 128, vol2d_smem_bytes(true), s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Gs);
             else
-                k_vol2d<MODE_RHS, true><<<c->vol_blocks, 128, vol2d_smem_bytes(true), s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Gs);
+                launch_pdl(k_vol2d<MODE_RHS, true>, c->vol_blocks, 128, vol2d_smem_bytes(true), s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Gs);
         } else {
             if (sp.mode == MODE_STAGE)
-                k_vol2d<MODE_STAGE, false><<<c->vol_blocks, 128, vol2d_smem_bytes(false), s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, nullptr);
+                launch_pdl(k_vol2d<MODE_STAGE, false>, c->vol_blocks, 128, vol2d_smem_bytes(false), s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, nullptr);
             else
-                k_vol2d<MODE_RHS, false><<<c->vol_blocks, 128, vol2d_smem_bytes(false), s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, nullptr);
+                launch_pdl(k_vol2d<MODE_RHS, false>, c->vol_blocks, 128, vol2d_smem_bytes(false), s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, nullptr);
         }
     } else if (c->nv == 1) {
         if (sp.mode == MODE_STAGE)
@@ -277,14 +294,14 @@ static void launch_br1(perk_ctx *c, cudaStream_t s, const StageParams &sp, const
     const MeshDev &md = c->md;
     prof_mark(p, s, 4);
     if (sp.mode == MODE_STAGE)
-        k_gsurf2d<MODE_STAGE><<<c->surf_blocks, 256, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs);
+        launch_pdl(k_gsurf2d<MODE_STAGE>, c->surf_blocks, 256, 0, s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs);
     else
-        k_gsurf2d<MODE_RHS><<<c->surf_blocks, 256, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs);
+        launch_pdl(k_gsurf2d<MODE_RHS>, c->surf_blocks, 256, 0, s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs);
     prof_mark(p, s, 5);
     if (sp.mode == MODE_STAGE)
-        k_grad2d<MODE_STAGE><<<c->grad_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs, c->Vt);
+        launch_pdl(k_grad2d<MODE_STAGE>, c->grad_blocks, 128, 0, s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs, c->Vt);
     else
-        k_grad2d<MODE_RHS><<<c->grad_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs, c->Vt);
+        launch_pdl(k_grad2d<MODE_RHS>, c->grad_blocks, 128, 0, s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs, c->Vt);
 }
 
 static void launch_step(perk_ctx *c, cudaStream_t s, double *U, double dt, Prof *p)
@@ -464,7 +481,9 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
         int occg = 0;
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occg, k_grad2d<MODE_STAGE>, 128, 0));
         c->grad_blocks = std::min(want, SM_COUNT_B200 * std::max(occg, 1));
-        c->surf_blocks = std::min(blocks_for(4ll * c->cap_faces, 256), SM_COUNT_B200 * 8);
+        int occf = 0;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occf, k_surf2d<MODE_STAGE, false>, 256, 0));
+        c->surf_blocks = std::min(blocks_for(4ll * c->cap_faces, 256), SM_COUNT_B200 * std::max(occf, 1));
     } else {
         c->vol_blocks = std::min(blocks_for(c->cap, 128), SM_COUNT_B200 * 8);
         c->surf_blocks = std::min(blocks_for(c->cap_faces, 256), SM_COUNT_B200 * 8);
