@@ -158,7 +158,7 @@ static void partition(perk_ctx *c, cudaStream_t s, KeyFn kf, const int *n_ptr, i
 
 __global__ void k_set_count(int *dst, const int *seg, int idx) { *dst = seg[idx + 1] - seg[idx]; }
 
-// launch with programmatic stream serialisation (PDL): the kernels call pdl_trigger()/pdl_wait()
+// launch with programmatic stream serialisation (PDL): the kernels call pdl_wait() (common.cuh)
 template <typename... KArgs, typename... Args>
 static void launch_pdl(void (*k)(KArgs...), int grid, int block, size_t smem, cudaStream_t s, Args... args)
 {
