@@ -1,0 +1,41 @@
+"""Small end-to-end run of every code path for compute-sanitizer (memcheck / racecheck / initcheck):
+cfg 1, 2 (1D), cfg 3 structure (2D Euler, mortars), a non-periodic 2D variant (boundary faces),
+cfg 5 structure (BR1), rhs_eval with masks, and a cfg-4 structure with two device re-meshes."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import workloads as W  # noqa: E402
+from paper_2403_05144_b200 import Perk  # noqa: E402
+
+
+def run(w, steps, problem=None, remesh=False):
+    p = Perk(problem or w.problem, w.level_map, w.S, w.E, max_cells=4 * W.configs.count_leaves(w))
+    U = p.initial_state(w.ic)
+    p.step(U, w.dt, steps)
+    for mask in (1, (1 << len(w.E)) - 1):
+        p.rhs(U, mask)
+    if remesh:
+        for k in (1, 2):
+            p.repartition(w.level_map_seq(k), U)
+            p.step(U, w.dt, 2)
+    torch.cuda.synchronize()
+    p.sync()
+    assert torch.isfinite(U[: p.n_cells]).all()
+    p.close()
+
+
+run(W.make(1), 3)
+run(W.make(2, n_base=32, w1=8, w2=4), 3)
+w3 = W.make(3, n_base=8)
+run(w3, 2)
+run(w3, 2, problem=dict(w3.problem, periodic=(0, 1), bc_state=(1.0, 1.0, 1.0, 1.0 / 0.4 + 1.0)))
+run(W.make(5, n_base=8), 2)
+w4 = W.make(4, n_base=16, max_level=3, widths=(0.3, 0.15, 0.06))
+w4.S, w4.E = 16, [4, 6, 10, 16]
+run(w4, 2, remesh=True)
+print("sanitize run ok")
