@@ -308,3 +308,49 @@ def test_ns_nonperiodic_rejected():
     with pytest.raises(PerkError) as ei:
         Perk(p, w.level_map, w.S, w.E)
     assert ei.value.code == -6
+
+
+def test_cfg4_full_size_remesh():
+    """BASELINE cfg 4 (64^2 base, Lmax 4, {4,6,10,16,28}, ~77.7k cells) in the bench launch
+    configuration: 5 steps, one device re-mesh (lists bit-exact, transfer), 5 more steps."""
+    w = W.make(4)
+    fam = T.family(w.S, w.E, w.alpha_rule)
+    ora, gpu = build_pair(w)
+    Uo = ora.initial_state(w.ic)
+    Ug = gpu.initial_state(w.ic)
+    ora.step(Uo, w.dt, 5)
+    gpu.step(Ug, w.dt, 5)
+    lm = w.level_map_seq(1)
+    ora_new = O.OracleMesh(w.problem, lm, fam)
+    Uo = O.transfer(ora, ora_new, Uo)
+    ora = ora_new
+    gpu.repartition(lm, Ug)
+    gpu.sync()
+    compare_mesh(ora, gpu)
+    assert rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo).max() <= TOL
+    ora.step(Uo, w.dt, 5)
+    gpu.step(Ug, w.dt, 5)
+    torch.cuda.synchronize()
+    assert rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo).max() <= TOL
+
+
+def test_cfg4_long_run_many_remeshes():
+    """cfg-4 structure on a 16^2 base (Lmax 3): 100 steps with a device re-mesh every 5 steps (20
+    re-meshes), the cadence of BASELINE cfg 4."""
+    w = W.make(4, n_base=16, max_level=3, widths=(0.3, 0.15, 0.06))
+    w.S, w.E = 16, [4, 6, 10, 16]
+    fam = T.family(w.S, w.E, "taylor")
+    ora, gpu = build_pair(w, max_cells=4 * W.configs.count_leaves(w))
+    Uo = ora.initial_state(w.ic)
+    Ug = gpu.initial_state(w.ic)
+    for k in range(1, 21):
+        ora.step(Uo, w.dt, 5)
+        gpu.step(Ug, w.dt, 5)
+        lm = w.level_map_seq(k)
+        ora_new = O.OracleMesh(w.problem, lm, fam)
+        Uo = O.transfer(ora, ora_new, Uo)
+        ora = ora_new
+        gpu.repartition(lm, Ug)
+    gpu.sync()
+    compare_mesh(ora, gpu)
+    assert rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo).max() <= TOL
