@@ -96,62 +96,106 @@ __global__ void __launch_bounds__(256, 3) k_gsurf2d(MeshDev md, StageParams sp, 
 
 // 8 threads per element as in k_vol2d: gradients along the x-lines and y-lines, exchanged through
 // shared memory, then the normal viscous flux at the two end nodes of every line = the face nodes.
+// Persistent CTAs of 16 elements; the element's stage state and its 48 central traces are staged
+// with cp.async one group ahead (commit groups as in k_vol2d).
 constexpr int GRAD2D_LS = VOL2D_LS;
+constexpr int G_V1 = 0, G_V2 = 1, G_T = 2, G_Q = 3;     // shared fields: v1, v2, T, gradients (3)
+__host__ __device__ constexpr size_t grad2d_smem_bytes()
+{
+    return sizeof(double) * ((size_t)6 * 2 * GRAD2D_LS + VOL2D_EPB * 2 * 64 + VOL2D_EPB * 4 * GV * NP);
+}
 
 template <int MODE>
-__global__ void __launch_bounds__(128) k_grad2d(MeshDev md, StageParams sp, const double *__restrict__ Un,
-                                                const double *__restrict__ Ubuf, const double *__restrict__ K1,
-                                                const double *__restrict__ Uin, const double *__restrict__ Gs,
-                                                double *__restrict__ Vt)
+__global__ void __launch_bounds__(128, 4) k_grad2d(MeshDev md, StageParams sp, const double *__restrict__ Un,
+                                                   const double *__restrict__ Ubuf, const double *__restrict__ K1,
+                                                   const double *__restrict__ Uin, const double *__restrict__ Gs,
+                                                   double *__restrict__ Vt)
 {
-    // field slots follow k_vol2d's numbering (F_V1, F_V2, F_T; gradients in 4..6)
-    __shared__ double sm[8][2][GRAD2D_LS];
-    pdl_wait();
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double (*sm)[2][GRAD2D_LS] = reinterpret_cast<double (*)[2][GRAD2D_LS]>(smraw);
+    double (*stg)[2][64] = reinterpret_cast<double (*)[2][64]>(smraw + sizeof(double) * 6 * 2 * GRAD2D_LS);
+    double (*gst)[4 * GV * NP] = reinterpret_cast<double (*)[4 * GV * NP]>(reinterpret_cast<unsigned char *>(stg) +
+                                                                           sizeof(double) * VOL2D_EPB * 2 * 64);
     const int t8 = threadIdx.x & 7, le = threadIdx.x >> 3;
     const int n_act = MODE == MODE_STAGE ? md.count_active[EXT_OFF + KIND_EL * MAXS + sp.stage - 1] : md.n[0];
     const double gm1 = md.gamma - 1.0;
-    const StateBufs sb{Un, Ubuf, K1, Uin};
     const double dtc = sp.dt * sp.c_stage;
     const int q0 = 2 * t8;
     const int o = t8 >> 2, ln = t8 & 3;
-    const int eo = le * 17, yo = 2;
-    for (int base = blockIdx.x * VOL2D_EPB; base < n_act; base += gridDim.x * VOL2D_EPB) {
-        const int t = base + le;
-        const bool valid = t < n_act;
-        const int tt = valid ? t : base;
-        const int e = MODE == MODE_STAGE ? md.list[KIND_EL][tt] : tt;
-        const int src = state_src(sp, md.mem[e]);
-        const size_t eb = (size_t)e * 64;
-        const double hcell = md.hf * (double)(1 << (md.max_level - md.lev[e]));
+    const int eo = le * 18, yo = 2;
+    const int stride = gridDim.x * VOL2D_EPB;
+    int base = blockIdx.x * VOL2D_EPB;
+    auto entry_at = [&](int b) {
+        const int t = b + le;
+        const int tt = t < n_act ? t : b;
+        if (MODE == MODE_STAGE) return md.elpk[tt];
+        return tt | ((int)md.mem[tt] << PK_EBITS) | ((int)md.lev[tt] << (PK_EBITS + 3));
+    };
+    auto copy_chunks = [&](double *dst, const double *src, int nchunks) {   // 16 B chunks over 8 threads
+        for (int c = t8; c < nchunks; c += 8) cp_async16(dst + 2 * c, src + 2 * c);
+    };
+    auto issue_state = [&](int pkx) {
+        const size_t off = (size_t)pk_elem(pkx) * 64;
+        const int srce = state_src(sp, pk_member(pkx));
+        copy_chunks(stg[le][0], (srce == SRC_UN || srce == SRC_LAZY ? Un : (srce == SRC_BUF ? Ubuf : Uin)) + off, 32);
+        if (srce == SRC_LAZY) copy_chunks(stg[le][1], K1 + off, 32);
+    };
+    auto issue_gs = [&](int pkx) { copy_chunks(gst[le], Gs + (size_t)pk_elem(pkx) * 4 * GV * NP, 4 * GV * NP / 2); };
+    const int pk0 = base < n_act ? entry_at(base) : 0;
+    pdl_wait();
+    if (base >= n_act) return;
+    int pk = pk0;
+    issue_state(pk);
+    issue_gs(pk);
+    cp_async_commit();
+    for (; base < n_act; base += stride) {
+        const bool valid = base + le < n_act;
+        const bool has_next = base + stride < n_act;
+        const int pk_next = has_next ? entry_at(base + stride) : 0;
+        const int e = pk_elem(pk);
+        const int src = state_src(sp, pk_member(pk));
+        const double hcell = md.hf * (double)(1 << (md.max_level - pk_level(pk)));
+        cp_async_wait<0>();
+        __syncwarp();
         {
             double2 u[4];
 #pragma unroll
-            for (int v = 0; v < 4; ++v) u[v] = load_state2(sb, src, dtc, eb + v * 16 + q0);
+            for (int v = 0; v < 4; ++v) {
+                u[v] = *reinterpret_cast<const double2 *>(&stg[le][0][v * 16 + q0]);
+                if (src == SRC_LAZY) {
+                    const double2 k = *reinterpret_cast<const double2 *>(&stg[le][1][v * 16 + q0]);
+                    u[v] = make_double2(fma(dtc, k.x, u[v].x), fma(dtc, k.y, u[v].y));
+                }
+            }
+            const int i0 = q0 & 3, j0 = q0 >> 2;
+            double w[2][GV];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const int q = q0 + h, i = q & 3, j = q >> 2;
                 const double uu[4] = {h ? u[0].y : u[0].x, h ? u[1].y : u[1].x, h ? u[2].y : u[2].x, h ? u[3].y : u[3].x};
-                double w[GV];
-                prim_vT(uu, gm1, w);
-                const int fld[GV] = {F_V1, F_V2, F_T};
+                prim_vT(uu, gm1, w[h]);
+            }
 #pragma unroll
-                for (int c = 0; c < GV; ++c) {
-                    sm[fld[c]][0][eo + 4 * j + i] = w[c];
-                    sm[fld[c]][1][yo + eo + 4 * i + j] = w[c];
-                }
+            for (int c = 0; c < GV; ++c) {
+                *reinterpret_cast<double2 *>(&sm[G_V1 + c][0][eo + 4 * j0 + i0]) = make_double2(w[0][c], w[1][c]);
+                sm[G_V1 + c][1][yo + eo + 4 * i0 + j0] = w[0][c];
+                sm[G_V1 + c][1][yo + eo + 4 * (i0 + 1) + j0] = w[1][c];
             }
         }
         __syncwarp();
+        if (has_next) issue_state(pk_next);       // stg consumed
+        cp_async_commit();
         const int lo = o == 0 ? eo + 4 * ln : yo + eo + 4 * ln;
         double q[GV][NP];
-        const int fld[GV] = {F_V1, F_V2, F_T};
+        const int fld[GV] = {G_V1, G_V2, G_T};
         const double sc[GV] = {1.0, 1.0, 1.0};
-        line_gradient<GRAD2D_LS>(sm, o, lo, e, ln, Gs, 2.0 / hcell, fld, sc, q);
+        line_gradient<GRAD2D_LS>(sm, o, lo, ln, gst[le], 2.0 / hcell, fld, sc, q);
 #pragma unroll
         for (int c = 0; c < GV; ++c)
 #pragma unroll
-            for (int a = 0; a < NP; ++a) sm[4 + c][o][lo + a] = q[c][a];
+            for (int a = 0; a < NP; ++a) sm[G_Q + c][o][lo + a] = q[c][a];
         __syncwarp();
+        if (has_next) issue_gs(pk_next);          // gst consumed
+        cp_async_commit();
         if (valid) {
 #pragma unroll
             for (int end = 0; end < 2; ++end) {
@@ -161,9 +205,9 @@ __global__ void __launch_bounds__(128) k_grad2d(MeshDev md, StageParams sp, cons
 #pragma unroll
                 for (int c = 0; c < GV; ++c) {
                     qs[c] = q[c][a];
-                    qo[c] = sm[4 + c][1 - o][oi];
+                    qo[c] = sm[G_Q + c][1 - o][oi];
                 }
-                const double v1 = sm[F_V1][o][lo + a], v2 = sm[F_V2][o][lo + a];
+                const double v1 = sm[G_V1][o][lo + a], v2 = sm[G_V2][o][lo + a];
                 if (o == 0) visc_flux2d(v1, v2, qs, qo, 0, md.mu, md.kappa, fv);
                 else visc_flux2d(v1, v2, qo, qs, 1, md.mu, md.kappa, fv);
                 const int face = 2 * o + (end ? 0 : 1);      // a = N: +o face, a = 0: -o face
@@ -172,7 +216,9 @@ __global__ void __launch_bounds__(128) k_grad2d(MeshDev md, StageParams sp, cons
             }
         }
         __syncwarp();
+        pk = pk_next;
     }
+    cp_async_wait<0>();
 }
 
 }  // namespace perk

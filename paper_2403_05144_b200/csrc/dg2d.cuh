@@ -350,9 +350,10 @@ __device__ __forceinline__ double2 load_state2(const StateBufs &sb, int src, dou
 // central traces Gs:  q[c][a] = (2/h) [ -sum_k Dhat_ak w_c[k] + (delta_a3 w*_{+o} - delta_a0 w*_{-o}) / w_a ].
 // Component c is read from field fld[c] of layout o, which holds w_c / sc[c] (sc = 1 or 2: the volume
 // kernel stores half velocities; scaling by 2 is exact, so q is bitwise the unscaled result).
+// Ge = the element's 48 central traces ([face][c][k], e.g. a shared-memory staged copy).
 template <int LS>
-__device__ __forceinline__ void line_gradient(const double (*sm)[2][LS], int o, int lo, int e, int ln,
-                                              const double *__restrict__ Gs, double Jq, const int fld[GV],
+__device__ __forceinline__ void line_gradient(const double (*sm)[2][LS], int o, int lo, int ln,
+                                              const double *Ge, double Jq, const int fld[GV],
                                               const double sc[GV], double q[GV][NP])
 {
 #pragma unroll
@@ -361,8 +362,8 @@ __device__ __forceinline__ void line_gradient(const double (*sm)[2][LS], int o, 
 #pragma unroll
         for (int k = 0; k < NP; ++k) w[k] = sm[fld[c]][o][lo + k];
         const double isc = 1.0 / sc[c];
-        const double ghi = __ldg(Gs + gidx2d(e, 2 * o, c, ln)) * isc;
-        const double glo = __ldg(Gs + gidx2d(e, 2 * o + 1, c, ln)) * isc;
+        const double ghi = Ge[gidx2d(0, 2 * o, c, ln)] * isc;
+        const double glo = Ge[gidx2d(0, 2 * o + 1, c, ln)] * isc;
 #pragma unroll
         for (int a = 0; a < NP; ++a) {
             double t = 0.0;
@@ -379,14 +380,14 @@ __device__ __forceinline__ void line_gradient(const double (*sm)[2][LS], int o, 
 // coordinates: acc[.][1] normal, acc[.][2] tangential momentum), i.e. -(2/h)(...) of the weak-form
 // viscous divergence after the common -2/h scaling.  Fields 4..6 are overwritten with the gradients.
 template <int LS>
-__device__ __forceinline__ void visc_volume(double (*sm)[2][LS], int o, int lo, int eo, int yo, int ln, int e,
-                                            const double *__restrict__ Gs, double Jq, double mu, double kappa,
+__device__ __forceinline__ void visc_volume(double (*sm)[2][LS], int o, int lo, int eo, int yo, int ln,
+                                            const double *Ge, double Jq, double mu, double kappa,
                                             double acc[NP][4])
 {
     const int fld[GV] = {o == 0 ? F_HVN : F_HVT, o == 0 ? F_HVT : F_HVN, F_T};   // v1/2, v2/2, T
     const double sc[GV] = {2.0, 2.0, 1.0};
     double q[GV][NP];
-    line_gradient<LS>(sm, o, lo, e, ln, Gs, Jq, fld, sc, q);
+    line_gradient<LS>(sm, o, lo, ln, Ge, Jq, fld, sc, q);
     __syncwarp();   // every thread of the element is done with fields 4..6 (two-point fluxes)
 #pragma unroll
     for (int c = 0; c < GV; ++c)
@@ -424,9 +425,10 @@ __device__ __forceinline__ void visc_volume(double (*sm)[2][LS], int o, int lo, 
 
 // Dynamic shared memory of k_vol2d (bytes): field arrays, own-state staging, epilogue staging.
 __host__ __device__ constexpr int vol2d_nf(bool ns) { return ns ? 8 : 7; }
+__host__ __device__ constexpr int vol2d_epi_slots(bool ns) { return ns ? 4 : 3; }   // U_n, K_1, Fs (+ Gs)
 __host__ __device__ constexpr size_t vol2d_smem_bytes(bool ns)
 {
-    return sizeof(double) * ((size_t)vol2d_nf(ns) * 2 * VOL2D_LS + VOL2D_EPB * 2 * 64 + VOL2D_EPB * 3 * 64);
+    return sizeof(double) * ((size_t)vol2d_nf(ns) * 2 * VOL2D_LS + VOL2D_EPB * 2 * 64 + VOL2D_EPB * vol2d_epi_slots(ns) * 64);
 }
 
 // Volume + surface lift + Jacobian + stage epilogue.  Persistent grid-stride loop over groups of 16
@@ -449,8 +451,9 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
     extern __shared__ __align__(16) unsigned char smraw[];
     double (*sm)[2][VOL2D_LS] = reinterpret_cast<double (*)[2][VOL2D_LS]>(smraw);
     double (*stg)[2][64] = reinterpret_cast<double (*)[2][64]>(smraw + sizeof(double) * NF * 2 * VOL2D_LS);
-    double (*epi)[3][64] = reinterpret_cast<double (*)[3][64]>(reinterpret_cast<unsigned char *>(stg) +
-                                                                sizeof(double) * VOL2D_EPB * 2 * 64);
+    constexpr int NEPI = vol2d_epi_slots(NS);
+    double (*epi)[NEPI][64] = reinterpret_cast<double (*)[NEPI][64]>(reinterpret_cast<unsigned char *>(stg) +
+                                                                      sizeof(double) * VOL2D_EPB * 2 * 64);
     const int t8 = threadIdx.x & 7, le = threadIdx.x >> 3;
     const int n_act = MODE == MODE_STAGE ? md.count_active[KIND_EL * MAXS + sp.stage - 1] : md.n[0];
     const double g = md.gamma, gm1 = g - 1.0, inv_gm1 = 1.0 / gm1;
@@ -556,6 +559,11 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
             copy_block(epi[le][2], Fs + eb);
             if (need_un) copy_block(epi[le][0], Un + eb);
             if (need_k1) copy_block(epi[le][1], K1 + eb);
+            if (NS) {   // the element's 48 BR1 central traces (384 B = 24 chunks of 16 B)
+#pragma unroll
+                for (int r = 0; r < 3; ++r)
+                    cp_async16(&epi[le][3][2 * (t8 + 8 * r)], Gs + (size_t)e * 4 * GV * NP + 2 * (t8 + 8 * r));
+            }
             cp_async_commit();
         }
         if (has_next) issue_state(pk_next);
@@ -599,7 +607,12 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
             }
         }
         // NS: + sum_a Dhat_ia F^v(node a) along the line (BR1 gradients recomputed from Gs)
-        if (NS) visc_volume<VOL2D_LS>(sm, o, lo, eo, yo, ln, e, Gs, 2.0 / hcell, md.mu, md.kappa, acc);
+        if (NS) {
+            if (has_next) cp_async_wait<1>();
+            else cp_async_wait<0>();
+            __syncwarp();
+            visc_volume<VOL2D_LS>(sm, o, lo, eo, yo, ln, &epi[le][3][0], 2.0 / hcell, md.mu, md.kappa, acc);
+        }
         // surface lift: + f*_hi / w_N at the last node, - f*_lo / w_0 at the first node
         // line coordinates (normal, tangential) -> (momentum x, momentum y)
         if (o == 1) {

@@ -299,9 +299,9 @@ static void launch_br1(perk_ctx *c, cudaStream_t s, const StageParams &sp, const
         launch_pdl(k_gsurf2d<MODE_RHS>, c->surf_blocks, 256, 0, s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs);
     prof_mark(p, s, 5);
     if (sp.mode == MODE_STAGE)
-        launch_pdl(k_grad2d<MODE_STAGE>, c->grad_blocks, 128, 0, s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs, c->Vt);
+        launch_pdl(k_grad2d<MODE_STAGE>, c->grad_blocks, 128, grad2d_smem_bytes(), s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs, c->Vt);
     else
-        launch_pdl(k_grad2d<MODE_RHS>, c->grad_blocks, 128, 0, s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs, c->Vt);
+        launch_pdl(k_grad2d<MODE_RHS>, c->grad_blocks, 128, grad2d_smem_bytes(), s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs, c->Vt);
 }
 
 static void launch_step(perk_ctx *c, cudaStream_t s, double *U, double dt, Prof *p)
@@ -479,7 +479,9 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
         const int want = (c->cap + VOL2D_EPB - 1) / VOL2D_EPB;
         c->vol_blocks = std::min(want, SM_COUNT_B200 * std::max(occ, 1));
         int occg = 0;
-        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occg, k_grad2d<MODE_STAGE>, 128, 0));
+        CU(cudaFuncSetAttribute(k_grad2d<MODE_STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grad2d_smem_bytes()));
+        CU(cudaFuncSetAttribute(k_grad2d<MODE_RHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grad2d_smem_bytes()));
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occg, k_grad2d<MODE_STAGE>, 128, grad2d_smem_bytes()));
         c->grad_blocks = std::min(want, SM_COUNT_B200 * std::max(occg, 1));
         int occf = 0;
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occf, k_surf2d<MODE_STAGE, false>, 256, 0));
