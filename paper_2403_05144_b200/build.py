@@ -39,8 +39,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
-    with open(os.path.join(HERE, "lib", "ptxas_info.txt"), "w") as f:
-        f.write(res.stderr)
+    with open(os.path.join(HERE, "lib", "ptxas_info.txt"), "w") as f:   # registers / spills / smem per kernel
+        f.write("".join(l for l in res.stderr.splitlines(True) if "Compile time" not in l))
     if verbose:
         print(res.stderr)
     return OUT
