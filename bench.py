@@ -10,9 +10,9 @@ Timing: W warm-up steps, then K steps each bracketed by CUDA events on the launc
 an L2 flush (256 MB write) between timed steps; barrier + synchronize on both sides; max over
 ranks.  N > 1 runs independent replicas of the workload (weak scaling; no data-path collective:
 the multi-GPU domain decomposition of SURVEY §8(e) is not built).
-`other_configs` adds the same measurement for BASELINE cfg 4 (dynamic AMR: device re-mesh every
-5 steps inside the timed steps, repartition time reported separately) and cfg 5 (Navier-Stokes,
-BR1) so one run shows every 2D config (--extra none skips them).
+`other_configs` adds the same measurement for BASELINE cfg 1, 2 (1D, launch-latency bound), cfg 4
+(dynamic AMR: device re-mesh every 5 steps inside the timed steps, repartition time reported
+separately) and cfg 5 (Navier-Stokes, BR1), so one run shows every config (--extra none skips them).
 --impl reference times the oracle (oracle/, plain C, 1 host core) on a bounded sample of the same
 workload (full-mesh P-ERK steps, at most ~120 s of CPU work).
 """
@@ -447,7 +447,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--extra", default="4,5",
+    ap.add_argument("--extra", default="1,2,4,5",
                     help="other BASELINE configs measured into other_configs (comma list, or 'none')")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
