@@ -279,15 +279,24 @@ def run_ours(args):
     elem_rhs_per_step = res["element_rhs_per_step"]
     count_el = [int(x) for x in perk.count_active("elements")]
 
-    # per-kernel device time of the same step: CUDA events around every launch on the launch stream
+    # per-kernel device time: CUDA events around graph replays that contain only that kernel kind's
+    # launches of a step, launched exactly as perk_step launches them (perk_time_kernels); the eager
+    # numbers (events around every individual launch) include ~5 us of launch path per kernel
     prof_steps = 3
-    ms_k = np.zeros(6)
+    ms_e = np.zeros(6)
     U0 = perk.initial_state(w.ic)
+    Up = U0.clone()
     for _ in range(prof_steps):
-        m_, _l = perk.profile_step(U0, w.dt)
-        ms_k += np.array(m_)
-    ms_k /= prof_steps
-    kern = {"surface": round(ms_k[0], 5), "volume_stage": round(ms_k[1], 5)}
+        m_, _l = perk.profile_step(Up, w.dt)
+        ms_e += np.array(m_)
+    ms_e /= prof_steps
+    kinds = [0, 1] + ([4, 5] if w.problem["equation"] == "navier_stokes" else [])
+    ms_k = np.zeros(6)
+    for k in kinds:
+        ms_k[k] = perk.time_kernels(U0.clone(), w.dt, [k], reps=10)
+    ms_all = perk.time_kernels(U0.clone(), w.dt, kinds, reps=10)
+    kern = {"surface": round(ms_k[0], 5), "volume_stage": round(ms_k[1], 5), "all_kinds_graph": round(ms_all, 5),
+            "eager_launches": {"surface": round(ms_e[0], 5), "volume_stage": round(ms_e[1], 5)}}
     if w.problem["equation"] == "navier_stokes":
         kern.update(br1_gradient_traces=round(ms_k[4], 5), br1_gradients=round(ms_k[5], 5))
     vol_ms = ms_k[1]

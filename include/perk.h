@@ -163,6 +163,12 @@ const char *perk_last_error(perk_ctx *ctx);
 /* Profiling (synchronising): run one step eagerly (no graph) with CUDA events around every launch
  * on the context stream; ms_host[k] += device time of kernel kind k, launches_host[k] += launches. */
 int perk_profile_step(perk_ctx *ctx, double *U_dev, double dt, float *ms_host, int32_t *launches_host);
+/* Device time per step of only the kernels of the kinds in kind_mask (bit k = kind k above), launched
+ * exactly as perk_step launches them (captured graph, programmatic dependent launches): one warm-up
+ * replay, then CUDA events around `reps` replays on the context stream.  The other kinds' kernels are
+ * left out of the graph, so the state is NOT a valid P-ERK evolution afterwards (timing only).
+ * Synchronising. */
+int perk_time_kernels(perk_ctx *ctx, double *U_dev, double dt, uint32_t kind_mask, int32_t reps, float *ms_per_step);
 /* Same for one repartition (kinds 2 and 3). */
 int perk_profile_repartition(perk_ctx *ctx, const uint8_t *level_map_dev, double *U_dev, float *ms_host,
                              int32_t *launches_host);

@@ -47,6 +47,7 @@ struct perk_ctx {
     int *n_old = nullptr, *cell_of_old = nullptr, *fx_old = nullptr, *fy_old = nullptr;
     uint8_t *lev_old = nullptr;
     int vol_blocks = 0, surf_blocks = 0, grad_blocks = 0;
+    unsigned kind_mask = ~0u;              // kernel kinds launch_step issues (perk_time_kernels)
     cudaGraphExec_t gexec = nullptr;
     double *gU = nullptr;
     double gdt = 0.0;
@@ -293,12 +294,14 @@ static void launch_br1(perk_ctx *c, cudaStream_t s, const StageParams &sp, const
 {
     const MeshDev &md = c->md;
     prof_mark(p, s, 4);
-    if (sp.mode == MODE_STAGE)
+    if (!((c->kind_mask >> 4) & 1u)) {
+    } else if (sp.mode == MODE_STAGE)
         launch_pdl(k_gsurf2d<MODE_STAGE>, c->surf_blocks, 256, 0, s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs);
     else
         launch_pdl(k_gsurf2d<MODE_RHS>, c->surf_blocks, 256, 0, s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs);
     prof_mark(p, s, 5);
-    if (sp.mode == MODE_STAGE)
+    if (!((c->kind_mask >> 5) & 1u)) {
+    } else if (sp.mode == MODE_STAGE)
         launch_pdl(k_grad2d<MODE_STAGE>, c->grad_blocks, 128, grad2d_smem_bytes(), s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs, c->Vt);
     else
         launch_pdl(k_grad2d<MODE_RHS>, c->grad_blocks, 128, grad2d_smem_bytes(), s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs, c->Vt);
@@ -310,9 +313,9 @@ static void launch_step(perk_ctx *c, cudaStream_t s, double *U, double dt, Prof 
         const StageParams sp = stage_params(c, i, dt, MODE_STAGE, 0u);
         if (c->ns) launch_br1(c, s, sp, U, nullptr, p);
         prof_mark(p, s, 0);
-        launch_surface(c, s, sp, U, nullptr);
+        if ((c->kind_mask >> 0) & 1u) launch_surface(c, s, sp, U, nullptr);
         prof_mark(p, s, 1);
-        launch_volume(c, s, sp, U, nullptr, nullptr);
+        if ((c->kind_mask >> 1) & 1u) launch_volume(c, s, sp, U, nullptr, nullptr);
         prof_mark(p, s, -1);
     }
 }
@@ -770,6 +773,39 @@ extern "C" int perk_profile_step(perk_ctx *c, double *U, double dt, float *ms, i
     launch_step(c, c->stream, U, dt, &p);
     CU(cudaGetLastError());
     return finish_prof(c, p, ms, launches);
+}
+
+extern "C" int perk_time_kernels(perk_ctx *c, double *U, double dt, uint32_t kind_mask, int32_t reps, float *ms_per_step)
+{
+    if (!c) return PERK_ENOTINIT;
+    if (!U || !ms_per_step || reps < 1) return set_err(c, PERK_EINVAL, "U_dev / ms / reps");
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    c->kind_mask = kind_mask;
+    cudaError_t ce = cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal);
+    if (ce == cudaSuccess) {
+        launch_step(c, c->cap_stream, U, dt, nullptr);
+        ce = cudaStreamEndCapture(c->cap_stream, &g);
+    }
+    c->kind_mask = ~0u;
+    if (ce != cudaSuccess) return set_err(c, PERK_ECUDA, std::string("capture: ") + cudaGetErrorString(ce));
+    CU(cudaGraphInstantiate(&ge, g, 0));
+    cudaGraphDestroy(g);
+    cudaEvent_t a, b;
+    CU(cudaEventCreate(&a));
+    CU(cudaEventCreate(&b));
+    CU(cudaGraphLaunch(ge, c->stream));   // warm-up
+    CU(cudaEventRecord(a, c->stream));
+    for (int r = 0; r < reps; ++r) CU(cudaGraphLaunch(ge, c->stream));
+    CU(cudaEventRecord(b, c->stream));
+    CU(cudaEventSynchronize(b));
+    float t = 0.f;
+    CU(cudaEventElapsedTime(&t, a, b));
+    *ms_per_step = t / reps;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaGraphExecDestroy(ge);
+    return check_device_err(c);
 }
 
 extern "C" int perk_profile_repartition(perk_ctx *c, const uint8_t *lmap, double *U, float *ms, int32_t *launches)

@@ -75,6 +75,7 @@ def lib():
         L.perk_last_error.argtypes = [P]
         L.perk_last_error.restype = C.c_char_p
         L.perk_profile_step.argtypes = [P, P, dbl, P, P]
+        L.perk_time_kernels.argtypes = [P, P, dbl, C.c_uint32, i32, C.POINTER(C.c_float)]
         L.perk_profile_repartition.argtypes = [P, P, P, P, P]
         L.perk_launches_per_step.argtypes = [P, C.POINTER(i32)]
         _lib = L
@@ -85,7 +86,8 @@ def exported_symbols():
     return ["perk_alpha_taylor", "perk_tableau_p2", "perk_init", "perk_destroy", "perk_set_stream", "perk_step",
             "perk_run_host", "perk_repartition", "rhs_eval", "perk_num_cells", "perk_num_faces", "perk_node_coords",
             "perk_get_leaves", "perk_get_faces", "perk_get_list", "perk_get_count_active", "perk_get_counters",
-            "perk_sync", "perk_last_error", "perk_profile_step", "perk_profile_repartition", "perk_launches_per_step"]
+            "perk_sync", "perk_last_error", "perk_profile_step", "perk_time_kernels", "perk_profile_repartition",
+            "perk_launches_per_step"]
 
 
 def tableau_p2(S: int, E, alpha_rows=None) -> perk_tableau:
@@ -290,6 +292,16 @@ class Perk:
         nl = (C.c_int32 * NKINDS)()
         _check(self.h, lib().perk_profile_step(self.h, _ptr(U), float(dt), ms, nl))
         return list(ms), list(nl)
+
+    def time_kernels(self, U, dt, kinds, reps=10):
+        """device ms per step of only the kernels of `kinds` (0 surface, 1 volume+stage, 4/5 BR1),
+        launched as perk_step does (graph + programmatic launches); timing only, U is garbage after"""
+        mask = 0
+        for k in kinds:
+            mask |= 1 << k
+        ms = C.c_float()
+        _check(self.h, lib().perk_time_kernels(self.h, _ptr(U), float(dt), mask, int(reps), C.byref(ms)))
+        return ms.value
 
     def profile_repartition(self, level_map, U):
         lm = self._to_dev_u8(level_map)
