@@ -41,7 +41,7 @@ class OraProblem(C.Structure):
 
 class OraTableau(C.Structure):
     _fields_ = [("S", C.c_int32), ("R", C.c_int32), ("E", C.c_int32 * 8), ("c", C.c_double * 64),
-                ("a1", (C.c_double * 64) * 8), ("asub", (C.c_double * 64) * 8)]
+                ("b", C.c_double * 64), ("a1", (C.c_double * 64) * 8), ("asub", (C.c_double * 64) * 8)]
 
 
 _lib = None
@@ -111,8 +111,10 @@ def tableau_struct(fam: dict) -> OraTableau:
         for i in range(fam["S"]):
             t.a1[r][i] = fam["a1_f"][r][i]
             t.asub[r][i] = fam["asub_f"][r][i]
+    b = fam.get("b_f") or [0.0] * (fam["S"] - 1) + [1.0]      # P-ERK2: b = e_S
     for i in range(fam["S"]):
         t.c[i] = fam["c_f"][i]
+        t.b[i] = b[i]
     return t
 
 

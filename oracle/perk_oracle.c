@@ -58,6 +58,7 @@ typedef struct {
     int32_t S, R;
     int32_t E[MAXR];            /* ascending; member r has E[r] RHS evaluations */
     double c[MAXS];             /* c_i, index i-1 */
+    double b[MAXS];             /* b_i, index i-1 (P-ERK2: e_S; P-ERK3: 1/6, 0.., 1/6, 4/6) */
     double a1[MAXR][MAXS];      /* a_{i,1}^{(r)}   (index i-1) */
     double asub[MAXR][MAXS];    /* a_{i,i-1}^{(r)} (index i-1) */
 } OraTableau;
@@ -999,7 +1000,10 @@ typedef void (*rhs_fn)(void *ctx, const double *U, uint32_t mask, double *dU);
      K_1 = F(U_n)
      U^(i)|_r = U_n|_r + dt (a_{i,1}^(r) K_1|_r + a_{i,i-1}^(r) K_{i-1}|_r),  i = 2..S
      K_i|_r = I^(r) F(U^(i))  for the members r active at stage i (others: 0, never used)
-     U_{n+1} = U_n + dt K_S                                 (b = e_S)                */
+     U_{n+1} = U_n + dt sum_i b_i K_i   (shared b: P-ERK2 b = e_S, P:l.423; P-ERK3 Shu-Osher
+                                         b = (1/6, 0, .., 0, 1/6, 4/6), P:l.872-883)
+   The weighted sum is accumulated stage by stage in the order i = 1..S (terms with b_i = 0 add an
+   exact zero, so b = e_S gives U_n + dt K_S bitwise).                                      */
 static int64_t perk_step_generic(const OraTableau *t, int nunits, int usize, const int32_t *member,
                                  double *U, double dt, rhs_fn F, void *ctx)
 {
@@ -1008,11 +1012,13 @@ static int64_t perk_step_generic(const OraTableau *t, int nunits, int usize, con
     double *Kp = (double *)malloc(sizeof(double) * nd);
     double *Kn = (double *)malloc(sizeof(double) * nd);
     double *Us = (double *)malloc(sizeof(double) * nd);
+    double *Ksum = (double *)malloc(sizeof(double) * nd);
     int64_t evals = 0;
     uint32_t all = (t->R >= 32) ? 0xffffffffu : ((1u << t->R) - 1u);
     F(ctx, U, all, K1);
     evals += nunits;
     memcpy(Kp, K1, sizeof(double) * nd);
+    for (size_t d = 0; d < nd; ++d) Ksum[d] = 0.0 + t->b[0] * K1[d];
     for (int i = 2; i <= t->S; ++i) {
         for (int u = 0; u < nunits; ++u) {
             int r = member[u];
@@ -1031,9 +1037,10 @@ static int64_t perk_step_generic(const OraTableau *t, int nunits, int usize, con
             else for (int q = 0; q < usize; ++q) Kn[(size_t)u * usize + q] = 0.0;  /* K_i^(r) = 0: I^(r) mask */
         }
         double *tmp = Kp; Kp = Kn; Kn = tmp;
+        for (size_t d = 0; d < nd; ++d) Ksum[d] = Ksum[d] + t->b[i - 1] * Kp[d];
     }
-    for (size_t d = 0; d < nd; ++d) U[d] = U[d] + dt * Kp[d];
-    free(K1); free(Kp); free(Kn); free(Us);
+    for (size_t d = 0; d < nd; ++d) U[d] = U[d] + dt * Ksum[d];
+    free(K1); free(Kp); free(Kn); free(Us); free(Ksum);
     return evals;
 }
 
