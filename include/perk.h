@@ -89,14 +89,22 @@ typedef struct perk_problem {
     int64_t max_cells;
 } perk_problem;
 
-/* P-ERK2 family.  S stages, R members with E[0] < ... < E[R-1] <= S (E[r] >= 2).
+/* P-ERK family in the standard pattern (P:l.407-436): S stages, R members with
+ * E[0] < ... < E[R-1] <= S (E[r] >= 2); member r evaluates stages {1} u {S-E_r+2..S}.
  * c[i-1] = c_i, a_sub[r][i-1] = a_{i,i-1} of member r; a_{i,1} = c_i - a_{i,i-1} is derived.
- * b = e_S (P:l.423).  Member r is assigned to level l by r = clamp(R-1-(L-l), 0, R-1). */
+ * Shared weights b[i-1] = b_i, nonzero only at i = 1, S-1, S:
+ *   P-ERK2: b = e_S (P:l.423; perk_tableau_p2 fills it);
+ *   P-ERK3: b_1 = b_{S-1} = 1/6, b_S = 4/6 (Shu-Osher base, P:l.870-883), c_{S-1} = 1, c_S = 1/2,
+ *           coefficients computed offline (P:l.1067-1090) and passed in by the caller; requires
+ *           E[0] >= 3.  The final update U_n + dt (b_1 K_1 + b_{S-1} K_{S-1} + b_S K_S) is formed as
+ *           W = U_n + dt (b_1 K_1 + b_{S-1} K_{S-1}) in the stage S-1 epilogue, U_{n+1} = W + dt b_S K_S.
+ * Member r is assigned to level l by r = clamp(R-1-(L-l), 0, R-1). */
 typedef struct perk_tableau {
     int32_t S;
     int32_t R;
     int32_t E[PERK_MAX_MEMBERS];
     double c[PERK_MAX_STAGES];
+    double b[PERK_MAX_STAGES];
     double a_sub[PERK_MAX_MEMBERS][PERK_MAX_STAGES];
 } perk_tableau;
 
@@ -105,7 +113,7 @@ typedef struct perk_ctx perk_ctx;
 /* Host only.  Taylor rule of BASELINE.json cfg 1: alpha[k] = 1/k!, k = 0..E (alpha has E+1 entries). */
 int perk_alpha_taylor(int32_t E, double *alpha_host);
 
-/* Host only.  Build a P-ERK2 family from stability-polynomial coefficients:
+/* Host only.  Build a P-ERK2 family (b = e_S) from stability-polynomial coefficients:
  * alpha_host is R rows of (S+1) doubles, row r = alpha_0..alpha_S of member r (entries above E[r]
  * ignored).  c_i = (i-1)/(2(S-1)) (P:l.439-442); a_{i,i-1} by the recursion of P:l.1062 for
  * i = 0..E-3, all other a_{i,i-1} = 0.  EINVAL on bad sizes or a zero pivot. */

@@ -80,6 +80,9 @@ struct StageParams {
     int first[MAXR];             // f(r) = S - E_r + 2: first active stage after 1
     double a1_next[MAXR];        // a_{i+1,1}^{(r)}
     double asub_next[MAXR];      // a_{i+1,i}^{(r)}
+    double bS;                   // b_S: U_{n+1} = W + dt b_S K_S (W = U_n when b = e_S)
+    double wb1, wbS1;            // b_1, b_{S-1}: W = U_n + dt (b_1 K_1 + b_{S-1} K_{S-1}) ...
+    int wmode;                   // ... written by the stage S-1 epilogue when wmode = 1 (P-ERK3)
 };
 
 // Which buffer holds element e's stage-i state (SURVEY §7 rule):

@@ -98,7 +98,7 @@ template <int NV, int MODE>
 __global__ void __launch_bounds__(128) k_vol1d(MeshDev md, StageParams sp, double *__restrict__ Un,
                                               double *__restrict__ Ubuf, double *__restrict__ K1,
                                               const double *__restrict__ Fs, const double *__restrict__ Uin,
-                                              double *__restrict__ dU)
+                                              double *__restrict__ dU, double *__restrict__ Wb)
 {
     const int n_act = MODE == MODE_STAGE ? md.count_active[KIND_EL * MAXS + sp.stage - 1] : md.n[0];
     const StateBufs sb{Un, Ubuf, K1, Uin};
@@ -144,9 +144,11 @@ __global__ void __launch_bounds__(128) k_vol1d(MeshDev md, StageParams sp, doubl
                 } else if (sp.stage == 1) {
                     K1[idx] = K;
                 } else if (sp.stage == sp.S) {
-                    Un[idx] = fma(sp.dt, K, Un[idx]);
+                    Un[idx] = fma(sp.dt * sp.bS, K, Wb ? Wb[idx] : Un[idx]);
                 } else {
-                    Ubuf[idx] = fma(sp.dt, fma(sp.a1_next[m], K1[idx], sp.asub_next[m] * K), Un[idx]);
+                    const double un = Un[idx], k1 = K1[idx];
+                    Ubuf[idx] = fma(sp.dt, fma(sp.a1_next[m], k1, sp.asub_next[m] * K), un);
+                    if (sp.wmode) Wb[idx] = fma(sp.dt, fma(sp.wb1, k1, sp.wbS1 * K), un);
                 }
             }
         }

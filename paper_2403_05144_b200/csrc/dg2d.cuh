@@ -445,7 +445,8 @@ template <int MODE, bool NS>
 __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                                                  double *__restrict__ Ubuf, double *__restrict__ K1,
                                                  const double *__restrict__ Fs, const double *__restrict__ Uin,
-                                                 double *__restrict__ dU, const double *__restrict__ Gs)
+                                                 double *__restrict__ dU, const double *__restrict__ Gs,
+                                                 double *__restrict__ Wb)
 {
     constexpr int NF = vol2d_nf(NS);          // rho, v_n/2, v_t/2, p/2, ln rho, beta, ln beta (+ T)
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -557,7 +558,8 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
             const bool need_un = MODE == MODE_STAGE && sp.stage > 1;
             const bool need_k1 = MODE == MODE_STAGE && sp.stage > 1 && sp.stage < sp.S;
             copy_block(epi[le][2], Fs + eb);
-            if (need_un) copy_block(epi[le][0], Un + eb);
+            // stage S combines with W (P-ERK3) or U_n
+            if (need_un) copy_block(epi[le][0], (Wb && sp.stage == sp.S ? Wb : Un) + eb);
             if (need_k1) copy_block(epi[le][1], K1 + eb);
             if (NS) {   // the element's 48 BR1 central traces (384 B = 24 chunks of 16 B)
 #pragma unroll
@@ -660,14 +662,19 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
                 } else if (sp.stage == 1) {
                     *reinterpret_cast<double2 *>(K1 + idx) = K;
                 } else if (sp.stage == sp.S) {
-                    const double2 un = *reinterpret_cast<const double2 *>(&epi[le][0][v * 16 + q0]);
-                    *reinterpret_cast<double2 *>(Un + idx) = make_double2(fma(sp.dt, K.x, un.x), fma(sp.dt, K.y, un.y));
+                    const double2 w = *reinterpret_cast<const double2 *>(&epi[le][0][v * 16 + q0]);   // W or U_n
+                    const double db = sp.dt * sp.bS;
+                    *reinterpret_cast<double2 *>(Un + idx) = make_double2(fma(db, K.x, w.x), fma(db, K.y, w.y));
                 } else {
                     const double2 un = *reinterpret_cast<const double2 *>(&epi[le][0][v * 16 + q0]);
                     const double2 k1 = *reinterpret_cast<const double2 *>(&epi[le][1][v * 16 + q0]);
                     const double a1 = sp.a1_next[m], as = sp.asub_next[m];
                     *reinterpret_cast<double2 *>(Ubuf + idx) =
                         make_double2(fma(sp.dt, fma(a1, k1.x, as * K.x), un.x), fma(sp.dt, fma(a1, k1.y, as * K.y), un.y));
+                    if (sp.wmode)
+                        *reinterpret_cast<double2 *>(Wb + idx) =
+                            make_double2(fma(sp.dt, fma(sp.wb1, k1.x, sp.wbS1 * K.x), un.x),
+                                         fma(sp.dt, fma(sp.wb1, k1.y, sp.wbS1 * K.y), un.y));
                 }
             }
         }

@@ -4,6 +4,7 @@
 // allocations, launching the device mesh pipeline (mesh.cuh), capturing one CUDA graph per P-ERK
 // step (2 launches per stage: k_surf*, k_vol*), profiling hooks.  No step of the method runs on
 // the host: after perk_init the host never reads mesh data except in introspection calls.
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -40,6 +41,7 @@ struct perk_ctx {
     cudaStream_t cap_stream = nullptr;
     double *K1 = nullptr, *Ubuf = nullptr, *Fs = nullptr, *Utmp = nullptr, *Uhost_dev = nullptr;
     double *Gs = nullptr, *Vt = nullptr;   // BR1 (Navier-Stokes): central w* and viscous-flux traces
+    double *Wb = nullptr;                  // P-ERK3: W = U_n + dt (b_1 K_1 + b_{S-1} K_{S-1})
     bool ns = false;
     uint8_t *lmap = nullptr, *keys = nullptr;
     int *items = nullptr, *rank = nullptr, *blockcnt = nullptr, *blockoff = nullptr, *segtmp = nullptr;
@@ -106,6 +108,7 @@ extern "C" int perk_tableau_p2(int32_t S, int32_t R, const int32_t *E, const dou
     memset(out, 0, sizeof(*out));
     out->S = S;
     out->R = R;
+    out->b[S - 1] = 1.0;                       // b = e_S (P:l.423)
     for (int i = 1; i <= S; ++i) out->c[i - 1] = (double)(i - 1) / (double)(2 * (S - 1));
     for (int r = 0; r < R; ++r) {
         out->E[r] = E[r];
@@ -223,6 +226,10 @@ static StageParams stage_params(const perk_ctx *c, int i, double dt, int mode, u
     sp.mask = mask;
     sp.dt = dt;
     sp.c_stage = c->tab.c[i - 1];
+    sp.bS = c->tab.b[c->tab.S - 1];
+    sp.wb1 = c->tab.b[0];
+    sp.wbS1 = c->tab.b[c->tab.S - 2];
+    sp.wmode = (c->Wb && i == c->tab.S - 1) ? 1 : 0;
     for (int r = 0; r < c->tab.R; ++r) {
         sp.first[r] = c->tab.S - c->tab.E[r] + 2;
         if (i < c->tab.S) {
@@ -267,25 +274,25 @@ static void launch_volume(perk_ctx *c, cudaStream_t s, const StageParams &sp, do
     if (c->prob.dim == 2) {
         if (c->ns) {
             if (sp.mode == MODE_STAGE)
-                launch_pdl(k_vol2d<MODE_STAGE, true>, c->vol_blocks, 128, vol2d_smem_bytes(true), s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Gs);
+                launch_pdl(k_vol2d<MODE_STAGE, true>, c->vol_blocks, 128, vol2d_smem_bytes(true), s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Gs, c->Wb);
             else
-                launch_pdl(k_vol2d<MODE_RHS, true>, c->vol_blocks, 128, vol2d_smem_bytes(true), s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Gs);
+                launch_pdl(k_vol2d<MODE_RHS, true>, c->vol_blocks, 128, vol2d_smem_bytes(true), s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Gs, c->Wb);
         } else {
             if (sp.mode == MODE_STAGE)
-                launch_pdl(k_vol2d<MODE_STAGE, false>, c->vol_blocks, 128, vol2d_smem_bytes(false), s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, nullptr);
+                launch_pdl(k_vol2d<MODE_STAGE, false>, c->vol_blocks, 128, vol2d_smem_bytes(false), s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, nullptr, c->Wb);
             else
-                launch_pdl(k_vol2d<MODE_RHS, false>, c->vol_blocks, 128, vol2d_smem_bytes(false), s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, nullptr);
+                launch_pdl(k_vol2d<MODE_RHS, false>, c->vol_blocks, 128, vol2d_smem_bytes(false), s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, nullptr, c->Wb);
         }
     } else if (c->nv == 1) {
         if (sp.mode == MODE_STAGE)
-            k_vol1d<1, MODE_STAGE><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU);
+            k_vol1d<1, MODE_STAGE><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Wb);
         else
-            k_vol1d<1, MODE_RHS><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU);
+            k_vol1d<1, MODE_RHS><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Wb);
     } else {
         if (sp.mode == MODE_STAGE)
-            k_vol1d<3, MODE_STAGE><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU);
+            k_vol1d<3, MODE_STAGE><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Wb);
         else
-            k_vol1d<3, MODE_RHS><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU);
+            k_vol1d<3, MODE_RHS><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Wb);
     }
 }
 
@@ -373,6 +380,16 @@ static int validate(perk_ctx *c, const perk_problem *p, const perk_tableau *t)
         if (t->E[r] < 2 || t->E[r] > t->S || (r > 0 && t->E[r] <= t->E[r - 1]))
             return set_err(c, PERK_EINVAL, "E must be ascending in [2, S]");
     }
+    // shared weights: nonzero only at stages 1, S-1, S, summing to 1 (b^T 1 = 1, P:l.236)
+    double bsum = 0.0;
+    for (int i = 0; i < t->S; ++i) {
+        if (t->b[i] != 0.0 && i != 0 && i != t->S - 2 && i != t->S - 1)
+            return set_err(c, PERK_EUNSUPPORTED, "b may be nonzero only at stages 1, S-1, S");
+        bsum += t->b[i];
+    }
+    if (std::fabs(bsum - 1.0) > 1e-14) return set_err(c, PERK_EINVAL, "b must sum to 1");
+    if ((t->b[0] != 0.0 || (t->S >= 2 && t->b[t->S - 2] != 0.0)) && t->E[0] < 3)
+        return set_err(c, PERK_EINVAL, "b_1, b_{S-1} != 0 (P-ERK3) needs every member active at stage S-1 (E >= 3)");
     return PERK_OK;
 }
 
@@ -456,6 +473,7 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
     CU(dalloc(c, &c->K1, (size_t)c->cap * rowd));
     CU(dalloc(c, &c->Ubuf, (size_t)c->cap * rowd));
     CU(dalloc(c, &c->Fs, (size_t)c->cap * (dim == 1 ? 2 * c->nv : 4 * c->nv * NP)));
+    if (tab->b[0] != 0.0 || tab->b[tab->S - 2] != 0.0) CU(dalloc(c, &c->Wb, (size_t)c->cap * rowd));
     if (c->ns) {
         CU(dalloc(c, &c->Gs, (size_t)c->cap * 4 * GV * NP));
         CU(dalloc(c, &c->Vt, (size_t)c->cap * 4 * GV * NP));

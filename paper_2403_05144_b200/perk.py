@@ -40,7 +40,7 @@ class perk_problem(C.Structure):
 
 class perk_tableau(C.Structure):
     _fields_ = [("S", C.c_int32), ("R", C.c_int32), ("E", C.c_int32 * 8), ("c", C.c_double * 64),
-                ("a_sub", (C.c_double * 64) * 8)]
+                ("b", C.c_double * 64), ("a_sub", (C.c_double * 64) * 8)]
 
 
 _lib = None
@@ -112,6 +112,22 @@ def tableau_p2(S: int, E, alpha_rows=None) -> perk_tableau:
     return t
 
 
+def tableau_from(family: dict) -> perk_tableau:
+    """Marshal an explicit family (e.g. a P-ERK3 family of workloads/perk3.py: c_f, b_f, asub_f, E) into
+    the C struct; the library validates it at perk_init."""
+    t = perk_tableau()
+    S, E = int(family["S"]), [int(e) for e in family["E"]]
+    t.S, t.R = S, len(E)
+    for i in range(S):
+        t.c[i] = family["c_f"][i]
+        t.b[i] = family["b_f"][i]
+    for r, e in enumerate(E):
+        t.E[r] = e
+        for i in range(S):
+            t.a_sub[r][i] = family["asub_f"][r][i]
+    return t
+
+
 def _check(h, rc):
     if rc != 0:
         msg = lib().perk_last_error(h).decode() if h else ""
@@ -143,7 +159,8 @@ def _ptr(t):
 class Perk:
     """One P-ERK multirate DGSEM context on the current CUDA device (all work on the current stream)."""
 
-    def __init__(self, problem: dict, level_map, S: int, E, alpha_rows=None, max_cells=None, stream=None):
+    def __init__(self, problem: dict, level_map, S: int, E, alpha_rows=None, max_cells=None, stream=None,
+                 family=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("CUDA device required: libperk_b200 has no CPU path")
@@ -156,7 +173,7 @@ class Perk:
         self.E = list(E)
         self.R = len(self.E)
         self.max_cells = int(max_cells or problem["max_cells"])
-        self._tab = tableau_p2(S, self.E, alpha_rows)
+        self._tab = tableau_p2(S, self.E, alpha_rows) if family is None else tableau_from(family)
         self._prob = _problem_struct(problem, self.max_cells)
         lm = self._to_dev_u8(level_map)
         self.stream = stream if stream is not None else torch.cuda.current_stream()

@@ -354,3 +354,58 @@ def test_cfg4_long_run_many_remeshes():
     gpu.sync()
     compare_mesh(ora, gpu)
     assert rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo).max() <= TOL
+
+
+# ----------------------------------------------------------------------------------------------
+# P-ERK3 families: explicit tableaux from workloads/perk3.py, general weights b
+# ----------------------------------------------------------------------------------------------
+def _pair_p3(w, fam, problem=None, level_map=None):
+    from paper_2403_05144_b200 import Perk
+    problem = problem or w.problem
+    lm = w.level_map if level_map is None else level_map
+    ora = O.OracleMesh(problem, lm, fam)
+    gpu = Perk(problem, lm, fam["S"], fam["E"], family=fam, max_cells=problem["max_cells"])
+    return ora, gpu
+
+
+def test_p3_cfg3_small_100_steps():
+    from workloads import perk3 as P3
+    w = W.make(3, n_base=16)
+    ora, gpu = _pair_p3(w, P3.family3(16, (4, 8, 16)))
+    Uo, Ug = _run_both(w, 100, ora, gpu)
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
+
+
+def test_p3_cfg3_full_size_steps():
+    from workloads import perk3 as P3
+    w = W.make(3)
+    ora, gpu = _pair_p3(w, P3.family3(16, (4, 8, 16)))
+    Uo, Ug = _run_both(w, 2, ora, gpu)
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
+
+
+def test_p3_1d_euler_full_run():
+    from workloads import perk3 as P3
+    w = W.make(2)
+    ora, gpu = _pair_p3(w, P3.family3(12, (3, 6, 12)))
+    Uo, Ug = _run_both(w, w.steps, ora, gpu)
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
+
+
+def test_p3_ns_small_run():
+    from workloads import perk3 as P3
+    w = W.make(5, n_base=8)
+    ora, gpu = _pair_p3(w, P3.family3(32, (4, 8, 16, 32)))
+    Uo, Ug = _run_both(w, 50, ora, gpu)
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
+
+
+def test_p3_rejects_E2_member():
+    from paper_2403_05144_b200 import Perk, PerkError
+    from workloads import perk3 as P3
+    w = W.make(3, n_base=8)
+    fam = dict(P3.family3(16, (4, 8, 16)))
+    fam["E"] = [2, 8, 16]
+    with pytest.raises(PerkError) as ei:
+        Perk(w.problem, w.level_map, 16, fam["E"], family=fam)
+    assert ei.value.code == -1
