@@ -12,7 +12,8 @@ ranks.  N > 1 runs independent replicas of the workload (weak scaling; no data-p
 the multi-GPU domain decomposition of SURVEY §8(e) is not built).
 `other_configs` adds the same measurement for BASELINE cfg 1, 2 (1D, launch-latency bound), cfg 4
 (dynamic AMR: device re-mesh every 5 steps inside the timed steps, repartition time reported
-separately) and cfg 5 (Navier-Stokes, BR1), so one run shows every config (--extra none skips them).
+separately), cfg 5 (Navier-Stokes, BR1) and cfg 3 with the third-order P-ERK3 family (SURVEY §8(f)
+f1), so one run shows every config (--extra none skips them).
 --impl reference times the oracle (oracle/, plain C, 1 host core) on a bounded sample of the same
 workload (full-mesh P-ERK steps, at most ~120 s of CPU work).
 """
@@ -191,14 +192,20 @@ def replica_value(ws, elem_rhs_per_step, ms_max):
     return ws * elem_rhs_per_step / (ms_max * 1e-3)
 
 
-def measure_config(cfg, K, Wm, timer, torch, dist, ws, dev, with_single=True):
+def measure_config(cfg, K, Wm, timer, torch, dist, ws, dev, with_single=True, order=2):
     """Device time per P-ERK step of BASELINE config `cfg` (and of the single-rate S-stage P-ERK on
-    the same mesh); cfg 4 re-meshes on the device every 5 steps inside the timed steps."""
+    the same mesh); cfg 4 re-meshes on the device every 5 steps inside the timed steps.  order = 3
+    runs the P-ERK3 family with the same S and E (workloads/perk3.py)."""
     from paper_2403_05144_b200 import Perk
     w = W.make(cfg)
-    perk = Perk(w.problem, w.level_map, w.S, w.E)
+    fam = single_fam = None
+    if order == 3:
+        from workloads import perk3 as P3
+        fam, single_fam = P3.family3(w.S, w.E), P3.family3(w.S, [w.S])
+    perk = Perk(w.problem, w.level_map, w.S, w.E, family=fam)
     U = perk.initial_state(w.ic)
-    res = {"workload": w.name, "cells": perk.n_cells, "S": w.S, "E": w.E, "dt": w.dt}
+    res = {"workload": w.name + ("_perk3" if order == 3 else ""), "cells": perk.n_cells, "S": w.S, "E": w.E,
+           "order": order, "dt": w.dt}
     remesh = []
     if w.remesh_every:
         # level maps of the re-meshes inside the measured window, uploaded before the timed region
@@ -234,7 +241,7 @@ def measure_config(cfg, K, Wm, timer, torch, dist, ws, dev, with_single=True):
     res.update(ms_per_step=round(ms, 5), element_rhs_per_step=round(float(elem_rhs_per_step), 1),
                value=round(replica_value(ws, elem_rhs_per_step, ms), 1), n_cells_now=perk.n_cells)
     if with_single and not w.remesh_every:
-        single = Perk(w.problem, w.level_map, w.S, [w.S])
+        single = Perk(w.problem, w.level_map, w.S, [w.S], family=single_fam)
         Us = single.initial_state(w.ic)
         ms_s = _max_over_ranks(torch, dist, ws, dev,
                                float(np.mean(timer.steps(lambda k: single.step(Us, w.dt), max(3, K // 2), Wm))))
@@ -338,16 +345,19 @@ def run_ours(args):
 
     others = {}
     if args.extra != "none":
-        for c in [int(x) for x in args.extra.split(",") if x and int(x) != args.config]:
+        for item in [x for x in args.extra.split(",") if x]:
+            c, order = (int(item[:-2]), 3) if item.endswith("p3") else (int(item), 2)
+            if c == args.config and order == 2:
+                continue
             try:
                 p2, _U, _w, r2 = measure_config(c, max(5, min(args.steps, 20)), args.warmup, timer, torch, dist,
-                                                 ws, dev)
+                                                 ws, dev, order=order)
                 r2["dof_stage_updates_per_s"] = round(r2["value"] * 4 ** _w.problem["dim"], 1)
                 r2["gpu_launches_per_step"] = p2.launches_per_step()
                 p2.close()
-                others[f"cfg{c}"] = r2
+                others[f"cfg{item}"] = r2
             except Exception as ex:       # report, do not hide: the line records the failure
-                others[f"cfg{c}"] = {"error": repr(ex)[:200]}
+                others[f"cfg{item}"] = {"error": repr(ex)[:200]}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -456,8 +466,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--extra", default="1,2,4,5",
-                    help="other BASELINE configs measured into other_configs (comma list, or 'none')")
+    ap.add_argument("--extra", default="1,2,4,5,3p3",
+                    help="other BASELINE configs measured into other_configs (comma list, 'Np3' = config N "
+                         "with the P-ERK3 family, or 'none')")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true",
