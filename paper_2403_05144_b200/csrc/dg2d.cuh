@@ -221,7 +221,36 @@ __global__ void __launch_bounds__(256, 3) k_surf2d(MeshDev md, StageParams sp, c
     const int lane = threadIdx.x & 31;
     const unsigned gmask = 0xFu << (lane & ~3);
     pdl_wait();
-    for (int gt = blockIdx.x * blockDim.x + threadIdx.x; gt < total; gt += gridDim.x * blockDim.x) {
+    const int GS = gridDim.x * blockDim.x;
+    const int nI = 4 * nif;
+    int gt = blockIdx.x * blockDim.x + threadIdx.x;
+    // two interface face nodes per iteration while both are interfaces: twice the loads in flight
+    // per thread (the kernel is bound by the latency of the record -> trace gathers)
+    for (; gt + GS < nI; gt += 2 * GS) {
+        const int ka = gt & 3, kb = (gt + GS) & 3;
+        const int4 Ia = MODE == MODE_STAGE ? md.ifcs[gt >> 2] : md.ifc[gt >> 2];
+        const int4 Ib = MODE == MODE_STAGE ? md.ifcs[(gt + GS) >> 2] : md.ifc[(gt + GS) >> 2];
+        const int srca = state_src(sp, Ia.w), srcb = state_src(sp, Ib.w);
+        double uLa[4], uRa[4], uLb[4], uRb[4], fa[4], fb[4];
+        trace2d(sb, srca, dtc, Ia.x, 2 * Ia.z, ka, uLa);
+        trace2d(sb, srca, dtc, Ia.y, 2 * Ia.z + 1, ka, uRa);
+        trace2d(sb, srcb, dtc, Ib.x, 2 * Ib.z, kb, uLb);
+        trace2d(sb, srcb, dtc, Ib.y, 2 * Ib.z + 1, kb, uRb);
+        numflux2d(uLa, uRa, Ia.z, g, md.surface, fa);
+        numflux2d(uLb, uRb, Ib.z, g, md.surface, fb);
+        if (NS) {
+#pragma unroll
+            for (int c = 0; c < GV; ++c) {
+                fa[1 + c] -= 0.5 * (__ldg(Vt + gidx2d(Ia.x, 2 * Ia.z, c, ka)) + __ldg(Vt + gidx2d(Ia.y, 2 * Ia.z + 1, c, ka)));
+                fb[1 + c] -= 0.5 * (__ldg(Vt + gidx2d(Ib.x, 2 * Ib.z, c, kb)) + __ldg(Vt + gidx2d(Ib.y, 2 * Ib.z + 1, c, kb)));
+            }
+        }
+        store_face2d(Fs, Ia.x, 2 * Ia.z, ka, fa);
+        store_face2d(Fs, Ia.y, 2 * Ia.z + 1, ka, fa);
+        store_face2d(Fs, Ib.x, 2 * Ib.z, kb, fb);
+        store_face2d(Fs, Ib.y, 2 * Ib.z + 1, kb, fb);
+    }
+    for (; gt < total; gt += GS) {
         const int item = gt >> 2, k = gt & 3;
         if (item < nif) {
             const int4 I = MODE == MODE_STAGE ? md.ifcs[item] : md.ifc[item];
