@@ -18,6 +18,7 @@
 #include "dg1d.cuh"
 #include "dg2d.cuh"
 #include "br1.cuh"
+#include "step1d.cuh"
 #include "transfer.cuh"
 
 using namespace perk;
@@ -50,6 +51,9 @@ struct perk_ctx {
     uint8_t *lev_old = nullptr;
     int vol_blocks = 0, surf_blocks = 0, grad_blocks = 0;
     unsigned kind_mask = ~0u;              // kernel kinds launch_step issues (perk_time_kernels)
+    bool step1d = false;                   // small 1D mesh: whole step in one single-CTA launch
+    StepTab1D *tb1d = nullptr;
+    size_t step1d_smem = 0;
     cudaGraphExec_t gexec = nullptr;
     double *gU = nullptr;
     double gdt = 0.0;
@@ -316,6 +320,15 @@ static void launch_br1(perk_ctx *c, cudaStream_t s, const StageParams &sp, const
 
 static void launch_step(perk_ctx *c, cudaStream_t s, double *U, double dt, Prof *p)
 {
+    if (c->step1d) {
+        prof_mark(p, s, 1);
+        if ((c->kind_mask >> 1) & 1u) {
+            if (c->nv == 1) k_step1d<1><<<1, step1d_threads(1), c->step1d_smem, s>>>(c->md, c->tb1d, U, dt, c->Wb != nullptr);
+            else k_step1d<3><<<1, step1d_threads(3), c->step1d_smem, s>>>(c->md, c->tb1d, U, dt, c->Wb != nullptr);
+        }
+        prof_mark(p, s, -1);
+        return;
+    }
     for (int i = 1; i <= c->tab.S; ++i) {
         const StageParams sp = stage_params(c, i, dt, MODE_STAGE, 0u);
         if (c->ns) launch_br1(c, s, sp, U, nullptr, p);
@@ -516,6 +529,36 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
     CU(cudaGetLastError());
     rc = check_device_err(c);
     *out = c;
+    if (rc == PERK_OK && dim == 1) {
+        // small 1D meshes (static: 1D has no re-mesh): one single-CTA launch per step if the whole
+        // state fits in shared memory
+        int n = 0;
+        CU(cudaMemcpy(&n, md.n, sizeof(int), cudaMemcpyDeviceToHost));
+        const size_t sh = step1d_smem_bytes(n, c->nv, c->Wb != nullptr);
+        if (sh <= 200u * 1024u) {
+            StepTab1D h;
+            memset(&h, 0, sizeof(h));
+            h.S = tab->S;
+            h.R = tab->R;
+            for (int r = 0; r < tab->R; ++r) {
+                h.first[r] = tab->S - tab->E[r] + 2;
+                for (int i = 0; i < tab->S; ++i) {
+                    h.asub[r][i] = tab->a_sub[r][i];
+                    h.a1[r][i] = tab->c[i] - tab->a_sub[r][i];
+                }
+            }
+            for (int i = 0; i < tab->S; ++i) h.c[i] = tab->c[i];
+            h.b1 = tab->b[0];
+            h.bS1 = tab->S >= 2 ? tab->b[tab->S - 2] : 0.0;
+            h.bS = tab->b[tab->S - 1];
+            CU(dalloc(c, &c->tb1d, 1));
+            CU(cudaMemcpy(c->tb1d, &h, sizeof(h), cudaMemcpyHostToDevice));
+            CU(cudaFuncSetAttribute(k_step1d<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            CU(cudaFuncSetAttribute(k_step1d<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            c->step1d_smem = sh;
+            c->step1d = true;
+        }
+    }
     return rc;
 }
 
@@ -569,7 +612,7 @@ extern "C" int perk_launches_per_step(perk_ctx *c, int32_t *launches)
 {
     if (!c) return PERK_ENOTINIT;
     if (!launches) return PERK_EINVAL;
-    *launches = (c->ns ? 4 : 2) * c->tab.S;
+    *launches = c->step1d ? 1 : (c->ns ? 4 : 2) * c->tab.S;
     return PERK_OK;
 }
 

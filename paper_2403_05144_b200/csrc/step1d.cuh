@@ -1,0 +1,152 @@
+// step1d.cuh -- a whole P-ERK step of a small 1D mesh in ONE single-CTA launch (BASELINE cfg 1/2:
+// 48 / 352 cells, SURVEY §7 "tiny configs are latency-bound").
+//
+// The state (U_n, K_1, the stage buffer, the current K and the face fluxes; W for P-ERK3) lives in
+// shared memory for the whole step; the S stages are separated by __syncthreads instead of kernel
+// boundaries.  Per stage the threads loop over the ACTIVE prefixes only (interfaces, boundaries, then
+// element nodes), so a stage costs ceil(active / blockDim) passes: the multirate saving shows up in
+// wall time, which it cannot with two ~3 us launches per stage.  Same arithmetic as k_surf1d /
+// k_vol1d (weak form, upwind / Rusanov, lazy first-order states, fused stage combination).
+#pragma once
+#include "dg1d.cuh"
+
+namespace perk {
+
+struct StepTab1D {
+    int S, R;
+    int first[MAXR];             // f(r) = S - E_r + 2
+    double c[MAXS];
+    double b1, bS1, bS;          // shared weights at stages 1, S-1, S
+    double a1[MAXR][MAXS];       // a_{i,1}^{(r)}, index i-1
+    double asub[MAXR][MAXS];     // a_{i,i-1}^{(r)}, index i-1
+};
+
+// threads per CTA: the per-stage cost is ceil(active nodes / threads) dependent passes; measured
+// best (B200): 256 for advection (cfg 1: 0.018 ms/step), 512 for Euler (cfg 2: 0.070 ms/step)
+__host__ __device__ constexpr int step1d_threads(int nv) { return nv == 1 ? 256 : 512; }
+
+__host__ __device__ inline size_t step1d_smem_bytes(int n, int nv, bool use_w)
+{
+    return sizeof(double) * ((size_t)n * nv * NP * (use_w ? 5 : 4) + (size_t)n * 2 * nv);
+}
+
+template <int NV>
+__global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const StepTab1D *__restrict__ tb,
+                                                            double *__restrict__ U, double dt, int use_w)
+{
+    extern __shared__ __align__(16) double sh[];
+    __shared__ StepTab1D T;
+    const int n = md.n[0];
+    const int rowd = NV * NP;
+    double *sUn = sh, *sK1 = sUn + (size_t)n * rowd, *sUb = sK1 + (size_t)n * rowd, *sKi = sUb + (size_t)n * rowd;
+    double *sW = sKi + (size_t)n * rowd;
+    double *sFs = use_w ? sW + (size_t)n * rowd : sW;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    {
+        const int *src = reinterpret_cast<const int *>(tb);
+        int *dst = reinterpret_cast<int *>(&T);
+        for (int k = tid; k < (int)(sizeof(StepTab1D) / sizeof(int)); k += nt) dst[k] = src[k];
+    }
+    for (int k = tid; k < n * rowd; k += nt) sUn[k] = U[k];
+    __syncthreads();
+    const int S = T.S;
+    for (int i = 1; i <= S; ++i) {
+        const int nif = md.count_active[KIND_IF * MAXS + i - 1];
+        const int nbd = md.count_active[KIND_BD * MAXS + i - 1];
+        const int nel = md.count_active[KIND_EL * MAXS + i - 1];
+        const double dtc = dt * T.c[i - 1];
+        // the stage-i state of element e (member m), variable v, node j (SURVEY §7 rule)
+        auto state = [&](int e, int m, int v, int j) {
+            const size_t x = ((size_t)e * NV + v) * NP + j;
+            if (i == 1) return sUn[x];
+            if (i > T.first[m]) return sUb[x];
+            return fma(dtc, sK1[x], sUn[x]);
+        };
+        // surface fluxes over the active interfaces and boundaries
+        for (int t = tid; t < nif + nbd; t += nt) {
+            double uL[NV], uR[NV], f[NV];
+            if (t < nif) {
+                const int4 I = md.ifc[md.list[KIND_IF][t]];
+                const int mL = md.mem[I.x], mR = md.mem[I.y];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    uL[v] = state(I.x, mL, v, NP - 1);
+                    uR[v] = state(I.y, mR, v, 0);
+                }
+                numflux1d<NV>(uL, uR, md.gamma, md.adv, f);
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    sFs[((size_t)I.x * 2 + 0) * NV + v] = f[v];
+                    sFs[((size_t)I.y * 2 + 1) * NV + v] = f[v];
+                }
+            } else {
+                const int2 B = md.bnd[md.list[KIND_BD][t - nif]];
+                const int face = B.y & 7;
+                double u[NV], gst[NV];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    u[v] = state(B.x, B.y >> 8, v, face == 0 ? NP - 1 : 0);
+                    gst[v] = md.bc[v];
+                }
+                if (face == 0) numflux1d<NV>(u, gst, md.gamma, md.adv, f);
+                else numflux1d<NV>(gst, u, md.gamma, md.adv, f);
+#pragma unroll
+                for (int v = 0; v < NV; ++v) sFs[((size_t)B.x * 2 + face) * NV + v] = f[v];
+            }
+        }
+        __syncthreads();
+        // K_i at the active element nodes (one thread per node)
+        for (int t = tid; t < NP * nel; t += nt) {
+            const int e = md.list[KIND_EL][t / NP], j = t % NP;
+            const int m = md.mem[e];
+            double f[NP][NV];
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+                double u[NV];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) u[v] = state(e, m, v, k);
+                phys_flux1d<NV>(u, md.gamma, md.adv, f[k]);
+            }
+            const double J = 2.0 / (md.hf * (double)(1 << (md.max_level - md.lev[e])));
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                double s = 0.0;
+#pragma unroll
+                for (int k = 0; k < NP; ++k) s = fma(cB.Dhat[j][k], f[k][v], s);
+                if (j == 0) s = fma(sFs[((size_t)e * 2 + 1) * NV + v], cB.invw[0], s);
+                if (j == NP - 1) s = fma(-sFs[((size_t)e * 2 + 0) * NV + v], cB.invw[NP - 1], s);
+                sKi[((size_t)e * NV + v) * NP + j] = J * s;
+            }
+        }
+        __syncthreads();
+        // stage combination (every state read of this stage is done)
+        for (int t = tid; t < NP * nel; t += nt) {
+            const int e = md.list[KIND_EL][t / NP], j = t % NP;
+            const int m = md.mem[e];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const size_t x = ((size_t)e * NV + v) * NP + j;
+                const double K = sKi[x];
+                if (i == 1) {
+                    sK1[x] = K;
+                } else if (i == S) {
+                    sUn[x] = fma(dt * T.bS, K, use_w ? sW[x] : sUn[x]);
+                } else {
+                    const double un = sUn[x], k1 = sK1[x];
+                    sUb[x] = fma(dt, fma(T.a1[m][i], k1, T.asub[m][i] * K), un);    // U^(i+1)
+                    if (use_w && i == S - 1) sW[x] = fma(dt, fma(T.b1, k1, T.bS1 * K), un);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    for (int k = tid; k < n * rowd; k += nt) U[k] = sUn[k];
+    if (tid == 0) {
+        unsigned long long tot = 0;
+        for (int i = 0; i < S; ++i) tot += (unsigned long long)md.count_active[KIND_EL * MAXS + i];
+        atomicAdd(md.evals, tot);
+        atomicAdd(md.evals + 1, 1ull);
+    }
+}
+
+}  // namespace perk
