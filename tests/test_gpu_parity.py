@@ -409,3 +409,34 @@ def test_p3_rejects_E2_member():
     with pytest.raises(PerkError) as ei:
         Perk(w.problem, w.level_map, 16, fam["E"], family=fam)
     assert ei.value.code == -1
+
+
+@pytest.mark.parametrize("order", [2, 3])
+def test_ns_repartition(order):
+    """BR1 Navier-Stokes across device re-meshes (cfg-4 structure, KH state, mu = 1e-3), P-ERK2 and
+    P-ERK3: lists bit-exact after each re-mesh, states <= 1e-10."""
+    from paper_2403_05144_b200 import Perk
+    from workloads import perk3 as P3
+    w = W.make(4, n_base=16, max_level=3, widths=(0.3, 0.15, 0.06))
+    w.S, w.E = 16, [4, 6, 10, 16]
+    prob = dict(w.problem, equation="navier_stokes", mu=1e-3, prandtl=0.72)
+    fam = T.family(w.S, w.E, "taylor") if order == 2 else P3.family3(w.S, w.E)
+    cap = 4 * W.configs.count_leaves(w)
+    ora = O.OracleMesh(prob, w.level_map, fam)
+    gpu = Perk(prob, w.level_map, w.S, w.E, max_cells=cap, family=None if order == 2 else fam)
+    Uo = ora.initial_state(w.ic)
+    Ug = gpu.initial_state(w.ic)
+    for k in range(1, 4):
+        ora.step(Uo, w.dt, 5)
+        gpu.step(Ug, w.dt, 5)
+        lm = w.level_map_seq(k)
+        ora_new = O.OracleMesh(prob, lm, fam)
+        Uo = O.transfer(ora, ora_new, Uo)
+        ora = ora_new
+        gpu.repartition(lm, Ug)
+        gpu.sync()
+        compare_mesh(ora, gpu)
+    ora.step(Uo, w.dt, 5)
+    gpu.step(Ug, w.dt, 5)
+    torch.cuda.synchronize()
+    assert rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo).max() <= TOL
