@@ -3,11 +3,14 @@
 // The paper cites BR1 (P:l.1419-1420) without defining it.  Per stage, before the inviscid+viscous
 // surface kernel (k_surf2d<.., NS>) and the volume kernel (k_vol2d<.., NS>):
 //   k_gsurf2d : central traces w* = (w_L + w_R)/2 of the gradient variables w = (v1, v2, T) on the
-//               interfaces and mortars of the EXTENDED prefix (active members + the next coarser
-//               member: the coarse neighbours across active mortars need gradients too); mortars:
-//               halves (P w_large + w_small)/2, the large side gets R_lower w*_lo + R_upper w*_hi.
-//   k_grad2d  : on the elements of the extended prefix, q = grad w (weak form with w*), then the
+//               active interfaces and mortars PLUS the faces of the halo (the large elements of the
+//               active mortars, which belong to the next coarser member and whose gradients the
+//               active viscous face fluxes need; MeshDev::halo); mortars: halves
+//               (P w_large + w_small)/2, the large side gets R_lower w*_lo + R_upper w*_hi.
+//   k_grad2d  : on the active elements and the halo, q = grad w (weak form with w*), then the
 //               normal viscous flux F^v_n(u, q) at the 12 face nodes -> Vt, read by k_surf2d.
+// (The oracle evaluates gradients on the whole next coarser member instead; both give the same
+// gradients on every element whose viscous face flux is used.)
 // The volume kernel recomputes q from the state and w* (cheaper than storing 16 x 6 gradients).
 #pragma once
 #include "dg2d.cuh"
@@ -20,13 +23,18 @@ __global__ void __launch_bounds__(256, 3) k_gsurf2d(MeshDev md, StageParams sp, 
                                                 const double *__restrict__ Uin, double *__restrict__ Gs)
 {
     pdl_wait();
-    int nif, nmo;
+    // items: [active interfaces | halo interfaces | active mortars | halo mortars]
+    int nif_a, nmo_a;
+    int2 hif = make_int2(0, 0), hmo = make_int2(0, 0);
     if (MODE == MODE_STAGE) {
-        nif = md.count_active[EXT_OFF + KIND_IF * MAXS + sp.stage - 1];
-        nmo = md.count_active[EXT_OFF + KIND_MO * MAXS + sp.stage - 1];
+        nif_a = md.count_active[KIND_IF * MAXS + sp.stage - 1];
+        nmo_a = md.count_active[KIND_MO * MAXS + sp.stage - 1];
+        hif = md.hrng[KIND_IF * MAXS + sp.stage - 1];
+        hmo = md.hrng[KIND_MO * MAXS + sp.stage - 1];
     } else {
-        nif = md.n[1]; nmo = md.n[2];
+        nif_a = md.n[1]; nmo_a = md.n[2];
     }
+    const int nif = nif_a + hif.y, nmo = nmo_a + hmo.y;
     const int total = 4 * (nif + nmo);
     const StateBufs sb{Un, Ubuf, K1, Uin};
     const double dtc = sp.dt * sp.c_stage;
@@ -36,8 +44,8 @@ __global__ void __launch_bounds__(256, 3) k_gsurf2d(MeshDev md, StageParams sp, 
     for (int gt = blockIdx.x * blockDim.x + threadIdx.x; gt < total; gt += gridDim.x * blockDim.x) {
         const int item = gt >> 2, k = gt & 3;
         if (item < nif) {
-            const int f = MODE == MODE_STAGE ? md.list[KIND_IF][item] : item;
-            const int4 I = md.ifc[f];
+            const int4 I = MODE == MODE_RHS ? md.ifc[item]
+                                            : (item < nif_a ? md.ifcs[item] : md.ifc[md.hlist[KIND_IF][hif.x + item - nif_a]]);
             const int o = I.z;
             const int src = state_src(sp, I.w);
             double uL[4], uR[4], wL[GV], wR[GV];
@@ -53,8 +61,7 @@ __global__ void __launch_bounds__(256, 3) k_gsurf2d(MeshDev md, StageParams sp, 
             }
         } else {
             const int q = item - nif;
-            const int mo = MODE == MODE_STAGE ? md.list[KIND_MO][q] : q;
-            const int4 M = md.mor[mo];
+            const int4 M = MODE == MODE_RHS ? md.mor[q] : (q < nmo_a ? md.mors[q] : md.mor[md.hlist[KIND_MO][hmo.x + q - nmo_a]]);
             const int o = M.w & 1, side = (M.w >> 1) & 1, mfine = M.w >> 8;
             const int lf = 2 * o + side, sf = 2 * o + 1 - side;
             double ul[4], us0[4], us1[4], wl[GV], ws0[GV], ws1[GV];
@@ -117,7 +124,10 @@ __global__ void __launch_bounds__(128, 4) k_grad2d(MeshDev md, StageParams sp, c
     double (*gst)[4 * GV * NP] = reinterpret_cast<double (*)[4 * GV * NP]>(reinterpret_cast<unsigned char *>(stg) +
                                                                            sizeof(double) * VOL2D_EPB * 2 * 64);
     const int t8 = threadIdx.x & 7, le = threadIdx.x >> 3;
-    const int n_act = MODE == MODE_STAGE ? md.count_active[EXT_OFF + KIND_EL * MAXS + sp.stage - 1] : md.n[0];
+    // items: [active elements | halo elements of the member below the lowest active one]
+    const int n_el_a = MODE == MODE_STAGE ? md.count_active[KIND_EL * MAXS + sp.stage - 1] : md.n[0];
+    const int2 hel = MODE == MODE_STAGE ? md.hrng[KIND_EL * MAXS + sp.stage - 1] : make_int2(0, 0);
+    const int n_act = n_el_a + hel.y;
     const double gm1 = md.gamma - 1.0;
     const double dtc = sp.dt * sp.c_stage;
     const int q0 = 2 * t8;
@@ -128,7 +138,7 @@ __global__ void __launch_bounds__(128, 4) k_grad2d(MeshDev md, StageParams sp, c
     auto entry_at = [&](int b) {
         const int t = b + le;
         const int tt = t < n_act ? t : b;
-        if (MODE == MODE_STAGE) return md.elpk[tt];
+        if (MODE == MODE_STAGE) return tt < n_el_a ? md.elpk[tt] : md.hpk[hel.x + tt - n_el_a];
         return tt | ((int)md.mem[tt] << PK_EBITS) | ((int)md.lev[tt] << (PK_EBITS + 3));
     };
     auto copy_chunks = [&](double *dst, const double *src, int nchunks) {   // 16 B chunks over 8 threads

@@ -19,9 +19,6 @@ constexpr int MAXR = 8;
 constexpr int SM_COUNT_B200 = 148;
 
 enum Kind { KIND_EL = 0, KIND_IF = 1, KIND_MO = 2, KIND_BD = 3 };
-// count_active[EXT_OFF + kind * MAXS + i - 1]: items of the active members at stage i plus the next
-// coarser member (BR1 gradients are needed one element beyond the active set across mortars)
-constexpr int EXT_OFF = 4 * MAXS;
 enum Mode { MODE_STAGE = 0, MODE_RHS = 1 };
 enum ErrBits { ERR_UNBALANCED = 1, ERR_CAPACITY = 2, ERR_TRANSFER = 4 };
 
@@ -48,7 +45,7 @@ struct MeshDev {
     int cap;                     // cell capacity
     // device pointers
     int *n;                      // [4]: cells, interfaces, mortars, boundaries
-    int *count_active;           // [4][MAXS] stage prefix counts, then [4][MAXS] BR1 gradient prefixes (EXT_OFF)
+    int *count_active;           // [4][MAXS] stage prefix counts
     int *seg;                    // [4][MAXR+1]
     int *err;                    // error flag bits
     unsigned long long *evals;   // element-RHS evaluation counter
@@ -60,6 +57,16 @@ struct MeshDev {
     // hot-path copies in list (member-sorted) order, so a stage kernel reaches its item with one load:
     int *elpk;                   // elements: e | member << 24 | level << 27 (PK_* below)
     int4 *ifcs; int4 *mors;      // interface / mortar records in list order
+    // BR1 halo (Navier-Stokes): the gradients of an active element's neighbours across mortars are
+    // needed; those neighbours are the LARGE sides of mortars of the finer member.  halo[e] = 1 for
+    // such elements; per member, halo element / interface / mortar lists (faces of halo elements
+    // that belong to the halo's own member); hrng[kind][stage] = {start, count} of the halo lists
+    // a stage needs (the halo of the lowest active member; empty at stage 1).
+    uint8_t *halo;
+    int *hlist[3];               // elements, interfaces, mortars (member-sorted, descending)
+    int *hseg;                   // [3][MAXR + 1]
+    int2 *hrng;                  // [3][MAXS]
+    int *hpk;                    // packed entries of hlist[KIND_EL]
 };
 
 // packed element entry of md.elpk (cells < 2^24, members < 8, levels < 16)

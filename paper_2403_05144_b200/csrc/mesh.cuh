@@ -13,6 +13,7 @@
 // interface and a level-jump interface belongs to the fine side's member.
 #pragma once
 #include "common.cuh"
+#include "partition.cuh"
 
 namespace perk {
 
@@ -215,6 +216,38 @@ __global__ void k_hot_lists(MeshDev md)
     }
     if (t < md.n[1]) md.ifcs[t] = md.ifc[md.list[KIND_IF][t]];
     if (t < md.n[2]) md.mors[t] = md.mor[md.list[KIND_MO][t]];
+}
+
+// BR1 halo flags: the large side of a mortar whose fine side belongs to another member
+__global__ void k_halo_clear(MeshDev md)
+{
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < md.cap) md.halo[e] = 0;
+}
+__global__ void k_halo_flags(MeshDev md)
+{
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= md.n[2]) return;
+    const int4 M = md.mor[q];
+    if ((int)md.mem[M.x] != (M.w >> 8)) md.halo[M.x] = 1;
+}
+// per stage, the halo lists of the member just below the lowest active one; packed halo entries
+__global__ void k_halo_ranges(MeshDev md, ActiveDesc ad)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < 3 * ad.S) {
+        const int kind = t / ad.S, i = t % ad.S + 1;
+        int k = 0;
+        for (int r = 0; r < ad.R; ++r)
+            if (i == 1 || ad.E[r] >= ad.S - i + 2) ++k;
+        const int *sg = md.hseg + kind * (MAXR + 1);
+        md.hrng[kind * MAXS + i - 1] = k < ad.R ? make_int2(sg[k], sg[k + 1] - sg[k]) : make_int2(0, 0);
+    }
+    const int total = md.hseg[KIND_EL * (MAXR + 1) + ad.R];
+    for (int h = t; h < total; h += gridDim.x * blockDim.x) {
+        const int e = md.hlist[KIND_EL][h];
+        md.hpk[h] = e | ((int)md.mem[e] << PK_EBITS) | ((int)md.lev[e] << (PK_EBITS + 3));
+    }
 }
 
 __global__ void k_node_coords(MeshDev md, double *xy)

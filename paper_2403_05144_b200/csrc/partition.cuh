@@ -28,6 +28,21 @@ struct KeyBnd {
     const int2 *a;
     __device__ int operator()(int i) const { return a[i].y >> 8; }
 };
+// BR1 halo keys: the member for flagged items, -1 (not partitioned) otherwise
+struct KeyHaloEl {
+    const uint8_t *halo, *mem;
+    __device__ int operator()(int i) const { return halo[i] ? (int)mem[i] : -1; }
+};
+struct KeyHaloIf {
+    const int4 *a;
+    const uint8_t *halo;
+    __device__ int operator()(int i) const { const int4 I = a[i]; return (halo[I.x] | halo[I.y]) ? I.w : -1; }
+};
+struct KeyHaloMo {
+    const int4 *a;
+    const uint8_t *halo;
+    __device__ int operator()(int i) const { const int4 M = a[i]; return (halo[M.y] | halo[M.z]) ? (M.w >> 8) : -1; }
+};
 
 // Stage-activity description for the count_active table (P:l.428: member r evaluates stage i iff
 // i == 1 or E_r >= S - i + 2).
@@ -83,8 +98,7 @@ __device__ __forceinline__ int block_incl_scan(int v, int *wsum, int &total)
 
 // One block.  blockoff[b][r] = start of block b's bucket-r items; seg[s] = start of segment s
 // (key R-1-s), seg[R] = total.  Optionally: *total_out = total, and count_active[i-1] for the
-// member partitions (active members are the top ones, i.e. a prefix of the segments), and
-// count_active[EXT_OFF + i-1] for the prefix extended by the next coarser member (BR1 gradients).
+// member partitions (active members are the top ones, i.e. a prefix of the segments).
 __global__ void __launch_bounds__(PART_T) k_part_offsets(const int *blockcnt, int nblocks, int R, int *blockoff, int *seg,
                                                         int *total_out, ActiveDesc ad, int *count_active)
 {
@@ -113,7 +127,6 @@ __global__ void __launch_bounds__(PART_T) k_part_offsets(const int *blockcnt, in
         for (int r = 0; r < ad.R; ++r)
             if (i == 1 || ad.E[r] >= ad.S - i + 2) ++k;
         count_active[i - 1] = seg[k];
-        count_active[EXT_OFF + i - 1] = seg[k < ad.R ? k + 1 : ad.R];
     }
 }
 

@@ -214,6 +214,17 @@ static void build_mesh(perk_ctx *c, cudaStream_t s, const uint8_t *lmap)
     partition(c, s, KeyBnd{md.bnd}, md.n + 3, 1, c->cap_faces, R, md.list[KIND_BD], nullptr, md.seg + 3 * (MAXR + 1),
               nullptr, md.count_active + KIND_BD * MAXS);
     k_hot_lists<<<blocks_for(c->cap_faces, 256), 256, 0, s>>>(md);
+    if (c->ns) {   // BR1 halo lists (see MeshDev::halo)
+        k_halo_clear<<<blocks_for(c->cap, 256), 256, 0, s>>>(md);
+        k_halo_flags<<<blocks_for(c->cap_faces, 256), 256, 0, s>>>(md);
+        partition(c, s, KeyHaloEl{md.halo, md.mem}, md.n + 0, 1, c->cap, R, md.hlist[KIND_EL], nullptr,
+                  md.hseg + KIND_EL * (MAXR + 1), nullptr, nullptr);
+        partition(c, s, KeyHaloIf{md.ifc, md.halo}, md.n + 1, 1, c->cap_faces, R, md.hlist[KIND_IF], nullptr,
+                  md.hseg + KIND_IF * (MAXR + 1), nullptr, nullptr);
+        partition(c, s, KeyHaloMo{md.mor, md.halo}, md.n + 2, 1, c->cap_faces, R, md.hlist[KIND_MO], nullptr,
+                  md.hseg + KIND_MO * (MAXR + 1), nullptr, nullptr);
+        k_halo_ranges<<<SM_COUNT_B200, 256, 0, s>>>(md, active_desc(c));
+    }
 }
 
 // ----------------------------------------------------------------------------------------------
@@ -466,7 +477,7 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
     const long long max_items = c->nmorton > (long long)c->nd * c->cap ? c->nmorton : (long long)c->nd * c->cap;
     const int nb_max = (int)((max_items + PART_T - 1) / PART_T) + 1;
     CU(dalloc(c, &md.n, 4));
-    CU(dalloc(c, &md.count_active, 2 * EXT_OFF));
+    CU(dalloc(c, &md.count_active, 4 * MAXS));
     CU(dalloc(c, &md.seg, 4 * (MAXR + 1)));
     CU(dalloc(c, &md.err, 1));
     CU(dalloc(c, &md.evals, 2));
@@ -488,6 +499,13 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
     CU(dalloc(c, &c->Fs, (size_t)c->cap * (dim == 1 ? 2 * c->nv : 4 * c->nv * NP)));
     if (tab->b[0] != 0.0 || tab->b[tab->S - 2] != 0.0) CU(dalloc(c, &c->Wb, (size_t)c->cap * rowd));
     if (c->ns) {
+        CU(dalloc(c, &md.halo, c->cap));
+        CU(dalloc(c, &md.hlist[KIND_EL], c->cap));
+        CU(dalloc(c, &md.hlist[KIND_IF], c->cap_faces));
+        CU(dalloc(c, &md.hlist[KIND_MO], c->cap_faces));
+        CU(dalloc(c, &md.hseg, 3 * (MAXR + 1)));
+        CU(dalloc(c, &md.hrng, 3 * MAXS));
+        CU(dalloc(c, &md.hpk, c->cap));
         CU(dalloc(c, &c->Gs, (size_t)c->cap * 4 * GV * NP));
         CU(dalloc(c, &c->Vt, (size_t)c->cap * 4 * GV * NP));
     }
