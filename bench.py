@@ -206,49 +206,63 @@ def measure_config(cfg, K, Wm, timer, torch, dist, ws, dev, with_single=True, or
     U = perk.initial_state(w.ic)
     res = {"workload": w.name + ("_perk3" if order == 3 else ""), "cells": perk.n_cells, "S": w.S, "E": w.E,
            "order": order, "dt": w.dt}
-    remesh = []
+    maps = []
     if w.remesh_every:
         # level maps of the re-meshes inside the measured window, uploaded before the timed region
         nmaps = (K + Wm) // w.remesh_every + 1
         maps = [torch.from_numpy(np.ascontiguousarray(w.level_map_seq(k))).to(dev) for k in range(1, nmaps + 1)]
+
+    def timed(p, Ux, Kx):
+        """mean ms per step; with re-meshing, the device repartition every remesh_every steps is inside
+        the timed steps and timed separately as well"""
+        if not w.remesh_every:
+            return float(np.mean(timer.steps(lambda k: p.step(Ux, w.dt), Kx, Wm))), []
         state = {"n": 0, "k": 0}
         rp_ev = []
 
         def run_step(_):
-            perk.step(U, w.dt)
+            p.step(Ux, w.dt)
             state["n"] += 1
             if state["n"] % w.remesh_every == 0 and state["k"] < len(maps):
                 a = torch.cuda.Event(enable_timing=True)
                 b = torch.cuda.Event(enable_timing=True)
                 a.record(timer.stream)
-                perk.repartition(maps[state["k"]], U)
+                p.repartition(maps[state["k"]], Ux)
                 b.record(timer.stream)
                 rp_ev.append((a, b))
                 state["k"] += 1
-        times = timer.steps(run_step, K, Wm)
+        t = timer.steps(run_step, Kx, Wm)
         torch.cuda.synchronize()
-        perk.sync()
-        remesh = [a.elapsed_time(b) for a, b in rp_ev]
+        p.sync()
+        return float(np.mean(t)), [a.elapsed_time(b) for a, b in rp_ev]
+
+    ms_raw, remesh = timed(perk, U, K)
+    if w.remesh_every:
         res["remesh_every"] = w.remesh_every
         res["repartitions_in_run"] = len(remesh)
         res["repartition_ms_mean"] = round(float(np.mean(remesh)), 5) if remesh else None
         ev, st = perk.counters()
         elem_rhs_per_step = ev / max(st, 1)
     else:
-        times = timer.steps(lambda k: perk.step(U, w.dt), K, Wm)
         elem_rhs_per_step = int(sum(int(x) for x in perk.count_active("elements")))
-    ms = _max_over_ranks(torch, dist, ws, dev, float(np.mean(times)))
+    ms = _max_over_ranks(torch, dist, ws, dev, ms_raw)
     res.update(ms_per_step=round(ms, 5), element_rhs_per_step=round(float(elem_rhs_per_step), 1),
                value=round(replica_value(ws, elem_rhs_per_step, ms), 1), n_cells_now=perk.n_cells)
-    if with_single and not w.remesh_every:
-        single = Perk(w.problem, w.level_map, w.S, [w.S], family=single_fam)
+    if with_single:
+        # single-rate S-stage P-ERK on the same mesh (and the same re-mesh sequence)
+        single = Perk(w.problem, w.level_map, w.S, [w.S], family=single_fam,
+                      max_cells=w.problem["max_cells"])
         Us = single.initial_state(w.ic)
-        ms_s = _max_over_ranks(torch, dist, ws, dev,
-                               float(np.mean(timer.steps(lambda k: single.step(Us, w.dt), max(3, K // 2), Wm))))
+        ms_s = _max_over_ranks(torch, dist, ws, dev, timed(single, Us, max(3, K // 2) if not w.remesh_every else K)[0])
+        if w.remesh_every:
+            ev_s, st_s = single.counters()
+            cells_per_step = ev_s / max(st_s, 1) / w.S       # mean cell count over the run
+        else:
+            cells_per_step = perk.n_cells
         single.close()
         res["single_rate_ms_per_step"] = round(ms_s, 5)
         res["multirate_speedup"] = round(ms_s / ms, 4)
-        res["ideal_multirate_speedup"] = round(w.S * perk.n_cells / elem_rhs_per_step, 4)
+        res["ideal_multirate_speedup"] = round(w.S * cells_per_step / elem_rhs_per_step, 4)
     return perk, U, w, res
 
 
