@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -61,7 +62,9 @@ struct perk_ctx {
     std::string err;
 };
 
-static bool g_basis_uploaded = false;
+// __constant__ basis tables are per device: one upload per device a context is created on
+static std::mutex g_basis_mutex;
+static unsigned long long g_basis_uploaded = 0;   // bit d: uploaded on device d
 
 static int set_err(perk_ctx *c, int code, const std::string &msg)
 {
@@ -467,11 +470,16 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
     if (c->nmorton > (1ll << 30)) { *out = c; return set_err(c, PERK_EINVAL, "finest grid too large"); }
 
     CU(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
-    if (!g_basis_uploaded) {
-        BasisTables B;
-        build_basis(B);
-        CU(cudaMemcpyToSymbol(cB, &B, sizeof(B)));
-        g_basis_uploaded = true;
+    {
+        int dev = 0;
+        CU(cudaGetDevice(&dev));
+        std::lock_guard<std::mutex> lock(g_basis_mutex);
+        if (dev >= 64 || !((g_basis_uploaded >> dev) & 1ull)) {
+            BasisTables B;
+            build_basis(B);
+            CU(cudaMemcpyToSymbol(cB, &B, sizeof(B)));
+            if (dev < 64) g_basis_uploaded |= 1ull << dev;
+        }
     }
     const size_t rowd = (size_t)c->nv * c->npe;
     const long long max_items = c->nmorton > (long long)c->nd * c->cap ? c->nmorton : (long long)c->nd * c->cap;

@@ -440,3 +440,14 @@ def test_ns_repartition(order):
     gpu.step(Ug, w.dt, 5)
     torch.cuda.synchronize()
     assert rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo).max() <= TOL
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_e2_member(cfg):
+    """degenerate member E = 2 (evaluates stages 1 and S only; its stage-S state is the lazy
+    U_n + dt c_S K_1 while U_n is updated in place at stage S): 1D single-CTA path and 2D path"""
+    w = W.make(cfg, n_base=64 if cfg == 2 else 16, **({"w1": 16, "w2": 4} if cfg == 2 else {}))
+    w.S, w.E = 8, [2, 4, 8]
+    ora, gpu = build_pair(w)
+    Uo, Ug = _run_both(w, 40, ora, gpu)
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
