@@ -140,7 +140,10 @@ int perk_run_host(perk_ctx *ctx, double *U_host, double dt, int64_t nsteps);
 
 /* Re-mesh, asynchronous: rebuild leaves, faces, per-member lists and stage prefix tables from a new
  * level map on the device (no host round trip), and transfer U_dev in place (refine: interpolation,
- * coarsen: exact L2 projection; |level change| <= 1 per finest cell required). */
+ * coarsen: exact L2 projection; |level change| <= 1 per finest cell required).  2D only (1D meshes
+ * are static: EUNSUPPORTED).  An unbalanced / misaligned map (EUNBALANCED), a level jump > 1
+ * (EUNBALANCED) or more cells than max_cells (ECAPACITY) latch the device error flag and are
+ * reported by the next synchronising call; U_dev and the mesh are then undefined. */
 int perk_repartition(perk_ctx *ctx, const uint8_t *level_map_dev, double *U_dev);
 
 /* dU = sum_{r in mask} I^(r) F(U) (P:l.289-301): zero on cells of unmasked members.  Asynchronous.

@@ -362,8 +362,9 @@ static int check_device_err(perk_ctx *c)
     if (e) {
         int z = 0;
         CU(cudaMemcpy(c->md.err, &z, sizeof(int), cudaMemcpyHostToDevice));
-        if (e & ERR_UNBALANCED) return set_err(c, PERK_EUNBALANCED, "level map not block-aligned or not 2:1 face balanced");
+        // capacity first: an overflowing mesh is truncated, which the later checks then also flag
         if (e & ERR_CAPACITY) return set_err(c, PERK_ECAPACITY, "cell / face capacity exceeded");
+        if (e & ERR_UNBALANCED) return set_err(c, PERK_EUNBALANCED, "level map not block-aligned or not 2:1 face balanced");
         if (e & ERR_TRANSFER) return set_err(c, PERK_EUNBALANCED, "re-mesh changed a level by more than one");
     }
     return PERK_OK;

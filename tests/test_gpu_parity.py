@@ -451,3 +451,37 @@ def test_e2_member(cfg):
     ora, gpu = build_pair(w)
     Uo, Ug = _run_both(w, 40, ora, gpu)
     assert rel_err_per_var(Ug, Uo).max() <= TOL
+
+
+def test_repartition_errors_latch():
+    """capacity overflow and an unbalanced map during a device re-mesh are reported by the next
+    synchronising call (no host round trip inside perk_repartition)"""
+    from paper_2403_05144_b200 import Perk, PerkError
+    w = W.make(4, n_base=16, max_level=3, widths=(0.3, 0.15, 0.06))
+    w.S, w.E = 16, [4, 6, 10, 16]
+    n0 = W.configs.count_leaves(w)
+    gpu = Perk(w.problem, w.level_map, w.S, w.E, max_cells=n0)
+    U = gpu.initial_state(w.ic)
+    fine = np.minimum(w.level_map + 1, 3).astype(np.uint8)   # every leaf refined once: ~4x the cells
+    gpu.repartition(fine, U)
+    with pytest.raises(PerkError) as ei:
+        gpu.sync()
+    assert ei.value.code == -3
+    gpu2 = Perk(w.problem, w.level_map, w.S, w.E, max_cells=4 * n0)
+    U2 = gpu2.initial_state(w.ic)
+    bad = np.zeros_like(w.level_map)
+    bad[0:8, 0:8] = 3                                         # a level-3 block next to level 0
+    gpu2.repartition(bad, U2)
+    with pytest.raises(PerkError) as ei:
+        gpu2.sync()
+    assert ei.value.code == -2
+
+
+def test_1d_repartition_unsupported():
+    from paper_2403_05144_b200 import Perk, PerkError
+    w = W.make(1)
+    gpu = Perk(w.problem, w.level_map, w.S, w.E)
+    U = gpu.initial_state(w.ic)
+    with pytest.raises(PerkError) as ei:
+        gpu.repartition(w.level_map, U)
+    assert ei.value.code == -6
