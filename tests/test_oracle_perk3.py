@@ -67,6 +67,14 @@ def test_family_order_conditions_and_polynomial(S, Es):
             assert abs(np.array(fam["b_f"]) @ Ad @ cd - 1 / 6) < 1e-15
 
 
+def test_S3_is_shu_osher_ssprk3():
+    """S = E = 3: the Shu-Osher base of P:l.870-880 (c = (0, 1, 1/2), a_21 = 1, a_31 = a_32 = 1/4,
+    b = (1/6, 1/6, 4/6)) -- also SPEC.md's tableau example"""
+    fam = P3.family3(3, (3,))
+    assert fam["c_f"] == [0.0, 1.0, 0.5] and fam["b_f"] == [1 / 6, 1 / 6, 4 / 6]
+    assert fam["a1_f"][0] == [0.0, 1.0, 0.25] and fam["asub_f"][0] == [0.0, 0.0, 0.25]
+
+
 def test_E3_member_is_shu_osher():
     for S in (4, 8, 16):
         fam = P3.family3(S, (3,))

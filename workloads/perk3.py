@@ -37,6 +37,8 @@ DPS = 80
 
 
 def abscissae3(S: int) -> list:
+    if S == 3:                                   # the Shu-Osher base itself: c = (0, 1, 1/2)
+        return [Fr(0), Fr(1), Fr(1, 2)]
     return [Fr(i - 1, S - 3) for i in range(1, S - 1)] + [Fr(1), Fr(1, 2)]
 
 
@@ -75,7 +77,7 @@ def _admissible(x, c):
 @lru_cache(maxsize=None)
 def member3(S: int, E: int, alpha_rule: str = "taylor") -> dict:
     """x_i = a_{i,i-1} (i -> mpf) of the P-ERK3 member with E evaluations (reading P3b)."""
-    assert 3 <= E <= S and S >= 4
+    assert 3 <= E <= S and S >= 3
     with mp.workdps(DPS):
         c = [mp.mpf(v.numerator) / v.denominator for v in abscissae3(S)]
         b = [mp.mpf(v.numerator) / v.denominator for v in weights3(S)]
