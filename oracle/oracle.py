@@ -44,6 +44,28 @@ class OraTableau(C.Structure):
                 ("b", C.c_double * 64), ("a1", (C.c_double * 64) * 8), ("asub", (C.c_double * 64) * 8)]
 
 
+class OraAmr(C.Structure):
+    _fields_ = [("indicator", C.c_int32), ("variable", C.c_int32), ("base_level", C.c_int32),
+                ("med_level", C.c_int32), ("max_level", C.c_int32), ("_pad", C.c_int32),
+                ("med_threshold", C.c_double), ("max_threshold", C.c_double),
+                ("alpha_max", C.c_double), ("alpha_min", C.c_double), ("f_wave", C.c_double)]
+
+
+INDICATORS = {"hennemann_gassner": 0, "lohner": 1, "enstrophy": 2}
+AMR_VARIABLES = {"rho": 0, "p": 1, "rho_p": 2, "v_x": 3, "v_y": 4}
+
+
+def amr_struct(a: dict) -> OraAmr:
+    s = OraAmr()
+    s.indicator = INDICATORS[a["indicator"]]
+    s.variable = AMR_VARIABLES[a.get("variable", "rho")]
+    s.base_level, s.med_level, s.max_level = a["base_level"], a["med_level"], a["max_level"]
+    s.med_threshold, s.max_threshold = a["med_threshold"], a["max_threshold"]
+    s.alpha_max, s.alpha_min = a.get("alpha_max", 0.5), a.get("alpha_min", 0.001)
+    s.f_wave = a.get("f_wave", 0.2)
+    return s
+
+
 _lib = None
 
 
@@ -82,6 +104,10 @@ def lib():
         L.ora_flux_ranocha.argtypes = [dp, dp, C.c_int, C.c_double, dp]
         L.ora_num_flux_pub.argtypes = [P, dp, dp, C.c_int, dp]
         L.ora_get_basis.argtypes = [dp]
+        L.ora_amr_indicator.restype = C.c_int
+        L.ora_amr_indicator.argtypes = [P, dp, C.POINTER(OraAmr), dp]
+        L.ora_amr_adapt.restype = C.c_int
+        L.ora_amr_adapt.argtypes = [P, dp, C.POINTER(OraAmr), up]
         _lib = L
     return _lib
 
@@ -232,6 +258,27 @@ class OracleMesh:
         """In place; returns element-RHS evaluations.  mode 1 = restricted (default), 0 = reference."""
         assert U.flags["C_CONTIGUOUS"] and U.dtype == np.float64
         return lib().ora_steps(self.h, U.reshape(-1), dt, nsteps, mode)
+
+
+    def amr_indicator(self, U, amr: dict):
+        """per-leaf AMR indicator (section 8 of perk_oracle.c), canonical leaf order"""
+        ind = np.zeros(self.n)
+        a = amr_struct(amr)
+        rc = lib().ora_amr_indicator(self.h, np.ascontiguousarray(U, np.float64).ravel(), C.byref(a), ind)
+        if rc:
+            raise ValueError(f"amr_indicator: {'unsupported problem' if rc == -2 else 'invalid parameters'}")
+        return ind
+
+    def amr_adapt(self, U, amr: dict):
+        """new finest-grid level map (uint8, x fastest) from the controller + 2:1 balance"""
+        p = self.problem
+        nf = [p["n_base"][0] << p["max_level"], p["n_base"][1] << p["max_level"]]
+        lmap = np.zeros(nf[0] * nf[1], np.uint8)
+        a = amr_struct(amr)
+        rc = lib().ora_amr_adapt(self.h, np.ascontiguousarray(U, np.float64).ravel(), C.byref(a), lmap)
+        if rc:
+            raise ValueError(f"amr_adapt: {'unsupported problem' if rc == -2 else 'invalid parameters'}")
+        return lmap.reshape(nf[1], nf[0])
 
 
 def transfer(old: OracleMesh, new: OracleMesh, U_old):

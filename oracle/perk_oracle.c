@@ -22,10 +22,14 @@
  *   5. Partitioned P-ERK step, materialised stage states   P:l.209-218, l.407-436
  *   6. Re-mesh solution transfer (refine = interpolation, coarsen = exact L2)
  *   7. FV Godunov testbed (linear advection / Burgers)     P:l.479-520
+ *   8. AMR indicators (Hennemann-Gassner, Loehner, enstrophy) and the level
+ *      controller with 2:1 balance     P:l.1440-1441, l.1548, l.1615-1622
  *
  * Parity status: every function here is pinned by tests/test_oracle_*.py; the
  * Navier-Stokes BR1 operator (section 4b) by tests/test_oracle_ns.py (free stream,
- * conservation, manufactured viscous terms term by term, restricted == reference).
+ * conservation, manufactured viscous terms term by term, restricted == reference);
+ * section 8 by tests/test_oracle_amr.py (closed-form modal energies, hand-computed Loehner
+ * ratios, exact vorticity of polynomial fields, brute-force minimal balanced trees).
  */
 #include <math.h>
 #include <stdint.h>
@@ -1163,4 +1167,222 @@ void ora_fv_step(int n, const double *dx, const int32_t *member, const OraTablea
 {
     FvCtx c = {n, dx, kind, a};
     perk_step_generic(t, n, 1, member, U, dt, fv_rhs_cb, &c);
+}
+
+/* ------------------------------------------------------------------------- */
+/* 8. AMR indicators and the level controller (A1-A6).  2D, Euler / NS.  */
+/*    The paper uses indicator-driven AMR (Loehner on v_x, P:l.1440-1441; Hennemann-Gassner on rho  */
+/*    or rho*p, P:l.1548, l.1731, l.1886; enstrophy eps = 0.5 rho w.w with a threshold, P:l.1615-   */
+/*    1622, eq. Enstrophy) but defines neither the cited indicators nor the controller: the         */
+/*    readings below restate the cited published methods and are listed in DESIGN.md.              */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+    int32_t indicator;      /* 0 Hennemann-Gassner, 1 Loehner, 2 enstrophy */
+    int32_t variable;       /* 0 rho, 1 p, 2 rho*p, 3 v_x, 4 v_y (ignored by enstrophy) */
+    int32_t base_level, med_level, max_level, _pad;
+    double med_threshold, max_threshold;
+    double alpha_max, alpha_min;   /* Hennemann-Gassner */
+    double f_wave;                 /* Loehner */
+} OraAmr;
+
+/* indicator variable at one node from the conserved state (rho, rho v1, rho v2, E) */
+static double amr_variable(const Ora *o, const double *u, int var)
+{
+    double rho = u[0], vx = u[1] / rho, vy = u[2] / rho;
+    double p = (o->prob.gamma - 1.0) * (u[3] - 0.5 * rho * (vx * vx + vy * vy));
+    switch (var) {
+    case 0: return rho;
+    case 1: return p;
+    case 2: return rho * p;
+    case 3: return vx;
+    default: return vy;
+    }
+}
+
+/* orthonormal Legendre polynomial Ptilde_k(x) = sqrt((2k+1)/2) P_k(x), Bonnet's recursion */
+static double legendre_orthonormal(int k, double x)
+{
+    double p0 = 1.0, p1 = x;
+    if (k == 0) return sqrt(0.5);
+    for (int m = 1; m < k; ++m) {
+        double p2 = ((2.0 * m + 1.0) * x * p1 - m * p0) / (m + 1.0);
+        p0 = p1;
+        p1 = p2;
+    }
+    return sqrt((2.0 * k + 1.0) / 2.0) * p1;
+}
+
+/* A1 Hennemann-Gassner (cited at P:l.1548): modal coefficients m_kl of the nodal values in the
+   orthonormal Legendre basis (u(x,y) = sum_kl m_kl Ptilde_k(x) Ptilde_l(y) interpolates the nodes);
+   energy fractions of the highest mode and of the second-highest mode:
+     E = max((sum_all - sum_{k,l<=N-1}) / sum_all, (sum_{k,l<=N-1} - sum_{k,l<=N-2}) / sum_{k,l<=N-1})
+   (a quotient with a zero denominator counts as 0); threshold T = 0.5 10^(-1.8 (N+1)^(1/4)),
+   sharpness s = ln((1 - 1e-4) / 1e-4), alpha = 1 / (1 + exp(-(s / T)(E - T))); alpha < alpha_min -> 0,
+   alpha > 1 - alpha_min -> 1; alpha = min(alpha, alpha_max). */
+static double indicator_hg(const Ora *o, const double *val, const OraAmr *a)
+{
+    double V[NP][NP], Vinv[NP][NP];
+    for (int i = 0; i < NP; ++i)
+        for (int k = 0; k < NP; ++k) V[i][k] = legendre_orthonormal(k, o->B.xi[i]);
+    for (int c = 0; c < NP; ++c) {      /* column c of V^-1: solve V x = e_c */
+        double col[NP] = {0, 0, 0, 0};
+        col[c] = 1.0;
+        solve4(V, col);
+        for (int k = 0; k < NP; ++k) Vinv[k][c] = col[k];
+    }
+    double tot = 0.0, clip1 = 0.0, clip2 = 0.0;
+    for (int l = 0; l < NP; ++l)
+        for (int k = 0; k < NP; ++k) {
+            double m = 0.0;
+            for (int j = 0; j < NP; ++j)
+                for (int i = 0; i < NP; ++i) m += Vinv[k][i] * Vinv[l][j] * val[j * NP + i];
+            double m2 = m * m;
+            tot += m2;
+            if (k <= NP - 2 && l <= NP - 2) clip1 += m2;
+            if (k <= NP - 3 && l <= NP - 3) clip2 += m2;
+        }
+    double e1 = tot > 0.0 ? (tot - clip1) / tot : 0.0;
+    double e2 = clip1 > 0.0 ? (clip1 - clip2) / clip1 : 0.0;
+    double E = e1 > e2 ? e1 : e2;
+    double T = 0.5 * pow(10.0, -1.8 * pow((double)NP, 0.25));
+    double s = log((1.0 - 0.0001) / 0.0001);
+    double alpha = 1.0 / (1.0 + exp(-(s / T) * (E - T)));
+    if (alpha < a->alpha_min) alpha = 0.0;
+    else if (alpha > 1.0 - a->alpha_min) alpha = 1.0;
+    return alpha < a->alpha_max ? alpha : a->alpha_max;
+}
+
+/* A2 Loehner (cited at P:l.1440-1441, LGL adaptation of P:l.1441): along every x and y node line,
+   at every interior node: |u+ - 2 u0 + u-| / (|u+ - u0| + |u0 - u-| + f_wave (|u+| + 2|u0| + |u-|)),
+   0 where the denominator vanishes; the element value is the maximum. */
+static double lohner_estimate(double um, double u0, double up, double fw)
+{
+    double num = fabs(up - 2.0 * u0 + um);
+    double den = fabs(up - u0) + fabs(u0 - um) + fw * (fabs(up) + 2.0 * fabs(u0) + fabs(um));
+    return den > 0.0 ? num / den : 0.0;
+}
+
+static double indicator_lohner(const double *val, const OraAmr *a)
+{
+    double mx = 0.0;
+    for (int j = 0; j < NP; ++j)
+        for (int i = 1; i < NP - 1; ++i) {
+            double ex = lohner_estimate(val[j * NP + i - 1], val[j * NP + i], val[j * NP + i + 1], a->f_wave);
+            double ey = lohner_estimate(val[(i - 1) * NP + j], val[i * NP + j], val[(i + 1) * NP + j], a->f_wave);
+            if (ex > mx) mx = ex;
+            if (ey > mx) mx = ey;
+        }
+    return mx;
+}
+
+/* A3 enstrophy eps = 0.5 rho w.w (P:l.1615-1622, eq. Enstrophy), 2D vorticity w = dv_y/dx - dv_x/dy
+   of the nodal interpolant (D_ij = l_j'(xi_i), times 2/h); the element value is the maximum over
+   its nodes. */
+static double indicator_enstrophy(const Ora *o, const double *U, int e)
+{
+    double J = 2.0 / cell_h(o, e), mx = 0.0;
+    double vx[NP * NP], vy[NP * NP];
+    for (int q = 0; q < NP * NP; ++q) {
+        vx[q] = U[UIDX(o, e, 1, q)] / U[UIDX(o, e, 0, q)];
+        vy[q] = U[UIDX(o, e, 2, q)] / U[UIDX(o, e, 0, q)];
+    }
+    for (int j = 0; j < NP; ++j)
+        for (int i = 0; i < NP; ++i) {
+            double dvydx = 0.0, dvxdy = 0.0;
+            for (int k = 0; k < NP; ++k) {
+                dvydx += o->B.D[i][k] * vy[j * NP + k];
+                dvxdy += o->B.D[j][k] * vx[k * NP + i];
+            }
+            double w = J * dvydx - J * dvxdy;
+            double eps = 0.5 * U[UIDX(o, e, 0, j * NP + i)] * w * w;
+            if (eps > mx) mx = eps;
+        }
+    return mx;
+}
+
+static int amr_check(const Ora *o, const OraAmr *a)
+{
+    if (o->prob.dim != 2 || o->prob.equation == 0) return -2;
+    if (a->indicator < 0 || a->indicator > 2 || a->variable < 0 || a->variable > 4) return -1;
+    if (a->base_level < 0 || a->base_level > a->med_level || a->med_level > a->max_level ||
+        a->max_level > o->prob.max_level || !(a->med_threshold <= a->max_threshold)) return -1;
+    return 0;
+}
+
+int ora_amr_indicator(void *p, const double *U, const OraAmr *a, double *ind)
+{
+    Ora *o = (Ora *)p;
+    int rc = amr_check(o, a);
+    if (rc) return rc;
+    for (int e = 0; e < o->n; ++e) {
+        if (a->indicator == 2) { ind[e] = indicator_enstrophy(o, U, e); continue; }
+        double val[NP * NP];
+        for (int q = 0; q < NP * NP; ++q) {
+            double u[MAXV];
+            for (int v = 0; v < 4; ++v) u[v] = U[UIDX(o, e, v, q)];
+            val[q] = amr_variable(o, u, a->variable);
+        }
+        ind[e] = a->indicator == 0 ? indicator_hg(o, val, a) : indicator_lohner(val, a);
+    }
+    return 0;
+}
+
+/* A4-A6 controller (three levels) and 2:1 balance, writing the new finest-grid level map:
+   A4 target(e) = base_level if ind <= med_threshold, med_level if ind <= max_threshold, else
+      max_level; a leaf moves at most one level per adaptation toward its target;
+   A5 a leaf coarsens only together with its three siblings (all four leaves at the same level,
+      all four wanting to coarsen);
+   A6 2:1 face balance (the condition perk_init / perk_repartition check) is restored by refining:
+      while some leaf has a face neighbour two or more levels finer, split that leaf. */
+int ora_amr_adapt(void *p, const double *U, const OraAmr *a, uint8_t *lmap)
+{
+    Ora *o = (Ora *)p;
+    int rc = amr_check(o, a);
+    if (rc) return rc;
+    int L = o->prob.max_level;
+    double *ind = (double *)malloc(sizeof(double) * o->n);
+    int *want = (int *)malloc(sizeof(int) * o->n);
+    ora_amr_indicator(p, U, a, ind);
+    for (int e = 0; e < o->n; ++e) {
+        int target = ind[e] <= a->med_threshold ? a->base_level
+                   : (ind[e] <= a->max_threshold ? a->med_level : a->max_level);
+        int l = o->lev[e];
+        want[e] = target > l ? l + 1 : (target < l ? l - 1 : l);
+    }
+    for (int e = 0; e < o->n; ++e) {
+        int l = o->lev[e], s = 1 << (L - l), newl = want[e];
+        if (want[e] < l) {              /* A5: the four children of the parent block */
+            int px = o->fx[e] - o->fx[e] % (2 * s), py = o->fy[e] - o->fy[e] % (2 * s);
+            for (int cy = 0; cy < 2; ++cy)
+                for (int cx = 0; cx < 2; ++cx) {
+                    int c = o->cell_of[(int64_t)(py + cy * s) * o->nfx + px + cx * s];
+                    if (o->lev[c] != l || want[c] >= l) newl = l;
+                }
+        }
+        for (int y = 0; y < s; ++y)
+            for (int x = 0; x < s; ++x) lmap[(int64_t)(o->fy[e] + y) * o->nfx + o->fx[e] + x] = (uint8_t)newl;
+    }
+    int changed = 1;
+    while (changed) {               /* A6 */
+        changed = 0;
+        for (int y = 0; y < o->nfy; ++y)
+            for (int x = 0; x < o->nfx; ++x) {
+                int l = lmap[(int64_t)y * o->nfx + x];
+                for (int d = 0; d < 4; ++d) {
+                    int nx = x + (d == 0) - (d == 1), ny = y + (d == 2) - (d == 3);
+                    if (nx < 0 || nx >= o->nfx) { if (!o->prob.periodic[0]) continue; nx = wrapi(nx, o->nfx); }
+                    if (ny < 0 || ny >= o->nfy) { if (!o->prob.periodic[1]) continue; ny = wrapi(ny, o->nfy); }
+                    if (lmap[(int64_t)ny * o->nfx + nx] >= l + 2) {   /* split the leaf holding (x, y) */
+                        int s = 1 << (L - l), ox = x - x % s, oy = y - y % s;
+                        for (int yy = 0; yy < s; ++yy)
+                            for (int xx = 0; xx < s; ++xx) lmap[(int64_t)(oy + yy) * o->nfx + ox + xx] = (uint8_t)(l + 1);
+                        changed = 1;
+                        break;
+                    }
+                }
+            }
+    }
+    free(ind);
+    free(want);
+    return 0;
 }
