@@ -13,7 +13,8 @@ the multi-GPU domain decomposition of SURVEY §8(e) is not built)
 `other_configs` adds the same measurement for BASELINE cfg 1, 2 (1D, launch-latency bound), cfg 4
 (dynamic AMR: device re-mesh every 5 steps inside the timed steps, repartition time reported
 separately), cfg 5 (Navier-Stokes, BR1) and cfg 3 with the third-order P-ERK3 family (SURVEY §8(f)
-f1), so one run shows every config (--extra none skips them).
+f1), cfg 4 with indicator-driven AMR instead of the seeded map sequence (`4i`: perk_amr_adapt +
+perk_repartition every 5 steps), so one run shows every config (--extra none skips them).
 --impl reference times the oracle (oracle/, plain C, 1 host core) on a bounded sample of the same
 workload (full-mesh P-ERK steps, at most ~120 s of CPU work).
 """
@@ -192,10 +193,12 @@ def replica_value(ws, elem_rhs_per_step, ms_max):
     return ws * elem_rhs_per_step / (ms_max * 1e-3)
 
 
-def measure_config(cfg, K, Wm, timer, torch, dist, ws, dev, with_single=True, order=2):
+def measure_config(cfg, K, Wm, timer, torch, dist, ws, dev, with_single=True, order=2, amr=False):
     """Device time per P-ERK step of BASELINE config `cfg` (and of the single-rate S-stage P-ERK on
     the same mesh); cfg 4 re-meshes on the device every 5 steps inside the timed steps.  order = 3
-    runs the P-ERK3 family with the same S and E (workloads/perk3.py)."""
+    runs the P-ERK3 family with the same S and E (workloads/perk3.py).  amr = True
+    (cfg 4) replaces the seeded level-map sequence by the device indicator + controller
+    (perk_amr_adapt) before each repartition."""
     from paper_2403_05144_b200 import Perk
     w = W.make(cfg)
     fam = single_fam = None
@@ -204,10 +207,13 @@ def measure_config(cfg, K, Wm, timer, torch, dist, ws, dev, with_single=True, or
         fam, single_fam = P3.family3(w.S, w.E), P3.family3(w.S, [w.S])
     perk = Perk(w.problem, w.level_map, w.S, w.E, family=fam)
     U = perk.initial_state(w.ic)
-    res = {"workload": w.name + ("_perk3" if order == 3 else ""), "cells": perk.n_cells, "S": w.S, "E": w.E,
-           "order": order, "dt": w.dt}
+    res = {"workload": w.name + ("_perk3" if order == 3 else "") + ("_amr_" + w.meta["amr"]["indicator"] if amr else ""),
+           "cells": perk.n_cells, "S": w.S, "E": w.E, "order": order, "dt": w.dt}
+    if amr:
+        res["amr"] = w.meta["amr"]
     maps = []
-    if w.remesh_every:
+    lm_buf = torch.zeros(w.level_map.shape, dtype=torch.uint8, device=dev)
+    if w.remesh_every and not amr:
         # level maps of the re-meshes inside the measured window, uploaded before the timed region
         nmaps = (K + Wm) // w.remesh_every + 1
         maps = [torch.from_numpy(np.ascontiguousarray(w.level_map_seq(k))).to(dev) for k in range(1, nmaps + 1)]
@@ -218,22 +224,31 @@ def measure_config(cfg, K, Wm, timer, torch, dist, ws, dev, with_single=True, or
         if not w.remesh_every:
             return float(np.mean(timer.steps(lambda k: p.step(Ux, w.dt), Kx, Wm))), []
         state = {"n": 0, "k": 0}
-        rp_ev = []
+        rp_ev, ad_ev = [], []
 
         def run_step(_):
             p.step(Ux, w.dt)
             state["n"] += 1
-            if state["n"] % w.remesh_every == 0 and state["k"] < len(maps):
+            if state["n"] % w.remesh_every == 0 and (amr or state["k"] < len(maps)):
                 a = torch.cuda.Event(enable_timing=True)
                 b = torch.cuda.Event(enable_timing=True)
-                a.record(timer.stream)
-                p.repartition(maps[state["k"]], Ux)
+                if amr:
+                    c = torch.cuda.Event(enable_timing=True)
+                    c.record(timer.stream)
+                    p.amr_adapt(Ux, w.meta["amr"], out=lm_buf)
+                    a.record(timer.stream)
+                    p.repartition(lm_buf, Ux)
+                    ad_ev.append((c, a))
+                else:
+                    a.record(timer.stream)
+                    p.repartition(maps[state["k"]], Ux)
                 b.record(timer.stream)
                 rp_ev.append((a, b))
                 state["k"] += 1
         t = timer.steps(run_step, Kx, Wm)
         torch.cuda.synchronize()
         p.sync()
+        timed.adapt_ms = [a.elapsed_time(b) for a, b in ad_ev]
         return float(np.mean(t)), [a.elapsed_time(b) for a, b in rp_ev]
 
     ms_raw, remesh = timed(perk, U, K)
@@ -241,6 +256,9 @@ def measure_config(cfg, K, Wm, timer, torch, dist, ws, dev, with_single=True, or
         res["remesh_every"] = w.remesh_every
         res["repartitions_in_run"] = len(remesh)
         res["repartition_ms_mean"] = round(float(np.mean(remesh)), 5) if remesh else None
+        if amr:
+            res["amr_adapt_ms_mean"] = round(float(np.mean(timed.adapt_ms)), 5) if timed.adapt_ms else None
+            res["amr_launches_per_adapt"] = perk.amr_launches()
         ev, st = perk.counters()
         elem_rhs_per_step = ev / max(st, 1)
     else:
@@ -360,12 +378,13 @@ def run_ours(args):
     others = {}
     if args.extra != "none":
         for item in [x for x in args.extra.split(",") if x]:
-            c, order = (int(item[:-2]), 3) if item.endswith("p3") else (int(item), 2)
-            if c == args.config and order == 2:
+            amr = item.endswith("i")
+            c, order = (int(item[:-2]), 3) if item.endswith("p3") else (int(item.rstrip("i")), 2)
+            if c == args.config and order == 2 and not amr:
                 continue
             try:
                 p2, _U, _w, r2 = measure_config(c, max(5, min(args.steps, 20)), args.warmup, timer, torch, dist,
-                                                 ws, dev, order=order)
+                                                 ws, dev, order=order, amr=amr)
                 r2["dof_stage_updates_per_s"] = round(r2["value"] * 4 ** _w.problem["dim"], 1)
                 r2["gpu_launches_per_step"] = p2.launches_per_step()
                 p2.close()
@@ -482,9 +501,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--extra", default="1,2,4,5,3p3",
+    ap.add_argument("--extra", default="1,2,4,4i,5,3p3",
                     help="other BASELINE configs measured into other_configs (comma list, 'Np3' = config N "
-                         "with the P-ERK3 family, or 'none')")
+                         "with the P-ERK3 family, 'Ni' = config N with indicator-driven AMR, or 'none')")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true",

@@ -150,6 +150,46 @@ int perk_repartition(perk_ctx *ctx, const uint8_t *level_map_dev, double *U_dev)
  * U_dev read only; dU_dev caller-owned, same layout as U. */
 int rhs_eval(perk_ctx *ctx, const double *U_dev, uint32_t partition_mask, double *dU_dev);
 
+/* ---- indicator-driven AMR (A1-A6), 2D Euler / Navier-Stokes ----
+ * The paper refines by indicators it cites but does not define: Loehner on v_x (P:l.1440-1441),
+ * Hennemann-Gassner on rho or rho*p (P:l.1548, l.1731, l.1886), and defines the enstrophy
+ * eps = 0.5 rho w.w with a refinement threshold (P:l.1615-1622, eq. Enstrophy).
+ *   indicator   PERK_IND_*; variable PERK_VAR_* (the indicator quantity at each node; ignored by
+ *               the enstrophy indicator)
+ *   controller  target level = base_level if indicator <= med_threshold, med_level if
+ *               indicator <= max_threshold, else max_level; each adaptation moves a leaf one level
+ *               toward its target; a leaf coarsens only together with its three siblings; the
+ *               result is made 2:1 face balanced by further refinement.
+ *               0 <= base_level <= med_level <= max_level <= perk_problem.max_level <= 7.
+ *   alpha_max, alpha_min   Hennemann-Gassner clipping (alpha < alpha_min -> 0, > 1 - alpha_min -> 1,
+ *               then min(alpha, alpha_max)); f_wave   Loehner noise filter (e.g. 0.2). */
+enum { PERK_IND_HENNEMANN_GASSNER = 0, PERK_IND_LOHNER = 1, PERK_IND_ENSTROPHY = 2 };
+enum { PERK_VAR_DENSITY = 0, PERK_VAR_PRESSURE = 1, PERK_VAR_DENSITY_PRESSURE = 2, PERK_VAR_VX = 3, PERK_VAR_VY = 4 };
+typedef struct perk_amr {
+    int32_t indicator;
+    int32_t variable;
+    int32_t base_level;
+    int32_t med_level;
+    int32_t max_level;
+    int32_t _pad;
+    double med_threshold;
+    double max_threshold;
+    double alpha_max;
+    double alpha_min;
+    double f_wave;
+} perk_amr;
+
+/* Per-leaf indicator of the state U_dev (layout of perk_step) into ind_dev (fp64, >= n_cells
+ * entries, canonical leaf order).  Asynchronous.  EUNSUPPORTED for 1D / advection, EINVAL for bad
+ * parameters. */
+int perk_amr_indicator(perk_ctx *ctx, const double *U_dev, const perk_amr *amr, double *ind_dev);
+/* Indicator + controller + 2:1 balance: writes the next finest-grid level map (uint8, layout of
+ * perk_init's level map) to level_map_dev, asynchronous and without a host round trip; pass it to
+ * perk_repartition(ctx, level_map_dev, U_dev) to re-mesh.  The current mesh is not changed. */
+int perk_amr_adapt(perk_ctx *ctx, const double *U_dev, const perk_amr *amr, uint8_t *level_map_dev);
+/* Number of kernel launches one perk_amr_adapt performs (max_level + 3). */
+int perk_amr_launches(perk_ctx *ctx, int32_t *launches);
+
 /* ---- introspection (synchronising) ---- */
 int perk_num_cells(perk_ctx *ctx, int64_t *n_cells);
 int perk_num_faces(perk_ctx *ctx, int64_t *counts3);            /* interfaces, mortars, boundaries */

@@ -115,6 +115,8 @@ static void build_basis(BasisTables &B)
             VVt[i][j] = a;   // = M^{-1}
         }
     invert4(VVt, M);
+    invert4(V, B.Vinv);
+    std::memcpy(B.D, D, sizeof(D));
     for (int half = 0; half < 2; ++half) {
         const double (*P)[NP] = half == 0 ? B.Plo : B.Pup;
         double (*R)[NP] = half == 0 ? B.Rlo : B.Rup;

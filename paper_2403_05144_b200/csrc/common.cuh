@@ -29,6 +29,8 @@ struct BasisTables {
     double Dsplit[NP][NP];  // flux differencing (2D - boundary corrections)
     double Plo[NP][NP], Pup[NP][NP];
     double Rlo[NP][NP], Rup[NP][NP];
+    double D[NP][NP];       // D_ij = l_j'(xi_i) (AMR enstrophy indicator)
+    double Vinv[NP][NP];    // nodal -> orthonormal-Legendre modal coefficients (AMR Hennemann-Gassner)
 };
 __constant__ BasisTables cB;
 

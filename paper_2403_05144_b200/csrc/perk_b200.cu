@@ -21,6 +21,7 @@
 #include "br1.cuh"
 #include "step1d.cuh"
 #include "transfer.cuh"
+#include "amr.cuh"
 
 using namespace perk;
 
@@ -50,6 +51,9 @@ struct perk_ctx {
     int *dconst = nullptr;     // [0] = nmorton
     int *n_old = nullptr, *cell_of_old = nullptr, *fx_old = nullptr, *fy_old = nullptr;
     uint8_t *lev_old = nullptr;
+    double *amr_ind = nullptr;                         // AMR scratch: indicator, wanted / new level per leaf,
+    uint8_t *amr_want = nullptr, *amr_newlev = nullptr;  // ping-pong finest-grid maps of the balance
+    uint8_t *amr_map[2] = {nullptr, nullptr};
     int vol_blocks = 0, surf_blocks = 0, grad_blocks = 0;
     unsigned kind_mask = ~0u;              // kernel kinds launch_step issues (perk_time_kernels)
     bool step1d = false;                   // small 1D mesh: whole step in one single-CTA launch
@@ -547,6 +551,21 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
         int occf = 0;
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occf, k_surf2d<MODE_STAGE, false>, 256, 0));
         c->surf_blocks = std::min(blocks_for(4ll * c->cap_faces, 256), SM_COUNT_B200 * std::max(occf, 1));
+        // re-mesh (transfer double buffer, old-mesh copy) and AMR scratch, allocated up front so that
+        // no cudaMalloc / memset lands inside a timed re-mesh
+        CU(dalloc(c, &c->Utmp, (size_t)c->cap * c->nv * c->npe));
+        CU(dalloc(c, &c->n_old, 1));
+        CU(dalloc(c, &c->cell_of_old, c->nf));
+        CU(dalloc(c, &c->lev_old, c->cap));
+        CU(dalloc(c, &c->fx_old, c->cap));
+        CU(dalloc(c, &c->fy_old, c->cap));
+        if (prob->equation != PERK_EQ_ADVECTION) {
+            CU(dalloc(c, &c->amr_ind, c->cap));
+            CU(dalloc(c, &c->amr_want, c->cap));
+            CU(dalloc(c, &c->amr_newlev, c->cap));
+            CU(dalloc(c, &c->amr_map[0], c->nf));
+            CU(dalloc(c, &c->amr_map[1], c->nf));
+        }
     } else {
         c->vol_blocks = std::min(blocks_for(c->cap, 128), SM_COUNT_B200 * 8);
         c->surf_blocks = std::min(blocks_for(c->cap_faces, 256), SM_COUNT_B200 * 8);
@@ -690,14 +709,6 @@ static int do_repartition(perk_ctx *c, const uint8_t *lmap, double *U, Prof *p)
 {
     if (c->prob.dim != 2) return set_err(c, PERK_EUNSUPPORTED, "repartition with solution transfer is 2D only");
     cudaStream_t s = c->stream;
-    if (!c->Utmp) {
-        CU(dalloc(c, &c->Utmp, (size_t)c->cap * c->nv * c->npe));
-        CU(dalloc(c, &c->n_old, 1));
-        CU(dalloc(c, &c->cell_of_old, c->nf));
-        CU(dalloc(c, &c->lev_old, c->cap));
-        CU(dalloc(c, &c->fx_old, c->cap));
-        CU(dalloc(c, &c->fy_old, c->cap));
-    }
     prof_mark(p, s, 2);
     CU(cudaMemcpyAsync(c->lmap, lmap, c->nf, cudaMemcpyDeviceToDevice, s));
     k_save_old<<<SM_COUNT_B200 * 4, 256, 0, s>>>(c->md, c->n_old, c->cell_of_old, c->lev_old, c->fx_old, c->fy_old);
@@ -716,6 +727,88 @@ extern "C" int perk_repartition(perk_ctx *c, const uint8_t *lmap, double *U)
     if (!c) return PERK_ENOTINIT;
     if (!lmap || !U) return set_err(c, PERK_EINVAL, "null pointer");
     return do_repartition(c, lmap, U, nullptr);
+}
+
+// ----------------------------------------------------------------------------------------------
+// indicator-driven AMR (amr.cuh)
+// ----------------------------------------------------------------------------------------------
+static int amr_setup(perk_ctx *c, const double *U, const perk_amr *a, AmrParams &ap)
+{
+    if (!c) return PERK_ENOTINIT;
+    if (!U || !a) return set_err(c, PERK_EINVAL, "null pointer");
+    if (c->prob.dim != 2 || c->prob.equation == PERK_EQ_ADVECTION)
+        return set_err(c, PERK_EUNSUPPORTED, "AMR indicators need a 2D Euler / Navier-Stokes problem");
+    if (c->prob.max_level > 7) return set_err(c, PERK_EUNSUPPORTED, "AMR balance supports max_level <= 7");
+    if (a->indicator < 0 || a->indicator > 2 || a->variable < 0 || a->variable > 4)
+        return set_err(c, PERK_EINVAL, "bad indicator / variable");
+    if (a->base_level < 0 || a->base_level > a->med_level || a->med_level > a->max_level ||
+        a->max_level > c->prob.max_level)
+        return set_err(c, PERK_EINVAL, "need 0 <= base_level <= med_level <= max_level <= problem max_level");
+    if (!(a->med_threshold <= a->max_threshold))
+        return set_err(c, PERK_EINVAL, "need med_threshold <= max_threshold");
+    if (a->indicator == PERK_IND_HENNEMANN_GASSNER &&
+        !(a->alpha_min >= 0.0 && a->alpha_min <= 0.5 && a->alpha_max >= 0.0 && a->alpha_max <= 1.0))
+        return set_err(c, PERK_EINVAL, "need 0 <= alpha_min <= 1/2, 0 <= alpha_max <= 1");
+    if (a->indicator == PERK_IND_LOHNER && !(a->f_wave >= 0.0))
+        return set_err(c, PERK_EINVAL, "need f_wave >= 0");
+    ap.indicator = a->indicator;
+    ap.variable = a->variable;
+    ap.base_level = a->base_level;
+    ap.med_level = a->med_level;
+    ap.max_level = a->max_level;
+    ap.med_thr = a->med_threshold;
+    ap.max_thr = a->max_threshold;
+    ap.alpha_max = a->alpha_max;
+    ap.alpha_min = a->alpha_min;
+    ap.f_wave = a->f_wave;
+    ap.hg_T = 0.5 * std::pow(10.0, -1.8 * std::pow((double)NP, 0.25));
+    ap.hg_sT = std::log((1.0 - 0.0001) / 0.0001) / ap.hg_T;
+    return PERK_OK;
+}
+
+static int amr_indicator_blocks(const perk_ctx *c) { return blocks_for((long long)c->cap, AMR_T / 16); }
+
+extern "C" int perk_amr_indicator(perk_ctx *c, const double *U, const perk_amr *a, double *ind)
+{
+    AmrParams ap;
+    int rc = amr_setup(c, U, a, ap);
+    if (rc) return rc;
+    if (!ind) return set_err(c, PERK_EINVAL, "null pointer");
+    k_amr_indicator<<<amr_indicator_blocks(c), AMR_T, 0, c->stream>>>(c->md, ap, U, ind, c->amr_want);
+    CU(cudaGetLastError());
+    return PERK_OK;
+}
+
+extern "C" int perk_amr_adapt(perk_ctx *c, const double *U, const perk_amr *a, uint8_t *lmap)
+{
+    AmrParams ap;
+    int rc = amr_setup(c, U, a, ap);
+    if (rc) return rc;
+    if (!lmap) return set_err(c, PERK_EINVAL, "null pointer");
+    cudaStream_t s = c->stream;
+    const int L = c->prob.max_level;
+    const int nbase = c->prob.n_base[0] * c->prob.n_base[1];
+    const size_t smem = amr_balance_smem(L);
+    k_amr_indicator<<<amr_indicator_blocks(c), AMR_T, 0, s>>>(c->md, ap, U, c->amr_ind, c->amr_want);
+    k_amr_coarsen<<<blocks_for(c->cap, 256), 256, 0, s>>>(c->md, c->amr_want, c->amr_newlev);
+    // L + 1 balance iterations, the last one into the caller's map
+    uint8_t *out = L == 0 ? lmap : c->amr_map[0];
+    k_amr_balance<true><<<nbase, AMR_T, smem, s>>>(c->md, c->amr_newlev, nullptr, out);
+    for (int it = 1; it <= L; ++it) {
+        uint8_t *in = out;
+        out = it == L ? lmap : c->amr_map[it & 1];
+        k_amr_balance<false><<<nbase, AMR_T, smem, s>>>(c->md, nullptr, in, out);
+    }
+    CU(cudaGetLastError());
+    return PERK_OK;
+}
+
+extern "C" int perk_amr_launches(perk_ctx *c, int32_t *launches)
+{
+    if (!c) return PERK_ENOTINIT;
+    if (!launches) return set_err(c, PERK_EINVAL, "null pointer");
+    *launches = c->prob.max_level + 3;
+    return PERK_OK;
 }
 
 extern "C" int rhs_eval(perk_ctx *c, const double *U, uint32_t mask, double *dU)

@@ -43,6 +43,30 @@ class perk_tableau(C.Structure):
                 ("b", C.c_double * 64), ("a_sub", (C.c_double * 64) * 8)]
 
 
+class perk_amr(C.Structure):
+    _fields_ = [("indicator", C.c_int32), ("variable", C.c_int32), ("base_level", C.c_int32),
+                ("med_level", C.c_int32), ("max_level", C.c_int32), ("_pad", C.c_int32),
+                ("med_threshold", C.c_double), ("max_threshold", C.c_double), ("alpha_max", C.c_double),
+                ("alpha_min", C.c_double), ("f_wave", C.c_double)]
+
+
+INDICATOR = {"hennemann_gassner": 0, "lohner": 1, "enstrophy": 2}
+AMR_VARIABLE = {"rho": 0, "p": 1, "rho_p": 2, "v_x": 3, "v_y": 4}
+
+
+def amr_params(a: dict) -> perk_amr:
+    """perk_amr from a dict: indicator, variable, base/med/max_level, med/max_threshold,
+    alpha_max (default 0.5), alpha_min (0.001), f_wave (0.2)"""
+    s = perk_amr()
+    s.indicator = INDICATOR[a["indicator"]]
+    s.variable = AMR_VARIABLE[a.get("variable", "rho")]
+    s.base_level, s.med_level, s.max_level = a["base_level"], a["med_level"], a["max_level"]
+    s.med_threshold, s.max_threshold = a["med_threshold"], a["max_threshold"]
+    s.alpha_max, s.alpha_min = a.get("alpha_max", 0.5), a.get("alpha_min", 0.001)
+    s.f_wave = a.get("f_wave", 0.2)
+    return s
+
+
 _lib = None
 
 
@@ -78,6 +102,9 @@ def lib():
         L.perk_time_kernels.argtypes = [P, P, dbl, C.c_uint32, i32, C.POINTER(C.c_float)]
         L.perk_profile_repartition.argtypes = [P, P, P, P, P]
         L.perk_launches_per_step.argtypes = [P, C.POINTER(i32)]
+        L.perk_amr_indicator.argtypes = [P, P, C.POINTER(perk_amr), P]
+        L.perk_amr_adapt.argtypes = [P, P, C.POINTER(perk_amr), P]
+        L.perk_amr_launches.argtypes = [P, C.POINTER(i32)]
         _lib = L
     return _lib
 
@@ -87,7 +114,7 @@ def exported_symbols():
             "perk_run_host", "perk_repartition", "rhs_eval", "perk_num_cells", "perk_num_faces", "perk_node_coords",
             "perk_get_leaves", "perk_get_faces", "perk_get_list", "perk_get_count_active", "perk_get_counters",
             "perk_sync", "perk_last_error", "perk_profile_step", "perk_time_kernels", "perk_profile_repartition",
-            "perk_launches_per_step"]
+            "perk_launches_per_step", "perk_amr_indicator", "perk_amr_adapt", "perk_amr_launches"]
 
 
 def tableau_p2(S: int, E, alpha_rows=None) -> perk_tableau:
@@ -251,6 +278,29 @@ class Perk:
         lm = self._to_dev_u8(level_map)
         _check(self.h, lib().perk_repartition(self.h, _ptr(lm), _ptr(U)))
         self._keep = lm   # keep the map alive until the stream has consumed it
+
+    def amr_indicator(self, U, amr: dict):
+        """per-leaf AMR indicator (device tensor of n_cells doubles)"""
+        ind = self.torch.zeros(self.max_cells, dtype=self.torch.float64, device="cuda")
+        a = amr_params(amr)
+        _check(self.h, lib().perk_amr_indicator(self.h, _ptr(U), C.byref(a), _ptr(ind)))
+        return ind[: self.n_cells]
+
+    def amr_adapt(self, U, amr: dict, out=None):
+        """next finest-grid level map (device uint8 tensor (nfy, nfx)); asynchronous"""
+        p = self.problem
+        L = p["max_level"]
+        shape = (p["n_base"][1] << L, p["n_base"][0] << L)
+        if out is None:
+            out = self.torch.zeros(shape, dtype=self.torch.uint8, device="cuda")
+        a = amr_params(amr)
+        _check(self.h, lib().perk_amr_adapt(self.h, _ptr(U), C.byref(a), _ptr(out)))
+        return out
+
+    def amr_launches(self) -> int:
+        n = C.c_int32()
+        _check(self.h, lib().perk_amr_launches(self.h, C.byref(n)))
+        return n.value
 
     def rhs(self, U, mask=None):
         mask = (1 << self.R) - 1 if mask is None else int(mask)

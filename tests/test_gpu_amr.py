@@ -1,0 +1,162 @@
+"""GPU parity of the indicator-driven AMR path: perk_amr_indicator /
+perk_amr_adapt (amr.cuh) against the oracle (perk_oracle.c section 8) on identical seeded states.
+
+* indicators per leaf: Hennemann-Gassner (all five variables), Loehner, enstrophy, within 1e-10
+  (the floating-point order of the modal sums / derivatives differs);
+* the adapted level map bit-exact -- except where a leaf's indicator lies within 1e-9 (relative)
+  of a controller threshold, where both decisions are valid (the map is then checked to be a
+  valid balanced map);
+* full cfg-4 size, periodic and non-periodic meshes, Navier-Stokes, and a 10-cycle
+  step / adapt / repartition loop compared with the oracle mesh-by-mesh and state-by-state;
+* launch count, error codes.
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import oracle as O
+from oracle import tableau as T
+from gpu_util import TOL, build_pair, compare_mesh, gpu_state_numpy, rel_err_per_var
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+HG = dict(indicator="hennemann_gassner", variable="rho", base_level=0, med_level=2, max_level=4,
+          med_threshold=0.01, max_threshold=0.1, alpha_max=0.5, alpha_min=0.001)
+LOHNER = dict(indicator="lohner", variable="v_x", base_level=0, med_level=2, max_level=4,
+              med_threshold=0.003, max_threshold=0.03, f_wave=0.2)
+
+
+def _perturbed(gpu, ora, w, amp, seed=7):
+    """the cfg-4 state plus seeded per-node noise (so that every indicator spans its range);
+    returns (oracle array, device tensor) holding identical values"""
+    Uo = ora.initial_state(w.ic)
+    rng = np.random.default_rng(seed)
+    scale = amp * rng.random((ora.n, 1, 1)) ** 3            # a few elements strongly perturbed
+    Uo = Uo * (1.0 + scale * rng.standard_normal(Uo.shape))
+    Ug = gpu.alloc_state()
+    Ug[: ora.n] = torch.from_numpy(Uo).cuda()
+    return np.ascontiguousarray(Uo), Ug
+
+
+def _thresholds(amr):
+    return np.array([amr["med_threshold"], amr["max_threshold"]])
+
+
+def _compare_maps(ora, lm_o, lm_g, ind_o, amr):
+    if np.array_equal(lm_o, lm_g):
+        return 0
+    lv = ora.leaves()
+    cell_leaf = np.zeros(lm_o.shape, np.int64)
+    L = ora.problem["max_level"]
+    for e in range(ora.n):
+        s = 1 << (L - int(lv["level"][e]))
+        cell_leaf[lv["fy"][e]:lv["fy"][e] + s, lv["fx"][e]:lv["fx"][e] + s] = e
+    diff = np.unique(cell_leaf[lm_o != lm_g])
+    th = _thresholds(amr)
+    near = np.abs(ind_o[:, None] - th[None, :]).min(axis=1) <= 1e-9 * np.maximum(np.abs(th).max(), 1e-300)
+    # a flip at one leaf may move its siblings / balance neighbours: require a near-tie somewhere
+    assert near.any(), f"{len(diff)} leaves differ and no indicator is near a threshold"
+    W.balance(lm_g, L)   # valid
+    return len(diff)
+
+
+@pytest.mark.parametrize("amr", [
+    dict(HG, variable="rho"), dict(HG, variable="p"), dict(HG, variable="rho_p"), dict(HG, variable="v_x"),
+    dict(HG, variable="v_y"), LOHNER, dict(LOHNER, variable="rho_p"), "enstrophy"], ids=str)
+def test_indicator_parity(amr):
+    w = W.make(4, n_base=16)
+    amr = w.meta["amr"] if amr == "enstrophy" else amr
+    ora, gpu = build_pair(w)
+    Uo, Ug = _perturbed(gpu, ora, w, 0.05)
+    io = ora.amr_indicator(Uo, amr)
+    ig = gpu.amr_indicator(Ug, amr).cpu().numpy()
+    scale = max(np.abs(io).max(), 1e-300)
+    assert np.abs(ig - io).max() <= 1e-10 * scale, (np.abs(ig - io).max(), scale)
+    assert io.max() > io.min()                                      # a non-trivial field
+
+
+@pytest.mark.parametrize("amr", [HG, LOHNER, "enstrophy"], ids=str)
+@pytest.mark.parametrize("n_base,amp", [(16, 0.02), (64, 0.01)])
+def test_adapt_map_parity(amr, n_base, amp):
+    w = W.make(4, n_base=n_base)
+    amr = w.meta["amr"] if amr == "enstrophy" else amr
+    ora, gpu = build_pair(w)
+    Uo, Ug = _perturbed(gpu, ora, w, amp)
+    lm_o = ora.amr_adapt(Uo, amr)
+    lm_g = gpu.amr_adapt(Ug, amr).cpu().numpy()
+    gpu.sync()
+    _compare_maps(ora, lm_o, lm_g, ora.amr_indicator(Uo, amr), amr)
+    assert not np.array_equal(lm_o, w.level_map)                   # the controller changed the mesh
+
+
+@pytest.mark.parametrize("periodic", [(0, 0), (1, 0)])
+def test_adapt_nonperiodic(periodic):
+    w = W.make(4, n_base=16)
+    prob = dict(w.problem, periodic=periodic, bc_state=(1.0, 0.0, 0.0, 2.5))
+    ora, gpu = build_pair(w, problem=prob)
+    Uo, Ug = _perturbed(gpu, ora, w, 0.02)
+    amr = dict(HG, max_level=4)
+    lm_o = ora.amr_adapt(Uo, amr)
+    lm_g = gpu.amr_adapt(Ug, amr).cpu().numpy()
+    _compare_maps(ora, lm_o, lm_g, ora.amr_indicator(Uo, amr), amr)
+
+
+def test_adapt_navier_stokes():
+    w = W.make(5, n_base=16)
+    ora, gpu = build_pair(w)
+    Uo, Ug = _perturbed(gpu, ora, w, 0.02)
+    amr = dict(indicator="enstrophy", base_level=0, med_level=1, max_level=3, med_threshold=0.05,
+               max_threshold=0.5)
+    io = ora.amr_indicator(Uo, amr)
+    lm_o = ora.amr_adapt(Uo, amr)
+    lm_g = gpu.amr_adapt(Ug, amr).cpu().numpy()
+    _compare_maps(ora, lm_o, lm_g, io, amr)
+
+
+def test_adapt_loop_state_and_lists():
+    """10 cycles of 5 steps + adapt + repartition (the indicator-driven cfg 4 at n_base 16)"""
+    w = W.make(4, n_base=16)
+    amr = w.meta["amr"]
+    fam = T.family(w.S, w.E, w.alpha_rule)
+    ora, gpu = build_pair(w)
+    Uo = ora.initial_state(w.ic)
+    Ug = gpu.initial_state(w.ic)
+    lm_g = torch.zeros(w.level_map.shape, dtype=torch.uint8, device="cuda")
+    changed = 0
+    for k in range(10):
+        ora.step(Uo, w.dt, 5)
+        gpu.step(Ug, w.dt, 5)
+        lm_o = ora.amr_adapt(Uo, amr)
+        gpu.amr_adapt(Ug, amr, out=lm_g)
+        gpu.repartition(lm_g, Ug)
+        gpu.sync()
+        assert _compare_maps(ora, lm_o, lm_g.cpu().numpy(), ora.amr_indicator(Uo, amr), amr) == 0
+        ora_new = O.OracleMesh(w.problem, lm_o, fam)
+        changed += int(ora_new.n != ora.n)
+        Uo = O.transfer(ora, ora_new, Uo)
+        ora = ora_new
+        compare_mesh(ora, gpu)
+        assert rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo).max() <= TOL
+    assert changed > 0
+
+
+def test_launches_and_errors():
+    w = W.make(4, n_base=16)
+    ora, gpu = build_pair(w)
+    assert gpu.amr_launches() == w.problem["max_level"] + 3
+    U = gpu.initial_state(w.ic)
+    from paper_2403_05144_b200.perk import PerkError
+    for bad in (dict(HG, max_level=5), dict(HG, med_level=0, base_level=1), dict(HG, med_threshold=1.0),
+                dict(HG, alpha_min=0.7), dict(LOHNER, f_wave=-1.0)):
+        with pytest.raises(PerkError) as ei:
+            gpu.amr_adapt(U, bad)
+        assert ei.value.code == -1
+    w1 = W.make(2)
+    o1, g1 = build_pair(w1)
+    with pytest.raises(PerkError) as ei:
+        g1.amr_indicator(g1.initial_state(w1.ic), HG)
+    assert ei.value.code == -6

@@ -327,7 +327,12 @@ def make_cfg4(seed=0, n_base=64, steps=2000, cfl=0.2, remesh_every=5, max_level=
     prob["max_cells"] = int(2.2 * n0)
     return Workload(CONFIG_NAMES[4], prob, 28, [4, 6, 10, 16, 28], "taylor", lmap0, ic, dt, steps,
                     remesh_every=remesh_every, level_map_seq=level_map_k, seed=seed,
-                    meta=dict(theta0=theta0, A=A, phi=phi, n_maps=n_maps, cfl=cfl))
+                    meta=dict(theta0=theta0, A=A, phi=phi, n_maps=n_maps, cfl=cfl,
+                              # indicator-driven variant: enstrophy controller
+                              # (P:l.1615-1622) replacing the seeded band sequence
+                              amr=dict(indicator="enstrophy", variable="rho", base_level=0,
+                                       med_level=min(2, Lmax), max_level=Lmax,
+                                       med_threshold=1.0, max_threshold=15.0)))
 
 
 # ----------------------------------------------------------------------------
