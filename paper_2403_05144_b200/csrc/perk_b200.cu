@@ -54,6 +54,7 @@ struct perk_ctx {
     double *amr_ind = nullptr;                         // AMR scratch: indicator, wanted / new level per leaf,
     uint8_t *amr_want = nullptr, *amr_newlev = nullptr;  // ping-pong finest-grid maps of the balance
     uint8_t *amr_map[2] = {nullptr, nullptr};
+    int *amr_flags = nullptr;                            // balance: iteration k changed a cell
     int vol_blocks = 0, surf_blocks = 0, grad_blocks = 0;
     unsigned kind_mask = ~0u;              // kernel kinds launch_step issues (perk_time_kernels)
     bool step1d = false;                   // small 1D mesh: whole step in one single-CTA launch
@@ -565,6 +566,7 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
             CU(dalloc(c, &c->amr_newlev, c->cap));
             CU(dalloc(c, &c->amr_map[0], c->nf));
             CU(dalloc(c, &c->amr_map[1], c->nf));
+            CU(dalloc(c, &c->amr_flags, 16));
         }
     } else {
         c->vol_blocks = std::min(blocks_for(c->cap, 128), SM_COUNT_B200 * 8);
@@ -766,7 +768,21 @@ static int amr_setup(perk_ctx *c, const double *U, const perk_amr *a, AmrParams 
     return PERK_OK;
 }
 
-static int amr_indicator_blocks(const perk_ctx *c) { return blocks_for((long long)c->cap, AMR_T / 16); }
+// persistent indicator grid: 4 CTAs per SM (24 KB shared memory each), at most one tile per CTA
+static int amr_indicator_blocks(const perk_ctx *c)
+{
+    return std::min(blocks_for((long long)c->cap, AMR_TILE), SM_COUNT_B200 * 4);
+}
+
+static void launch_amr_indicator(perk_ctx *c, cudaStream_t s, const AmrParams &ap, const double *U, double *ind)
+{
+    const int g = amr_indicator_blocks(c);
+    switch (ap.indicator) {
+    case IND_HG: launch_pdl(k_amr_indicator<IND_HG>, g, AMR_T, 0, s, c->md, ap, U, ind, c->amr_want); break;
+    case IND_LOHNER: launch_pdl(k_amr_indicator<IND_LOHNER>, g, AMR_T, 0, s, c->md, ap, U, ind, c->amr_want); break;
+    default: launch_pdl(k_amr_indicator<IND_ENSTROPHY>, g, AMR_T, 0, s, c->md, ap, U, ind, c->amr_want); break;
+    }
+}
 
 extern "C" int perk_amr_indicator(perk_ctx *c, const double *U, const perk_amr *a, double *ind)
 {
@@ -774,7 +790,7 @@ extern "C" int perk_amr_indicator(perk_ctx *c, const double *U, const perk_amr *
     int rc = amr_setup(c, U, a, ap);
     if (rc) return rc;
     if (!ind) return set_err(c, PERK_EINVAL, "null pointer");
-    k_amr_indicator<<<amr_indicator_blocks(c), AMR_T, 0, c->stream>>>(c->md, ap, U, ind, c->amr_want);
+    launch_amr_indicator(c, c->stream, ap, U, ind);
     CU(cudaGetLastError());
     return PERK_OK;
 }
@@ -787,17 +803,25 @@ extern "C" int perk_amr_adapt(perk_ctx *c, const double *U, const perk_amr *a, u
     if (!lmap) return set_err(c, PERK_EINVAL, "null pointer");
     cudaStream_t s = c->stream;
     const int L = c->prob.max_level;
+    if (L == 0) {   // no refinement allowed: the only map is all zeros
+        CU(cudaMemsetAsync(lmap, 0, c->nf, s));
+        return PERK_OK;
+    }
     const int nbase = c->prob.n_base[0] * c->prob.n_base[1];
-    const size_t smem = amr_balance_smem(L);
-    k_amr_indicator<<<amr_indicator_blocks(c), AMR_T, 0, s>>>(c->md, ap, U, c->amr_ind, c->amr_want);
-    k_amr_coarsen<<<blocks_for(c->cap, 256), 256, 0, s>>>(c->md, c->amr_want, c->amr_newlev);
+    const int bpc = amr_base_per_cta(L);
+    const int bal_blocks = (nbase + bpc - 1) / bpc;
+    const size_t smem = (size_t)bpc * amr_pyramid_bytes(L);
+    const uint8_t *none = nullptr;
+    launch_amr_indicator(c, s, ap, U, c->amr_ind);
+    launch_pdl(k_amr_coarsen, blocks_for(c->cap, 256), 256, 0, s, c->md, (const uint8_t *)c->amr_want, c->amr_newlev);
     // L + 1 balance iterations, the last one into the caller's map
-    uint8_t *out = L == 0 ? lmap : c->amr_map[0];
-    k_amr_balance<true><<<nbase, AMR_T, smem, s>>>(c->md, c->amr_newlev, nullptr, out);
+    uint8_t *out = c->amr_map[0];
+    launch_pdl(k_amr_balance<true>, bal_blocks, AMR_T, smem, s, c->md, (const uint8_t *)c->amr_newlev, none, out,
+               c->amr_flags, 0);
     for (int it = 1; it <= L; ++it) {
-        uint8_t *in = out;
+        const uint8_t *in = out;
         out = it == L ? lmap : c->amr_map[it & 1];
-        k_amr_balance<false><<<nbase, AMR_T, smem, s>>>(c->md, nullptr, in, out);
+        launch_pdl(k_amr_balance<false>, bal_blocks, AMR_T, smem, s, c->md, none, in, out, c->amr_flags, it);
     }
     CU(cudaGetLastError());
     return PERK_OK;

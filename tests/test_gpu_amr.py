@@ -80,10 +80,12 @@ def test_indicator_parity(amr):
 
 
 @pytest.mark.parametrize("amr", [HG, LOHNER, "enstrophy"], ids=str)
-@pytest.mark.parametrize("n_base,amp", [(16, 0.02), (64, 0.01)])
-def test_adapt_map_parity(amr, n_base, amp):
-    w = W.make(4, n_base=n_base)
-    amr = w.meta["amr"] if amr == "enstrophy" else amr
+@pytest.mark.parametrize("n_base,L,amp", [(16, 4, 0.02), (64, 4, 0.01), (12, 1, 0.02), (12, 2, 0.02),
+                                          (6, 6, 0.02)])
+def test_adapt_map_parity(amr, n_base, L, amp):
+    """maximum levels 1..6 (one balance CTA holds 1..256 base cells), ragged base grids"""
+    w = W.make(4, n_base=n_base, max_level=L, widths=(0.3, 0.15, 0.06, 0.015, 0.008, 0.004)[:L])
+    amr = w.meta["amr"] if amr == "enstrophy" else dict(amr, max_level=min(4, L), med_level=min(2, L))
     ora, gpu = build_pair(w)
     Uo, Ug = _perturbed(gpu, ora, w, amp)
     lm_o = ora.amr_adapt(Uo, amr)
