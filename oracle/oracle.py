@@ -41,7 +41,8 @@ class OraProblem(C.Structure):
 
 class OraTableau(C.Structure):
     _fields_ = [("S", C.c_int32), ("R", C.c_int32), ("E", C.c_int32 * 8), ("c", C.c_double * 64),
-                ("b", C.c_double * 64), ("a1", (C.c_double * 64) * 8), ("asub", (C.c_double * 64) * 8)]
+                ("b", C.c_double * 64), ("a1", (C.c_double * 64) * 8), ("asub", (C.c_double * 64) * 8),
+                ("active", C.c_uint64 * 8)]
 
 
 class OraAmr(C.Structure):
@@ -141,6 +142,8 @@ def tableau_struct(fam: dict) -> OraTableau:
     for i in range(fam["S"]):
         t.c[i] = fam["c_f"][i]
         t.b[i] = b[i]
+    for r, m in enumerate(fam.get("active_mask") or []):      # stage patterns (0 = standard)
+        t.active[r] = int(m)
     return t
 
 

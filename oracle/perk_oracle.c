@@ -64,8 +64,20 @@ typedef struct {
     double c[MAXS];             /* c_i, index i-1 */
     double b[MAXS];             /* b_i, index i-1 (P-ERK2: e_S; P-ERK3: 1/6, 0.., 1/6, 4/6) */
     double a1[MAXR][MAXS];      /* a_{i,1}^{(r)}   (index i-1) */
-    double asub[MAXR][MAXS];    /* a_{i,i-1}^{(r)} (index i-1) */
+    double asub[MAXR][MAXS];    /* a_{i,p(i)}^{(r)} (index i-1): the coefficient of K_{p(i)}, p(i) = the
+                                   member's previous evaluated stage > 1 (= i-1 in the standard pattern) */
+    uint64_t active[MAXR];      /* bit i-1: member r evaluates stage i; 0 = the standard pattern
+                                   {1} u {S-E+2..S} (P:l.428); other patterns P:l.642-700 */
 } OraTableau;
+
+/* stage i (1-based) is evaluated by member r: standard pattern i == 1 or i >= S - E_r + 2
+   (P:l.407-436, eq. PERK_ButcherTableauClassic: member E evaluates K_1 and the last E-1 stages),
+   or the member's explicit stage set (alternating / early-shared patterns, P:l.642-700) */
+static int tab_active(const OraTableau *t, int r, int i)
+{
+    if (t->active[r]) return (int)((t->active[r] >> (i - 1)) & 1u);
+    return i == 1 || i >= t->S - t->E[r] + 2;
+}
 
 /* ------------------------------------------------------------------------- */
 /* 1. basis                                                                  */
@@ -249,12 +261,8 @@ static int member_of_level(const Ora *o, int l)
     return m;
 }
 
-/* stage i (1-based) is evaluated by member r iff i == 1 or i >= S - E_r + 2 (P:l.407-436,
-   eq. PERK_ButcherTableauClassic: member E evaluates K_1 and the last E-1 stages) */
-static int member_active(const Ora *o, int r, int i)
-{
-    return i == 1 || i >= o->tab.S - o->tab.E[r] + 2;
-}
+/* stage i (1-based) is evaluated by member r (tab_active above) */
+static int member_active(const Ora *o, int r, int i) { return tab_active(&o->tab, r, i); }
 
 static int wrapi(int v, int n) { return ((v % n) + n) % n; }
 
@@ -1000,14 +1008,20 @@ int ora_rhs(void *p, const double *U, uint32_t mask, double *dU, int mode)
 /* ------------------------------------------------------------------------- */
 typedef void (*rhs_fn)(void *ctx, const double *U, uint32_t mask, double *dU);
 
-/* Generic partitioned P-ERK step over `nunits` units of `usize` doubles, unit u in member[u]:
+/* Generic partitioned P-ERK step over `nunits` units of `usize` doubles, unit u in member[u]
+   (P:l.209-218, eq. PartitionedRKSystem, with the two-nonzero rows of the P-ERK tableaux):
      K_1 = F(U_n)
-     U^(i)|_r = U_n|_r + dt (a_{i,1}^(r) K_1|_r + a_{i,i-1}^(r) K_{i-1}|_r),  i = 2..S
+     U^(i)|_r = U_n|_r + dt (a_{i,1}^(r) K_1|_r + a_{i,p(i)}^(r) K_{p(i)}|_r),  i = 2..S
+        p(i) = the member's previous evaluated stage > 1 (= i-1 in the standard pattern; the
+        alternating / early-shared rows of P:l.655-700); the row has no other nonzero a_{i,j}
      K_i|_r = I^(r) F(U^(i))  for the members r active at stage i (others: 0, never used)
-     U_{n+1} = U_n + dt sum_i b_i K_i   (shared b: P-ERK2 b = e_S, P:l.423; P-ERK3 Shu-Osher
-                                         b = (1/6, 0, .., 0, 1/6, 4/6), P:l.872-883)
-   The weighted sum is accumulated stage by stage in the order i = 1..S (terms with b_i = 0 add an
-   exact zero, so b = e_S gives U_n + dt K_S bitwise).                                      */
+     U_{n+1} = U_n + dt sum_i b_i K_i   (shared b: P-ERK2 b = e_S, P:l.423; Heun / Ralston b_1, b_S,
+                                         P:l.439-442; P-ERK3 Shu-Osher b = (1/6, 0, .., 0, 1/6, 4/6),
+                                         P:l.872-883)
+   Kp holds, per unit, K of its member's most recent evaluated stage > 1 (zero before the first),
+   which is K_{p(i)} when stage i is evaluated.  The weighted sum is accumulated stage by stage in
+   the order i = 1..S (terms with b_i = 0 add an exact zero, so b = e_S gives U_n + dt K_S
+   bitwise).                                                                                  */
 static int64_t perk_step_generic(const OraTableau *t, int nunits, int usize, const int32_t *member,
                                  double *U, double dt, rhs_fn F, void *ctx)
 {
@@ -1021,7 +1035,7 @@ static int64_t perk_step_generic(const OraTableau *t, int nunits, int usize, con
     uint32_t all = (t->R >= 32) ? 0xffffffffu : ((1u << t->R) - 1u);
     F(ctx, U, all, K1);
     evals += nunits;
-    memcpy(Kp, K1, sizeof(double) * nd);
+    memset(Kp, 0, sizeof(double) * nd);
     for (size_t d = 0; d < nd; ++d) Ksum[d] = 0.0 + t->b[0] * K1[d];
     for (int i = 2; i <= t->S; ++i) {
         for (int u = 0; u < nunits; ++u) {
@@ -1034,14 +1048,18 @@ static int64_t perk_step_generic(const OraTableau *t, int nunits, int usize, con
         }
         uint32_t mask = 0;
         for (int r = 0; r < t->R; ++r)
-            if (i >= t->S - t->E[r] + 2) mask |= 1u << r;
+            if (tab_active(t, r, i)) mask |= 1u << r;
         F(ctx, Us, mask, Kn);
         for (int u = 0; u < nunits; ++u) {
-            if ((mask >> member[u]) & 1u) evals++;
-            else for (int q = 0; q < usize; ++q) Kn[(size_t)u * usize + q] = 0.0;  /* K_i^(r) = 0: I^(r) mask */
+            size_t d0 = (size_t)u * usize;
+            if ((mask >> member[u]) & 1u) {
+                evals++;
+                for (int q = 0; q < usize; ++q) Kp[d0 + q] = Kn[d0 + q];
+            } else {
+                for (int q = 0; q < usize; ++q) Kn[d0 + q] = 0.0;   /* K_i^(r) = 0: I^(r) mask */
+            }
         }
-        double *tmp = Kp; Kp = Kn; Kn = tmp;
-        for (size_t d = 0; d < nd; ++d) Ksum[d] = Ksum[d] + t->b[i - 1] * Kp[d];
+        for (size_t d = 0; d < nd; ++d) Ksum[d] = Ksum[d] + t->b[i - 1] * Kn[d];
     }
     for (size_t d = 0; d < nd; ++d) U[d] = U[d] + dt * Ksum[d];
     free(K1); free(Kp); free(Kn); free(Us); free(Ksum);
@@ -1049,7 +1067,12 @@ static int64_t perk_step_generic(const OraTableau *t, int nunits, int usize, con
 }
 
 static int g_rhs_mode;
-static void dg_rhs_cb(void *ctx, const double *U, uint32_t mask, double *dU) { (void)ora_rhs(ctx, U, mask, dU, g_rhs_mode); }
+/* restricted mode needs an upward-closed member mask (every standard-pattern stage); the stage masks of
+   other patterns can be any set, and fall back to the definition (full F, then the mask) */
+static void dg_rhs_cb(void *ctx, const double *U, uint32_t mask, double *dU)
+{
+    if (ora_rhs(ctx, U, mask, dU, g_rhs_mode) != 0) (void)ora_rhs(ctx, U, mask, dU, 0);
+}
 
 /* one P-ERK step of the DG system; returns element-RHS evaluations of this step */
 int64_t ora_step(void *p, double *U, double dt, int mode)
