@@ -89,9 +89,14 @@ typedef struct perk_problem {
     int64_t max_cells;
 } perk_problem;
 
-/* P-ERK family in the standard pattern (P:l.407-436): S stages, R members with
- * E[0] < ... < E[R-1] <= S (E[r] >= 2); member r evaluates stages {1} u {S-E_r+2..S}.
- * c[i-1] = c_i, a_sub[r][i-1] = a_{i,i-1} of member r; a_{i,1} = c_i - a_{i,i-1} is derived.
+/* P-ERK family: S stages, R members with E[0] < ... < E[R-1] <= S (E[r] >= 2).
+ * Stage pattern (which stages member r evaluates): active[r] bit i-1 = stage i.  All zero = the
+ * standard pattern {1} u {S-E_r+2..S} (P:l.407-436); otherwise every member's set must hold stages 1
+ * and S and E[r] stages in total, e.g. the alternating and early-shared patterns of P:l.642-700.
+ * c[i-1] = c_i; a_sub[r][i-1] = a_{i,p(i)} of member r, the coefficient of K_{p(i)} in stage i's
+ * state, where p(i) is the member's previous evaluated stage > 1 (= i-1 in the standard pattern);
+ * it may be nonzero only at evaluated stages that have such a predecessor.  a_{i,1} = c_i - a_sub is
+ * derived.  Non-standard patterns: 1D / 2D Euler (not Navier-Stokes).
  * Shared weights b[i-1] = b_i, nonzero only at i = 1, S-1, S:
  *   P-ERK2: b = e_S (P:l.423; perk_tableau_p2 fills it);
  *   P-ERK3: b_1 = b_{S-1} = 1/6, b_S = 4/6 (Shu-Osher base, P:l.870-883), c_{S-1} = 1, c_S = 1/2,
@@ -106,6 +111,7 @@ typedef struct perk_tableau {
     double c[PERK_MAX_STAGES];
     double b[PERK_MAX_STAGES];
     double a_sub[PERK_MAX_MEMBERS][PERK_MAX_STAGES];
+    uint64_t active[PERK_MAX_MEMBERS];
 } perk_tableau;
 
 typedef struct perk_ctx perk_ctx;
@@ -118,6 +124,14 @@ int perk_alpha_taylor(int32_t E, double *alpha_host);
  * ignored).  c_i = (i-1)/(2(S-1)) (P:l.439-442); a_{i,i-1} by the recursion of P:l.1062 for
  * i = 0..E-3, all other a_{i,i-1} = 0.  EINVAL on bad sizes or a zero pivot. */
 int perk_tableau_p2(int32_t S, int32_t R, const int32_t *E_host, const double *alpha_host, perk_tableau *out);
+/* Host only.  perk_tableau_p2 generalised: stage pattern active_host[R] (NULL or
+ * all zero = standard) and abscissa c_S (0.5 = the standard midpoint choice; 1 = Heun, 2/3 = Ralston,
+ * P:l.439-442): c_i = c_S (i-1)/(S-1), b_S = 1/(2 c_S), b_1 = 1 - b_S.  Along member r's evaluated
+ * stages after 1, s_1 < ... < s_{E-1} = S, the row coefficients a_k of stage s_k follow
+ * a_{E-1-i} = alpha_{3+i} / (b_S c_{s_{E-2-i}} prod_{m<i} a_{E-1-m}), i = 0..E-3 (the recursion of
+ * P:l.1058-1064 along the chain).  EINVAL on bad sizes, patterns or a zero pivot. */
+int perk_tableau_p2_ex(int32_t S, int32_t R, const int32_t *E_host, const double *alpha_host,
+                       const uint64_t *active_host, double c_S, perk_tableau *out);
 
 /* Create a context: validates prob/tab (EINVAL, EUNSUPPORTED), uploads the tableau, allocates
  * capacity-sized device buffers and builds the mesh and per-member lists on the device from the

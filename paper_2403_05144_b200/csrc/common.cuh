@@ -50,7 +50,7 @@ struct MeshDev {
     int *count_active;           // [4][MAXS] stage prefix counts
     int *seg;                    // [4][MAXR+1]
     int *err;                    // error flag bits
-    unsigned long long *evals;   // element-RHS evaluation counter
+    unsigned long long *evals;   // [3]: element-RHS evaluations, steps, evaluations per step
     int *list[4];                // per-kind member-sorted item lists
     int *fx, *fy;                // leaf origin (finest grid)
     uint8_t *lev, *mem;          // leaf level, member
@@ -86,23 +86,28 @@ struct StageParams {
     unsigned mask;               // rhs_eval partition mask
     double dt;
     double c_stage;              // c_i (lazy state U_n + dt c_i K_1)
-    int first[MAXR];             // f(r) = S - E_r + 2: first active stage after 1
-    double a1_next[MAXR];        // a_{i+1,1}^{(r)}
-    double asub_next[MAXR];      // a_{i+1,i}^{(r)}
+    unsigned actmask;            // members evaluating this stage (the launch covers a superset prefix)
+    unsigned bufmask;            // members whose stage state is in Ubuf (evaluated, with an earlier
+                                 // evaluated stage > 1); the others form U_n + dt c_i K_1 on the fly
+    double a1_next[MAXR];        // a_{n,1}^{(r)}, n = the member's next evaluated stage after this one
+    double asub_next[MAXR];      // a_{n,i}^{(r)} (standard pattern: n = i + 1)
     double bS;                   // b_S: U_{n+1} = W + dt b_S K_S (W = U_n when b = e_S)
     double wb1, wbS1;            // b_1, b_{S-1}: W = U_n + dt (b_1 K_1 + b_{S-1} K_{S-1}) ...
     int wmode;                   // ... written by the stage S-1 epilogue when wmode = 1 (P-ERK3)
+    int fin_k1;                  // stage S with b_1 != 0 and b_{S-1} = 0 (Heun / Ralston weights, P:l.439-442):
+                                 // U_{n+1} = U_n + dt (b_1 K_1 + b_S K_S), no W buffer
 };
 
 // Which buffer holds element e's stage-i state (SURVEY §7 rule):
-//   i == 1: U_n;  i > f(e): Ubuf;  2 <= i <= f(e): U_n + dt c_i K_1 (formed on the fly)
+//   i == 1: U_n;  i evaluated after an earlier evaluated stage > 1 (standard: i > f(e) = S - E + 2):
+//   Ubuf;  otherwise U_n + dt c_i K_1 (formed on the fly)
 enum StateSrc { SRC_UN = 0, SRC_BUF = 1, SRC_LAZY = 2, SRC_IN = 3 };
 
 __device__ __forceinline__ int state_src(const StageParams &sp, int member)
 {
     if (sp.mode == MODE_RHS) return SRC_IN;
     if (sp.stage == 1) return SRC_UN;
-    return sp.stage > sp.first[member] ? SRC_BUF : SRC_LAZY;
+    return ((sp.bufmask >> member) & 1u) ? SRC_BUF : SRC_LAZY;
 }
 
 struct StateBufs {

@@ -104,14 +104,13 @@ __global__ void __launch_bounds__(128) k_vol1d(MeshDev md, StageParams sp, doubl
     const StateBufs sb{Un, Ubuf, K1, Uin};
     const double dtc = sp.dt * sp.c_stage;
     if (MODE == MODE_STAGE && sp.stage == sp.S && blockIdx.x == 0 && threadIdx.x == 0) {
-        unsigned long long tot = 0;
-        for (int i = 0; i < sp.S; ++i) tot += (unsigned long long)md.count_active[KIND_EL * MAXS + i];
-        atomicAdd(md.evals, tot);
+        atomicAdd(md.evals, md.evals[2]);           // sum_r E_r N_C(r), set by the mesh pipeline
         atomicAdd(md.evals + 1, 1ull);
     }
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_act; t += gridDim.x * blockDim.x) {
         const int e = MODE == MODE_STAGE ? md.list[KIND_EL][t] : t;
         const int m = md.mem[e];
+        if (MODE == MODE_STAGE && !((sp.actmask >> m) & 1u)) continue;   // surplus member of the prefix
         const int src = state_src(sp, m);
         const size_t eb = (size_t)e * NV * NP;
         double u[NP][NV], f[NP][NV];
@@ -144,7 +143,8 @@ __global__ void __launch_bounds__(128) k_vol1d(MeshDev md, StageParams sp, doubl
                 } else if (sp.stage == 1) {
                     K1[idx] = K;
                 } else if (sp.stage == sp.S) {
-                    Un[idx] = fma(sp.dt * sp.bS, K, Wb ? Wb[idx] : Un[idx]);
+                    if (sp.fin_k1) Un[idx] = fma(sp.dt, fma(sp.wb1, K1[idx], sp.bS * K), Un[idx]);
+                    else Un[idx] = fma(sp.dt * sp.bS, K, Wb ? Wb[idx] : Un[idx]);
                 } else {
                     const double un = Un[idx], k1 = K1[idx];
                     Ubuf[idx] = fma(sp.dt, fma(sp.a1_next[m], k1, sp.asub_next[m] * K), un);

@@ -500,9 +500,7 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
     const int pk0 = base < n_act ? (MODE == MODE_STAGE ? md.elpk[base + le < n_act ? base + le : base] : 0) : 0;
     pdl_wait();
     if (MODE == MODE_STAGE && sp.stage == sp.S && blockIdx.x == 0 && threadIdx.x == 0) {
-        unsigned long long tot = 0;
-        for (int i = 0; i < sp.S; ++i) tot += (unsigned long long)md.count_active[KIND_EL * MAXS + i];
-        atomicAdd(md.evals, tot);
+        atomicAdd(md.evals, md.evals[2]);           // sum_r E_r N_C(r), set by the mesh pipeline
         atomicAdd(md.evals + 1, 1ull);
     }
     if (base >= n_act) return;
@@ -585,7 +583,7 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
         __syncwarp();   // the warp has read stg: refill it (next group) and stage this group's epilogue operands
         {
             const bool need_un = MODE == MODE_STAGE && sp.stage > 1;
-            const bool need_k1 = MODE == MODE_STAGE && sp.stage > 1 && sp.stage < sp.S;
+            const bool need_k1 = MODE == MODE_STAGE && sp.stage > 1 && (sp.stage < sp.S || sp.fin_k1);
             copy_block(epi[le][2], Fs + eb);
             // stage S combines with W (P-ERK3) or U_n
             if (need_un) copy_block(epi[le][0], (Wb && sp.stage == sp.S ? Wb : Un) + eb);
@@ -674,8 +672,9 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
         }
         __syncwarp();
 
-        // phase 3: K = -(2/h) (x + y contributions), stage epilogue for nodes q0, q0+1
-        if (valid) {
+        // phase 3: K = -(2/h) (x + y contributions), stage epilogue for nodes q0, q0+1; members in the
+        // launch's prefix that do not evaluate this stage (non-standard patterns) write nothing
+        if (valid && (MODE == MODE_RHS || ((sp.actmask >> m) & 1u))) {
             const double J = -2.0 / hcell;
             const int i0 = q0 & 3, j0 = q0 >> 2;   // q0 + 1 has i0 + 1
 #pragma unroll
@@ -692,8 +691,15 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
                     *reinterpret_cast<double2 *>(K1 + idx) = K;
                 } else if (sp.stage == sp.S) {
                     const double2 w = *reinterpret_cast<const double2 *>(&epi[le][0][v * 16 + q0]);   // W or U_n
-                    const double db = sp.dt * sp.bS;
-                    *reinterpret_cast<double2 *>(Un + idx) = make_double2(fma(db, K.x, w.x), fma(db, K.y, w.y));
+                    if (sp.fin_k1) {
+                        const double2 k1 = *reinterpret_cast<const double2 *>(&epi[le][1][v * 16 + q0]);
+                        *reinterpret_cast<double2 *>(Un + idx) =
+                            make_double2(fma(sp.dt, fma(sp.wb1, k1.x, sp.bS * K.x), w.x),
+                                         fma(sp.dt, fma(sp.wb1, k1.y, sp.bS * K.y), w.y));
+                    } else {
+                        const double db = sp.dt * sp.bS;
+                        *reinterpret_cast<double2 *>(Un + idx) = make_double2(fma(db, K.x, w.x), fma(db, K.y, w.y));
+                    }
                 } else {
                     const double2 un = *reinterpret_cast<const double2 *>(&epi[le][0][v * 16 + q0]);
                     const double2 k1 = *reinterpret_cast<const double2 *>(&epi[le][1][v * 16 + q0]);

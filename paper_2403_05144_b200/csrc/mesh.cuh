@@ -237,9 +237,7 @@ __global__ void k_halo_ranges(MeshDev md, ActiveDesc ad)
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t < 3 * ad.S) {
         const int kind = t / ad.S, i = t % ad.S + 1;
-        int k = 0;
-        for (int r = 0; r < ad.R; ++r)
-            if (i == 1 || ad.E[r] >= ad.S - i + 2) ++k;
+        const int k = active_segments(ad, i);    // Navier-Stokes runs the standard pattern only
         const int *sg = md.hseg + kind * (MAXR + 1);
         md.hrng[kind * MAXS + i - 1] = k < ad.R ? make_int2(sg[k], sg[k + 1] - sg[k]) : make_int2(0, 0);
     }

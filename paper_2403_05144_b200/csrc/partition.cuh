@@ -49,7 +49,19 @@ struct KeyHaloMo {
 struct ActiveDesc {
     int S, R;
     int E[MAXR];
+    unsigned long long act[MAXR];   // evaluated stages of member r (bit i-1), standard or not
 };
+
+// members are sorted by descending E in the lists; the stage-i launch covers the segments of every
+// member from the top down to the lowest-index member evaluating stage i (standard pattern: exactly
+// the evaluating members, a prefix; other patterns: a superset whose surplus members are skipped)
+__device__ __forceinline__ int active_segments(const ActiveDesc &ad, int i)
+{
+    int rmin = ad.R;
+    for (int r = ad.R - 1; r >= 0; --r)
+        if ((ad.act[r] >> (i - 1)) & 1ull) rmin = r;
+    return ad.R - rmin;
+}
 
 template <class KeyFn>
 __global__ void __launch_bounds__(PART_T) k_part_count(KeyFn kf, const int *n_ptr, int mult, int R, int *blockcnt)
@@ -100,7 +112,8 @@ __device__ __forceinline__ int block_incl_scan(int v, int *wsum, int &total)
 // (key R-1-s), seg[R] = total.  Optionally: *total_out = total, and count_active[i-1] for the
 // member partitions (active members are the top ones, i.e. a prefix of the segments).
 __global__ void __launch_bounds__(PART_T) k_part_offsets(const int *blockcnt, int nblocks, int R, int *blockoff, int *seg,
-                                                        int *total_out, ActiveDesc ad, int *count_active)
+                                                        int *total_out, ActiveDesc ad, int *count_active,
+                                                        unsigned long long *evals_per_step = nullptr)
 {
     __shared__ int wsum[32];
     int base = 0;
@@ -123,10 +136,13 @@ __global__ void __launch_bounds__(PART_T) k_part_offsets(const int *blockcnt, in
     __syncthreads();
     if (count_active && threadIdx.x < ad.S) {
         const int i = threadIdx.x + 1;
-        int k = 0;   // number of active members (they are the highest-E ones)
+        count_active[i - 1] = seg[active_segments(ad, i)];
+    }
+    if (evals_per_step && threadIdx.x == 0) {      // sum_r E_r N_C(r) (P:l.1282-1289)
+        unsigned long long tot = 0;
         for (int r = 0; r < ad.R; ++r)
-            if (i == 1 || ad.E[r] >= ad.S - i + 2) ++k;
-        count_active[i - 1] = seg[k];
+            tot += (unsigned long long)ad.E[r] * (unsigned long long)(seg[R - r] - seg[R - 1 - r]);
+        *evals_per_step = tot;
     }
 }
 

@@ -46,6 +46,8 @@ struct perk_ctx {
     double *Gs = nullptr, *Vt = nullptr;   // BR1 (Navier-Stokes): central w* and viscous-flux traces
     double *Wb = nullptr;                  // P-ERK3: W = U_n + dt (b_1 K_1 + b_{S-1} K_{S-1})
     bool ns = false;
+    unsigned long long act[MAXR] = {};     // evaluated stages per member (bit i-1), standard or given
+    bool std_pattern = true;
     uint8_t *lmap = nullptr, *keys = nullptr;
     int *items = nullptr, *rank = nullptr, *blockcnt = nullptr, *blockoff = nullptr, *segtmp = nullptr;
     int *dconst = nullptr;     // [0] = nmorton
@@ -110,33 +112,60 @@ extern "C" int perk_alpha_taylor(int32_t E, double *alpha)
     return PERK_OK;
 }
 
-extern "C" int perk_tableau_p2(int32_t S, int32_t R, const int32_t *E, const double *alpha, perk_tableau *out)
+extern "C" int perk_tableau_p2_ex(int32_t S, int32_t R, const int32_t *E, const double *alpha,
+                                  const uint64_t *active, double c_S, perk_tableau *out)
 {
     if (!E || !alpha || !out || S < 2 || S > PERK_MAX_STAGES || R < 1 || R > PERK_MAX_MEMBERS) return PERK_EINVAL;
+    if (!(c_S > 0.0) || !(c_S <= 1.0)) return PERK_EINVAL;
+    bool any = false;
     for (int r = 0; r < R; ++r) {
         if (E[r] < 2 || E[r] > S) return PERK_EINVAL;
         if (r > 0 && E[r] <= E[r - 1]) return PERK_EINVAL;
+        if (active && active[r]) any = true;
     }
     memset(out, 0, sizeof(*out));
     out->S = S;
     out->R = R;
-    out->b[S - 1] = 1.0;                       // b = e_S (P:l.423)
-    for (int i = 1; i <= S; ++i) out->c[i - 1] = (double)(i - 1) / (double)(2 * (S - 1));
+    const double bS = 1.0 / (2.0 * c_S);
+    out->b[S - 1] = bS;                        // b = e_S for c_S = 1/2 (P:l.423); Heun / Ralston (P:l.439-442)
+    out->b[0] += 1.0 - bS;
+    for (int i = 1; i <= S; ++i)
+        out->c[i - 1] = c_S == 0.5 ? (double)(i - 1) / (double)(2 * (S - 1)) : c_S * (double)(i - 1) / (double)(S - 1);
     for (int r = 0; r < R; ++r) {
         out->E[r] = E[r];
-        const double *al = alpha + (size_t)r * (S + 1);
-        double a[PERK_MAX_STAGES + 1] = {0};
-        // a_{S-i} = alpha_{3+i} / (c_{S-i-1} prod_{j<i} a_{S-j}),  i = 0..E-3   (P:l.1058-1064)
-        for (int i = 0; i <= E[r] - 3; ++i) {
-            double prod = 1.0;
-            for (int j = 0; j < i; ++j) prod *= a[S - j];
-            const double den = out->c[S - i - 2] * prod;
-            if (den == 0.0) return PERK_EINVAL;
-            a[S - i] = al[3 + i] / den;
+        unsigned long long act = 1ull;
+        if (any) {
+            act = active[r];
+            const unsigned long long allowed = S == 64 ? ~0ull : ((1ull << S) - 1ull);
+            if ((act & ~allowed) || !(act & 1ull) || !((act >> (S - 1)) & 1ull) || __builtin_popcountll(act) != E[r])
+                return PERK_EINVAL;
+            out->active[r] = act;
+        } else {
+            for (int i = S - E[r] + 2; i <= S; ++i) act |= 1ull << (i - 1);
         }
-        for (int m = 1; m <= S; ++m) out->a_sub[r][m - 1] = a[m];
+        // chain of evaluated stages after 1: s[1] < ... < s[E-1] = S
+        int st[PERK_MAX_STAGES + 1], ns = 0;
+        for (int i = 2; i <= S; ++i)
+            if ((act >> (i - 1)) & 1ull) st[++ns] = i;
+        const double *al = alpha + (size_t)r * (S + 1);
+        double a[PERK_MAX_STAGES + 1] = {0};   // chain position k -> a_k
+        // a_{E-1-i} = alpha_{3+i} / (b_S c_{s_{E-2-i}} prod_{m<i} a_{E-1-m}),  i = 0..E-3   (P:l.1058-1064)
+        for (int i = 0; i <= E[r] - 3; ++i) {
+            const int k = E[r] - 1 - i;
+            double prod = 1.0;
+            for (int m = E[r] - 1; m >= k + 1; --m) prod *= a[m];
+            const double den = bS * out->c[st[k - 1] - 1] * prod;
+            if (den == 0.0) return PERK_EINVAL;
+            a[k] = al[3 + i] / den;
+        }
+        for (int k = 2; k <= E[r] - 1; ++k) out->a_sub[r][st[k] - 1] = a[k];
     }
     return PERK_OK;
+}
+
+extern "C" int perk_tableau_p2(int32_t S, int32_t R, const int32_t *E, const double *alpha, perk_tableau *out)
+{
+    return perk_tableau_p2_ex(S, R, E, alpha, nullptr, 0.5, out);
 }
 
 // ----------------------------------------------------------------------------------------------
@@ -147,7 +176,10 @@ static ActiveDesc active_desc(const perk_ctx *c)
     ActiveDesc ad;
     ad.S = c->tab.S;
     ad.R = c->tab.R;
-    for (int r = 0; r < MAXR; ++r) ad.E[r] = r < c->tab.R ? c->tab.E[r] : 0;
+    for (int r = 0; r < MAXR; ++r) {
+        ad.E[r] = r < c->tab.R ? c->tab.E[r] : 0;
+        ad.act[r] = r < c->tab.R ? c->act[r] : 0ull;
+    }
     return ad;
 }
 
@@ -163,12 +195,14 @@ static void prof_mark(Prof *p, cudaStream_t s, int kind)
 
 template <class KeyFn>
 static void partition(perk_ctx *c, cudaStream_t s, KeyFn kf, const int *n_ptr, int mult, long long max_items, int R,
-                      int *out, int *rank, int *seg, int *total_out, int *count_active)
+                      int *out, int *rank, int *seg, int *total_out, int *count_active,
+                      unsigned long long *evals_per_step = nullptr)
 {
     int nb = (int)((max_items + PART_T - 1) / PART_T);
     if (nb < 1) nb = 1;
     k_part_count<<<nb, PART_T, 0, s>>>(kf, n_ptr, mult, R, c->blockcnt);
-    k_part_offsets<<<1, PART_T, 0, s>>>(c->blockcnt, nb, R, c->blockoff, seg, total_out, active_desc(c), count_active);
+    k_part_offsets<<<1, PART_T, 0, s>>>(c->blockcnt, nb, R, c->blockoff, seg, total_out, active_desc(c), count_active,
+                                        evals_per_step);
     k_part_scatter<<<nb, PART_T, 0, s>>>(kf, n_ptr, mult, R, c->blockoff, out, rank);
 }
 
@@ -214,7 +248,7 @@ static void build_mesh(perk_ctx *c, cudaStream_t s, const uint8_t *lmap)
     k_face_counts<<<1, 1, 0, s>>>(md, c->segtmp, c->cap_faces);
     k_face_records<<<blocks_for((long long)c->nd * c->cap, 256), 256, 0, s>>>(md, c->items, c->segtmp, R);
     partition(c, s, KeyU8{md.mem}, md.n + 0, 1, c->cap, R, md.list[KIND_EL], nullptr, md.seg + 0 * (MAXR + 1), nullptr,
-              md.count_active + KIND_EL * MAXS);
+              md.count_active + KIND_EL * MAXS, md.evals + 2);
     partition(c, s, KeyIfc{md.ifc}, md.n + 1, 1, c->cap_faces, R, md.list[KIND_IF], nullptr, md.seg + 1 * (MAXR + 1),
               nullptr, md.count_active + KIND_IF * MAXS);
     partition(c, s, KeyMor{md.mor}, md.n + 2, 1, c->cap_faces, R, md.list[KIND_MO], nullptr, md.seg + 2 * (MAXR + 1),
@@ -253,11 +287,20 @@ static StageParams stage_params(const perk_ctx *c, int i, double dt, int mode, u
     sp.wb1 = c->tab.b[0];
     sp.wbS1 = c->tab.b[c->tab.S - 2];
     sp.wmode = (c->Wb && i == c->tab.S - 1) ? 1 : 0;
+    sp.fin_k1 = (!c->Wb && i == c->tab.S && c->tab.b[0] != 0.0) ? 1 : 0;
     for (int r = 0; r < c->tab.R; ++r) {
-        sp.first[r] = c->tab.S - c->tab.E[r] + 2;
-        if (i < c->tab.S) {
-            sp.asub_next[r] = c->tab.a_sub[r][i];                  // a_{i+1,i}
-            sp.a1_next[r] = c->tab.c[i] - c->tab.a_sub[r][i];       // a_{i+1,1} = c_{i+1} - a_{i+1,i}
+        const unsigned long long a = c->act[r];
+        if ((a >> (i - 1)) & 1ull) sp.actmask |= 1u << r;
+        // stage i state in Ubuf: evaluated at i and at some stage in (1, i)
+        if (i > 1 && ((a >> (i - 1)) & 1ull) && (a & (((1ull << (i - 1)) - 1ull) & ~1ull))) sp.bufmask |= 1u << r;
+        // after evaluating stage i: the state of the next evaluated stage n,
+        // U^(n) = U_n + dt (a_{n,1} K_1 + a_{n,i} K_i)   (standard pattern: n = i + 1)
+        int n = 0;
+        for (int j = i + 1; j <= c->tab.S; ++j)
+            if ((a >> (j - 1)) & 1ull) { n = j; break; }
+        if (n) {
+            sp.asub_next[r] = c->tab.a_sub[r][n - 1];
+            sp.a1_next[r] = c->tab.c[n - 1] - c->tab.a_sub[r][n - 1];
         }
     }
     return sp;
@@ -421,8 +464,39 @@ static int validate(perk_ctx *c, const perk_problem *p, const perk_tableau *t)
         bsum += t->b[i];
     }
     if (std::fabs(bsum - 1.0) > 1e-14) return set_err(c, PERK_EINVAL, "b must sum to 1");
-    if ((t->b[0] != 0.0 || (t->S >= 2 && t->b[t->S - 2] != 0.0)) && t->E[0] < 3)
-        return set_err(c, PERK_EINVAL, "b_1, b_{S-1} != 0 (P-ERK3) needs every member active at stage S-1 (E >= 3)");
+    // stage patterns: all zero = standard, else every member's set holds 1 and S and E[r] stages
+    bool any = false;
+    for (int r = 0; r < t->R; ++r) any |= t->active[r] != 0;
+    unsigned long long act[MAXR] = {};
+    for (int r = 0; r < t->R; ++r) {
+        if (!any) {
+            act[r] = 1ull;
+            for (int i = t->S - t->E[r] + 2; i <= t->S; ++i) act[r] |= 1ull << (i - 1);
+        } else {
+            act[r] = t->active[r];
+            const unsigned long long allowed = t->S == 64 ? ~0ull : ((1ull << t->S) - 1ull);
+            if ((act[r] & ~allowed) || !(act[r] & 1ull) || !((act[r] >> (t->S - 1)) & 1ull) ||
+                __builtin_popcountll(act[r]) != t->E[r])
+                return set_err(c, PERK_EINVAL, "active[r] must hold stages 1 and S and E[r] stages in [1, S]");
+        }
+        for (int i = 1; i <= t->S; ++i) {       // a_{i,p(i)} only at evaluated stages with a predecessor > 1
+            const bool ok = i > 1 && ((act[r] >> (i - 1)) & 1ull) && (act[r] & (((1ull << (i - 1)) - 1ull) & ~1ull));
+            if (t->a_sub[r][i - 1] != 0.0 && !ok)
+                return set_err(c, PERK_EINVAL, "a_sub[r][i-1] != 0 at a stage without an evaluated predecessor > 1");
+        }
+    }
+    if (any && p->equation == PERK_EQ_NAVIER_STOKES)
+        return set_err(c, PERK_EUNSUPPORTED, "non-standard stage patterns: Euler / advection only (BR1 halo needs nesting)");
+    // b_{S-1} != 0 (P-ERK3): W = U_n + dt (b_1 K_1 + b_{S-1} K_{S-1}) is formed in the stage S-1 epilogue;
+    // b_1 alone (Heun / Ralston) is added at stage S
+    if (t->S >= 3 && t->b[t->S - 2] != 0.0)
+        for (int r = 0; r < t->R; ++r)
+            if (!((act[r] >> (t->S - 2)) & 1ull))
+                return set_err(c, PERK_EINVAL, "b_{S-1} != 0 needs every member to evaluate stage S-1");
+    if (c) {
+        for (int r = 0; r < MAXR; ++r) c->act[r] = r < t->R ? act[r] : 0ull;
+        c->std_pattern = !any;
+    }
     return PERK_OK;
 }
 
@@ -494,7 +568,7 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
     CU(dalloc(c, &md.count_active, 4 * MAXS));
     CU(dalloc(c, &md.seg, 4 * (MAXR + 1)));
     CU(dalloc(c, &md.err, 1));
-    CU(dalloc(c, &md.evals, 2));
+    CU(dalloc(c, &md.evals, 3));
     CU(dalloc(c, &md.list[KIND_EL], c->cap));
     for (int k = 1; k < 4; ++k) CU(dalloc(c, &md.list[k], c->cap_faces));
     CU(dalloc(c, &md.fx, c->cap));
@@ -511,7 +585,7 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
     CU(dalloc(c, &c->K1, (size_t)c->cap * rowd));
     CU(dalloc(c, &c->Ubuf, (size_t)c->cap * rowd));
     CU(dalloc(c, &c->Fs, (size_t)c->cap * (dim == 1 ? 2 * c->nv : 4 * c->nv * NP)));
-    if (tab->b[0] != 0.0 || tab->b[tab->S - 2] != 0.0) CU(dalloc(c, &c->Wb, (size_t)c->cap * rowd));
+    if (tab->S >= 3 && tab->b[tab->S - 2] != 0.0) CU(dalloc(c, &c->Wb, (size_t)c->cap * rowd));   // P-ERK3
     if (c->ns) {
         CU(dalloc(c, &md.halo, c->cap));
         CU(dalloc(c, &md.hlist[KIND_EL], c->cap));
@@ -588,11 +662,13 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
             memset(&h, 0, sizeof(h));
             h.S = tab->S;
             h.R = tab->R;
-            for (int r = 0; r < tab->R; ++r) {
-                h.first[r] = tab->S - tab->E[r] + 2;
-                for (int i = 0; i < tab->S; ++i) {
-                    h.asub[r][i] = tab->a_sub[r][i];
-                    h.a1[r][i] = tab->c[i] - tab->a_sub[r][i];
+            for (int i = 1; i <= tab->S; ++i) {
+                const StageParams sp = stage_params(c, i, 0.0, MODE_STAGE, 0u);
+                h.actmask[i - 1] = sp.actmask;
+                h.bufmask[i - 1] = sp.bufmask;
+                for (int r = 0; r < tab->R; ++r) {
+                    h.a1n[r][i - 1] = sp.a1_next[r];
+                    h.asubn[r][i - 1] = sp.asub_next[r];
                 }
             }
             for (int i = 0; i < tab->S; ++i) h.c[i] = tab->c[i];

@@ -14,11 +14,12 @@ namespace perk {
 
 struct StepTab1D {
     int S, R;
-    int first[MAXR];             // f(r) = S - E_r + 2
+    unsigned actmask[MAXS];      // stage i (index i-1): members evaluating it
+    unsigned bufmask[MAXS];      // stage i: members whose stage state is in the stage buffer
     double c[MAXS];
     double b1, bS1, bS;          // shared weights at stages 1, S-1, S
-    double a1[MAXR][MAXS];       // a_{i,1}^{(r)}, index i-1
-    double asub[MAXR][MAXS];     // a_{i,i-1}^{(r)}, index i-1
+    double a1n[MAXR][MAXS];      // after evaluating stage i (index i-1): a_{n,1}^{(r)} of the next
+    double asubn[MAXR][MAXS];    // evaluated stage n, and a_{n,i}^{(r)} (standard pattern: n = i+1)
 };
 
 // threads per CTA: the per-stage cost is ceil(active nodes / threads) dependent passes; measured
@@ -59,7 +60,7 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
         auto state = [&](int e, int m, int v, int j) {
             const size_t x = ((size_t)e * NV + v) * NP + j;
             if (i == 1) return sUn[x];
-            if (i > T.first[m]) return sUb[x];
+            if ((T.bufmask[i - 1] >> m) & 1u) return sUb[x];
             return fma(dtc, sK1[x], sUn[x]);
         };
         // surface fluxes over the active interfaces and boundaries
@@ -95,10 +96,12 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
             }
         }
         __syncthreads();
-        // K_i at the active element nodes (one thread per node)
+        // K_i at the active element nodes (one thread per node); surplus members of the prefix skip
+        const unsigned act = T.actmask[i - 1];
         for (int t = tid; t < NP * nel; t += nt) {
             const int e = md.list[KIND_EL][t / NP], j = t % NP;
             const int m = md.mem[e];
+            if (!((act >> m) & 1u)) continue;
             double f[NP][NV];
 #pragma unroll
             for (int k = 0; k < NP; ++k) {
@@ -123,6 +126,7 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
         for (int t = tid; t < NP * nel; t += nt) {
             const int e = md.list[KIND_EL][t / NP], j = t % NP;
             const int m = md.mem[e];
+            if (!((act >> m) & 1u)) continue;
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
                 const size_t x = ((size_t)e * NV + v) * NP + j;
@@ -130,10 +134,11 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
                 if (i == 1) {
                     sK1[x] = K;
                 } else if (i == S) {
-                    sUn[x] = fma(dt * T.bS, K, use_w ? sW[x] : sUn[x]);
+                    if (!use_w && T.b1 != 0.0) sUn[x] = fma(dt, fma(T.b1, sK1[x], T.bS * K), sUn[x]);   // Heun / Ralston
+                    else sUn[x] = fma(dt * T.bS, K, use_w ? sW[x] : sUn[x]);
                 } else {
                     const double un = sUn[x], k1 = sK1[x];
-                    sUb[x] = fma(dt, fma(T.a1[m][i], k1, T.asub[m][i] * K), un);    // U^(i+1)
+                    sUb[x] = fma(dt, fma(T.a1n[m][i - 1], k1, T.asubn[m][i - 1] * K), un);   // next evaluated stage
                     if (use_w && i == S - 1) sW[x] = fma(dt, fma(T.b1, k1, T.bS1 * K), un);
                 }
             }
@@ -142,9 +147,7 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
     }
     for (int k = tid; k < n * rowd; k += nt) U[k] = sUn[k];
     if (tid == 0) {
-        unsigned long long tot = 0;
-        for (int i = 0; i < S; ++i) tot += (unsigned long long)md.count_active[KIND_EL * MAXS + i];
-        atomicAdd(md.evals, tot);
+        atomicAdd(md.evals, md.evals[2]);
         atomicAdd(md.evals + 1, 1ull);
     }
 }

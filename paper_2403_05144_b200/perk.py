@@ -40,7 +40,7 @@ class perk_problem(C.Structure):
 
 class perk_tableau(C.Structure):
     _fields_ = [("S", C.c_int32), ("R", C.c_int32), ("E", C.c_int32 * 8), ("c", C.c_double * 64),
-                ("b", C.c_double * 64), ("a_sub", (C.c_double * 64) * 8)]
+                ("b", C.c_double * 64), ("a_sub", (C.c_double * 64) * 8), ("active", C.c_uint64 * 8)]
 
 
 class perk_amr(C.Structure):
@@ -80,6 +80,8 @@ def lib():
         i32, i64, dbl = C.c_int32, C.c_int64, C.c_double
         L.perk_alpha_taylor.argtypes = [i32, C.POINTER(dbl)]
         L.perk_tableau_p2.argtypes = [i32, i32, C.POINTER(i32), C.POINTER(dbl), C.POINTER(perk_tableau)]
+        L.perk_tableau_p2_ex.argtypes = [i32, i32, C.POINTER(i32), C.POINTER(dbl), C.POINTER(C.c_uint64), dbl,
+                                         C.POINTER(perk_tableau)]
         L.perk_init.argtypes = [C.POINTER(P), C.POINTER(perk_problem), P, C.POINTER(perk_tableau), P]
         L.perk_destroy.argtypes = [P]
         L.perk_set_stream.argtypes = [P, P]
@@ -110,16 +112,37 @@ def lib():
 
 
 def exported_symbols():
-    return ["perk_alpha_taylor", "perk_tableau_p2", "perk_init", "perk_destroy", "perk_set_stream", "perk_step",
+    return ["perk_alpha_taylor", "perk_tableau_p2", "perk_tableau_p2_ex", "perk_init", "perk_destroy", "perk_set_stream", "perk_step",
             "perk_run_host", "perk_repartition", "rhs_eval", "perk_num_cells", "perk_num_faces", "perk_node_coords",
             "perk_get_leaves", "perk_get_faces", "perk_get_list", "perk_get_count_active", "perk_get_counters",
             "perk_sync", "perk_last_error", "perk_profile_step", "perk_time_kernels", "perk_profile_repartition",
             "perk_launches_per_step", "perk_amr_indicator", "perk_amr_adapt", "perk_amr_launches"]
 
 
-def tableau_p2(S: int, E, alpha_rows=None) -> perk_tableau:
+def pattern_mask(S: int, E: int, pattern) -> int:
+    """Evaluated-stage bitmask (bit i-1 = stage i) of a member with E evaluations: "standard"
+    {1} u {S-E+2..S} (P:l.407-436), "early" {1..E-1} u {S} (P:l.683-700), "alternating"
+    {1} u {S - floor((E-1-k)(S-1)/(E-1) + 1/2) : k = 1..E-1} (P:l.655-675 at S = 6, E = 4; F1),
+    or an explicit iterable of stages."""
+    if pattern == "standard":
+        st = [1] + list(range(S - E + 2, S + 1))
+    elif pattern == "early":
+        st = list(range(1, E)) + [S]
+    elif pattern == "alternating":
+        st = [1] + [S - ((E - 1 - k) * (S - 1) * 2 + (E - 1)) // (2 * (E - 1)) for k in range(1, E)]
+    else:
+        st = [int(i) for i in pattern]
+    m = 0
+    for i in st:
+        m |= 1 << (i - 1)
+    return m
+
+
+def tableau_p2(S: int, E, alpha_rows=None, pattern=None, c_S: float = 0.5) -> perk_tableau:
     """P-ERK2 family via the library (C recursion).  alpha_rows: R rows of S+1 coefficients; default
-    the Taylor rule alpha_k = 1/k! (BASELINE.json cfg 1), also built by the library."""
+    the Taylor rule alpha_k = 1/k! (BASELINE.json cfg 1), also built by the library.  pattern: None /
+    "standard", a pattern name for every member, or one name / stage list per member (SURVEY §8(f) f2);
+    c_S: 1/2 standard, 1 Heun, 2/3 Ralston (P:l.439-442)."""
     E = [int(e) for e in E]
     R = len(E)
     al = np.zeros((R, S + 1))
@@ -135,7 +158,15 @@ def tableau_p2(S: int, E, alpha_rows=None) -> perk_tableau:
     al = np.ascontiguousarray(al)
     t = perk_tableau()
     Ea = (C.c_int32 * R)(*E)
-    _check(None, lib().perk_tableau_p2(S, R, Ea, al.ctypes.data_as(C.POINTER(C.c_double)), C.byref(t)))
+    act = None
+    if pattern is not None and pattern != "standard":
+        pats = pattern if isinstance(pattern, (list, tuple)) and len(pattern) == R and \
+            not all(isinstance(x, int) for x in pattern) else [pattern] * R
+        masks = [pattern_mask(S, e, pt) for e, pt in zip(E, pats)]
+        if masks != [pattern_mask(S, e, "standard") for e in E]:
+            act = (C.c_uint64 * R)(*masks)
+    _check(None, lib().perk_tableau_p2_ex(S, R, Ea, al.ctypes.data_as(C.POINTER(C.c_double)), act, float(c_S),
+                                          C.byref(t)))
     return t
 
 
@@ -152,6 +183,8 @@ def tableau_from(family: dict) -> perk_tableau:
         t.E[r] = e
         for i in range(S):
             t.a_sub[r][i] = family["asub_f"][r][i]
+    for r, m in enumerate(family.get("active_mask") or []):
+        t.active[r] = int(m)
     return t
 
 
@@ -187,7 +220,7 @@ class Perk:
     """One P-ERK multirate DGSEM context on the current CUDA device (all work on the current stream)."""
 
     def __init__(self, problem: dict, level_map, S: int, E, alpha_rows=None, max_cells=None, stream=None,
-                 family=None):
+                 family=None, pattern=None, c_S: float = 0.5):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("CUDA device required: libperk_b200 has no CPU path")
@@ -200,7 +233,7 @@ class Perk:
         self.E = list(E)
         self.R = len(self.E)
         self.max_cells = int(max_cells or problem["max_cells"])
-        self._tab = tableau_p2(S, self.E, alpha_rows) if family is None else tableau_from(family)
+        self._tab = tableau_p2(S, self.E, alpha_rows, pattern, c_S) if family is None else tableau_from(family)
         self._prob = _problem_struct(problem, self.max_cells)
         lm = self._to_dev_u8(level_map)
         self.stream = stream if stream is not None else torch.cuda.current_stream()

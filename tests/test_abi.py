@@ -84,3 +84,30 @@ def test_product_path_fails_loudly_without_gpu(lib):
     w = W.make(1)
     with pytest.raises(RuntimeError):
         lib.Perk(w.problem, w.level_map, w.S, w.E)
+
+
+@pytest.mark.parametrize("pattern", ["alternating", "early", [[1, 3, 6, 8], [1, 2, 4, 5, 8], "standard"]])
+@pytest.mark.parametrize("c_S", [0.5, 1.0, 2.0 / 3.0])
+def test_library_pattern_tableau_matches_oracle(lib, pattern, c_S):
+    """stage patterns and Heun / Ralston weights: the library's masks, c, b and chain
+    coefficients agree with the oracle's exact ones (independent implementations)"""
+    from fractions import Fraction as Fr
+    S, E = 8, [4, 5, 8]
+    cS = Fr(2, 3) if abs(c_S - 2 / 3) < 1e-12 else Fr(c_S)
+    fam = T.family(S, E, "taylor", pattern=pattern, c_S=cS)
+    t = lib.tableau_p2(S, E, pattern=pattern, c_S=c_S)
+    masks = fam["active_mask"] or [0] * 3
+    assert [t.active[r] for r in range(3)] == masks
+    for i in range(S):
+        assert abs(t.c[i] - fam["c_f"][i]) <= 1e-16 and abs(t.b[i] - fam["b_f"][i]) <= 1e-16
+        for r in range(3):
+            want = fam["asub_f"][r][i]
+            assert (want == 0) == (t.a_sub[r][i] == 0) and abs(t.a_sub[r][i] - want) <= 1e-14 * abs(want)
+
+
+def test_invalid_patterns_rejected(lib):
+    for pat in ([[1, 2, 8], [1, 3, 4, 5, 8], "standard"],      # member 0 holds 3 stages, E = 4
+                [[2, 3, 4, 8], [1, 2, 4, 5, 8], "standard"],   # stage 1 missing
+                [[1, 2, 3, 4], [1, 2, 4, 5, 8], "standard"]):  # stage S missing
+        with pytest.raises(lib.PerkError):
+            lib.tableau_p2(8, [4, 5, 8], pattern=pat)
