@@ -127,3 +127,21 @@ def test_patterns_rejected_for_navier_stokes_and_bad_masks():
     w3 = W.make(3, n_base=8)
     with pytest.raises(PerkError):
         tableau_p2(w3.S, w3.E, pattern=[[1, 2, 16], [1, 2, 4, 5, 6, 7, 8, 16], "standard"])
+
+
+def test_maximum_stage_count_s64():
+    """S = PERK_MAX_STAGES = 64 (stage masks use all 64 bits), standard and alternating"""
+    w = W.make(3, n_base=8)
+    w.S, w.E = 64, [16, 32, 64]
+    dt = w.dt * 4
+    for pattern in ("standard", "alternating"):
+        fam, ora, gpu = _pair(w, pattern)
+        Uo = ora.initial_state(w.ic)
+        Ug = gpu.initial_state(w.ic)
+        ev_o = ora.step(Uo, dt, 2)
+        gpu.step(Ug, dt, 2)
+        torch.cuda.synchronize()
+        gpu.sync()
+        assert gpu.counters()[0] == ev_o
+        assert gpu.launches_per_step() == 2 * 64
+        assert rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo).max() <= TOL
