@@ -102,7 +102,7 @@ static cudaError_t dalloc(perk_ctx *c, T **p, size_t n)
 // ----------------------------------------------------------------------------------------------
 extern "C" int perk_alpha_taylor(int32_t E, double *alpha)
 {
-    if (!alpha || E < 0 || E >= PERK_MAX_STAGES) return PERK_EINVAL;
+    if (!alpha || E < 0 || E > PERK_MAX_STAGES) return PERK_EINVAL;
     double f = 1.0;
     alpha[0] = 1.0;
     for (int k = 1; k <= E; ++k) {
