@@ -200,8 +200,14 @@ __device__ __forceinline__ void store_face2d(double *Fs, int e, int face, int k,
 
 // NS: the face flux is HLL(u_L, u_R) - (F^v_L + F^v_R)/2 (central BR1 viscous flux from the
 // normal viscous-flux traces Vt of k_grad2d), so the volume kernel lifts one combined flux.
+#ifndef SURF2D_MINB
+#define SURF2D_MINB 3
+#endif
+#ifndef SURF2D_PAIRED
+#define SURF2D_PAIRED 1
+#endif
 template <int MODE, bool NS>
-__global__ void __launch_bounds__(256, 3) k_surf2d(MeshDev md, StageParams sp, const double *__restrict__ Un,
+__global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StageParams sp, const double *__restrict__ Un,
                                                const double *__restrict__ Ubuf, const double *__restrict__ K1,
                                                const double *__restrict__ Uin, double *__restrict__ Fs,
                                                const double *__restrict__ Vt)
@@ -226,7 +232,7 @@ __global__ void __launch_bounds__(256, 3) k_surf2d(MeshDev md, StageParams sp, c
     int gt = blockIdx.x * blockDim.x + threadIdx.x;
     // two interface face nodes per iteration while both are interfaces: twice the loads in flight
     // per thread (the kernel is bound by the latency of the record -> trace gathers)
-    for (; gt + GS < nI; gt += 2 * GS) {
+    for (; SURF2D_PAIRED && gt + GS < nI; gt += 2 * GS) {
         const int ka = gt & 3, kb = (gt + GS) & 3;
         const int4 Ia = MODE == MODE_STAGE ? md.ifcs[gt >> 2] : md.ifc[gt >> 2];
         const int4 Ib = MODE == MODE_STAGE ? md.ifcs[(gt + GS) >> 2] : md.ifc[(gt + GS) >> 2];
