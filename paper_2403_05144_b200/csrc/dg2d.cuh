@@ -460,7 +460,15 @@ __device__ __forceinline__ void visc_volume(double (*sm)[2][LS], int o, int lo, 
 
 // Dynamic shared memory of k_vol2d (bytes): field arrays, own-state staging, epilogue staging.
 __host__ __device__ constexpr int vol2d_nf(bool ns) { return ns ? 8 : 7; }
-__host__ __device__ constexpr int vol2d_epi_slots(bool ns) { return ns ? 4 : 3; }   // U_n, K_1, Fs (+ Gs)
+#ifndef VOL2D_STAGE_UNK1
+#define VOL2D_STAGE_UNK1 1     // 1: U_n / K_1 of the epilogue staged in shared memory; 0: read from global
+#endif
+#ifndef VOL2D_MINB
+#define VOL2D_MINB (VOL2D_STAGE_UNK1 ? 3 : 4)
+#endif
+constexpr int EPI_UN = 0, EPI_K1 = 1;                                   // (staged variant only)
+constexpr int EPI_FS = VOL2D_STAGE_UNK1 ? 2 : 0, EPI_GS = EPI_FS + 1;
+__host__ __device__ constexpr int vol2d_epi_slots(bool ns) { return (VOL2D_STAGE_UNK1 ? 3 : 1) + (ns ? 1 : 0); }   // (U_n, K_1,) Fs (+ Gs)
 __host__ __device__ constexpr size_t vol2d_smem_bytes(bool ns)
 {
     return sizeof(double) * ((size_t)vol2d_nf(ns) * 2 * VOL2D_LS + VOL2D_EPB * 2 * 64 + VOL2D_EPB * vol2d_epi_slots(ns) * 64);
@@ -477,7 +485,7 @@ __host__ __device__ constexpr size_t vol2d_smem_bytes(bool ns)
 // cp.async.bulk on mbarriers; issuing the per-element bulk copies through the uniform datapath cost
 // about a quarter of the kernel's issue slots.)
 template <int MODE, bool NS>
-__global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
+__global__ void __launch_bounds__(128, NS ? 3 : VOL2D_MINB) k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                                                  double *__restrict__ Ubuf, double *__restrict__ K1,
                                                  const double *__restrict__ Fs, const double *__restrict__ Uin,
                                                  double *__restrict__ dU, const double *__restrict__ Gs,
@@ -590,14 +598,19 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
         {
             const bool need_un = MODE == MODE_STAGE && sp.stage > 1;
             const bool need_k1 = MODE == MODE_STAGE && sp.stage > 1 && (sp.stage < sp.S || sp.fin_k1);
-            copy_block(epi[le][2], Fs + eb);
+            copy_block(epi[le][EPI_FS], Fs + eb);
             // stage S combines with W (P-ERK3) or U_n
-            if (need_un) copy_block(epi[le][0], (Wb && sp.stage == sp.S ? Wb : Un) + eb);
-            if (need_k1) copy_block(epi[le][1], K1 + eb);
+            if (VOL2D_STAGE_UNK1) {
+                if (need_un) copy_block(epi[le][EPI_UN], (Wb && sp.stage == sp.S ? Wb : Un) + eb);
+                if (need_k1) copy_block(epi[le][EPI_K1], K1 + eb);
+            } else if (valid) {   // pull the epilogue operands' lines into L1 for phase 3
+                const double *src = (t8 < 4) ? (need_un ? (Wb && sp.stage == sp.S ? Wb : Un) : nullptr) : (need_k1 ? K1 : nullptr);
+                if (src) asm volatile("prefetch.global.L1 [%0];" ::"l"(src + eb + 16 * (t8 & 3)));
+            }
             if (NS) {   // the element's 48 BR1 central traces (384 B = 24 chunks of 16 B)
 #pragma unroll
                 for (int r = 0; r < 3; ++r)
-                    cp_async16(&epi[le][3][2 * (t8 + 8 * r)], Gs + (size_t)e * 4 * GV * NP + 2 * (t8 + 8 * r));
+                    cp_async16(&epi[le][EPI_GS][2 * (t8 + 8 * r)], Gs + (size_t)e * 4 * GV * NP + 2 * (t8 + 8 * r));
             }
             cp_async_commit();
         }
@@ -646,7 +659,7 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
             if (has_next) cp_async_wait<1>();
             else cp_async_wait<0>();
             __syncwarp();
-            visc_volume<VOL2D_LS>(sm, o, lo, eo, yo, ln, &epi[le][3][0], 2.0 / hcell, md.mu, md.kappa, acc);
+            visc_volume<VOL2D_LS>(sm, o, lo, eo, yo, ln, &epi[le][EPI_GS][0], 2.0 / hcell, md.mu, md.kappa, acc);
         }
         // surface lift: + f*_hi / w_N at the last node, - f*_lo / w_0 at the first node
         // line coordinates (normal, tangential) -> (momentum x, momentum y)
@@ -662,8 +675,8 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
         else cp_async_wait<0>();
         __syncwarp();
         {
-            const double *Fhi = &epi[le][2][(2 * o) * 16 + ln];
-            const double *Flo = &epi[le][2][(2 * o + 1) * 16 + ln];
+            const double *Fhi = &epi[le][EPI_FS][(2 * o) * 16 + ln];
+            const double *Flo = &epi[le][EPI_FS][(2 * o + 1) * 16 + ln];
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
                 acc[3][v] = fma(Fhi[v * 4], cB.invw[3], acc[3][v]);
@@ -696,9 +709,11 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
                 } else if (sp.stage == 1) {
                     *reinterpret_cast<double2 *>(K1 + idx) = K;
                 } else if (sp.stage == sp.S) {
-                    const double2 w = *reinterpret_cast<const double2 *>(&epi[le][0][v * 16 + q0]);   // W or U_n
+                    const double2 w = VOL2D_STAGE_UNK1 ? *reinterpret_cast<const double2 *>(&epi[le][EPI_UN][v * 16 + q0])
+                                                       : __ldg(reinterpret_cast<const double2 *>((Wb ? Wb : Un) + idx));   // W or U_n
                     if (sp.fin_k1) {
-                        const double2 k1 = *reinterpret_cast<const double2 *>(&epi[le][1][v * 16 + q0]);
+                        const double2 k1 = VOL2D_STAGE_UNK1 ? *reinterpret_cast<const double2 *>(&epi[le][EPI_K1][v * 16 + q0])
+                                                            : __ldg(reinterpret_cast<const double2 *>(K1 + idx));
                         *reinterpret_cast<double2 *>(Un + idx) =
                             make_double2(fma(sp.dt, fma(sp.wb1, k1.x, sp.bS * K.x), w.x),
                                          fma(sp.dt, fma(sp.wb1, k1.y, sp.bS * K.y), w.y));
@@ -707,8 +722,10 @@ __global__ void __launch_bounds__(128, 3) k_vol2d(MeshDev md, StageParams sp, do
                         *reinterpret_cast<double2 *>(Un + idx) = make_double2(fma(db, K.x, w.x), fma(db, K.y, w.y));
                     }
                 } else {
-                    const double2 un = *reinterpret_cast<const double2 *>(&epi[le][0][v * 16 + q0]);
-                    const double2 k1 = *reinterpret_cast<const double2 *>(&epi[le][1][v * 16 + q0]);
+                    const double2 un = VOL2D_STAGE_UNK1 ? *reinterpret_cast<const double2 *>(&epi[le][EPI_UN][v * 16 + q0])
+                                                        : *reinterpret_cast<const double2 *>(Un + idx);
+                    const double2 k1 = VOL2D_STAGE_UNK1 ? *reinterpret_cast<const double2 *>(&epi[le][EPI_K1][v * 16 + q0])
+                                                        : __ldg(reinterpret_cast<const double2 *>(K1 + idx));
                     const double a1 = sp.a1_next[m], as = sp.asub_next[m];
                     *reinterpret_cast<double2 *>(Ubuf + idx) =
                         make_double2(fma(sp.dt, fma(a1, k1.x, as * K.x), un.x), fma(sp.dt, fma(a1, k1.y, as * K.y), un.y));
