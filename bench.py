@@ -266,7 +266,10 @@ def measure_config(cfg, K, Wm, timer, torch, dist, ws, dev, with_single=True, or
         ev, st = perk.counters()
         elem_rhs_per_step = ev / max(st, 1)
     else:
-        elem_rhs_per_step = int(sum(int(x) for x in perk.count_active("elements")))
+        # sum_r E_r N_C(r) from the device counter (the per-stage launch sizes over-count members that
+        # do not evaluate a stage under non-standard stage patterns)
+        ev, st = perk.counters()
+        elem_rhs_per_step = int(round(ev / max(st, 1)))
     ms = _max_over_ranks(torch, dist, ws, dev, ms_raw)
     res.update(ms_per_step=round(ms, 5), element_rhs_per_step=round(float(elem_rhs_per_step), 1),
                value=round(replica_value(ws, elem_rhs_per_step, ms), 1), n_cells_now=perk.n_cells)

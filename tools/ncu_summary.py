@@ -11,8 +11,8 @@ def launch_shares(path):
     agg = collections.defaultdict(lambda: [0, 0.0])
     for r in rows:
         name = r[4].split("(")[0].replace("void ", "")
-        if name in ("k_dfma",):      # bench.py's fp64-peak microbenchmark, not part of the step
-            continue
+        if name in ("k_dfma",) or name.startswith("at::"):   # bench.py's fp64-peak microbenchmark and
+            continue                                          # torch's L2-flush fills: not part of the step
         agg[name][0] += 1
         agg[name][1] += float(r[-1])
     tot = sum(v[1] for v in agg.values())
