@@ -111,7 +111,8 @@ __device__ __forceinline__ int block_incl_scan(int v, int *wsum, int &total)
 // One block.  blockoff[b][r] = start of block b's bucket-r items; seg[s] = start of segment s
 // (key R-1-s), seg[R] = total.  Optionally: *total_out = total, and count_active[i-1] for the
 // member partitions (active members are the top ones, i.e. a prefix of the segments).
-__global__ void __launch_bounds__(PART_T) k_part_offsets(const int *blockcnt, int nblocks, int R, int *blockoff, int *seg,
+constexpr int PART_OFF_T = 1024;   // k_part_offsets block: 4x fewer sequential chunk scans than PART_T
+__global__ void __launch_bounds__(PART_OFF_T) k_part_offsets(const int *blockcnt, int nblocks, int R, int *blockoff, int *seg,
                                                         int *total_out, ActiveDesc ad, int *count_active,
                                                         unsigned long long *evals_per_step = nullptr)
 {
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(PART_T) k_part_offsets(const int *blockcnt, in
     for (int s = 0; s < R; ++s) {
         const int r = R - 1 - s;
         if (threadIdx.x == 0) seg[s] = base;
-        for (int chunk = 0; chunk < nblocks; chunk += PART_T) {
+        for (int chunk = 0; chunk < nblocks; chunk += blockDim.x) {
             const int b = chunk + threadIdx.x;
             const int v = b < nblocks ? blockcnt[b * MAXR + r] : 0;
             int tot;

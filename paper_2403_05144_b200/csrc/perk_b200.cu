@@ -63,6 +63,8 @@ struct perk_ctx {
     StepTab1D *tb1d = nullptr;
     size_t step1d_smem = 0;
     cudaGraphExec_t gexec = nullptr;
+    cudaGraphExec_t rexec = nullptr;       // re-mesh graph (mesh pipeline + transfer), keyed on U
+    double *rU = nullptr;
     double *gU = nullptr;
     double gdt = 0.0;
     std::vector<void *> allocs;
@@ -201,7 +203,7 @@ static void partition(perk_ctx *c, cudaStream_t s, KeyFn kf, const int *n_ptr, i
     int nb = (int)((max_items + PART_T - 1) / PART_T);
     if (nb < 1) nb = 1;
     k_part_count<<<nb, PART_T, 0, s>>>(kf, n_ptr, mult, R, c->blockcnt);
-    k_part_offsets<<<1, PART_T, 0, s>>>(c->blockcnt, nb, R, c->blockoff, seg, total_out, active_desc(c), count_active,
+    k_part_offsets<<<1, PART_OFF_T, 0, s>>>(c->blockcnt, nb, R, c->blockoff, seg, total_out, active_desc(c), count_active,
                                         evals_per_step);
     k_part_scatter<<<nb, PART_T, 0, s>>>(kf, n_ptr, mult, R, c->blockoff, out, rank);
 }
@@ -690,6 +692,7 @@ extern "C" int perk_destroy(perk_ctx *c)
 {
     if (!c) return PERK_ENOTINIT;
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    if (c->rexec) cudaGraphExecDestroy(c->rexec);
     cudaDeviceSynchronize();
     for (void *p : c->allocs) cudaFree(p);
     if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
@@ -783,19 +786,43 @@ extern "C" int perk_run_host(perk_ctx *c, double *U_host, double dt, int64_t nst
     return PERK_OK;
 }
 
+// the re-mesh after the level map has been copied into c->lmap: old-mesh snapshot, mesh pipeline,
+// transfer (about 30 small launches)
+static void remesh_launches(perk_ctx *c, cudaStream_t s, double *U, Prof *p)
+{
+    k_save_old<<<SM_COUNT_B200 * 4, 256, 0, s>>>(c->md, c->n_old, c->cell_of_old, c->lev_old, c->fx_old, c->fy_old);
+    k_copy_rows<<<SM_COUNT_B200 * 4, 256, 0, s>>>(c->md.n, c->nv * c->npe, U, c->Utmp);
+    build_mesh(c, s, c->lmap);
+    prof_mark(p, s, 3);
+    OldMesh om{c->n_old, c->cell_of_old, c->lev_old, c->fx_old, c->fy_old};
+    k_transfer2d<<<std::min(blocks_for(c->cap, 16), SM_COUNT_B200 * 8), 256, 0, s>>>(c->md, om, c->nv, c->Utmp, U);
+}
+
 static int do_repartition(perk_ctx *c, const uint8_t *lmap, double *U, Prof *p)
 {
     if (c->prob.dim != 2) return set_err(c, PERK_EUNSUPPORTED, "repartition with solution transfer is 2D only");
     cudaStream_t s = c->stream;
     prof_mark(p, s, 2);
     CU(cudaMemcpyAsync(c->lmap, lmap, c->nf, cudaMemcpyDeviceToDevice, s));
-    k_save_old<<<SM_COUNT_B200 * 4, 256, 0, s>>>(c->md, c->n_old, c->cell_of_old, c->lev_old, c->fx_old, c->fy_old);
-    k_copy_rows<<<SM_COUNT_B200 * 4, 256, 0, s>>>(c->md.n, c->nv * c->npe, U, c->Utmp);
-    build_mesh(c, s, c->lmap);
-    prof_mark(p, s, 3);
-    OldMesh om{c->n_old, c->cell_of_old, c->lev_old, c->fx_old, c->fy_old};
-    k_transfer2d<<<SM_COUNT_B200 * 8, 256, 0, s>>>(c->md, om, c->nv, c->Utmp, U);
-    prof_mark(p, s, -1);
+    if (p) {                       // profiling: eager launches with events between the kinds
+        remesh_launches(c, s, U, p);
+        prof_mark(p, s, -1);
+    } else {                       // one graph launch instead of ~30 host-side kernel launches
+        if (!c->rexec || c->rU != U) {
+            if (c->rexec) {
+                cudaGraphExecDestroy(c->rexec);
+                c->rexec = nullptr;
+            }
+            cudaGraph_t g;
+            CU(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+            remesh_launches(c, c->cap_stream, U, nullptr);
+            CU(cudaStreamEndCapture(c->cap_stream, &g));
+            CU(cudaGraphInstantiate(&c->rexec, g, 0));
+            cudaGraphDestroy(g);
+            c->rU = U;
+        }
+        CU(cudaGraphLaunch(c->rexec, s));
+    }
     CU(cudaGetLastError());
     return PERK_OK;
 }
