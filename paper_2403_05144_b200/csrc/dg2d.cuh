@@ -469,9 +469,19 @@ __host__ __device__ constexpr int vol2d_nf(bool ns) { return ns ? 8 : 7; }
 constexpr int EPI_UN = 0, EPI_K1 = 1;                                   // (staged variant only)
 constexpr int EPI_FS = VOL2D_STAGE_UNK1 ? 2 : 0, EPI_GS = EPI_FS + 1;
 __host__ __device__ constexpr int vol2d_epi_slots(bool ns) { return (VOL2D_STAGE_UNK1 ? 3 : 1) + (ns ? 1 : 0); }   // (U_n, K_1,) Fs (+ Gs)
+// elements per CTA: 16 (Euler: 4.5 KB of shared memory per element, 3 CTAs = 48 elements per SM).
+// Navier-Stokes needs 5.4 KB per element: 16 per CTA fit 2 CTAs (32 elements) per SM, 8 per CTA
+// fit 5 (40 elements) but measured no faster (cfg 5 volume 3.66 vs 3.62 ms/step), so 16 stays
+#ifndef VOL2D_EPB_NS
+#define VOL2D_EPB_NS 16
+#endif
+__host__ __device__ constexpr int vol2d_epb(bool ns) { return ns ? VOL2D_EPB_NS : VOL2D_EPB; }
+__host__ __device__ constexpr int vol2d_ls(bool ns) { return 18 * vol2d_epb(ns); }   // == 0 mod 16 for 8 | EPB
+__host__ __device__ constexpr int vol2d_threads(bool ns) { return 8 * vol2d_epb(ns); }
 __host__ __device__ constexpr size_t vol2d_smem_bytes(bool ns)
 {
-    return sizeof(double) * ((size_t)vol2d_nf(ns) * 2 * VOL2D_LS + VOL2D_EPB * 2 * 64 + VOL2D_EPB * vol2d_epi_slots(ns) * 64);
+    return sizeof(double) * ((size_t)vol2d_nf(ns) * 2 * vol2d_ls(ns) + vol2d_epb(ns) * 2 * 64 +
+                             vol2d_epb(ns) * vol2d_epi_slots(ns) * 64);
 }
 
 // Volume + surface lift + Jacobian + stage epilogue.  Persistent grid-stride loop over groups of 16
@@ -485,19 +495,21 @@ __host__ __device__ constexpr size_t vol2d_smem_bytes(bool ns)
 // cp.async.bulk on mbarriers; issuing the per-element bulk copies through the uniform datapath cost
 // about a quarter of the kernel's issue slots.)
 template <int MODE, bool NS>
-__global__ void __launch_bounds__(128, NS ? 3 : VOL2D_MINB) k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
+__global__ void __launch_bounds__(vol2d_threads(NS), NS ? (VOL2D_EPB_NS == 8 ? 5 : 3) : VOL2D_MINB)
+k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                                                  double *__restrict__ Ubuf, double *__restrict__ K1,
                                                  const double *__restrict__ Fs, const double *__restrict__ Uin,
                                                  double *__restrict__ dU, const double *__restrict__ Gs,
                                                  double *__restrict__ Wb)
 {
     constexpr int NF = vol2d_nf(NS);          // rho, v_n/2, v_t/2, p/2, ln rho, beta, ln beta (+ T)
+    constexpr int EPB = vol2d_epb(NS), LS = vol2d_ls(NS);
     extern __shared__ __align__(16) unsigned char smraw[];
-    double (*sm)[2][VOL2D_LS] = reinterpret_cast<double (*)[2][VOL2D_LS]>(smraw);
-    double (*stg)[2][64] = reinterpret_cast<double (*)[2][64]>(smraw + sizeof(double) * NF * 2 * VOL2D_LS);
+    double (*sm)[2][LS] = reinterpret_cast<double (*)[2][LS]>(smraw);
+    double (*stg)[2][64] = reinterpret_cast<double (*)[2][64]>(smraw + sizeof(double) * NF * 2 * LS);
     constexpr int NEPI = vol2d_epi_slots(NS);
     double (*epi)[NEPI][64] = reinterpret_cast<double (*)[NEPI][64]>(reinterpret_cast<unsigned char *>(stg) +
-                                                                      sizeof(double) * VOL2D_EPB * 2 * 64);
+                                                                      sizeof(double) * EPB * 2 * 64);
     const int t8 = threadIdx.x & 7, le = threadIdx.x >> 3;
     const int n_act = MODE == MODE_STAGE ? md.count_active[KIND_EL * MAXS + sp.stage - 1] : md.n[0];
     const double g = md.gamma, gm1 = g - 1.0, inv_gm1 = 1.0 / gm1;
@@ -506,9 +518,9 @@ __global__ void __launch_bounds__(128, NS ? 3 : VOL2D_MINB) k_vol2d(MeshDev md, 
     const int o = t8 >> 2, ln = t8 & 3;
     const int eo = le * 18;                 // element offset inside a field array (even: 16 B aligned pairs)
     const int yo = 2;                       // y-layout offset
-    const int stride = gridDim.x * VOL2D_EPB;
+    const int stride = gridDim.x * EPB;
 
-    int base = blockIdx.x * VOL2D_EPB;
+    int base = blockIdx.x * EPB;
     // prologue before the dependency wait: indices only (lists are rebuilt by the mesh pipeline,
     // which completed before the step started)
     const int pk0 = base < n_act ? (MODE == MODE_STAGE ? md.elpk[base + le < n_act ? base + le : base] : 0) : 0;
@@ -626,12 +638,12 @@ __global__ void __launch_bounds__(128, NS ? 3 : VOL2D_MINB) k_vol2d(MeshDev md, 
         // the line's 4 nodes x 7 fields, loaded once with 16 B shared loads (the line is contiguous)
         LinePrim P[4];
         {
-            const double *L0 = &sm[0][o][lo];   // field k of line node a: L0[k * 2 * VOL2D_LS + a]
+            const double *L0 = &sm[0][o][lo];   // field k of line node a: L0[k * 2 * LS + a]
             double fv[7][4];
 #pragma unroll
             for (int k = 0; k < 7; ++k) {
-                const double2 x01 = *reinterpret_cast<const double2 *>(L0 + k * 2 * VOL2D_LS);
-                const double2 x23 = *reinterpret_cast<const double2 *>(L0 + k * 2 * VOL2D_LS + 2);
+                const double2 x01 = *reinterpret_cast<const double2 *>(L0 + k * 2 * LS);
+                const double2 x23 = *reinterpret_cast<const double2 *>(L0 + k * 2 * LS + 2);
                 fv[k][0] = x01.x;
                 fv[k][1] = x01.y;
                 fv[k][2] = x23.x;
@@ -659,7 +671,7 @@ __global__ void __launch_bounds__(128, NS ? 3 : VOL2D_MINB) k_vol2d(MeshDev md, 
             if (has_next) cp_async_wait<1>();
             else cp_async_wait<0>();
             __syncwarp();
-            visc_volume<VOL2D_LS>(sm, o, lo, eo, yo, ln, &epi[le][EPI_GS][0], 2.0 / hcell, md.mu, md.kappa, acc);
+            visc_volume<LS>(sm, o, lo, eo, yo, ln, &epi[le][EPI_GS][0], 2.0 / hcell, md.mu, md.kappa, acc);
         }
         // surface lift: + f*_hi / w_N at the last node, - f*_lo / w_0 at the first node
         // line coordinates (normal, tangential) -> (momentum x, momentum y)

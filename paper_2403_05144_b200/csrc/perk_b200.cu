@@ -342,9 +342,9 @@ static void launch_volume(perk_ctx *c, cudaStream_t s, const StageParams &sp, do
     if (c->prob.dim == 2) {
         if (c->ns) {
             if (sp.mode == MODE_STAGE)
-                launch_pdl(k_vol2d<MODE_STAGE, true>, c->vol_blocks, 128, vol2d_smem_bytes(true), s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Gs, c->Wb);
+                launch_pdl(k_vol2d<MODE_STAGE, true>, c->vol_blocks, vol2d_threads(true), vol2d_smem_bytes(true), s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Gs, c->Wb);
             else
-                launch_pdl(k_vol2d<MODE_RHS, true>, c->vol_blocks, 128, vol2d_smem_bytes(true), s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Gs, c->Wb);
+                launch_pdl(k_vol2d<MODE_RHS, true>, c->vol_blocks, vol2d_threads(true), vol2d_smem_bytes(true), s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Gs, c->Wb);
         } else {
             if (sp.mode == MODE_STAGE)
                 launch_pdl(k_vol2d<MODE_STAGE, false>, c->vol_blocks, 128, vol2d_smem_bytes(false), s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, nullptr, c->Wb);
@@ -616,9 +616,9 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
         CU(cudaFuncSetAttribute(k_vol2d<MODE_RHS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vol2d_smem_bytes(true)));
         CU(cudaFuncSetAttribute(k_vol2d<MODE_STAGE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vol2d_smem_bytes(false)));
         CU(cudaFuncSetAttribute(k_vol2d<MODE_RHS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vol2d_smem_bytes(false)));
-        if (c->ns) CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vol2d<MODE_STAGE, true>, 128, vol2d_smem_bytes(true)));
-        else CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vol2d<MODE_STAGE, false>, 128, vol2d_smem_bytes(false)));
-        const int want = (c->cap + VOL2D_EPB - 1) / VOL2D_EPB;
+        if (c->ns) CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vol2d<MODE_STAGE, true>, vol2d_threads(true), vol2d_smem_bytes(true)));
+        else CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vol2d<MODE_STAGE, false>, vol2d_threads(false), vol2d_smem_bytes(false)));
+        const int want = (c->cap + vol2d_epb(c->ns) - 1) / vol2d_epb(c->ns);
         c->vol_blocks = std::min(want, SM_COUNT_B200 * std::max(occ, 1));
         int occg = 0;
         CU(cudaFuncSetAttribute(k_grad2d<MODE_STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grad2d_smem_bytes()));
