@@ -466,6 +466,9 @@ __host__ __device__ constexpr int vol2d_nf(bool ns) { return ns ? 8 : 7; }
 #ifndef VOL2D_MINB
 #define VOL2D_MINB (VOL2D_STAGE_UNK1 ? 3 : 4)
 #endif
+#ifndef VOL2D_P3X
+#define VOL2D_P3X 0            // 1: the x-line threads finalise their own lines (y contributions via smem)
+#endif
 constexpr int EPI_UN = 0, EPI_K1 = 1;                                   // (staged variant only)
 constexpr int EPI_FS = VOL2D_STAGE_UNK1 ? 2 : 0, EPI_GS = EPI_FS + 1;
 __host__ __device__ constexpr int vol2d_epi_slots(bool ns) { return (VOL2D_STAGE_UNK1 ? 3 : 1) + (ns ? 1 : 0); }   // (U_n, K_1,) Fs (+ Gs)
@@ -695,6 +698,68 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                 acc[0][v] = fma(-Flo[v * 4], cB.invw[0], acc[0][v]);
             }
         }
+        // stage epilogue of one node pair (qq, qq + 1) of variable v (K = the pair's RHS values)
+        auto epilogue = [&](int v, int qq, double2 K) {
+            const size_t idx = eb + v * 16 + qq;
+            if (MODE == MODE_RHS) {
+                const bool on = (sp.mask >> m) & 1u;
+                *reinterpret_cast<double2 *>(dU + idx) = on ? K : make_double2(0.0, 0.0);
+            } else if (sp.stage == 1) {
+                *reinterpret_cast<double2 *>(K1 + idx) = K;
+            } else if (sp.stage == sp.S) {
+                const double2 w = VOL2D_STAGE_UNK1 ? *reinterpret_cast<const double2 *>(&epi[le][EPI_UN][v * 16 + qq])
+                                                   : __ldg(reinterpret_cast<const double2 *>((Wb ? Wb : Un) + idx));   // W or U_n
+                if (sp.fin_k1) {
+                    const double2 k1 = VOL2D_STAGE_UNK1 ? *reinterpret_cast<const double2 *>(&epi[le][EPI_K1][v * 16 + qq])
+                                                        : __ldg(reinterpret_cast<const double2 *>(K1 + idx));
+                    *reinterpret_cast<double2 *>(Un + idx) =
+                        make_double2(fma(sp.dt, fma(sp.wb1, k1.x, sp.bS * K.x), w.x),
+                                     fma(sp.dt, fma(sp.wb1, k1.y, sp.bS * K.y), w.y));
+                } else {
+                    const double db = sp.dt * sp.bS;
+                    *reinterpret_cast<double2 *>(Un + idx) = make_double2(fma(db, K.x, w.x), fma(db, K.y, w.y));
+                }
+            } else {
+                const double2 un = VOL2D_STAGE_UNK1 ? *reinterpret_cast<const double2 *>(&epi[le][EPI_UN][v * 16 + qq])
+                                                    : *reinterpret_cast<const double2 *>(Un + idx);
+                const double2 k1 = VOL2D_STAGE_UNK1 ? *reinterpret_cast<const double2 *>(&epi[le][EPI_K1][v * 16 + qq])
+                                                    : __ldg(reinterpret_cast<const double2 *>(K1 + idx));
+                const double a1 = sp.a1_next[m], as = sp.asub_next[m];
+                *reinterpret_cast<double2 *>(Ubuf + idx) =
+                    make_double2(fma(sp.dt, fma(a1, k1.x, as * K.x), un.x), fma(sp.dt, fma(a1, k1.y, as * K.y), un.y));
+                if (sp.wmode)
+                    *reinterpret_cast<double2 *>(Wb + idx) =
+                        make_double2(fma(sp.dt, fma(sp.wb1, k1.x, sp.wbS1 * K.x), un.x),
+                                     fma(sp.dt, fma(sp.wb1, k1.y, sp.wbS1 * K.y), un.y));
+            }
+        };
+        // members in the launch's prefix that do not evaluate this stage (non-standard patterns) write nothing
+        const bool writes = valid && (MODE == MODE_RHS || ((sp.actmask >> m) & 1u));
+        const double J = -2.0 / hcell;
+#if VOL2D_P3X
+        // phase 3 on the x-line threads: each finalises its own line's 4 nodes from its registers plus
+        // the y-line threads' contributions handed over through shared memory
+        __syncwarp();   // all primitives consumed: reuse sm[v][1] as the y-contribution arrays
+        if (o == 1) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                *reinterpret_cast<double2 *>(&sm[v][1][lo]) = make_double2(acc[0][v], acc[1][v]);
+                *reinterpret_cast<double2 *>(&sm[v][1][lo + 2]) = make_double2(acc[2][v], acc[3][v]);
+            }
+        }
+        __syncwarp();
+        if (o == 0 && writes) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const double s0 = acc[2 * h][v] + sm[v][1][yo + eo + 4 * (2 * h) + ln];
+                    const double s1 = acc[2 * h + 1][v] + sm[v][1][yo + eo + 4 * (2 * h + 1) + ln];
+                    epilogue(v, 4 * ln + 2 * h, make_double2(J * s0, J * s1));
+                }
+            }
+        }
+#else
         __syncwarp();   // all primitives consumed: reuse sm[v][o] as the accumulator arrays
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
@@ -703,51 +768,18 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
         }
         __syncwarp();
 
-        // phase 3: K = -(2/h) (x + y contributions), stage epilogue for nodes q0, q0+1; members in the
-        // launch's prefix that do not evaluate this stage (non-standard patterns) write nothing
-        if (valid && (MODE == MODE_RHS || ((sp.actmask >> m) & 1u))) {
-            const double J = -2.0 / hcell;
+        // phase 3: K = -(2/h) (x + y contributions), stage epilogue for nodes q0, q0+1
+        if (writes) {
             const int i0 = q0 & 3, j0 = q0 >> 2;   // q0 + 1 has i0 + 1
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
-                const size_t idx = eb + v * 16 + q0;
                 const double2 sx = *reinterpret_cast<const double2 *>(&sm[v][0][eo + q0]);
                 const double s0 = sx.x + sm[v][1][yo + eo + 4 * i0 + j0];
                 const double s1 = sx.y + sm[v][1][yo + eo + 4 * (i0 + 1) + j0];
-                const double2 K = make_double2(J * s0, J * s1);
-                if (MODE == MODE_RHS) {
-                    const bool on = (sp.mask >> m) & 1u;
-                    *reinterpret_cast<double2 *>(dU + idx) = on ? K : make_double2(0.0, 0.0);
-                } else if (sp.stage == 1) {
-                    *reinterpret_cast<double2 *>(K1 + idx) = K;
-                } else if (sp.stage == sp.S) {
-                    const double2 w = VOL2D_STAGE_UNK1 ? *reinterpret_cast<const double2 *>(&epi[le][EPI_UN][v * 16 + q0])
-                                                       : __ldg(reinterpret_cast<const double2 *>((Wb ? Wb : Un) + idx));   // W or U_n
-                    if (sp.fin_k1) {
-                        const double2 k1 = VOL2D_STAGE_UNK1 ? *reinterpret_cast<const double2 *>(&epi[le][EPI_K1][v * 16 + q0])
-                                                            : __ldg(reinterpret_cast<const double2 *>(K1 + idx));
-                        *reinterpret_cast<double2 *>(Un + idx) =
-                            make_double2(fma(sp.dt, fma(sp.wb1, k1.x, sp.bS * K.x), w.x),
-                                         fma(sp.dt, fma(sp.wb1, k1.y, sp.bS * K.y), w.y));
-                    } else {
-                        const double db = sp.dt * sp.bS;
-                        *reinterpret_cast<double2 *>(Un + idx) = make_double2(fma(db, K.x, w.x), fma(db, K.y, w.y));
-                    }
-                } else {
-                    const double2 un = VOL2D_STAGE_UNK1 ? *reinterpret_cast<const double2 *>(&epi[le][EPI_UN][v * 16 + q0])
-                                                        : *reinterpret_cast<const double2 *>(Un + idx);
-                    const double2 k1 = VOL2D_STAGE_UNK1 ? *reinterpret_cast<const double2 *>(&epi[le][EPI_K1][v * 16 + q0])
-                                                        : __ldg(reinterpret_cast<const double2 *>(K1 + idx));
-                    const double a1 = sp.a1_next[m], as = sp.asub_next[m];
-                    *reinterpret_cast<double2 *>(Ubuf + idx) =
-                        make_double2(fma(sp.dt, fma(a1, k1.x, as * K.x), un.x), fma(sp.dt, fma(a1, k1.y, as * K.y), un.y));
-                    if (sp.wmode)
-                        *reinterpret_cast<double2 *>(Wb + idx) =
-                            make_double2(fma(sp.dt, fma(sp.wb1, k1.x, sp.wbS1 * K.x), un.x),
-                                         fma(sp.dt, fma(sp.wb1, k1.y, sp.wbS1 * K.y), un.y));
-                }
+                epilogue(v, q0, make_double2(J * s0, J * s1));
             }
         }
+#endif
         __syncwarp();
         pk = pk_next;
     }
