@@ -26,9 +26,13 @@ struct StepTab1D {
 // best (B200): 256 for advection (cfg 1: 0.018 ms/step), 512 for Euler (cfg 2: 0.070 ms/step)
 __host__ __device__ constexpr int step1d_threads(int nv) { return nv == 1 ? 256 : 512; }
 
+// state (U_n, K_1, stage buffer, K_i, W) + face fluxes, then the step's read-only mesh data staged once
+// per step so the per-stage loops never wait on global memory: interface pairs (list order, <= n),
+// boundaries (<= 2), the element list, member and level per element
 __host__ __device__ inline size_t step1d_smem_bytes(int n, int nv, bool use_w)
 {
-    return sizeof(double) * ((size_t)n * nv * NP * (use_w ? 5 : 4) + (size_t)n * 2 * nv);
+    return sizeof(double) * ((size_t)n * nv * NP * (use_w ? 5 : 4) + (size_t)n * 2 * nv) +
+           (size_t)n * 8 + 16 + (size_t)n * 4 + (size_t)n * 2;
 }
 
 template <int NV>
@@ -42,6 +46,11 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
     double *sUn = sh, *sK1 = sUn + (size_t)n * rowd, *sUb = sK1 + (size_t)n * rowd, *sKi = sUb + (size_t)n * rowd;
     double *sW = sKi + (size_t)n * rowd;
     double *sFs = use_w ? sW + (size_t)n * rowd : sW;
+    int2 *sIf = reinterpret_cast<int2 *>(sFs + (size_t)n * 2 * NV);
+    int2 *sBd = sIf + n;
+    int *sEl = reinterpret_cast<int *>(sBd + 2);
+    uint8_t *sMem = reinterpret_cast<uint8_t *>(sEl + n);
+    uint8_t *sLev = sMem + n;
     const int tid = threadIdx.x, nt = blockDim.x;
     {
         const int *src = reinterpret_cast<const int *>(tb);
@@ -49,6 +58,19 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
         for (int k = tid; k < (int)(sizeof(StepTab1D) / sizeof(int)); k += nt) dst[k] = src[k];
     }
     for (int k = tid; k < n * rowd; k += nt) sUn[k] = U[k];
+    {
+        const int nif_all = md.n[1], nbd_all = md.n[3];
+        for (int k = tid; k < nif_all; k += nt) {
+            const int4 I = md.ifcs[k];
+            sIf[k] = make_int2(I.x, I.y);
+        }
+        for (int k = tid; k < nbd_all && k < 2; k += nt) sBd[k] = md.bnd[md.list[KIND_BD][k]];
+        for (int k = tid; k < n; k += nt) {
+            sEl[k] = md.list[KIND_EL][k];
+            sMem[k] = md.mem[k];
+            sLev[k] = md.lev[k];
+        }
+    }
     __syncthreads();
     const int S = T.S;
     for (int i = 1; i <= S; ++i) {
@@ -67,8 +89,8 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
         for (int t = tid; t < nif + nbd; t += nt) {
             double uL[NV], uR[NV], f[NV];
             if (t < nif) {
-                const int4 I = md.ifc[md.list[KIND_IF][t]];
-                const int mL = md.mem[I.x], mR = md.mem[I.y];
+                const int2 I = sIf[t];
+                const int mL = sMem[I.x], mR = sMem[I.y];
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
                     uL[v] = state(I.x, mL, v, NP - 1);
@@ -81,7 +103,7 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
                     sFs[((size_t)I.y * 2 + 1) * NV + v] = f[v];
                 }
             } else {
-                const int2 B = md.bnd[md.list[KIND_BD][t - nif]];
+                const int2 B = sBd[t - nif];
                 const int face = B.y & 7;
                 double u[NV], gst[NV];
 #pragma unroll
@@ -99,8 +121,8 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
         // K_i at the active element nodes (one thread per node); surplus members of the prefix skip
         const unsigned act = T.actmask[i - 1];
         for (int t = tid; t < NP * nel; t += nt) {
-            const int e = md.list[KIND_EL][t / NP], j = t % NP;
-            const int m = md.mem[e];
+            const int e = sEl[t / NP], j = t % NP;
+            const int m = sMem[e];
             if (!((act >> m) & 1u)) continue;
             double f[NP][NV];
 #pragma unroll
@@ -110,7 +132,7 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
                 for (int v = 0; v < NV; ++v) u[v] = state(e, m, v, k);
                 phys_flux1d<NV>(u, md.gamma, md.adv, f[k]);
             }
-            const double J = 2.0 / (md.hf * (double)(1 << (md.max_level - md.lev[e])));
+            const double J = 2.0 / (md.hf * (double)(1 << (md.max_level - sLev[e])));
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
                 double s = 0.0;
@@ -124,8 +146,8 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
         __syncthreads();
         // stage combination (every state read of this stage is done)
         for (int t = tid; t < NP * nel; t += nt) {
-            const int e = md.list[KIND_EL][t / NP], j = t % NP;
-            const int m = md.mem[e];
+            const int e = sEl[t / NP], j = t % NP;
+            const int m = sMem[e];
             if (!((act >> m) & 1u)) continue;
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
