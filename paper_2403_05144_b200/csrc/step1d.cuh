@@ -22,9 +22,16 @@ struct StepTab1D {
     double asubn[MAXR][MAXS];    // evaluated stage n, and a_{n,i}^{(r)} (standard pattern: n = i+1)
 };
 
-// threads per CTA: the per-stage cost is ceil(active nodes / threads) dependent passes; measured
-// best (B200): 256 for advection (cfg 1: 0.018 ms/step), 512 for Euler (cfg 2: 0.070 ms/step)
-__host__ __device__ constexpr int step1d_threads(int nv) { return nv == 1 ? 256 : 512; }
+// threads per CTA: the per-stage cost is ceil(active / blockDim) dependent passes; measured best
+// (B200, mesh data staged in shared memory): 256 for advection (cfg 1: 0.0205 ms/step; 512 the same,
+// 128 0.024), 1024 for Euler (cfg 2: 0.0655 ms/step; 512 0.0676, 256 0.086)
+#ifndef STEP1D_T1
+#define STEP1D_T1 256
+#endif
+#ifndef STEP1D_T3
+#define STEP1D_T3 1024
+#endif
+__host__ __device__ constexpr int step1d_threads(int nv) { return nv == 1 ? STEP1D_T1 : STEP1D_T3; }
 
 // state (U_n, K_1, stage buffer, K_i, W) + face fluxes, then the step's read-only mesh data staged once
 // per step so the per-stage loops never wait on global memory: interface pairs (list order, <= n),
