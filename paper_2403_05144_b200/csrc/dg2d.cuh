@@ -460,18 +460,26 @@ __device__ __forceinline__ void visc_volume(double (*sm)[2][LS], int o, int lo, 
 
 // Dynamic shared memory of k_vol2d (bytes): field arrays, own-state staging, epilogue staging.
 __host__ __device__ constexpr int vol2d_nf(bool ns) { return ns ? 8 : 7; }
-#ifndef VOL2D_STAGE_UNK1
-#define VOL2D_STAGE_UNK1 1     // 1: U_n / K_1 of the epilogue staged in shared memory; 0: read from global
+// U_n / K_1 operands of the stage epilogue: 1 = staged in shared memory with the Fs fluxes, 0 = read
+// from global memory in the epilogue, 2 = loaded into registers before the two-point-flux loop.
+// Measured (cfg 3 / cfg 5 volume ms/step): Euler 1: 0.361, 0: 0.406, 2: 0.378; Navier-Stokes 1: 3.60,
+// 2: 3.52 (its 16 KB smaller footprint fits 3 instead of 2 CTAs per SM)
+#ifndef VOL2D_EPI_MODE_EULER
+#define VOL2D_EPI_MODE_EULER 1
+#endif
+#ifndef VOL2D_EPI_MODE_NS
+#define VOL2D_EPI_MODE_NS 2
 #endif
 #ifndef VOL2D_MINB
-#define VOL2D_MINB (VOL2D_STAGE_UNK1 ? 3 : 4)
+#define VOL2D_MINB (VOL2D_EPI_MODE_EULER == 0 ? 4 : 3)
 #endif
 #ifndef VOL2D_P3X
 #define VOL2D_P3X 0            // 1: the x-line threads finalise their own lines (y contributions via smem)
 #endif
-constexpr int EPI_UN = 0, EPI_K1 = 1;                                   // (staged variant only)
-constexpr int EPI_FS = VOL2D_STAGE_UNK1 ? 2 : 0, EPI_GS = EPI_FS + 1;
-__host__ __device__ constexpr int vol2d_epi_slots(bool ns) { return (VOL2D_STAGE_UNK1 ? 3 : 1) + (ns ? 1 : 0); }   // (U_n, K_1,) Fs (+ Gs)
+__host__ __device__ constexpr int vol2d_epi_mode(bool ns) { return ns ? VOL2D_EPI_MODE_NS : VOL2D_EPI_MODE_EULER; }
+constexpr int EPI_UN = 0, EPI_K1 = 1;                                   // (mode 1 only)
+__host__ __device__ constexpr int vol2d_epi_fs(bool ns) { return vol2d_epi_mode(ns) == 1 ? 2 : 0; }
+__host__ __device__ constexpr int vol2d_epi_slots(bool ns) { return (vol2d_epi_mode(ns) == 1 ? 3 : 1) + (ns ? 1 : 0); }   // (U_n, K_1,) Fs (+ Gs)
 // elements per CTA: 16 (Euler: 4.5 KB of shared memory per element, 3 CTAs = 48 elements per SM).
 // Navier-Stokes needs 5.4 KB per element: 16 per CTA fit 2 CTAs (32 elements) per SM, 8 per CTA
 // fit 5 (40 elements) but measured no faster (cfg 5 volume 3.66 vs 3.62 ms/step), so 16 stays
@@ -511,6 +519,7 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
     double (*sm)[2][LS] = reinterpret_cast<double (*)[2][LS]>(smraw);
     double (*stg)[2][64] = reinterpret_cast<double (*)[2][64]>(smraw + sizeof(double) * NF * 2 * LS);
     constexpr int NEPI = vol2d_epi_slots(NS);
+    constexpr int EM = vol2d_epi_mode(NS), EPI_FS = vol2d_epi_fs(NS), EPI_GS = EPI_FS + 1;
     double (*epi)[NEPI][64] = reinterpret_cast<double (*)[NEPI][64]>(reinterpret_cast<unsigned char *>(stg) +
                                                                       sizeof(double) * EPB * 2 * 64);
     const int t8 = threadIdx.x & 7, le = threadIdx.x >> 3;
@@ -565,6 +574,7 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
         const int src = state_src(sp, m);
         const size_t eb = (size_t)e * 64;
         const double hcell = md.hf * (double)(1 << (md.max_level - pk_level(pk)));
+        double2 pre_un[4], pre_k1[4];          // epilogue operands held in registers (EM == 2)
 
         // phase 1: nodes q0, q0+1 -> primitives + logs, stored in x-line and y-line layouts
         cp_async_wait<0>();
@@ -615,7 +625,16 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
             const bool need_k1 = MODE == MODE_STAGE && sp.stage > 1 && (sp.stage < sp.S || sp.fin_k1);
             copy_block(epi[le][EPI_FS], Fs + eb);
             // stage S combines with W (P-ERK3) or U_n
-            if (VOL2D_STAGE_UNK1) {
+            if (EM == 2) {
+                if (valid) {
+                    const double *usrc = (Wb && sp.stage == sp.S) ? Wb : Un;
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        if (need_un) pre_un[v] = __ldg(reinterpret_cast<const double2 *>(usrc + eb + v * 16 + q0));
+                        if (need_k1) pre_k1[v] = __ldg(reinterpret_cast<const double2 *>(K1 + eb + v * 16 + q0));
+                    }
+                }
+            } else if (EM) {
                 if (need_un) copy_block(epi[le][EPI_UN], (Wb && sp.stage == sp.S ? Wb : Un) + eb);
                 if (need_k1) copy_block(epi[le][EPI_K1], K1 + eb);
             } else if (valid) {   // pull the epilogue operands' lines into L1 for phase 3
@@ -707,10 +726,12 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
             } else if (sp.stage == 1) {
                 *reinterpret_cast<double2 *>(K1 + idx) = K;
             } else if (sp.stage == sp.S) {
-                const double2 w = VOL2D_STAGE_UNK1 ? *reinterpret_cast<const double2 *>(&epi[le][EPI_UN][v * 16 + qq])
+                const double2 w = EM == 2 ? pre_un[v]
+                                : EM ? *reinterpret_cast<const double2 *>(&epi[le][EPI_UN][v * 16 + qq])
                                                    : __ldg(reinterpret_cast<const double2 *>((Wb ? Wb : Un) + idx));   // W or U_n
                 if (sp.fin_k1) {
-                    const double2 k1 = VOL2D_STAGE_UNK1 ? *reinterpret_cast<const double2 *>(&epi[le][EPI_K1][v * 16 + qq])
+                    const double2 k1 = EM == 2 ? pre_k1[v]
+                                     : EM ? *reinterpret_cast<const double2 *>(&epi[le][EPI_K1][v * 16 + qq])
                                                         : __ldg(reinterpret_cast<const double2 *>(K1 + idx));
                     *reinterpret_cast<double2 *>(Un + idx) =
                         make_double2(fma(sp.dt, fma(sp.wb1, k1.x, sp.bS * K.x), w.x),
@@ -720,9 +741,11 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                     *reinterpret_cast<double2 *>(Un + idx) = make_double2(fma(db, K.x, w.x), fma(db, K.y, w.y));
                 }
             } else {
-                const double2 un = VOL2D_STAGE_UNK1 ? *reinterpret_cast<const double2 *>(&epi[le][EPI_UN][v * 16 + qq])
+                const double2 un = EM == 2 ? pre_un[v]
+                                 : EM ? *reinterpret_cast<const double2 *>(&epi[le][EPI_UN][v * 16 + qq])
                                                     : *reinterpret_cast<const double2 *>(Un + idx);
-                const double2 k1 = VOL2D_STAGE_UNK1 ? *reinterpret_cast<const double2 *>(&epi[le][EPI_K1][v * 16 + qq])
+                const double2 k1 = EM == 2 ? pre_k1[v]
+                                 : EM ? *reinterpret_cast<const double2 *>(&epi[le][EPI_K1][v * 16 + qq])
                                                     : __ldg(reinterpret_cast<const double2 *>(K1 + idx));
                 const double a1 = sp.a1_next[m], as = sp.asub_next[m];
                 *reinterpret_cast<double2 *>(Ubuf + idx) =
