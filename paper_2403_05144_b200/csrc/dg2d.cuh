@@ -191,6 +191,41 @@ __device__ __forceinline__ void trace2d(const StateBufs &sb, int src, double dtc
     }
 }
 
+// face nodes kp, kp + 1 (kp even) of element e: node stride 1 on y faces, NP on x faces
+__device__ __forceinline__ void trace2d_pair(const StateBufs &sb, int src, double dtc, int e, int face, int kp,
+                                             double a[4], double b[4])
+{
+    const size_t n0 = (size_t)e * 64 + face_node2d(face, kp);
+    const int st = face >= 2 ? 1 : NP;
+    const double *P = state_base(sb, src);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+        a[v] = __ldg(P + n0 + v * 16);
+        b[v] = __ldg(P + n0 + st + v * 16);
+    }
+    if (src == SRC_LAZY) {
+        double ka[4], kb[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            ka[v] = __ldg(sb.K1 + n0 + v * 16);
+            kb[v] = __ldg(sb.K1 + n0 + st + v * 16);
+        }
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            a[v] = fma(dtc, ka[v], a[v]);
+            b[v] = fma(dtc, kb[v], b[v]);
+        }
+    }
+}
+
+// flux slots of face nodes kp, kp + 1 (kp even): adjacent in [face][v][k], one 16 B store per variable
+__device__ __forceinline__ void store_face2d_pair(double *Fs, int e, int face, int kp, const double fa[4], const double fb[4])
+{
+    const size_t b = ((size_t)e * 4 + face) * 16 + kp;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) *reinterpret_cast<double2 *>(Fs + b + v * 4) = make_double2(fa[v], fb[v]);
+}
+
 __device__ __forceinline__ void store_face2d(double *Fs, int e, int face, int k, const double f[4])
 {
     const size_t b = ((size_t)e * 4 + face) * 16 + k;
@@ -205,6 +240,9 @@ __device__ __forceinline__ void store_face2d(double *Fs, int e, int face, int k,
 #endif
 #ifndef SURF2D_PAIRED
 #define SURF2D_PAIRED 1
+#endif
+#ifndef SURF2D_NPAIR
+#define SURF2D_NPAIR 0         // 1: interfaces with two face nodes of the same interface per thread
 #endif
 template <int MODE, bool NS>
 __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StageParams sp, const double *__restrict__ Un,
@@ -230,9 +268,34 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
     const int GS = gridDim.x * blockDim.x;
     const int nI = 4 * nif;
     int gt = blockIdx.x * blockDim.x + threadIdx.x;
+#if SURF2D_NPAIR
+    for (int t = gt; t < 2 * nif; t += GS) {
+        const int item = t >> 1, kp = (t & 1) * 2;
+        const int4 I = MODE == MODE_STAGE ? md.ifcs[item] : md.ifc[item];
+        const int o = I.z;
+        const int src = state_src(sp, I.w);
+        double uL0[4], uL1[4], uR0[4], uR1[4], f0[4], f1[4];
+        trace2d_pair(sb, src, dtc, I.x, 2 * o, kp, uL0, uL1);
+        trace2d_pair(sb, src, dtc, I.y, 2 * o + 1, kp, uR0, uR1);
+        numflux2d(uL0, uR0, o, g, md.surface, f0);
+        numflux2d(uL1, uR1, o, g, md.surface, f1);
+        if (NS) {
+#pragma unroll
+            for (int c = 0; c < GV; ++c) {
+                const double2 va = __ldg(reinterpret_cast<const double2 *>(Vt + gidx2d(I.x, 2 * o, c, kp)));
+                const double2 vb = __ldg(reinterpret_cast<const double2 *>(Vt + gidx2d(I.y, 2 * o + 1, c, kp)));
+                f0[1 + c] -= 0.5 * (va.x + vb.x);
+                f1[1 + c] -= 0.5 * (va.y + vb.y);
+            }
+        }
+        store_face2d_pair(Fs, I.x, 2 * o, kp, f0, f1);
+        store_face2d_pair(Fs, I.y, 2 * o + 1, kp, f0, f1);
+    }
+    gt += nI;                     // mortars and boundaries: four threads per item, lane-aligned
+#endif
     // two interface face nodes per iteration while both are interfaces: twice the loads in flight
     // per thread (the kernel is bound by the latency of the record -> trace gathers)
-    for (; SURF2D_PAIRED && gt + GS < nI; gt += 2 * GS) {
+    for (; !SURF2D_NPAIR && SURF2D_PAIRED && gt + GS < nI; gt += 2 * GS) {
         const int ka = gt & 3, kb = (gt + GS) & 3;
         const int4 Ia = MODE == MODE_STAGE ? md.ifcs[gt >> 2] : md.ifc[gt >> 2];
         const int4 Ib = MODE == MODE_STAGE ? md.ifcs[(gt + GS) >> 2] : md.ifc[(gt + GS) >> 2];
