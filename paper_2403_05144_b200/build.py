@@ -46,5 +46,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return OUT
 
 
+def build_debug() -> str:
+    """lib/libperk_debug.so: the same library with the device-side bounds checks (PERK_DASSERT) on;
+    run the GPU tests against it with PERK_LIB_PATH=<that path> (compute-sanitizer is not available on
+    the GPU pool)."""
+    out = os.path.join(HERE, "lib", "libperk_debug.so")
+    cmd = [NVCC] + [f for f in FLAGS if f not in ("-Xptxas", "-v")] + ["-DPERK_DEBUG", "-I", os.path.join(ROOT, "include"),
+                                                                      "-o", out, SRC]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+    return out
+
+
 if __name__ == "__main__":
-    print(build(force=True))
+    import sys
+    print(build_debug() if "--debug" in sys.argv else build(force=True))

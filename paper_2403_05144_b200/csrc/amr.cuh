@@ -203,6 +203,7 @@ __global__ void k_amr_coarsen(MeshDev md, const uint8_t *__restrict__ want, uint
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int c = md.cell_of[(size_t)(py + (k >> 1) * s) * md.nfx + px + (k & 1) * s];
+                PERK_DASSERT(c >= 0 && c < md.n[0]);
                 if (md.lev[c] != l || want[c] >= l) nl = l;
             }
         }

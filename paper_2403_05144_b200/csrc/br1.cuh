@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(256, 3) k_gsurf2d(MeshDev md, StageParams sp, 
         if (item < nif) {
             const int4 I = MODE == MODE_RHS ? md.ifc[item]
                                             : (item < nif_a ? md.ifcs[item] : md.ifc[md.hlist[KIND_IF][hif.x + item - nif_a]]);
+            PERK_DASSERT(I.x >= 0 && I.x < md.n[0] && I.y >= 0 && I.y < md.n[0]);
             const int o = I.z;
             const int src = state_src(sp, I.w);
             double uL[4], uR[4], wL[GV], wR[GV];
@@ -62,6 +63,7 @@ __global__ void __launch_bounds__(256, 3) k_gsurf2d(MeshDev md, StageParams sp, 
         } else {
             const int q = item - nif;
             const int4 M = MODE == MODE_RHS ? md.mor[q] : (q < nmo_a ? md.mors[q] : md.mor[md.hlist[KIND_MO][hmo.x + q - nmo_a]]);
+            PERK_DASSERT(M.x >= 0 && M.x < md.n[0] && M.y >= 0 && M.y < md.n[0] && M.z >= 0 && M.z < md.n[0]);
             const int o = M.w & 1, side = (M.w >> 1) & 1, mfine = M.w >> 8;
             const int lf = 2 * o + side, sf = 2 * o + 1 - side;
             double ul[4], us0[4], us1[4], wl[GV], ws0[GV], ws1[GV];
@@ -163,6 +165,7 @@ __global__ void __launch_bounds__(128, 4) k_grad2d(MeshDev md, StageParams sp, c
         const bool has_next = base + stride < n_act;
         const int pk_next = has_next ? entry_at(base + stride) : 0;
         const int e = pk_elem(pk);
+        PERK_DASSERT(e >= 0 && e < md.n[0]);
         const int src = state_src(sp, pk_member(pk));
         const double hcell = md.hf * (double)(1 << (md.max_level - pk_level(pk)));
         cp_async_wait<0>();

@@ -10,6 +10,23 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Device-side bounds checks of the gather indices (build with -DPERK_DEBUG; compute-sanitizer is not
+// available on this GPU pool): a violated check prints its location and traps the kernel.
+#ifdef PERK_DEBUG
+#include <cstdio>
+#define PERK_DASSERT(c)                                                                   \
+    do {                                                                                  \
+        if (!(c)) {                                                                       \
+            printf("PERK_DASSERT failed %s:%d: %s\n", __FILE__, __LINE__, #c);           \
+            __trap();                                                                     \
+        }                                                                                 \
+    } while (0)
+#else
+#define PERK_DASSERT(c) \
+    do {                \
+    } while (0)
+#endif
+
 namespace perk {
 
 constexpr int NP = 4;          // N + 1 LGL nodes per direction (N = 3)

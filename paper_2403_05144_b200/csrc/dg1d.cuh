@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(256) k_surf1d(MeshDev md, StageParams sp, cons
         if (it < nif) {
             const int fi = MODE == MODE_STAGE ? md.list[KIND_IF][it] : it;
             const int4 I = md.ifc[fi];
+            PERK_DASSERT(I.x >= 0 && I.x < md.n[0] && I.y >= 0 && I.y < md.n[0]);
             const int sL = state_src(sp, md.mem[I.x]), sR = state_src(sp, md.mem[I.y]);
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
@@ -78,6 +79,7 @@ __global__ void __launch_bounds__(256) k_surf1d(MeshDev md, StageParams sp, cons
             const int q = it - nif;
             const int bi = MODE == MODE_STAGE ? md.list[KIND_BD][q] : q;
             const int2 B = md.bnd[bi];
+            PERK_DASSERT(B.x >= 0 && B.x < md.n[0]);
             const int face = B.y & 7;
             const int s = state_src(sp, B.y >> 8);
             double u[NV], gst[NV];

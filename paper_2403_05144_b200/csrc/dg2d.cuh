@@ -272,6 +272,7 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
     for (int t = gt; t < 2 * nif; t += GS) {
         const int item = t >> 1, kp = (t & 1) * 2;
         const int4 I = MODE == MODE_STAGE ? md.ifcs[item] : md.ifc[item];
+        PERK_DASSERT(I.x >= 0 && I.x < md.n[0] && I.y >= 0 && I.y < md.n[0]);
         const int o = I.z;
         const int src = state_src(sp, I.w);
         double uL0[4], uL1[4], uR0[4], uR1[4], f0[4], f1[4];
@@ -299,6 +300,8 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
         const int ka = gt & 3, kb = (gt + GS) & 3;
         const int4 Ia = MODE == MODE_STAGE ? md.ifcs[gt >> 2] : md.ifc[gt >> 2];
         const int4 Ib = MODE == MODE_STAGE ? md.ifcs[(gt + GS) >> 2] : md.ifc[(gt + GS) >> 2];
+        PERK_DASSERT(Ia.x >= 0 && Ia.x < md.n[0] && Ia.y >= 0 && Ia.y < md.n[0] && Ib.x >= 0 && Ib.x < md.n[0] &&
+                     Ib.y >= 0 && Ib.y < md.n[0]);
         const int srca = state_src(sp, Ia.w), srcb = state_src(sp, Ib.w);
         double uLa[4], uRa[4], uLb[4], uRb[4], fa[4], fb[4];
         trace2d(sb, srca, dtc, Ia.x, 2 * Ia.z, ka, uLa);
@@ -323,6 +326,7 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
         const int item = gt >> 2, k = gt & 3;
         if (item < nif) {
             const int4 I = MODE == MODE_STAGE ? md.ifcs[item] : md.ifc[item];
+            PERK_DASSERT(I.x >= 0 && I.x < md.n[0] && I.y >= 0 && I.y < md.n[0]);
             const int o = I.z;
             const int src = state_src(sp, I.w);    // conforming: both sides share the member
             double uL[4], uR[4], fl[4];
@@ -339,6 +343,7 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
         } else if (item < nif + nmo) {
             const int q = item - nif;
             const int4 M = MODE == MODE_STAGE ? md.mors[q] : md.mor[q];
+            PERK_DASSERT(M.x >= 0 && M.x < md.n[0] && M.y >= 0 && M.y < md.n[0] && M.z >= 0 && M.z < md.n[0]);
             const int o = M.w & 1, side = (M.w >> 1) & 1, mfine = M.w >> 8;
             const int lf = 2 * o + side, sf = 2 * o + 1 - side;
             const int srcL = state_src(sp, md.mem[M.x]);
@@ -404,6 +409,7 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
             const int q = item - nif - nmo;
             const int bi = MODE == MODE_STAGE ? md.list[KIND_BD][q] : q;
             const int2 B = md.bnd[bi];
+            PERK_DASSERT(B.x >= 0 && B.x < md.n[0]);
             const int face = B.y & 7, o = face >> 1;
             const int src = state_src(sp, B.y >> 8);
             double u[4], fl[4];
@@ -633,6 +639,7 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
         const bool has_next = base + stride < n_act;     // uniform across the CTA
         const int pk_next = has_next ? entry_at(base + stride) : 0;   // consumed after phase 1
         const int e = pk_elem(pk);
+        PERK_DASSERT(!valid || (e >= 0 && e < md.n[0]));
         const int m = pk_member(pk);
         const int src = state_src(sp, m);
         const size_t eb = (size_t)e * 64;

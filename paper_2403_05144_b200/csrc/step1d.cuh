@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
         const int nif_all = md.n[1], nbd_all = md.n[3];
         for (int k = tid; k < nif_all; k += nt) {
             const int4 I = md.ifcs[k];
+            PERK_DASSERT(I.x >= 0 && I.x < n && I.y >= 0 && I.y < n);
             sIf[k] = make_int2(I.x, I.y);
         }
         for (int k = tid; k < nbd_all && k < 2; k += nt) sBd[k] = md.bnd[md.list[KIND_BD][k]];
