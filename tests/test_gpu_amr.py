@@ -162,3 +162,29 @@ def test_launches_and_errors():
     with pytest.raises(PerkError) as ei:
         g1.amr_indicator(g1.initial_state(w1.ic), HG)
     assert ei.value.code == -6
+
+
+def test_adapt_cycle_full_size():
+    """BASELINE cfg 4 at full size (77,728 leaves): 2 steps, enstrophy adapt + device repartition,
+    1 step; maps, lists and state against the oracle"""
+    w = W.make(4)
+    amr = w.meta["amr"]
+    fam = T.family(w.S, w.E, w.alpha_rule)
+    ora, gpu = build_pair(w)
+    Uo = ora.initial_state(w.ic)
+    Ug = gpu.initial_state(w.ic)
+    ora.step(Uo, w.dt, 2)
+    gpu.step(Ug, w.dt, 2)
+    lm_o = ora.amr_adapt(Uo, amr)
+    lm_g = gpu.amr_adapt(Ug, amr)
+    gpu.repartition(lm_g, Ug)
+    gpu.sync()
+    assert _compare_maps(ora, lm_o, lm_g.cpu().numpy(), ora.amr_indicator(Uo, amr), amr) == 0
+    new = O.OracleMesh(w.problem, lm_o, fam)
+    Uo = O.transfer(ora, new, Uo)
+    compare_mesh(new, gpu)
+    assert rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo).max() <= TOL
+    new.step(Uo, w.dt, 1)
+    gpu.step(Ug, w.dt, 1)
+    torch.cuda.synchronize()
+    assert rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo).max() <= TOL
