@@ -549,6 +549,18 @@ __host__ __device__ constexpr int vol2d_epi_mode(bool ns) { return ns ? VOL2D_EP
 constexpr int EPI_UN = 0, EPI_K1 = 1;                                   // (mode 1 only)
 __host__ __device__ constexpr int vol2d_epi_fs(bool ns) { return vol2d_epi_mode(ns) == 1 ? 2 : 0; }
 __host__ __device__ constexpr int vol2d_epi_slots(bool ns) { return (vol2d_epi_mode(ns) == 1 ? 3 : 1) + (ns ? 1 : 0); }   // (U_n, K_1,) Fs (+ Gs)
+// Staged face fluxes: face stride 18 doubles (instead of 16) and an element block of 200 doubles
+// (== 8 mod 16) in the Euler kernel, so that the lift's scalar reads of the x-line threads (faces 0/1)
+// and y-line threads (faces 2/3) of the two elements of a half-warp fall into 4 disjoint bank groups
+// (with 16 / 192 they were 4-way conflicts).  Navier-Stokes keeps the unpadded layout.
+#ifndef VOL2D_FS_PAD
+#define VOL2D_FS_PAD 1
+#endif
+__host__ __device__ constexpr int vol2d_fs_face(bool ns) { return (!ns && VOL2D_FS_PAD && vol2d_epi_mode(ns) == 1) ? 18 : 16; }
+__host__ __device__ constexpr int vol2d_epi_stride(bool ns)      // doubles per element block
+{
+    return vol2d_fs_face(ns) == 18 ? 200 : vol2d_epi_slots(ns) * 64;
+}
 // elements per CTA: 16 (Euler: 4.5 KB of shared memory per element, 3 CTAs = 48 elements per SM).
 // Navier-Stokes needs 5.4 KB per element: 16 per CTA fit 2 CTAs (32 elements) per SM, 8 per CTA
 // fit 5 (40 elements) but measured no faster (cfg 5 volume 3.66 vs 3.62 ms/step), so 16 stays
@@ -561,7 +573,7 @@ __host__ __device__ constexpr int vol2d_threads(bool ns) { return 8 * vol2d_epb(
 __host__ __device__ constexpr size_t vol2d_smem_bytes(bool ns)
 {
     return sizeof(double) * ((size_t)vol2d_nf(ns) * 2 * vol2d_ls(ns) + vol2d_epb(ns) * 2 * 64 +
-                             vol2d_epb(ns) * vol2d_epi_slots(ns) * 64);
+                             vol2d_epb(ns) * vol2d_epi_stride(ns));
 }
 
 // Volume + surface lift + Jacobian + stage epilogue.  Persistent grid-stride loop over groups of 16
@@ -589,9 +601,11 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
     double (*stg)[2][64] = reinterpret_cast<double (*)[2][64]>(smraw + sizeof(double) * NF * 2 * LS);
     constexpr int NEPI = vol2d_epi_slots(NS);
     constexpr int EM = vol2d_epi_mode(NS), EPI_FS = vol2d_epi_fs(NS), EPI_GS = EPI_FS + 1;
-    double (*epi)[NEPI][64] = reinterpret_cast<double (*)[NEPI][64]>(reinterpret_cast<unsigned char *>(stg) +
-                                                                      sizeof(double) * EPB * 2 * 64);
+    constexpr int FSF = vol2d_fs_face(NS), EPS = vol2d_epi_stride(NS);
+    static_assert(NEPI * 64 <= EPS, "epilogue block");
+    double *epi_all = reinterpret_cast<double *>(reinterpret_cast<unsigned char *>(stg) + sizeof(double) * EPB * 2 * 64);
     const int t8 = threadIdx.x & 7, le = threadIdx.x >> 3;
+    auto EP = [&](int slot) { return epi_all + (size_t)le * EPS + slot * 64; };   // slot base of this element
     const int n_act = MODE == MODE_STAGE ? md.count_active[KIND_EL * MAXS + sp.stage - 1] : md.n[0];
     const double g = md.gamma, gm1 = g - 1.0, inv_gm1 = 1.0 / gm1;
     const double dtc = sp.dt * sp.c_stage;
@@ -693,7 +707,12 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
         {
             const bool need_un = MODE == MODE_STAGE && sp.stage > 1;
             const bool need_k1 = MODE == MODE_STAGE && sp.stage > 1 && (sp.stage < sp.S || sp.fin_k1);
-            copy_block(epi[le][EPI_FS], Fs + eb);
+            if (FSF == 18) {   // padded face layout: chunk c of the 512 B block -> 2c + 2 (c / 8)
+#pragma unroll
+                for (int r = 0; r < 4; ++r) cp_async16(EP(EPI_FS) + 2 * (t8 + 8 * r) + 2 * r, Fs + eb + 2 * (t8 + 8 * r));
+            } else {
+                copy_block(EP(EPI_FS), Fs + eb);
+            }
             // stage S combines with W (P-ERK3) or U_n
             if (EM == 2) {
                 if (valid) {
@@ -705,8 +724,8 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                     }
                 }
             } else if (EM) {
-                if (need_un) copy_block(epi[le][EPI_UN], (Wb && sp.stage == sp.S ? Wb : Un) + eb);
-                if (need_k1) copy_block(epi[le][EPI_K1], K1 + eb);
+                if (need_un) copy_block(EP(EPI_UN), (Wb && sp.stage == sp.S ? Wb : Un) + eb);
+                if (need_k1) copy_block(EP(EPI_K1), K1 + eb);
             } else if (valid) {   // pull the epilogue operands' lines into L1 for phase 3
                 const double *src = (t8 < 4) ? (need_un ? (Wb && sp.stage == sp.S ? Wb : Un) : nullptr) : (need_k1 ? K1 : nullptr);
                 if (src) asm volatile("prefetch.global.L1 [%0];" ::"l"(src + eb + 16 * (t8 & 3)));
@@ -714,7 +733,7 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
             if (NS) {   // the element's 48 BR1 central traces (384 B = 24 chunks of 16 B)
 #pragma unroll
                 for (int r = 0; r < 3; ++r)
-                    cp_async16(&epi[le][EPI_GS][2 * (t8 + 8 * r)], Gs + (size_t)e * 4 * GV * NP + 2 * (t8 + 8 * r));
+                    cp_async16(EP(EPI_GS) + 2 * (t8 + 8 * r), Gs + (size_t)e * 4 * GV * NP + 2 * (t8 + 8 * r));
             }
             cp_async_commit();
         }
@@ -763,7 +782,7 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
             if (has_next) cp_async_wait<1>();
             else cp_async_wait<0>();
             __syncwarp();
-            visc_volume<LS>(sm, o, lo, eo, yo, ln, &epi[le][EPI_GS][0], 2.0 / hcell, md.mu, md.kappa, acc);
+            visc_volume<LS>(sm, o, lo, eo, yo, ln, EP(EPI_GS), 2.0 / hcell, md.mu, md.kappa, acc);
         }
         // surface lift: + f*_hi / w_N at the last node, - f*_lo / w_0 at the first node
         // line coordinates (normal, tangential) -> (momentum x, momentum y)
@@ -779,8 +798,8 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
         else cp_async_wait<0>();
         __syncwarp();
         {
-            const double *Fhi = &epi[le][EPI_FS][(2 * o) * 16 + ln];
-            const double *Flo = &epi[le][EPI_FS][(2 * o + 1) * 16 + ln];
+            const double *Fhi = EP(EPI_FS) + (2 * o) * FSF + ln;
+            const double *Flo = EP(EPI_FS) + (2 * o + 1) * FSF + ln;
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
                 acc[3][v] = fma(Fhi[v * 4], cB.invw[3], acc[3][v]);
@@ -797,11 +816,11 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                 *reinterpret_cast<double2 *>(K1 + idx) = K;
             } else if (sp.stage == sp.S) {
                 const double2 w = EM == 2 ? pre_un[v]
-                                : EM ? *reinterpret_cast<const double2 *>(&epi[le][EPI_UN][v * 16 + qq])
+                                : EM ? *reinterpret_cast<const double2 *>(EP(EPI_UN) + v * 16 + qq)
                                                    : __ldg(reinterpret_cast<const double2 *>((Wb ? Wb : Un) + idx));   // W or U_n
                 if (sp.fin_k1) {
                     const double2 k1 = EM == 2 ? pre_k1[v]
-                                     : EM ? *reinterpret_cast<const double2 *>(&epi[le][EPI_K1][v * 16 + qq])
+                                     : EM ? *reinterpret_cast<const double2 *>(EP(EPI_K1) + v * 16 + qq)
                                                         : __ldg(reinterpret_cast<const double2 *>(K1 + idx));
                     *reinterpret_cast<double2 *>(Un + idx) =
                         make_double2(fma(sp.dt, fma(sp.wb1, k1.x, sp.bS * K.x), w.x),
@@ -812,10 +831,10 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                 }
             } else {
                 const double2 un = EM == 2 ? pre_un[v]
-                                 : EM ? *reinterpret_cast<const double2 *>(&epi[le][EPI_UN][v * 16 + qq])
+                                 : EM ? *reinterpret_cast<const double2 *>(EP(EPI_UN) + v * 16 + qq)
                                                     : *reinterpret_cast<const double2 *>(Un + idx);
                 const double2 k1 = EM == 2 ? pre_k1[v]
-                                 : EM ? *reinterpret_cast<const double2 *>(&epi[le][EPI_K1][v * 16 + qq])
+                                 : EM ? *reinterpret_cast<const double2 *>(EP(EPI_K1) + v * 16 + qq)
                                                     : __ldg(reinterpret_cast<const double2 *>(K1 + idx));
                 const double a1 = sp.a1_next[m], as = sp.asub_next[m];
                 *reinterpret_cast<double2 *>(Ubuf + idx) =
