@@ -109,9 +109,13 @@ __global__ void __launch_bounds__(256, 3) k_gsurf2d(MeshDev md, StageParams sp, 
 // with cp.async one group ahead (commit groups as in k_vol2d).
 constexpr int GRAD2D_LS = VOL2D_LS;
 constexpr int G_V1 = 0, G_V2 = 1, G_T = 2, G_Q = 3;     // shared fields: v1, v2, T, gradients (3)
+// staged central traces per element: 48 doubles padded to 52 (== 4 mod 16), so that the scalar trace
+// reads of the x-line threads (faces 0/1) and y-line threads (faces 2/3) of the two elements of a
+// half-warp fall into disjoint banks (with 48 the two elements collided)
+constexpr int GST_STRIDE = 4 * GV * NP + 4;
 __host__ __device__ constexpr size_t grad2d_smem_bytes()
 {
-    return sizeof(double) * ((size_t)6 * 2 * GRAD2D_LS + VOL2D_EPB * 2 * 64 + VOL2D_EPB * 4 * GV * NP);
+    return sizeof(double) * ((size_t)6 * 2 * GRAD2D_LS + VOL2D_EPB * 2 * 64 + VOL2D_EPB * GST_STRIDE);
 }
 
 template <int MODE>
@@ -123,8 +127,8 @@ __global__ void __launch_bounds__(128, 4) k_grad2d(MeshDev md, StageParams sp, c
     extern __shared__ __align__(16) unsigned char smraw[];
     double (*sm)[2][GRAD2D_LS] = reinterpret_cast<double (*)[2][GRAD2D_LS]>(smraw);
     double (*stg)[2][64] = reinterpret_cast<double (*)[2][64]>(smraw + sizeof(double) * 6 * 2 * GRAD2D_LS);
-    double (*gst)[4 * GV * NP] = reinterpret_cast<double (*)[4 * GV * NP]>(reinterpret_cast<unsigned char *>(stg) +
-                                                                           sizeof(double) * VOL2D_EPB * 2 * 64);
+    double (*gst)[GST_STRIDE] = reinterpret_cast<double (*)[GST_STRIDE]>(reinterpret_cast<unsigned char *>(stg) +
+                                                                         sizeof(double) * VOL2D_EPB * 2 * 64);
     const int t8 = threadIdx.x & 7, le = threadIdx.x >> 3;
     // items: [active elements | halo elements of the member below the lowest active one]
     const int n_el_a = MODE == MODE_STAGE ? md.count_active[KIND_EL * MAXS + sp.stage - 1] : md.n[0];
