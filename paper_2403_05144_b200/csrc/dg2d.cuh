@@ -549,17 +549,18 @@ __host__ __device__ constexpr int vol2d_epi_mode(bool ns) { return ns ? VOL2D_EP
 constexpr int EPI_UN = 0, EPI_K1 = 1;                                   // (mode 1 only)
 __host__ __device__ constexpr int vol2d_epi_fs(bool ns) { return vol2d_epi_mode(ns) == 1 ? 2 : 0; }
 __host__ __device__ constexpr int vol2d_epi_slots(bool ns) { return (vol2d_epi_mode(ns) == 1 ? 3 : 1) + (ns ? 1 : 0); }   // (U_n, K_1,) Fs (+ Gs)
-// Staged face fluxes: face stride 18 doubles (instead of 16) and an element block of 200 doubles
-// (== 8 mod 16) in the Euler kernel, so that the lift's scalar reads of the x-line threads (faces 0/1)
-// and y-line threads (faces 2/3) of the two elements of a half-warp fall into 4 disjoint bank groups
-// (with 16 / 192 they were 4-way conflicts).  Navier-Stokes keeps the unpadded layout.
+// Staged face fluxes: face stride 18 doubles (instead of 16) and an element block == 8 mod 16, so that
+// the lift's scalar reads of the x-line threads (faces 0/1) and y-line threads (faces 2/3) of the two
+// elements of a half-warp fall into 4 disjoint bank groups (unpadded they were 4-way conflicts).
 #ifndef VOL2D_FS_PAD
 #define VOL2D_FS_PAD 1
 #endif
-__host__ __device__ constexpr int vol2d_fs_face(bool ns) { return (!ns && VOL2D_FS_PAD && vol2d_epi_mode(ns) == 1) ? 18 : 16; }
-__host__ __device__ constexpr int vol2d_epi_stride(bool ns)      // doubles per element block
+__host__ __device__ constexpr int vol2d_fs_face(bool ns) { return VOL2D_FS_PAD ? 18 : 16; }
+// element block: [U_n 64][K_1 64] (mode 1) [Fs 4 x face stride] [Gs 48 (NS)]; Euler 200 doubles,
+// Navier-Stokes (mode 2) 72 + 48 = 120, both == 8 mod 16 with the padded faces
+__host__ __device__ constexpr int vol2d_epi_stride(bool ns)
 {
-    return vol2d_fs_face(ns) == 18 ? 200 : vol2d_epi_slots(ns) * 64;
+    return (vol2d_epi_mode(ns) == 1 ? 128 : 0) + 4 * vol2d_fs_face(ns) + (ns ? 4 * GV * NP : 0);
 }
 // elements per CTA: 16 (Euler: 4.5 KB of shared memory per element, 3 CTAs = 48 elements per SM).
 // Navier-Stokes needs 5.4 KB per element: 16 per CTA fit 2 CTAs (32 elements) per SM, 8 per CTA
@@ -602,10 +603,13 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
     constexpr int NEPI = vol2d_epi_slots(NS);
     constexpr int EM = vol2d_epi_mode(NS), EPI_FS = vol2d_epi_fs(NS), EPI_GS = EPI_FS + 1;
     constexpr int FSF = vol2d_fs_face(NS), EPS = vol2d_epi_stride(NS);
-    static_assert(NEPI * 64 <= EPS, "epilogue block");
+    static_assert(EPS >= (EM == 1 ? 128 : 0) + 4 * FSF + (NS ? 4 * GV * NP : 0), "epilogue block");
     double *epi_all = reinterpret_cast<double *>(reinterpret_cast<unsigned char *>(stg) + sizeof(double) * EPB * 2 * 64);
     const int t8 = threadIdx.x & 7, le = threadIdx.x >> 3;
-    auto EP = [&](int slot) { return epi_all + (size_t)le * EPS + slot * 64; };   // slot base of this element
+    // slot base of this element: U_n, K_1 (64 each, mode 1), Fs (4 faces x FSF), Gs (NS) right after Fs
+    auto EP = [&](int slot) {
+        return epi_all + (size_t)le * EPS + (slot <= EPI_FS ? slot * 64 : EPI_FS * 64 + 4 * FSF);
+    };
     const int n_act = MODE == MODE_STAGE ? md.count_active[KIND_EL * MAXS + sp.stage - 1] : md.n[0];
     const double g = md.gamma, gm1 = g - 1.0, inv_gm1 = 1.0 / gm1;
     const double dtc = sp.dt * sp.c_stage;
