@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(128, 4) k_grad2d(MeshDev md, StageParams sp, c
     const double dtc = sp.dt * sp.c_stage;
     const int q0 = 2 * t8;
     const int o = t8 >> 2, ln = t8 & 3;
-    const int eo = le * 18, yo = 2;
+    const int eox = le * 16, eoy = le * 20, yo = 2 - 2 * VOL2D_EPB;   // field layout as in k_vol2d
     const int stride = gridDim.x * VOL2D_EPB;
     int base = blockIdx.x * VOL2D_EPB;
     auto entry_at = [&](int b) {
@@ -193,15 +193,15 @@ __global__ void __launch_bounds__(128, 4) k_grad2d(MeshDev md, StageParams sp, c
             }
 #pragma unroll
             for (int c = 0; c < GV; ++c) {
-                *reinterpret_cast<double2 *>(&sm[G_V1 + c][0][eo + 4 * j0 + i0]) = make_double2(w[0][c], w[1][c]);
-                sm[G_V1 + c][1][yo + eo + 4 * i0 + j0] = w[0][c];
-                sm[G_V1 + c][1][yo + eo + 4 * (i0 + 1) + j0] = w[1][c];
+                *reinterpret_cast<double2 *>(&sm[G_V1 + c][0][eox + 4 * j0 + i0]) = make_double2(w[0][c], w[1][c]);
+                sm[G_V1 + c][1][yo + eoy + 4 * i0 + j0] = w[0][c];
+                sm[G_V1 + c][1][yo + eoy + 4 * (i0 + 1) + j0] = w[1][c];
             }
         }
         __syncwarp();
         if (has_next) issue_state(pk_next);       // stg consumed
         cp_async_commit();
-        const int lo = o == 0 ? eo + 4 * ln : yo + eo + 4 * ln;
+        const int lo = o == 0 ? eox + 4 * ln : yo + eoy + 4 * ln;
         double q[GV][NP];
         const int fld[GV] = {G_V1, G_V2, G_T};
         const double sc[GV] = {1.0, 1.0, 1.0};
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(128, 4) k_grad2d(MeshDev md, StageParams sp, c
 #pragma unroll
             for (int end = 0; end < 2; ++end) {
                 const int a = end ? NP - 1 : 0;
-                const int oi = o == 0 ? yo + eo + 4 * a + ln : eo + 4 * a + ln;
+                const int oi = o == 0 ? yo + eoy + 4 * a + ln : eox + 4 * a + ln;
                 double qo[GV], qs[GV], fv[GV];
 #pragma unroll
                 for (int c = 0; c < GV; ++c) {

@@ -425,12 +425,13 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
 // volume + surface lift + Jacobian + stage epilogue
 // ---------------------------------------------------------------------------------------------
 constexpr int VOL2D_EPB = 16;   // elements per 128-thread block (8 threads per element)
-// Shared-memory layout (bank-conflict free for the line loops): every field is
-// stored twice, once in x-line order (index le*17 + 4j + i) and once in y-line order
-// (index le*17 + 4i + j), the y copy offset by 2 doubles so that the 16 x-threads and 16 y-threads
-// of a warp hit 32 distinct banks.  The accumulators alias the first 4 field arrays; the BR1
-// gradients (NS) alias fields 4..6 once the two-point fluxes have consumed them.
-constexpr int VOL2D_LS = 288;   // doubles per field array: >= 16*17 + 2, and == 0 mod 16 so the +2 y offset shifts banks
+// Shared-memory layout (bank-conflict free): every field is stored twice, in
+// x-line order (index 16 le + 4j + i) and in y-line order (index 20 le + 4i + j, shifted by 2), in
+// the 2 LS doubles of the field; the x-line and y-line threads of an element hit disjoint banks in
+// the 16 B line loads, and the two elements of a half-warp hit disjoint banks in the scalar y-layout
+// stores / loads.  The accumulators alias the first 4 fields; the BR1 gradients (NS) alias fields
+// 4..6 once the two-point fluxes have consumed them.
+constexpr int VOL2D_LS = 288;   // half of the doubles per field (x part 16 EPB, y part 20 EPB + 2 < 2 LS)
 // k_vol2d fields (layout o = line direction): rho, v_n/2, v_t/2, p/2, ln rho, beta = rho/p, ln beta (+ T)
 constexpr int F_RHO = 0, F_HVN = 1, F_HVT = 2, F_HP = 3, F_LRHO = 4, F_BETA = 5, F_LBETA = 6, F_T = 7;
 // k_grad2d fields (both layouts): v1, v2, T
@@ -484,7 +485,7 @@ __device__ __forceinline__ void line_gradient(const double (*sm)[2][LS], int o, 
 // coordinates: acc[.][1] normal, acc[.][2] tangential momentum), i.e. -(2/h)(...) of the weak-form
 // viscous divergence after the common -2/h scaling.  Fields 4..6 are overwritten with the gradients.
 template <int LS>
-__device__ __forceinline__ void visc_volume(double (*sm)[2][LS], int o, int lo, int eo, int yo, int ln,
+__device__ __forceinline__ void visc_volume(double (*sm)[2][LS], int o, int lo, int eox, int eoy, int yo, int ln,
                                             const double *Ge, double Jq, double mu, double kappa,
                                             double acc[NP][4])
 {
@@ -502,8 +503,8 @@ __device__ __forceinline__ void visc_volume(double (*sm)[2][LS], int o, int lo, 
 #pragma unroll
     for (int a = 0; a < NP; ++a) {
         // the other direction's gradient at this node: node (a, ln) of an x-line lives at y-layout
-        // index yo + eo + 4a + ln; node (ln, a) of a y-line at x-layout index eo + 4a + ln
-        const int oi = o == 0 ? yo + eo + 4 * a + ln : eo + 4 * a + ln;
+        // index yo + eoy + 4a + ln; node (ln, a) of a y-line at x-layout index eox + 4a + ln
+        const int oi = o == 0 ? yo + eoy + 4 * a + ln : eox + 4 * a + ln;
         double qo[GV], qs[GV];
 #pragma unroll
         for (int c = 0; c < GV; ++c) {
@@ -615,8 +616,14 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
     const double dtc = sp.dt * sp.c_stage;
     const int q0 = 2 * t8;
     const int o = t8 >> 2, ln = t8 & 3;
-    const int eo = le * 18;                 // element offset inside a field array (even: 16 B aligned pairs)
-    const int yo = 2;                       // y-layout offset
+    // element offsets: x layout 16 per element, y layout 20 per element starting 2 doubles into the
+    // second half of the field's 2 LS doubles (yo < 0 indexes from [k][1] back into that half): the
+    // x-line and y-line threads of one element hit disjoint banks in the line loads (y - x == 2 mod 4)
+    // and the two elements of a half-warp hit disjoint banks in the scalar y-layout stores / loads
+    // (20 == 4 mod 8); with 18 / 18 and +2 the latter were 2-way conflicts
+    const int eox = le * 16, eoy = le * 20;
+    const int yo = 2 - 2 * EPB;
+    static_assert(16 * EPB + 20 * (EPB - 1) + 2 + 16 <= 2 * LS, "field layout");
     const int stride = gridDim.x * EPB;
 
     int base = blockIdx.x * EPB;
@@ -702,9 +709,9 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
             const int i0 = q0 & 3, j0 = q0 >> 2;
 #pragma unroll
             for (int k = 0; k < NF; ++k) {
-                *reinterpret_cast<double2 *>(&sm[k][0][eo + 4 * j0 + i0]) = make_double2(fx[0][k], fx[1][k]);
-                sm[k][1][yo + eo + 4 * i0 + j0] = fy[0][k];
-                sm[k][1][yo + eo + 4 * (i0 + 1) + j0] = fy[1][k];
+                *reinterpret_cast<double2 *>(&sm[k][0][eox + 4 * j0 + i0]) = make_double2(fx[0][k], fx[1][k]);
+                sm[k][1][yo + eoy + 4 * i0 + j0] = fy[0][k];
+                sm[k][1][yo + eoy + 4 * (i0 + 1) + j0] = fy[1][k];
             }
         }
         __syncwarp();   // the warp has read stg: refill it (next group) and stage this group's epilogue operands
@@ -744,7 +751,7 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
         if (has_next) issue_state(pk_next);
 
         // phase 2: 6 symmetric two-point fluxes along this thread's line (x-line j = ln, or y-line i = ln)
-        const int lo = o == 0 ? eo + 4 * ln : yo + eo + 4 * ln;   // line start in layout o
+        const int lo = o == 0 ? eox + 4 * ln : yo + eoy + 4 * ln;   // line start in layout o
         double acc[4][4];
 #pragma unroll
         for (int a = 0; a < 4; ++a)
@@ -786,7 +793,7 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
             if (has_next) cp_async_wait<1>();
             else cp_async_wait<0>();
             __syncwarp();
-            visc_volume<LS>(sm, o, lo, eo, yo, ln, EP(EPI_GS), 2.0 / hcell, md.mu, md.kappa, acc);
+            visc_volume<LS>(sm, o, lo, eox, eoy, yo, ln, EP(EPI_GS), 2.0 / hcell, md.mu, md.kappa, acc);
         }
         // surface lift: + f*_hi / w_N at the last node, - f*_lo / w_0 at the first node
         // line coordinates (normal, tangential) -> (momentum x, momentum y)
@@ -869,8 +876,8 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
             for (int h = 0; h < 2; ++h) {
 #pragma unroll
                 for (int v = 0; v < 4; ++v) {
-                    const double s0 = acc[2 * h][v] + sm[v][1][yo + eo + 4 * (2 * h) + ln];
-                    const double s1 = acc[2 * h + 1][v] + sm[v][1][yo + eo + 4 * (2 * h + 1) + ln];
+                    const double s0 = acc[2 * h][v] + sm[v][1][yo + eoy + 4 * (2 * h) + ln];
+                    const double s1 = acc[2 * h + 1][v] + sm[v][1][yo + eoy + 4 * (2 * h + 1) + ln];
                     epilogue(v, 4 * ln + 2 * h, make_double2(J * s0, J * s1));
                 }
             }
@@ -889,9 +896,9 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
             const int i0 = q0 & 3, j0 = q0 >> 2;   // q0 + 1 has i0 + 1
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
-                const double2 sx = *reinterpret_cast<const double2 *>(&sm[v][0][eo + q0]);
-                const double s0 = sx.x + sm[v][1][yo + eo + 4 * i0 + j0];
-                const double s1 = sx.y + sm[v][1][yo + eo + 4 * (i0 + 1) + j0];
+                const double2 sx = *reinterpret_cast<const double2 *>(&sm[v][0][eox + q0]);
+                const double s0 = sx.x + sm[v][1][yo + eoy + 4 * i0 + j0];
+                const double s1 = sx.y + sm[v][1][yo + eoy + 4 * (i0 + 1) + j0];
                 epilogue(v, q0, make_double2(J * s0, J * s1));
             }
         }
