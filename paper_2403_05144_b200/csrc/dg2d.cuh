@@ -464,8 +464,12 @@ __device__ __forceinline__ void line_gradient(const double (*sm)[2][LS], int o, 
 #pragma unroll
     for (int c = 0; c < GV; ++c) {
         double w[NP];
-#pragma unroll
-        for (int k = 0; k < NP; ++k) w[k] = sm[fld[c]][o][lo + k];
+        {   // the line is contiguous and 16 B aligned in either layout: two 16 B loads (one element per
+            // quarter-warp, conflict-free) instead of four scalar ones
+            const double2 w01 = *reinterpret_cast<const double2 *>(&sm[fld[c]][o][lo]);
+            const double2 w23 = *reinterpret_cast<const double2 *>(&sm[fld[c]][o][lo + 2]);
+            w[0] = w01.x; w[1] = w01.y; w[2] = w23.x; w[3] = w23.y;
+        }
         const double isc = 1.0 / sc[c];
         const double ghi = Ge[gidx2d(0, 2 * o, c, ln)] * isc;
         const double glo = Ge[gidx2d(0, 2 * o + 1, c, ln)] * isc;
