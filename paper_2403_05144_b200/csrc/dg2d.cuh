@@ -176,16 +176,19 @@ __device__ __forceinline__ const double *state_base(const StateBufs &sb, int src
 
 // the 4 conserved variables of face node k of element e in the stage state given by src; all loads
 // are issued before any use (the K_1 loads only when the state is formed lazily)
+#ifndef SURF2D_LD
+#define SURF2D_LD __ldg        // trace loads (A/B hook: __ldcg caches in L2 only)
+#endif
 __device__ __forceinline__ void trace2d(const StateBufs &sb, int src, double dtc, int e, int face, int k, double u[4])
 {
     const size_t b = (size_t)e * 64 + face_node2d(face, k);
     const double *P = state_base(sb, src);
 #pragma unroll
-    for (int v = 0; v < 4; ++v) u[v] = __ldg(P + b + v * 16);
+    for (int v = 0; v < 4; ++v) u[v] = SURF2D_LD(P + b + v * 16);
     if (src == SRC_LAZY) {
         double kk[4];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) kk[v] = __ldg(sb.K1 + b + v * 16);
+        for (int v = 0; v < 4; ++v) kk[v] = SURF2D_LD(sb.K1 + b + v * 16);
 #pragma unroll
         for (int v = 0; v < 4; ++v) u[v] = fma(dtc, kk[v], u[v]);
     }
