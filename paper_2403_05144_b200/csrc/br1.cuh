@@ -207,9 +207,10 @@ __global__ void __launch_bounds__(128, 4) k_grad2d(MeshDev md, StageParams sp, c
         const double sc[GV] = {1.0, 1.0, 1.0};
         line_gradient<GRAD2D_LS>(sm, o, lo, ln, gst[le], 2.0 / hcell, fld, sc, q);
 #pragma unroll
-        for (int c = 0; c < GV; ++c)
-#pragma unroll
-            for (int a = 0; a < NP; ++a) sm[G_Q + c][o][lo + a] = q[c][a];
+        for (int c = 0; c < GV; ++c) {   // the line is contiguous and 16 B aligned: two 16 B stores
+            *reinterpret_cast<double2 *>(&sm[G_Q + c][o][lo]) = make_double2(q[c][0], q[c][1]);
+            *reinterpret_cast<double2 *>(&sm[G_Q + c][o][lo + 2]) = make_double2(q[c][2], q[c][3]);
+        }
         __syncwarp();
         if (has_next) issue_gs(pk_next);          // gst consumed
         cp_async_commit();
