@@ -219,6 +219,20 @@ __global__ void k_hot_lists(MeshDev md)
 }
 
 // BR1 halo flags: the large side of a mortar whose fine side belongs to another member
+// gather the per-stage hot arrays: out position j <- hot-array position idx[j] (count from seg[1])
+__global__ void k_stage_gather(const int *__restrict__ seg, const int *__restrict__ idx, int kind, MeshDev md,
+                               int *el_out, int4 *f4_out, int *bd_out)
+{
+    const int n = seg[1];
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const int t = idx[j];
+        if (kind == KIND_EL) el_out[j] = md.elpk[t];
+        else if (kind == KIND_IF) f4_out[j] = md.ifcs[t];
+        else if (kind == KIND_MO) f4_out[j] = md.mors[t];
+        else bd_out[j] = md.list[KIND_BD][t];
+    }
+}
+
 __global__ void k_halo_clear(MeshDev md)
 {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;

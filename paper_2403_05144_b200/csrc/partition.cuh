@@ -44,6 +44,36 @@ struct KeyHaloMo {
     __device__ int operator()(int i) const { const int4 M = a[i]; return (halo[M.y] | halo[M.z]) ? (M.w >> 8) : -1; }
 };
 
+// Per-stage item lists for non-nested stage patterns (2D): key 0 = the item is needed at the stage
+// (an element / interface / boundary of an evaluating member, a mortar with an evaluating fine or
+// coarse side), -1 = dropped.  Items are positions in the member-sorted hot arrays.
+struct KeyStageEl {
+    const int *elpk;
+    unsigned mask;
+    __device__ int operator()(int t) const { return ((mask >> ((elpk[t] >> 24) & 7)) & 1u) ? 0 : -1; }
+};
+struct KeyStageIf {
+    const int4 *a;
+    unsigned mask;
+    __device__ int operator()(int t) const { return ((mask >> a[t].w) & 1u) ? 0 : -1; }
+};
+struct KeyStageMo {
+    const int4 *a;
+    const uint8_t *mem;
+    unsigned mask;
+    __device__ int operator()(int t) const
+    {
+        const int4 M = a[t];
+        return (((mask >> (M.w >> 8)) | (mask >> mem[M.x])) & 1u) ? 0 : -1;
+    }
+};
+struct KeyStageBd {
+    const int *list;
+    const int2 *bnd;
+    unsigned mask;
+    __device__ int operator()(int t) const { return ((mask >> (bnd[list[t]].y >> 8)) & 1u) ? 0 : -1; }
+};
+
 // Stage-activity description for the count_active table (P:l.428: member r evaluates stage i iff
 // i == 1 or E_r >= S - i + 2).
 struct ActiveDesc {

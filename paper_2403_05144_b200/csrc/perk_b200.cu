@@ -48,6 +48,11 @@ struct perk_ctx {
     bool ns = false;
     unsigned long long act[MAXR] = {};     // evaluated stages per member (bit i-1), standard or given
     bool std_pattern = true;
+    // non-nested stage patterns (2D): per-stage hot arrays [S][capacity] (elements, interfaces,
+    // mortars, boundary list), so every launch covers exactly the items its stage needs
+    bool stage_lists = false;
+    int *st_el = nullptr, *st_bd = nullptr, *st_idx = nullptr;
+    int4 *st_if = nullptr, *st_mo = nullptr;
     uint8_t *lmap = nullptr, *keys = nullptr;
     int *items = nullptr, *rank = nullptr, *blockcnt = nullptr, *blockoff = nullptr, *segtmp = nullptr;
     int *dconst = nullptr;     // [0] = nmorton
@@ -258,6 +263,27 @@ static void build_mesh(perk_ctx *c, cudaStream_t s, const uint8_t *lmap)
     partition(c, s, KeyBnd{md.bnd}, md.n + 3, 1, c->cap_faces, R, md.list[KIND_BD], nullptr, md.seg + 3 * (MAXR + 1),
               nullptr, md.count_active + KIND_BD * MAXS);
     k_hot_lists<<<blocks_for(c->cap_faces, 256), 256, 0, s>>>(md);
+    if (c->stage_lists) {   // per-stage lists (non-nested patterns): stable compaction per (stage, kind)
+        for (int i = 1; i <= c->tab.S; ++i) {
+            unsigned mask = 0;
+            for (int r = 0; r < R; ++r)
+                if ((c->act[r] >> (i - 1)) & 1ull) mask |= 1u << r;
+            const size_t oc = (size_t)(i - 1) * c->cap, of = (size_t)(i - 1) * c->cap_faces;
+            int *ca = md.count_active;
+            partition(c, s, KeyStageEl{md.elpk, mask}, md.n + 0, 1, c->cap, 1, c->st_idx, nullptr, c->segtmp, nullptr, nullptr);
+            k_stage_gather<<<blocks_for(c->cap, 256), 256, 0, s>>>(c->segtmp, c->st_idx, KIND_EL, md, c->st_el + oc, nullptr, nullptr);
+            k_set_count<<<1, 1, 0, s>>>(ca + KIND_EL * MAXS + i - 1, c->segtmp, 0);
+            partition(c, s, KeyStageIf{md.ifcs, mask}, md.n + 1, 1, c->cap_faces, 1, c->st_idx, nullptr, c->segtmp, nullptr, nullptr);
+            k_stage_gather<<<blocks_for(c->cap_faces, 256), 256, 0, s>>>(c->segtmp, c->st_idx, KIND_IF, md, nullptr, c->st_if + of, nullptr);
+            k_set_count<<<1, 1, 0, s>>>(ca + KIND_IF * MAXS + i - 1, c->segtmp, 0);
+            partition(c, s, KeyStageMo{md.mors, md.mem, mask}, md.n + 2, 1, c->cap_faces, 1, c->st_idx, nullptr, c->segtmp, nullptr, nullptr);
+            k_stage_gather<<<blocks_for(c->cap_faces, 256), 256, 0, s>>>(c->segtmp, c->st_idx, KIND_MO, md, nullptr, c->st_mo + of, nullptr);
+            k_set_count<<<1, 1, 0, s>>>(ca + KIND_MO * MAXS + i - 1, c->segtmp, 0);
+            partition(c, s, KeyStageBd{md.list[KIND_BD], md.bnd, mask}, md.n + 3, 1, c->cap_faces, 1, c->st_idx, nullptr, c->segtmp, nullptr, nullptr);
+            k_stage_gather<<<blocks_for(c->cap_faces, 256), 256, 0, s>>>(c->segtmp, c->st_idx, KIND_BD, md, nullptr, nullptr, c->st_bd + of);
+            k_set_count<<<1, 1, 0, s>>>(ca + KIND_BD * MAXS + i - 1, c->segtmp, 0);
+        }
+    }
     if (c->ns) {   // BR1 halo lists (see MeshDev::halo)
         k_halo_clear<<<blocks_for(c->cap, 256), 256, 0, s>>>(md);
         k_halo_flags<<<blocks_for(c->cap_faces, 256), 256, 0, s>>>(md);
@@ -308,9 +334,24 @@ static StageParams stage_params(const perk_ctx *c, int i, double dt, int mode, u
     return sp;
 }
 
+// the mesh view of one launch: for non-nested stage patterns, a stage launch reads the stage's own
+// hot arrays (count_active then holds their lengths); otherwise the shared member-sorted arrays
+static MeshDev stage_mesh(const perk_ctx *c, const StageParams &sp)
+{
+    MeshDev md = c->md;
+    if (c->stage_lists && sp.mode == MODE_STAGE) {
+        const size_t oc = (size_t)(sp.stage - 1) * c->cap, of = (size_t)(sp.stage - 1) * c->cap_faces;
+        md.elpk = c->st_el + oc;
+        md.ifcs = c->st_if + of;
+        md.mors = c->st_mo + of;
+        md.list[KIND_BD] = c->st_bd + of;
+    }
+    return md;
+}
+
 static void launch_surface(perk_ctx *c, cudaStream_t s, const StageParams &sp, const double *Un, const double *Uin)
 {
-    const MeshDev &md = c->md;
+    const MeshDev md = stage_mesh(c, sp);
     if (c->prob.dim == 2) {
         if (c->ns) {
             if (sp.mode == MODE_STAGE)
@@ -338,7 +379,7 @@ static void launch_surface(perk_ctx *c, cudaStream_t s, const StageParams &sp, c
 
 static void launch_volume(perk_ctx *c, cudaStream_t s, const StageParams &sp, double *Un, const double *Uin, double *dU)
 {
-    const MeshDev &md = c->md;
+    const MeshDev md = stage_mesh(c, sp);
     if (c->prob.dim == 2) {
         if (c->ns) {
             if (sp.mode == MODE_STAGE)
@@ -647,6 +688,25 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
     } else {
         c->vol_blocks = std::min(blocks_for(c->cap, 128), SM_COUNT_B200 * 8);
         c->surf_blocks = std::min(blocks_for(c->cap_faces, 256), SM_COUNT_B200 * 8);
+    }
+    if (dim == 2 && !c->std_pattern) {   // per-stage lists for non-nested stage patterns
+        bool nested = true;                // every stage's evaluating members form a prefix of the order?
+        for (int i = 1; i <= tab->S && nested; ++i) {
+            int rmin = tab->R;
+            for (int r = tab->R - 1; r >= 0; --r)
+                if ((c->act[r] >> (i - 1)) & 1ull) rmin = r;
+            for (int r = rmin; r < tab->R; ++r)
+                if (!((c->act[r] >> (i - 1)) & 1ull)) nested = false;
+        }
+        if (!nested) {
+            c->stage_lists = true;
+            const size_t S = (size_t)tab->S;
+            CU(dalloc(c, &c->st_el, S * c->cap));
+            CU(dalloc(c, &c->st_if, S * c->cap_faces));
+            CU(dalloc(c, &c->st_mo, S * c->cap_faces));
+            CU(dalloc(c, &c->st_bd, S * c->cap_faces));
+            CU(dalloc(c, &c->st_idx, (size_t)std::max(c->cap, c->cap_faces)));
+        }
     }
     CU(cudaMemcpyAsync(c->lmap, level_map_dev, c->nf, cudaMemcpyDeviceToDevice, c->stream));
     build_mesh(c, c->stream, c->lmap);

@@ -34,14 +34,21 @@ def _pair(w, pattern, c_S=Fr(1, 2), problem=None, level_map=None, max_cells=None
 
 
 def _check_counts(fam, gpu):
-    """stage-i launch size = the segments of members R-1 .. r_min(i), r_min = lowest evaluating member"""
-    for kind in ("elements", "interfaces", "mortars", "boundaries"):
-        _, seg = gpu.list(kind)
+    """stage-i launch size = the items the stage needs: elements / interfaces / boundaries of evaluating
+    members, mortars with an evaluating fine or coarse side (nested patterns: the member-sorted prefix;
+    non-nested: the per-stage lists)"""
+    lv = gpu.leaves()
+    mem_el = lv["member"]
+    members = {"elements": (mem_el, None), "interfaces": (gpu.faces("interfaces")[1], None),
+               "boundaries": (gpu.faces("boundaries")[1], None)}
+    rec, mfine = gpu.faces("mortars")
+    members["mortars"] = (mfine, mem_el[rec[:, 0]] if len(rec) else np.zeros(0, np.int32))
+    for kind, (m1, m2) in members.items():
         ca = gpu.count_active(kind)
-        R = fam["R"]
         for i in range(1, fam["S"] + 1):
-            rmin = min(r for r in range(R) if i in fam["stages"][r])
-            assert ca[i - 1] == seg[R - rmin], (kind, i)
+            on = np.array([i in fam["stages"][r] for r in range(fam["R"])])
+            need = on[m1] if m2 is None else (on[m1] | on[m2])
+            assert ca[i - 1] == int(need.sum()), (kind, i, ca[i - 1], int(need.sum()))
 
 
 def _run(w, fam, ora, gpu, steps):
