@@ -188,3 +188,40 @@ def test_adapt_cycle_full_size():
     gpu.step(Ug, w.dt, 1)
     torch.cuda.synchronize()
     assert rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo).max() <= TOL
+
+
+@pytest.mark.parametrize("variant", ["perk3", "alternating"])
+def test_adapt_loop_with_perk3_and_patterns(variant):
+    """indicator-driven re-meshing combined with the P-ERK3 family / a non-nested stage pattern"""
+    from paper_2403_05144_b200 import Perk
+    from workloads import perk3 as P3
+    w = W.make(4, n_base=16, max_level=3, widths=(0.3, 0.15, 0.06))
+    w.S, w.E = 16, [4, 8, 16]
+    amr = dict(w.meta["amr"], max_level=3, med_level=2)
+    if variant == "perk3":
+        fam = P3.family3(w.S, w.E)
+        gpu = Perk(w.problem, w.level_map, w.S, w.E, family=fam, max_cells=4 * W.configs.count_leaves(w))
+    else:
+        fam = T.family(w.S, w.E, w.alpha_rule, pattern="alternating")
+        gpu = Perk(w.problem, w.level_map, w.S, w.E, pattern="alternating", max_cells=4 * W.configs.count_leaves(w))
+    ora = O.OracleMesh(w.problem, w.level_map, fam)
+    Uo = ora.initial_state(w.ic)
+    Ug = gpu.initial_state(w.ic)
+    for _ in range(3):
+        ora.step(Uo, w.dt, 4)
+        gpu.step(Ug, w.dt, 4)
+        lm_o = ora.amr_adapt(Uo, amr)
+        lm_g = gpu.amr_adapt(Ug, amr)
+        gpu.repartition(lm_g, Ug)
+        gpu.sync()
+        assert _compare_maps(ora, lm_o, lm_g.cpu().numpy(), ora.amr_indicator(Uo, amr), amr) == 0
+        new = O.OracleMesh(w.problem, lm_o, fam)
+        Uo = O.transfer(ora, new, Uo)
+        ora = new
+        lo, lg = ora.leaves(), gpu.leaves()
+        assert all(np.array_equal(lo[k], lg[k]) for k in ("fx", "fy", "level", "member"))
+        assert rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo).max() <= TOL
+    ora.step(Uo, w.dt, 4)
+    gpu.step(Ug, w.dt, 4)
+    torch.cuda.synchronize()
+    assert rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo).max() <= TOL
