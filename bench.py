@@ -43,12 +43,12 @@ UNIT = "element-RHS/s"
 
 # Executed fp64 work of the hot kernels per element-RHS: counted with ncu
 # (smsp__sass_thread_inst_executed_op_{dfma,dmul,dadd}_pred_on.sum over all 32 launches of one cfg-3
-# step, profiles/r01_fp64_ops_dram_per_step_v10.csv) and divided by the step's 713,596 element-RHS;
+# step, profiles/r01_fp64_ops_dram_per_step_v13.csv) and divided by the step's 713,596 element-RHS;
 # flops = 2 DFMA + DMUL + DADD.  Cold-cache DRAM bytes of the same launches (ncu, per launch average)
 # give `traffic`.
-VOL_FLOPS_PER_ELEMENT_RHS = 6399.0        # k_vol2d (volume + lift + Jacobian + stage epilogue)
-SURF_FLOPS_PER_ELEMENT_RHS = 952.0        # k_surf2d (HLL interface / mortar fluxes)
-VOL_DRAM_BYTES_PER_LAUNCH = (1335868416.0 + 67343360.0) / 16   # k_vol2d, cold cache (ncu flushes)
+VOL_FLOPS_PER_ELEMENT_RHS = 6401.9        # k_vol2d (volume + lift + Jacobian + stage epilogue)
+SURF_FLOPS_PER_ELEMENT_RHS = 947.3        # k_surf2d (HLL interface / mortar fluxes)
+VOL_DRAM_BYTES_PER_LAUNCH = (1335842816.0 + 74005504.0) / 16   # k_vol2d, cold cache (ncu flushes)
 
 
 def _peaks():
