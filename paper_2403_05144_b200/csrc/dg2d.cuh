@@ -564,7 +564,7 @@ __host__ __device__ constexpr int vol2d_epi_slots(bool ns) { return (vol2d_epi_m
 #ifndef VOL2D_FS_PAD
 #define VOL2D_FS_PAD 1
 #endif
-__host__ __device__ constexpr int vol2d_fs_face(bool ns) { return VOL2D_FS_PAD ? 18 : 16; }
+__host__ __device__ constexpr int vol2d_fs_face(bool) { return VOL2D_FS_PAD ? 18 : 16; }
 // element block: [U_n 64][K_1 64] (mode 1) [Fs 4 x face stride] [Gs 48 (NS)]; Euler 200 doubles,
 // Navier-Stokes (mode 2) 72 + 48 = 120, both == 8 mod 16 with the padded faces
 __host__ __device__ constexpr int vol2d_epi_stride(bool ns)
