@@ -9,8 +9,9 @@
 // k_vol2d  : one launch per stage over the active element prefix, 8 threads per element (4 x-lines
 //            + 4 y-lines): primitives and logarithms per node once (shared memory), 48 symmetric
 //            Ranocha two-point fluxes (6 per line), surface lift (1/w) and Jacobian (-2/h), then the
-//            stage epilogue in registers: K_1 (stage 1), the next stage state
-//            U^(i+1) = U_n + dt (a_{i+1,1} K_1 + a_{i+1,i} K_i) (1 < i < S), or U_{n+1} = U_n + dt K_S.
+//            stage epilogue in registers: K_1 (stage 1), the state of the member's next evaluated
+//            stage n, U^(n) = U_n + dt (a_{n,1} K_1 + a_{n,i} K_i) (standard pattern: n = i + 1), or
+//            U_{n+1} = W + dt b_S K_S (W = U_n, or the P-ERK3 / Heun-Ralston combination).
 #pragma once
 #include "common.cuh"
 

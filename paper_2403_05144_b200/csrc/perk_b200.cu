@@ -1,9 +1,11 @@
 // perk_b200.cu -- libperk_b200.so: the C ABI of include/perk.h (host side) + all device kernels.
 //
-// Host-side responsibilities: argument validation, tableau construction (P:l.1062), capacity-sized
-// allocations, launching the device mesh pipeline (mesh.cuh), capturing one CUDA graph per P-ERK
-// step (2 launches per stage: k_surf*, k_vol*), profiling hooks.  No step of the method runs on
-// the host: after perk_init the host never reads mesh data except in introspection calls.
+// Host-side responsibilities: argument validation, tableau construction (P:l.1062; stage patterns
+// and Heun / Ralston weights), capacity-sized allocations, launching the device mesh pipeline
+// (mesh.cuh; captured as one graph per re-mesh), capturing one CUDA graph per P-ERK step (2 launches
+// per stage: k_surf*, k_vol*; + 2 BR1 launches for Navier-Stokes; one k_step1d launch for small 1D
+// meshes), the device AMR adapt (amr.cuh), profiling hooks.  No step of the method runs on the host:
+// after perk_init the host never reads mesh data except in introspection calls.
 #include <cmath>
 #include <cstdio>
 #include <cstring>
