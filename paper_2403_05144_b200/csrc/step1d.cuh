@@ -38,7 +38,7 @@ __host__ __device__ constexpr int step1d_threads(int nv) { return nv == 1 ? STEP
 // boundaries (<= 2), the element list, member and level per element
 __host__ __device__ inline size_t step1d_smem_bytes(int n, int nv, bool use_w)
 {
-    return sizeof(double) * ((size_t)n * nv * NP * (use_w ? 5 : 4) + (size_t)n * 2 * nv) +
+    return sizeof(double) * ((size_t)n * nv * NP * (use_w ? 4 : 3) + (size_t)n * 2 * nv) +
            (size_t)n * 8 + 16 + (size_t)n * 4 + (size_t)n * 2;
 }
 
@@ -50,8 +50,8 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
     __shared__ StepTab1D T;
     const int n = md.n[0];
     const int rowd = NV * NP;
-    double *sUn = sh, *sK1 = sUn + (size_t)n * rowd, *sUb = sK1 + (size_t)n * rowd, *sKi = sUb + (size_t)n * rowd;
-    double *sW = sKi + (size_t)n * rowd;
+    double *sUn = sh, *sK1 = sUn + (size_t)n * rowd, *sUb = sK1 + (size_t)n * rowd;
+    double *sW = sUb + (size_t)n * rowd;
     double *sFs = use_w ? sW + (size_t)n * rowd : sW;
     int2 *sIf = reinterpret_cast<int2 *>(sFs + (size_t)n * 2 * NV);
     int2 *sBd = sIf + n;
@@ -126,50 +126,57 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
             }
         }
         __syncthreads();
-        // K_i at the active element nodes (one thread per node); surplus members of the prefix skip
+        // K_i at the active element nodes (one thread per node; an element's 4 node threads are
+        // consecutive lanes of one warp) and, once the element's stage state has been read by all
+        // four (__syncwarp), the stage combination from registers; surplus members of the prefix skip
         const unsigned act = T.actmask[i - 1];
-        for (int t = tid; t < NP * nel; t += nt) {
-            const int e = sEl[t / NP], j = t % NP;
-            const int m = sMem[e];
-            if (!((act >> m) & 1u)) continue;
-            double f[NP][NV];
-#pragma unroll
-            for (int k = 0; k < NP; ++k) {
-                double u[NV];
-#pragma unroll
-                for (int v = 0; v < NV; ++v) u[v] = state(e, m, v, k);
-                phys_flux1d<NV>(u, md.gamma, md.adv, f[k]);
+        const int tot = NP * nel;
+        for (int t0 = 0; t0 < tot; t0 += nt) {
+            const int t = t0 + tid;
+            bool on = t < tot;
+            int e = 0, j = 0, m = 0;
+            if (on) {
+                e = sEl[t / NP];
+                j = t % NP;
+                m = sMem[e];
+                on = (act >> m) & 1u;
             }
-            const double J = 2.0 / (md.hf * (double)(1 << (md.max_level - sLev[e])));
+            double K[NV];
+            if (on) {
+                double f[NP][NV];
 #pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                double s = 0.0;
+                for (int k = 0; k < NP; ++k) {
+                    double u[NV];
 #pragma unroll
-                for (int k = 0; k < NP; ++k) s = fma(cB.Dhat[j][k], f[k][v], s);
-                if (j == 0) s = fma(sFs[((size_t)e * 2 + 1) * NV + v], cB.invw[0], s);
-                if (j == NP - 1) s = fma(-sFs[((size_t)e * 2 + 0) * NV + v], cB.invw[NP - 1], s);
-                sKi[((size_t)e * NV + v) * NP + j] = J * s;
+                    for (int v = 0; v < NV; ++v) u[v] = state(e, m, v, k);
+                    phys_flux1d<NV>(u, md.gamma, md.adv, f[k]);
+                }
+                const double J = 2.0 / (md.hf * (double)(1 << (md.max_level - sLev[e])));
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int k = 0; k < NP; ++k) s = fma(cB.Dhat[j][k], f[k][v], s);
+                    if (j == 0) s = fma(sFs[((size_t)e * 2 + 1) * NV + v], cB.invw[0], s);
+                    if (j == NP - 1) s = fma(-sFs[((size_t)e * 2 + 0) * NV + v], cB.invw[NP - 1], s);
+                    K[v] = J * s;
+                }
             }
-        }
-        __syncthreads();
-        // stage combination (every state read of this stage is done)
-        for (int t = tid; t < NP * nel; t += nt) {
-            const int e = sEl[t / NP], j = t % NP;
-            const int m = sMem[e];
-            if (!((act >> m) & 1u)) continue;
+            __syncwarp();
+            if (on) {
 #pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                const size_t x = ((size_t)e * NV + v) * NP + j;
-                const double K = sKi[x];
-                if (i == 1) {
-                    sK1[x] = K;
-                } else if (i == S) {
-                    if (!use_w && T.b1 != 0.0) sUn[x] = fma(dt, fma(T.b1, sK1[x], T.bS * K), sUn[x]);   // Heun / Ralston
-                    else sUn[x] = fma(dt * T.bS, K, use_w ? sW[x] : sUn[x]);
-                } else {
-                    const double un = sUn[x], k1 = sK1[x];
-                    sUb[x] = fma(dt, fma(T.a1n[m][i - 1], k1, T.asubn[m][i - 1] * K), un);   // next evaluated stage
-                    if (use_w && i == S - 1) sW[x] = fma(dt, fma(T.b1, k1, T.bS1 * K), un);
+                for (int v = 0; v < NV; ++v) {
+                    const size_t x = ((size_t)e * NV + v) * NP + j;
+                    if (i == 1) {
+                        sK1[x] = K[v];
+                    } else if (i == S) {
+                        if (!use_w && T.b1 != 0.0) sUn[x] = fma(dt, fma(T.b1, sK1[x], T.bS * K[v]), sUn[x]);   // Heun / Ralston
+                        else sUn[x] = fma(dt * T.bS, K[v], use_w ? sW[x] : sUn[x]);
+                    } else {
+                        const double un = sUn[x], k1 = sK1[x];
+                        sUb[x] = fma(dt, fma(T.a1n[m][i - 1], k1, T.asubn[m][i - 1] * K[v]), un);   // next evaluated stage
+                        if (use_w && i == S - 1) sW[x] = fma(dt, fma(T.b1, k1, T.bS1 * K[v]), un);
+                    }
                 }
             }
         }
