@@ -700,7 +700,10 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
             for (int r = rmin; r < tab->R; ++r)
                 if (!((c->act[r] >> (i - 1)) & 1ull)) nested = false;
         }
-        if (!nested) {
+        // per-stage arrays cost S x (4 B per cell + 36 B per face slot); beyond 8 GB keep the superset
+        // prefix (correct, surplus members skipped) instead
+        const double bytes = (double)tab->S * ((double)c->cap * 4.0 + (double)c->cap_faces * 36.0);
+        if (!nested && bytes <= 8.0e9) {
             c->stage_lists = true;
             const size_t S = (size_t)tab->S;
             CU(dalloc(c, &c->st_el, S * c->cap));
