@@ -8,6 +8,7 @@
 // after perk_init the host never reads mesh data except in introspection calls.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -703,7 +704,8 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
         // per-stage arrays cost S x (4 B per cell + 36 B per face slot); beyond 8 GB keep the superset
         // prefix (correct, surplus members skipped) instead
         const double bytes = (double)tab->S * ((double)c->cap * 4.0 + (double)c->cap_faces * 36.0);
-        if (!nested && bytes <= 8.0e9) {
+        const char *env = std::getenv("PERK_STAGE_LISTS");   // "0": force the superset path (tests)
+        if (!nested && bytes <= 8.0e9 && !(env && env[0] == '0')) {
             c->stage_lists = true;
             const size_t S = (size_t)tab->S;
             CU(dalloc(c, &c->st_el, S * c->cap));

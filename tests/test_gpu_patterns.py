@@ -152,3 +152,19 @@ def test_maximum_stage_count_s64():
         assert gpu.counters()[0] == ev_o
         assert gpu.launches_per_step() == 2 * 64
         assert rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo).max() <= TOL
+
+
+def test_non_nested_superset_path(monkeypatch):
+    """the 2D superset-prefix path (used when per-stage lists would exceed their memory budget):
+    forced with PERK_STAGE_LISTS=0; surplus members' faces computed, their elements skipped"""
+    monkeypatch.setenv("PERK_STAGE_LISTS", "0")
+    w = W.make(3, n_base=16)
+    fam, ora, gpu = _pair(w, NON_NESTED_16)
+    # launch sizes are the member-sorted prefixes down to the lowest evaluating member
+    _, seg = gpu.list("elements")
+    ca = gpu.count_active("elements")
+    for i in range(1, fam["S"] + 1):
+        rmin = min(r for r in range(fam["R"]) if i in fam["stages"][r])
+        assert ca[i - 1] == seg[fam["R"] - rmin]
+    Uo, Ug = _run(w, fam, ora, gpu, 20)
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
