@@ -1,0 +1,71 @@
+"""Full-run parity of the CUDA path against the oracle (BASELINE.json north_star: "within 1e-10 max
+relative fp64 state error per conserved variable after the full run"), one process per config so the
+single-threaded oracle runs use several host cores.  Step counts: the BASELINE ones for cfg 1-3, and
+bounded samples for cfg 4 (200 of 2000 steps, 40 device re-meshes) and cfg 5 (20 of 200 steps), whose
+full oracle runs would take hours on one core.  Prints one JSON object; development / evidence tool,
+not part of the test suite."""
+import json
+import multiprocessing as mp
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+PLAN = {1: None, 2: None, 3: None, 4: 200, 5: 20}   # None = the BASELINE step count
+
+
+def run(cfg):
+    import numpy as np
+    import torch
+    import workloads as W
+    from oracle import oracle as O
+    from oracle import tableau as T
+    from gpu_util import gpu_state_numpy, rel_err_per_var
+    from paper_2403_05144_b200 import Perk
+    w = W.make(cfg)
+    steps = PLAN[cfg] or w.steps
+    fam = T.family(w.S, w.E, w.alpha_rule)
+    ora = O.OracleMesh(w.problem, w.level_map, fam)
+    gpu = Perk(w.problem, w.level_map, w.S, w.E)
+    Uo = ora.initial_state(w.ic)
+    Ug = gpu.initial_state(w.ic)
+    t0 = time.time()
+    remeshes = 0
+    if w.remesh_every:
+        done = 0
+        k = 0
+        while done < steps:
+            n = min(w.remesh_every, steps - done)
+            ora.step(Uo, w.dt, n)
+            gpu.step(Ug, w.dt, n)
+            done += n
+            if done % w.remesh_every == 0 and done < steps:
+                k += 1
+                lm = w.level_map_seq(k)
+                new = O.OracleMesh(w.problem, lm, fam)
+                Uo = O.transfer(ora, new, Uo)
+                ora = new
+                gpu.repartition(lm, Ug)
+                remeshes += 1
+    else:
+        ora.step(Uo, w.dt, steps)
+        gpu.step(Ug, w.dt, steps)
+    torch.cuda.synchronize()
+    gpu.sync()
+    err = rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo)
+    lo, lg = ora.leaves(), gpu.leaves()
+    same_mesh = all(np.array_equal(lo[q], lg[q]) for q in ("fx", "fy", "level", "member"))
+    return cfg, {"workload": w.name, "steps": steps, "baseline_steps": w.steps, "re_meshes": remeshes,
+                 "cells": int(ora.n), "max_rel_err_per_var": [float(x) for x in err], "mesh_identical": same_mesh,
+                 "pass": bool(err.max() <= 1e-10 and same_mesh), "oracle_seconds": round(time.time() - t0, 1)}
+
+
+if __name__ == "__main__":
+    cfgs = [int(c) for c in (sys.argv[1] if len(sys.argv) > 1 else "1,2,3,4,5").split(",")]
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(len(cfgs)) as pool:
+        res = dict(pool.map(run, cfgs))
+    print(json.dumps({"tolerance": 1e-10, "configs": {f"cfg{c}": res[c] for c in cfgs}}, indent=1))
