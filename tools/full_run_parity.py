@@ -1,8 +1,8 @@
 """Full-run parity of the CUDA path against the oracle (BASELINE.json north_star: "within 1e-10 max
 relative fp64 state error per conserved variable after the full run"), one process per config so the
 single-threaded oracle runs use several host cores.  Step counts: the BASELINE ones for cfg 1-3, and
-bounded samples for cfg 4 (200 of 2000 steps, 40 device re-meshes) and cfg 5 (20 of 200 steps), whose
-full oracle runs would take hours on one core.  Prints one JSON object; development / evidence tool,
+by default bounded samples for cfg 4 (200 of 2000 steps, 40 device re-meshes) and cfg 5 (20 of 200
+steps), whose full oracle runs take hours on one core ("cfg:steps" overrides, e.g. "5:200").  Prints one JSON object; development / evidence tool,
 not part of the test suite."""
 import json
 import multiprocessing as mp
@@ -17,7 +17,8 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 PLAN = {1: None, 2: None, 3: None, 4: 200, 5: 20}   # None = the BASELINE step count
 
 
-def run(cfg):
+def run(arg):
+    cfg, steps_override = arg
     import numpy as np
     import torch
     import workloads as W
@@ -26,7 +27,7 @@ def run(cfg):
     from gpu_util import gpu_state_numpy, rel_err_per_var
     from paper_2403_05144_b200 import Perk
     w = W.make(cfg)
-    steps = PLAN[cfg] or w.steps
+    steps = steps_override or PLAN[cfg] or w.steps
     fam = T.family(w.S, w.E, w.alpha_rule)
     ora = O.OracleMesh(w.problem, w.level_map, fam)
     gpu = Perk(w.problem, w.level_map, w.S, w.E)
@@ -64,8 +65,10 @@ def run(cfg):
 
 
 if __name__ == "__main__":
-    cfgs = [int(c) for c in (sys.argv[1] if len(sys.argv) > 1 else "1,2,3,4,5").split(",")]
+    # argument: comma list of configs, each optionally "cfg:steps" (e.g. "4:1000,5:200")
+    items = [x for x in (sys.argv[1] if len(sys.argv) > 1 else "1,2,3,4,5").split(",") if x]
+    args = [(int(x.split(":")[0]), int(x.split(":")[1]) if ":" in x else None) for x in items]
     ctx = mp.get_context("spawn")
-    with ctx.Pool(len(cfgs)) as pool:
-        res = dict(pool.map(run, cfgs))
-    print(json.dumps({"tolerance": 1e-10, "configs": {f"cfg{c}": res[c] for c in cfgs}}, indent=1))
+    with ctx.Pool(len(args)) as pool:
+        res = dict(pool.map(run, args))
+    print(json.dumps({"tolerance": 1e-10, "configs": {f"cfg{c}": res[c] for c, _ in args}}, indent=1))
