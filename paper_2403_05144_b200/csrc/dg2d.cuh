@@ -177,57 +177,19 @@ __device__ __forceinline__ const double *state_base(const StateBufs &sb, int src
 
 // the 4 conserved variables of face node k of element e in the stage state given by src; all loads
 // are issued before any use (the K_1 loads only when the state is formed lazily)
-#ifndef SURF2D_LD
-#define SURF2D_LD __ldg        // trace loads (A/B hook: __ldcg caches in L2 only)
-#endif
 __device__ __forceinline__ void trace2d(const StateBufs &sb, int src, double dtc, int e, int face, int k, double u[4])
 {
     const size_t b = (size_t)e * 64 + face_node2d(face, k);
     const double *P = state_base(sb, src);
 #pragma unroll
-    for (int v = 0; v < 4; ++v) u[v] = SURF2D_LD(P + b + v * 16);
+    for (int v = 0; v < 4; ++v) u[v] = __ldg(P + b + v * 16);
     if (src == SRC_LAZY) {
         double kk[4];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) kk[v] = SURF2D_LD(sb.K1 + b + v * 16);
+        for (int v = 0; v < 4; ++v) kk[v] = __ldg(sb.K1 + b + v * 16);
 #pragma unroll
         for (int v = 0; v < 4; ++v) u[v] = fma(dtc, kk[v], u[v]);
     }
-}
-
-// face nodes kp, kp + 1 (kp even) of element e: node stride 1 on y faces, NP on x faces
-__device__ __forceinline__ void trace2d_pair(const StateBufs &sb, int src, double dtc, int e, int face, int kp,
-                                             double a[4], double b[4])
-{
-    const size_t n0 = (size_t)e * 64 + face_node2d(face, kp);
-    const int st = face >= 2 ? 1 : NP;
-    const double *P = state_base(sb, src);
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-        a[v] = __ldg(P + n0 + v * 16);
-        b[v] = __ldg(P + n0 + st + v * 16);
-    }
-    if (src == SRC_LAZY) {
-        double ka[4], kb[4];
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            ka[v] = __ldg(sb.K1 + n0 + v * 16);
-            kb[v] = __ldg(sb.K1 + n0 + st + v * 16);
-        }
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            a[v] = fma(dtc, ka[v], a[v]);
-            b[v] = fma(dtc, kb[v], b[v]);
-        }
-    }
-}
-
-// flux slots of face nodes kp, kp + 1 (kp even): adjacent in [face][v][k], one 16 B store per variable
-__device__ __forceinline__ void store_face2d_pair(double *Fs, int e, int face, int kp, const double fa[4], const double fb[4])
-{
-    const size_t b = ((size_t)e * 4 + face) * 16 + kp;
-#pragma unroll
-    for (int v = 0; v < 4; ++v) *reinterpret_cast<double2 *>(Fs + b + v * 4) = make_double2(fa[v], fb[v]);
 }
 
 __device__ __forceinline__ void store_face2d(double *Fs, int e, int face, int k, const double f[4])
@@ -241,12 +203,6 @@ __device__ __forceinline__ void store_face2d(double *Fs, int e, int face, int k,
 // normal viscous-flux traces Vt of k_grad2d), so the volume kernel lifts one combined flux.
 #ifndef SURF2D_MINB
 #define SURF2D_MINB 3
-#endif
-#ifndef SURF2D_PAIRED
-#define SURF2D_PAIRED 1
-#endif
-#ifndef SURF2D_NPAIR
-#define SURF2D_NPAIR 0         // 1: interfaces with two face nodes of the same interface per thread
 #endif
 template <int MODE, bool NS>
 __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StageParams sp, const double *__restrict__ Un,
@@ -272,35 +228,9 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
     const int GS = gridDim.x * blockDim.x;
     const int nI = 4 * nif;
     int gt = blockIdx.x * blockDim.x + threadIdx.x;
-#if SURF2D_NPAIR
-    for (int t = gt; t < 2 * nif; t += GS) {
-        const int item = t >> 1, kp = (t & 1) * 2;
-        const int4 I = MODE == MODE_STAGE ? md.ifcs[item] : md.ifc[item];
-        PERK_DASSERT(I.x >= 0 && I.x < md.n[0] && I.y >= 0 && I.y < md.n[0]);
-        const int o = I.z;
-        const int src = state_src(sp, I.w);
-        double uL0[4], uL1[4], uR0[4], uR1[4], f0[4], f1[4];
-        trace2d_pair(sb, src, dtc, I.x, 2 * o, kp, uL0, uL1);
-        trace2d_pair(sb, src, dtc, I.y, 2 * o + 1, kp, uR0, uR1);
-        numflux2d(uL0, uR0, o, g, md.surface, f0);
-        numflux2d(uL1, uR1, o, g, md.surface, f1);
-        if (NS) {
-#pragma unroll
-            for (int c = 0; c < GV; ++c) {
-                const double2 va = __ldg(reinterpret_cast<const double2 *>(Vt + gidx2d(I.x, 2 * o, c, kp)));
-                const double2 vb = __ldg(reinterpret_cast<const double2 *>(Vt + gidx2d(I.y, 2 * o + 1, c, kp)));
-                f0[1 + c] -= 0.5 * (va.x + vb.x);
-                f1[1 + c] -= 0.5 * (va.y + vb.y);
-            }
-        }
-        store_face2d_pair(Fs, I.x, 2 * o, kp, f0, f1);
-        store_face2d_pair(Fs, I.y, 2 * o + 1, kp, f0, f1);
-    }
-    gt += nI;                     // mortars and boundaries: four threads per item, lane-aligned
-#endif
     // two interface face nodes per iteration while both are interfaces: twice the loads in flight
     // per thread (the kernel is bound by the latency of the record -> trace gathers)
-    for (; !SURF2D_NPAIR && SURF2D_PAIRED && gt + GS < nI; gt += 2 * GS) {
+    for (; gt + GS < nI; gt += 2 * GS) {
         const int ka = gt & 3, kb = (gt + GS) & 3;
         const int4 Ia = MODE == MODE_STAGE ? md.ifcs[gt >> 2] : md.ifc[gt >> 2];
         const int4 Ib = MODE == MODE_STAGE ? md.ifcs[(gt + GS) >> 2] : md.ifc[(gt + GS) >> 2];
@@ -539,21 +469,15 @@ __device__ __forceinline__ void visc_volume(double (*sm)[2][LS], int o, int lo, 
 
 // Dynamic shared memory of k_vol2d (bytes): field arrays, own-state staging, epilogue staging.
 __host__ __device__ constexpr int vol2d_nf(bool ns) { return ns ? 8 : 7; }
-// U_n / K_1 operands of the stage epilogue: 1 = staged in shared memory with the Fs fluxes, 0 = read
-// from global memory in the epilogue, 2 = loaded into registers before the two-point-flux loop.
-// Measured (cfg 3 / cfg 5 volume ms/step): Euler 1: 0.361, 0: 0.406, 2: 0.378; Navier-Stokes 1: 3.60,
-// 2: 3.52 (its 16 KB smaller footprint fits 3 instead of 2 CTAs per SM)
+// U_n / K_1 operands of the stage epilogue: 1 = staged in shared memory with the Fs fluxes,
+// 2 = loaded into registers before the two-point-flux loop.  Measured (cfg 3 / cfg 5 volume ms/step):
+// Euler 1: 0.361, 2: 0.378; Navier-Stokes 1: 3.60, 2: 3.52 (its 16 KB smaller footprint fits 3
+// instead of 2 CTAs per SM); read from global memory in the epilogue instead: Euler 0.406
 #ifndef VOL2D_EPI_MODE_EULER
 #define VOL2D_EPI_MODE_EULER 1
 #endif
 #ifndef VOL2D_EPI_MODE_NS
 #define VOL2D_EPI_MODE_NS 2
-#endif
-#ifndef VOL2D_MINB
-#define VOL2D_MINB (VOL2D_EPI_MODE_EULER == 0 ? 4 : 3)
-#endif
-#ifndef VOL2D_P3X
-#define VOL2D_P3X 0            // 1: the x-line threads finalise their own lines (y contributions via smem)
 #endif
 __host__ __device__ constexpr int vol2d_epi_mode(bool ns) { return ns ? VOL2D_EPI_MODE_NS : VOL2D_EPI_MODE_EULER; }
 constexpr int EPI_UN = 0, EPI_K1 = 1;                                   // (mode 1 only)
@@ -598,7 +522,7 @@ __host__ __device__ constexpr size_t vol2d_smem_bytes(bool ns)
 // cp.async.bulk on mbarriers; issuing the per-element bulk copies through the uniform datapath cost
 // about a quarter of the kernel's issue slots.)
 template <int MODE, bool NS>
-__global__ void __launch_bounds__(vol2d_threads(NS), NS ? (VOL2D_EPB_NS == 8 ? 5 : 3) : VOL2D_MINB)
+__global__ void __launch_bounds__(vol2d_threads(NS), NS ? (VOL2D_EPB_NS == 8 ? 5 : 3) : 3)
 k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                                                  double *__restrict__ Ubuf, double *__restrict__ K1,
                                                  const double *__restrict__ Fs, const double *__restrict__ Uin,
@@ -743,12 +667,9 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                         if (need_k1) pre_k1[v] = __ldg(reinterpret_cast<const double2 *>(K1 + eb + v * 16 + q0));
                     }
                 }
-            } else if (EM) {
+            } else {
                 if (need_un) copy_block(EP(EPI_UN), (Wb && sp.stage == sp.S ? Wb : Un) + eb);
                 if (need_k1) copy_block(EP(EPI_K1), K1 + eb);
-            } else if (valid) {   // pull the epilogue operands' lines into L1 for phase 3
-                const double *src = (t8 < 4) ? (need_un ? (Wb && sp.stage == sp.S ? Wb : Un) : nullptr) : (need_k1 ? K1 : nullptr);
-                if (src) asm volatile("prefetch.global.L1 [%0];" ::"l"(src + eb + 16 * (t8 & 3)));
             }
             if (NS) {   // the element's 48 BR1 central traces (384 B = 24 chunks of 16 B)
 #pragma unroll
@@ -836,12 +757,9 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                 *reinterpret_cast<double2 *>(K1 + idx) = K;
             } else if (sp.stage == sp.S) {
                 const double2 w = EM == 2 ? pre_un[v]
-                                : EM ? *reinterpret_cast<const double2 *>(EP(EPI_UN) + v * 16 + qq)
-                                                   : __ldg(reinterpret_cast<const double2 *>((Wb ? Wb : Un) + idx));   // W or U_n
+                                          : *reinterpret_cast<const double2 *>(EP(EPI_UN) + v * 16 + qq);   // W or U_n
                 if (sp.fin_k1) {
-                    const double2 k1 = EM == 2 ? pre_k1[v]
-                                     : EM ? *reinterpret_cast<const double2 *>(EP(EPI_K1) + v * 16 + qq)
-                                                        : __ldg(reinterpret_cast<const double2 *>(K1 + idx));
+                    const double2 k1 = EM == 2 ? pre_k1[v] : *reinterpret_cast<const double2 *>(EP(EPI_K1) + v * 16 + qq);
                     *reinterpret_cast<double2 *>(Un + idx) =
                         make_double2(fma(sp.dt, fma(sp.wb1, k1.x, sp.bS * K.x), w.x),
                                      fma(sp.dt, fma(sp.wb1, k1.y, sp.bS * K.y), w.y));
@@ -850,12 +768,8 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                     *reinterpret_cast<double2 *>(Un + idx) = make_double2(fma(db, K.x, w.x), fma(db, K.y, w.y));
                 }
             } else {
-                const double2 un = EM == 2 ? pre_un[v]
-                                 : EM ? *reinterpret_cast<const double2 *>(EP(EPI_UN) + v * 16 + qq)
-                                                    : *reinterpret_cast<const double2 *>(Un + idx);
-                const double2 k1 = EM == 2 ? pre_k1[v]
-                                 : EM ? *reinterpret_cast<const double2 *>(EP(EPI_K1) + v * 16 + qq)
-                                                    : __ldg(reinterpret_cast<const double2 *>(K1 + idx));
+                const double2 un = EM == 2 ? pre_un[v] : *reinterpret_cast<const double2 *>(EP(EPI_UN) + v * 16 + qq);
+                const double2 k1 = EM == 2 ? pre_k1[v] : *reinterpret_cast<const double2 *>(EP(EPI_K1) + v * 16 + qq);
                 const double a1 = sp.a1_next[m], as = sp.asub_next[m];
                 *reinterpret_cast<double2 *>(Ubuf + idx) =
                     make_double2(fma(sp.dt, fma(a1, k1.x, as * K.x), un.x), fma(sp.dt, fma(a1, k1.y, as * K.y), un.y));
@@ -868,30 +782,6 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
         // members in the launch's prefix that do not evaluate this stage (non-standard patterns) write nothing
         const bool writes = valid && (MODE == MODE_RHS || ((sp.actmask >> m) & 1u));
         const double J = -2.0 / hcell;
-#if VOL2D_P3X
-        // phase 3 on the x-line threads: each finalises its own line's 4 nodes from its registers plus
-        // the y-line threads' contributions handed over through shared memory
-        __syncwarp();   // all primitives consumed: reuse sm[v][1] as the y-contribution arrays
-        if (o == 1) {
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-                *reinterpret_cast<double2 *>(&sm[v][1][lo]) = make_double2(acc[0][v], acc[1][v]);
-                *reinterpret_cast<double2 *>(&sm[v][1][lo + 2]) = make_double2(acc[2][v], acc[3][v]);
-            }
-        }
-        __syncwarp();
-        if (o == 0 && writes) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    const double s0 = acc[2 * h][v] + sm[v][1][yo + eoy + 4 * (2 * h) + ln];
-                    const double s1 = acc[2 * h + 1][v] + sm[v][1][yo + eoy + 4 * (2 * h + 1) + ln];
-                    epilogue(v, 4 * ln + 2 * h, make_double2(J * s0, J * s1));
-                }
-            }
-        }
-#else
         __syncwarp();   // all primitives consumed: reuse sm[v][o] as the accumulator arrays
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
@@ -911,7 +801,6 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                 epilogue(v, q0, make_double2(J * s0, J * s1));
             }
         }
-#endif
         __syncwarp();
         pk = pk_next;
     }
