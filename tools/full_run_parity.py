@@ -59,9 +59,14 @@ def run(arg):
     err = rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo)
     lo, lg = ora.leaves(), gpu.leaves()
     same_mesh = all(np.array_equal(lo[q], lg[q]) for q in ("fx", "fy", "level", "member"))
-    return cfg, {"workload": w.name, "steps": steps, "baseline_steps": w.steps, "re_meshes": remeshes,
-                 "cells": int(ora.n), "max_rel_err_per_var": [float(x) for x in err], "mesh_identical": same_mesh,
-                 "pass": bool(err.max() <= 1e-10 and same_mesh), "oracle_seconds": round(time.time() - t0, 1)}
+    res = {"workload": w.name, "steps": steps, "baseline_steps": w.steps, "re_meshes": remeshes,
+           "cells": int(ora.n), "max_rel_err_per_var": [float(x) for x in err], "mesh_identical": same_mesh,
+           "pass": bool(err.max() <= 1e-10 and same_mesh), "oracle_seconds": round(time.time() - t0, 1)}
+    out = os.path.join(ROOT, "gpurun_out")                # each config's result as soon as it is done
+    os.makedirs(out, exist_ok=True)
+    with open(os.path.join(out, f"full_run_parity_cfg{cfg}_{steps}.json"), "w") as f:
+        json.dump(res, f, indent=1)
+    return cfg, res
 
 
 if __name__ == "__main__":
