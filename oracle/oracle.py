@@ -14,7 +14,10 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "perk_oracle.c")
-LIB = os.path.join(HERE, "liboracle.so")
+# ORACLE_OMP=1: an OpenMP build (bitwise identical results, perk_oracle.c) for long full-run parity
+# checks only; the tests and the CPU baseline use the serial build
+OMP = os.environ.get("ORACLE_OMP") == "1"
+LIB = os.path.join(HERE, "liboracle_omp.so" if OMP else "liboracle.so")
 
 EQ = {"advection": 0, "euler": 1, "navier_stokes": 2}
 VOL = {"weak": 0, "fluxdiff": 1}
@@ -25,8 +28,8 @@ NP = 4
 def build(force: bool = False) -> str:
     """Compile the oracle with plain gcc: -O2 -ffp-contract=off, no fast-math."""
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
-        cmd = ["gcc", "-std=c99", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
-               "-o", LIB, SRC, "-lm"]
+        cmd = ["gcc", "-std=c99", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"] + \
+              (["-fopenmp"] if OMP else []) + ["-o", LIB, SRC, "-lm"]
         subprocess.check_call(cmd)
     return LIB
 

@@ -33,6 +33,11 @@
  */
 #include <math.h>
 #include <stdint.h>
+/* Optional OpenMP (oracle.build(omp=True), only for long full-run parity checks): every parallel loop
+   below writes disjoint per-element / per-face-slot outputs and has no reduction, so the results are
+   bitwise identical for any thread count; the default build has no -fopenmp and runs
+   the same loops serially. */
+#define OMP_FOR _Pragma("omp parallel for schedule(static)")
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -941,21 +946,31 @@ int ora_rhs(void *p, const double *U, uint32_t mask, double *dU, int mode)
     }
     if (mode == 0) {
         if (ns) {   /* BR1 step 1: gradients everywhere */
+            OMP_FOR
             for (int f = 0; f < o->n_if; ++f) central_interface(o, U, f, trace_w, o->Gs);
+            OMP_FOR
             for (int m = 0; m < o->n_mo; ++m) central_mortar(o, U, m, trace_w, o->Gs);
+            OMP_FOR
             for (int e = 0; e < o->n; ++e) element_grad(o, U, e);
         }
+        OMP_FOR
         for (int f = 0; f < o->n_if; ++f) interface_flux(o, U, f);
+        OMP_FOR
         for (int m = 0; m < o->n_mo; ++m) mortar_flux(o, U, m);
+        OMP_FOR
         for (int b = 0; b < o->n_bd; ++b) boundary_flux(o, U, b);
         if (ns) {
+            OMP_FOR
             for (int f = 0; f < o->n_if; ++f) central_interface(o, U, f, trace_fv, o->Fv);
+            OMP_FOR
             for (int m = 0; m < o->n_mo; ++m) central_mortar(o, U, m, trace_fv, o->Fv);
         }
+        OMP_FOR
         for (int e = 0; e < o->n; ++e) {
             element_rhs(o, U, e, dU);
             if (ns) element_visc(o, U, e, dU);
         }
+        OMP_FOR
         for (int e = 0; e < o->n; ++e)
             if (!((mask >> o->member[e]) & 1u))
                 for (int v = 0; v < o->nv; ++v)
@@ -972,29 +987,38 @@ int ora_rhs(void *p, const double *U, uint32_t mask, double *dU, int mode)
         for (int s = 0; s < R; ++s) {
             int r = R - 1 - s;
             if (!((ext >> r) & 1u)) continue;
+            OMP_FOR
             for (int64_t t = o->seg[1][s]; t < o->seg[1][s + 1]; ++t) central_interface(o, U, o->list[1][t], trace_w, o->Gs);
+            OMP_FOR
             for (int64_t t = o->seg[2][s]; t < o->seg[2][s + 1]; ++t) central_mortar(o, U, o->list[2][t], trace_w, o->Gs);
         }
         for (int s = 0; s < R; ++s) {
             int r = R - 1 - s;
             if (!((ext >> r) & 1u)) continue;
+            OMP_FOR
             for (int64_t t = o->seg[0][s]; t < o->seg[0][s + 1]; ++t) element_grad(o, U, o->list[0][t]);
         }
     }
     for (int s = 0; s < R; ++s) {
         int r = R - 1 - s;
         if (!((mask >> r) & 1u)) continue;
+        OMP_FOR
         for (int64_t t = o->seg[1][s]; t < o->seg[1][s + 1]; ++t) interface_flux(o, U, o->list[1][t]);
+        OMP_FOR
         for (int64_t t = o->seg[2][s]; t < o->seg[2][s + 1]; ++t) mortar_flux(o, U, o->list[2][t]);
+        OMP_FOR
         for (int64_t t = o->seg[3][s]; t < o->seg[3][s + 1]; ++t) boundary_flux(o, U, o->list[3][t]);
         if (ns) {
+            OMP_FOR
             for (int64_t t = o->seg[1][s]; t < o->seg[1][s + 1]; ++t) central_interface(o, U, o->list[1][t], trace_fv, o->Fv);
+            OMP_FOR
             for (int64_t t = o->seg[2][s]; t < o->seg[2][s + 1]; ++t) central_mortar(o, U, o->list[2][t], trace_fv, o->Fv);
         }
     }
     for (int s = 0; s < R; ++s) {
         int r = R - 1 - s;
         if (!((mask >> r) & 1u)) continue;
+        OMP_FOR
         for (int64_t t = o->seg[0][s]; t < o->seg[0][s + 1]; ++t) {
             element_rhs(o, U, o->list[0][t], dU);
             if (ns) element_visc(o, U, o->list[0][t], dU);
@@ -1038,6 +1062,7 @@ static int64_t perk_step_generic(const OraTableau *t, int nunits, int usize, con
     memset(Kp, 0, sizeof(double) * nd);
     for (size_t d = 0; d < nd; ++d) Ksum[d] = 0.0 + t->b[0] * K1[d];
     for (int i = 2; i <= t->S; ++i) {
+        OMP_FOR
         for (int u = 0; u < nunits; ++u) {
             int r = member[u];
             double a1 = t->a1[r][i - 1], as = t->asub[r][i - 1];

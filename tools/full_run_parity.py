@@ -2,8 +2,10 @@
 relative fp64 state error per conserved variable after the full run"), one process per config so the
 single-threaded oracle runs use several host cores.  Step counts: the BASELINE ones for cfg 1-3, and
 by default bounded samples for cfg 4 (200 of 2000 steps, 40 device re-meshes) and cfg 5 (20 of 200
-steps), whose full oracle runs take hours on one core ("cfg:steps" overrides, e.g. "5:200").  Prints one JSON object; development / evidence tool,
-not part of the test suite."""
+steps), whose full oracle runs take hours on one core ("cfg:steps" overrides, e.g. "5:200").  With
+ORACLE_OMP=1 the oracle is the OpenMP build (bitwise identical to the serial one; OMP_NUM_THREADS per
+process), which makes the full cfg 4 / cfg 5 runs fit one GPU call.  Prints one JSON object;
+development / evidence tool, not part of the test suite."""
 import json
 import multiprocessing as mp
 import os
