@@ -55,6 +55,11 @@ class OraAmr(C.Structure):
                 ("alpha_max", C.c_double), ("alpha_min", C.c_double), ("f_wave", C.c_double)]
 
 
+class OraSC(C.Structure):
+    _fields_ = [("variable", C.c_int32), ("smooth", C.c_int32), ("alpha_max", C.c_double),
+                ("alpha_min", C.c_double), ("alpha_fixed", C.c_double)]
+
+
 INDICATORS = {"hennemann_gassner": 0, "lohner": 1, "enstrophy": 2}
 AMR_VARIABLES = {"rho": 0, "p": 1, "rho_p": 2, "v_x": 3, "v_y": 4}
 
@@ -67,6 +72,18 @@ def amr_struct(a: dict) -> OraAmr:
     s.med_threshold, s.max_threshold = a["med_threshold"], a["max_threshold"]
     s.alpha_max, s.alpha_min = a.get("alpha_max", 0.5), a.get("alpha_min", 0.001)
     s.f_wave = a.get("f_wave", 0.2)
+    return s
+
+
+def sc_struct(sc: dict) -> OraSC:
+    """problem["shock_capturing"]: variable (AMR_VARIABLES name), alpha_max, alpha_min, smooth,
+    alpha_fixed (None / negative = the indicator)"""
+    s = OraSC()
+    s.variable = AMR_VARIABLES[sc.get("variable", "rho_p")]
+    s.smooth = int(sc.get("smooth", True))
+    s.alpha_max, s.alpha_min = sc.get("alpha_max", 0.5), sc.get("alpha_min", 0.001)
+    af = sc.get("alpha_fixed")
+    s.alpha_fixed = -1.0 if af is None else af
     return s
 
 
@@ -112,6 +129,10 @@ def lib():
         L.ora_amr_indicator.argtypes = [P, dp, C.POINTER(OraAmr), dp]
         L.ora_amr_adapt.restype = C.c_int
         L.ora_amr_adapt.argtypes = [P, dp, C.POINTER(OraAmr), up]
+        L.ora_set_shock_capturing.restype = C.c_int
+        L.ora_set_shock_capturing.argtypes = [P, C.POINTER(OraSC)]
+        L.ora_sc_alpha.restype = C.c_int
+        L.ora_sc_alpha.argtypes = [P, dp, dp, dp]
         _lib = L
     return _lib
 
@@ -189,6 +210,11 @@ class OracleMesh:
         if not self.h:
             raise ValueError(err.value.decode())
         self.n = lib().ora_num_cells(self.h)
+        if problem.get("shock_capturing") is not None:      # section 9 of perk_oracle.c
+            self._sc = sc_struct(problem["shock_capturing"])
+            rc = lib().ora_set_shock_capturing(self.h, C.byref(self._sc))
+            if rc:
+                raise ValueError("shock_capturing: " + ("unsupported problem" if rc == -2 else "invalid parameters"))
         self.nv = problem["nv"]
         self.npe = NP ** problem["dim"]
 
@@ -265,6 +291,13 @@ class OracleMesh:
         assert U.flags["C_CONTIGUOUS"] and U.dtype == np.float64
         return lib().ora_steps(self.h, U.reshape(-1), dt, nsteps, mode)
 
+
+    def sc_alpha(self, U):
+        """shock-capturing blending factors of state U: (raw indicator, smoothed), per leaf"""
+        raw, sm = np.zeros(self.n), np.zeros(self.n)
+        if lib().ora_sc_alpha(self.h, np.ascontiguousarray(U, np.float64).ravel(), raw, sm):
+            raise ValueError("shock capturing is off")
+        return raw, sm
 
     def amr_indicator(self, U, amr: dict):
         """per-leaf AMR indicator (section 8 of perk_oracle.c), canonical leaf order"""

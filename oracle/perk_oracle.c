@@ -24,12 +24,18 @@
  *   7. FV Godunov testbed (linear advection / Burgers)     P:l.479-520
  *   8. AMR indicators (Hennemann-Gassner, Loehner, enstrophy) and the level
  *      controller with 2:1 balance     P:l.1440-1441, l.1548, l.1615-1622
+ *   9. Subcell shock capturing (Hennemann-Gassner blending of the flux-differencing
+ *      volume integral with a first-order subcell finite-volume one)
+ *                                                          P:l.964, l.1729, l.1795-1799
  *
  * Parity status: every function here is pinned by tests/test_oracle_*.py; the
  * Navier-Stokes BR1 operator (section 4b) by tests/test_oracle_ns.py (free stream,
  * conservation, manufactured viscous terms term by term, restricted == reference);
  * section 8 by tests/test_oracle_amr.py (closed-form modal energies, hand-computed Loehner
- * ratios, exact vorticity of polynomial fields, brute-force minimal balanced trees).
+ * ratios, exact vorticity of polynomial fields, brute-force minimal balanced trees); section 9 by
+ * tests/test_oracle_sc.py (alpha = 1 equals an independent global first-order finite-volume scheme
+ * on the subcell grid, alpha = 0 is bitwise the unblended operator, free stream, conservation with
+ * mortars, smoothing against geometric brute-force neighbours, restricted == reference).
  */
 #include <math.h>
 #include <stdint.h>
@@ -74,6 +80,14 @@ typedef struct {
     uint64_t active[MAXR];      /* bit i-1: member r evaluates stage i; 0 = the standard pattern
                                    {1} u {S-E+2..S} (P:l.428); other patterns P:l.642-700 */
 } OraTableau;
+
+/* subcell shock capturing (section 9) */
+typedef struct {
+    int32_t variable;           /* indicator variable: 0 rho, 1 p, 2 rho*p, 3 v_x, 4 v_y */
+    int32_t smooth;             /* 1: alpha_e = max(alpha_e, alpha_nbr / 2) over face neighbours */
+    double alpha_max, alpha_min;
+    double alpha_fixed;         /* >= 0: this blending factor for every element (no indicator) */
+} OraSC;
 
 /* stage i (1-based) is evaluated by member r: standard pattern i == 1 or i >= S - E_r + 2
    (P:l.407-436, eq. PERK_ButcherTableauClassic: member E evaluates K_1 and the last E-1 stages),
@@ -237,6 +251,8 @@ typedef struct {
     double *Q;                /* BR1: gradients of w = (rho, v1, v2, T), [n][2 (x, y)][4][NP*NP] */
     double *Fv;               /* BR1: central viscous face flux per element face, [n][4][4][NP] */
     int64_t elem_rhs_count;   /* element-RHS evaluations (counter, P:l.1282-1289) */
+    int sc_on; OraSC sc;      /* subcell shock capturing (section 9) */
+    double *alpha_raw, *alpha;/* per element: indicator blending factor, after neighbour smoothing */
 } Ora;
 
 static uint64_t morton2(uint32_t x, uint32_t y)
@@ -301,6 +317,7 @@ void ora_destroy(void *p)
     free(o->if_member); free(o->mo_member); free(o->bd_member);
     for (int k = 0; k < 4; ++k) free(o->list[k]);
     free(o->Fs); free(o->Gs); free(o->Q); free(o->Fv);
+    free(o->alpha_raw); free(o->alpha);
     free(o);
 }
 
@@ -698,10 +715,13 @@ static void boundary_flux(Ora *o, const double *U, int b)
     }
 }
 
+static void sc_subcell_volume(Ora *o, const double *U, int e, int i, int j, double *fv);
+
 /* element RHS.  1D weak form (cfg 1-2):
      du_i = (2/h) [ sum_j Dhat_ij f(u_j) + (delta_i0 f*_L - delta_iN f*_R) / w_i ]
    2D flux differencing (cfg 3-5), per direction:
-     du_ij -= (2/h) [ sum_k Dsplit_ik f#(u_ij, u_kj) + (delta_iN f*_R - delta_i0 f*_L) / w_i ] */
+     du_ij -= (2/h) [ sum_k Dsplit_ik f#(u_ij, u_kj) + (delta_iN f*_R - delta_i0 f*_L) / w_i ]
+   with shock capturing the volume part sum_k ... is blended with the subcell FV one (section 9) */
 static void element_rhs(Ora *o, const double *U, int e, double *dU)
 {
     double h = cell_h(o, e), J = 2.0 / h;
@@ -740,6 +760,12 @@ static void element_rhs(Ora *o, const double *U, int e, double *dU)
                 for (int v = 0; v < nv; ++v) uk[v] = U[UIDX(o, e, v, k * NP + i)];
                 ora_flux_ranocha(ui, uk, 1, g, f);
                 for (int v = 0; v < nv; ++v) acc[v] += o->B.Dsplit[j][k] * f[v];
+            }
+            if (o->sc_on) {   /* section 9: (1 - alpha) V_DG + alpha V_FV */
+                double fv[MAXV];
+                sc_subcell_volume(o, U, e, i, j, fv);
+                double a = o->alpha[e];
+                for (int v = 0; v < nv; ++v) acc[v] = (1.0 - a) * acc[v] + a * fv[v];
             }
             for (int v = 0; v < nv; ++v) {
                 double s = acc[v];
@@ -931,11 +957,14 @@ static void element_visc(Ora *o, const double *U, int e, double *dU)
    mode 0 "reference": evaluate every face and element, then zero the unmasked elements.
    mode 1 "restricted": loop over the members in mask only, through the per-member lists;
    a mortar is evaluated whenever its (fine-side) member is in the mask (P:l.1256). */
+static void sc_alpha(Ora *o, const double *U);
+
 int ora_rhs(void *p, const double *U, uint32_t mask, double *dU, int mode)
 {
     Ora *o = (Ora *)p;
     int R = o->tab.R;
     int ns = o->prob.equation == 2;
+    if (o->sc_on) sc_alpha(o, U);   /* blending factors of every element from the stage state U */
     if (mode == 1) {
         /* the restricted loops are only equivalent to I^(r)F for upward-closed masks (every member
            finer than a masked one is masked too), which is what every P-ERK stage uses (P:l.428):
@@ -1432,5 +1461,102 @@ int ora_amr_adapt(void *p, const double *U, const OraAmr *a, uint8_t *lmap)
     }
     free(ind);
     free(want);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* 9. subcell shock capturing (Hennemann & Gassner 2021, cited by the paper   */
+/*    for every inviscid application: P:l.964, l.1729, l.1795-1799, l.1856)   */
+/*    DESIGN.md readings A7-A9.  Per element:                                 */
+/*      V = (1 - alpha) V_DG + alpha V_FV                                     */
+/*    V_DG = sum_k Dsplit_ik f#(u_i, u_k) (flux differencing, section 4);     */
+/*    V_FV = (F_{i+1/2} - F_{i-1/2}) / w_i along each node line, with the     */
+/*    subcell fluxes F_{i+1/2} = f*(u_i, u_{i+1}) (the surface flux of the    */
+/*    problem) between neighbouring LGL nodes and F_{-1/2} = F_{N+1/2} = 0:   */
+/*    with the unchanged surface term (f*_R at node N, f*_L at node 0) this   */
+/*    is the first-order FV scheme on the subcells of widths w_i h / 2.       */
+/*    alpha: Hennemann-Gassner indicator (section 8, A1) of the chosen        */
+/*    variable on the element's stage state, then optional smoothing         */
+/*    alpha_e = max(alpha_e, alpha_n / 2) over the face neighbours n (across  */
+/*    interfaces and mortars, raw neighbour values).                          */
+/* ------------------------------------------------------------------------- */
+static void sc_subcell_volume(Ora *o, const double *U, int e, int i, int j, double *fv)
+{
+    int nv = o->nv;
+    for (int v = 0; v < nv; ++v) fv[v] = 0.0;
+    for (int d = 0; d < 2; ++d) {              /* d = 0: x line j, node i; d = 1: y line i, node j */
+        int a = d == 0 ? i : j;
+        double u[NP][MAXV];
+        for (int k = 0; k < NP; ++k) {
+            int q = d == 0 ? j * NP + k : k * NP + i;
+            for (int v = 0; v < nv; ++v) u[k][v] = U[UIDX(o, e, v, q)];
+        }
+        double Fr[MAXV] = {0, 0, 0, 0}, Fl[MAXV] = {0, 0, 0, 0};
+        if (a < NP - 1) num_flux(o, u[a], u[a + 1], d, Fr);
+        if (a > 0) num_flux(o, u[a - 1], u[a], d, Fl);
+        for (int v = 0; v < nv; ++v) fv[v] += (Fr[v] - Fl[v]) / o->B.w[a];
+    }
+}
+
+static void sc_alpha(Ora *o, const double *U)
+{
+    OraAmr a;
+    memset(&a, 0, sizeof(a));
+    a.variable = o->sc.variable;
+    a.alpha_max = o->sc.alpha_max;
+    a.alpha_min = o->sc.alpha_min;
+    OMP_FOR
+    for (int e = 0; e < o->n; ++e) {
+        if (o->sc.alpha_fixed >= 0.0) { o->alpha_raw[e] = o->sc.alpha_fixed; continue; }
+        double val[NP * NP];
+        for (int q = 0; q < NP * NP; ++q) {
+            double u[MAXV];
+            for (int v = 0; v < 4; ++v) u[v] = U[UIDX(o, e, v, q)];
+            val[q] = amr_variable(o, u, a.variable);
+        }
+        o->alpha_raw[e] = indicator_hg(o, val, &a);
+    }
+    for (int e = 0; e < o->n; ++e) o->alpha[e] = o->alpha_raw[e];
+    if (!o->sc.smooth) return;
+    for (int f = 0; f < o->n_if; ++f) {
+        int eL = o->ifc[3 * f], eR = o->ifc[3 * f + 1];
+        o->alpha[eL] = fmax(o->alpha[eL], 0.5 * o->alpha_raw[eR]);
+        o->alpha[eR] = fmax(o->alpha[eR], 0.5 * o->alpha_raw[eL]);
+    }
+    for (int m = 0; m < o->n_mo; ++m) {
+        const int32_t *M = o->mor + 5 * m;
+        for (int h = 0; h < 2; ++h) {
+            o->alpha[M[0]] = fmax(o->alpha[M[0]], 0.5 * o->alpha_raw[M[1 + h]]);
+            o->alpha[M[1 + h]] = fmax(o->alpha[M[1 + h]], 0.5 * o->alpha_raw[M[0]]);
+        }
+    }
+}
+
+/* sc = NULL switches shock capturing off.  -2: not a 2D Euler / Navier-Stokes flux-differencing
+   problem; -1: invalid parameters */
+int ora_set_shock_capturing(void *p, const OraSC *sc)
+{
+    Ora *o = (Ora *)p;
+    if (!sc) { o->sc_on = 0; return 0; }
+    if (o->prob.dim != 2 || o->prob.equation == 0 || o->prob.volume != 1) return -2;
+    if (sc->variable < 0 || sc->variable > 4 || !(sc->alpha_min >= 0.0) || !(sc->alpha_max >= 0.0) ||
+        !(sc->alpha_max <= 1.0) || !(sc->alpha_fixed <= 1.0)) return -1;
+    o->sc = *sc;
+    if (!o->alpha) {
+        o->alpha_raw = (double *)calloc((size_t)o->n, sizeof(double));
+        o->alpha = (double *)calloc((size_t)o->n, sizeof(double));
+    }
+    o->sc_on = 1;
+    return 0;
+}
+
+/* blending factors of U (raw indicator and smoothed), canonical leaf order; -1 if off */
+int ora_sc_alpha(void *p, const double *U, double *raw, double *smoothed)
+{
+    Ora *o = (Ora *)p;
+    if (!o->sc_on) return -1;
+    sc_alpha(o, U);
+    memcpy(raw, o->alpha_raw, sizeof(double) * (size_t)o->n);
+    memcpy(smoothed, o->alpha, sizeof(double) * (size_t)o->n);
     return 0;
 }
