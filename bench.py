@@ -15,7 +15,8 @@ the multi-GPU domain decomposition of SURVEY §8(e) is not built)
 separately), cfg 5 (Navier-Stokes, BR1) and cfg 3 with the third-order P-ERK3 family (SURVEY §8(f)
 f1), cfg 4 with indicator-driven AMR instead of the seeded map sequence (`4i`: perk_amr_adapt +
 perk_repartition every 5 steps) and cfg 3 with the alternating / early-shared stage
-patterns (`3alt`, `3early`), so one run shows every config (--extra none skips them).
+patterns (`3alt`, `3early`) and cfg 3 / 5 with subcell shock capturing on a contact
+band (`3sc`, `5sc`), so one run shows every config (--extra none skips them).
 --impl reference times the oracle (oracle/, plain C, 1 host core) on a bounded sample of the same
 workload (full-mesh P-ERK steps, at most ~120 s of CPU work).
 """
@@ -194,14 +195,19 @@ def replica_value(ws, elem_rhs_per_step, ms_max):
     return ws * elem_rhs_per_step / (ms_max * 1e-3)
 
 
-def measure_config(cfg, K, Wm, timer, torch, dist, ws, dev, with_single=True, order=2, amr=False, pattern=None):
+def measure_config(cfg, K, Wm, timer, torch, dist, ws, dev, with_single=True, order=2, amr=False, pattern=None,
+                   sc=False):
     """Device time per P-ERK step of BASELINE config `cfg` (and of the single-rate S-stage P-ERK on
     the same mesh); cfg 4 re-meshes on the device every 5 steps inside the timed steps.  order = 3
     runs the P-ERK3 family with the same S and E (workloads/perk3.py).  amr = True
     (cfg 4) replaces the seeded level-map sequence by the device indicator + controller
-    (perk_amr_adapt) before each repartition."""
+    (perk_amr_adapt) before each repartition.  sc = True switches on the subcell
+    shock capturing and adds a contact band to the IC (workloads.configs)."""
     from paper_2403_05144_b200 import Perk
     w = W.make(cfg)
+    if sc:
+        w.problem = dict(w.problem, shock_capturing=W.configs.SHOCK_CAPTURING)
+        w.ic = W.configs.contact_band(w.ic)
     fam = single_fam = None
     if order == 3:
         from workloads import perk3 as P3
@@ -209,7 +215,7 @@ def measure_config(cfg, K, Wm, timer, torch, dist, ws, dev, with_single=True, or
     perk = Perk(w.problem, w.level_map, w.S, w.E, family=fam, pattern=pattern)
     U = perk.initial_state(w.ic)
     res = {"workload": w.name + ("_perk3" if order == 3 else "") + ("_amr_" + w.meta["amr"]["indicator"] if amr else "")
-           + ("_" + pattern if pattern else ""),
+           + ("_" + pattern if pattern else "") + ("_shock_capturing" if sc else ""),
            "cells": perk.n_cells, "S": w.S, "E": w.E, "order": order, "dt": w.dt}
     if pattern:
         res["pattern"] = pattern
@@ -386,13 +392,14 @@ def run_ours(args):
     if args.extra != "none":
         for item in [x for x in args.extra.split(",") if x]:
             amr = item.endswith("i")
+            sc = item.endswith("sc")
             pattern = {"alt": "alternating", "early": "early"}.get(item.lstrip("0123456789"))
-            c, order = (int(item[:-2]), 3) if item.endswith("p3") else (int(item.rstrip("ialtery")), 2)
+            c, order = (int(item[:-2]), 3) if item.endswith("p3") else (int(item.rstrip("ialterysc")), 2)
             if c == args.config and order == 2 and not amr and not pattern:
                 continue
             try:
                 p2, _U, _w, r2 = measure_config(c, max(5, min(args.steps, 20)), args.warmup, timer, torch, dist,
-                                                 ws, dev, order=order, amr=amr, pattern=pattern)
+                                                 ws, dev, order=order, amr=amr, pattern=pattern, sc=sc)
                 r2["dof_stage_updates_per_s"] = round(r2["value"] * 4 ** _w.problem["dim"], 1)
                 r2["gpu_launches_per_step"] = p2.launches_per_step()
                 p2.close()
@@ -509,7 +516,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--extra", default="1,2,4,4i,5,3p3,3alt,3early",
+    ap.add_argument("--extra", default="1,2,4,4i,5,3p3,3alt,3early,3sc,5sc",
                     help="other BASELINE configs measured into other_configs (comma list, 'Np3' = config N "
                          "with the P-ERK3 family, 'Ni' = config N with indicator-driven AMR, "
                          "'Nalt' / 'Nearly' = config N with the alternating / early-shared stage pattern, or 'none')")

@@ -54,8 +54,9 @@ enum { PERK_KIND_ELEMENTS = 0, PERK_KIND_INTERFACES = 1, PERK_KIND_MORTARS = 2, 
 
 #define PERK_MAX_STAGES 64
 #define PERK_MAX_MEMBERS 8
-#define PERK_NUM_KERNEL_KINDS 6   /* profile slots: 0 surface flux, 1 volume+stage, 2 mesh rebuild, 3 transfer,
-                                    4 BR1 gradient traces, 5 BR1 gradients + viscous-flux traces */
+#define PERK_NUM_KERNEL_KINDS 7   /* profile slots: 0 surface flux, 1 volume+stage, 2 mesh rebuild, 3 transfer,
+                                    4 BR1 gradient traces, 5 BR1 gradients + viscous-flux traces,
+                                    6 shock-capturing blending factors (+ smoothing) */
 
 /* Problem description.  DG degree N = 3 (LGL nodes) is fixed.
  *   dim            1 or 2
@@ -203,6 +204,32 @@ int perk_amr_indicator(perk_ctx *ctx, const double *U_dev, const perk_amr *amr, 
 int perk_amr_adapt(perk_ctx *ctx, const double *U_dev, const perk_amr *amr, uint8_t *level_map_dev);
 /* Number of kernel launches one perk_amr_adapt performs (max_level + 3). */
 int perk_amr_launches(perk_ctx *ctx, int32_t *launches);
+
+/* ---- subcell shock capturing ----
+ * The paper's inviscid applications use the Hennemann-Gassner shock capturing (P:l.964, l.1729,
+ * l.1795-1799; A7-A9): per element and stage the flux-differencing volume integral V_DG is
+ * replaced by (1 - alpha) V_DG + alpha V_FV, V_FV the first-order finite-volume divergence on the
+ * element's LGL subcells (widths w_i h / 2) with the problem's surface flux between neighbouring
+ * nodes.  alpha = alpha_fixed if alpha_fixed >= 0, else the Hennemann-Gassner indicator of
+ * `variable` (PERK_VAR_*) on the element's stage state, 0 below alpha_min, 1 above 1 - alpha_min,
+ * clipped to alpha_max; smooth != 0: alpha_e = max(alpha_e, alpha_n / 2) over face neighbours n.
+ * Each P-ERK stage then launches 2 more kernels (1 without smoothing) before its surface flux. */
+typedef struct perk_shock_capturing {
+    int32_t variable;
+    int32_t smooth;
+    double alpha_max;
+    double alpha_min;
+    double alpha_fixed;
+} perk_shock_capturing;
+
+/* Switch shock capturing on (sc != NULL; parameters copied) or off (sc = NULL) for the following
+ * steps and rhs_eval calls; re-mesh keeps it.  Synchronises the context stream.  EUNSUPPORTED for
+ * 1D / advection problems and non-standard stage patterns; EINVAL for parameters out of range
+ * (0 <= alpha_min <= 1/2, 0 <= alpha_max <= 1, alpha_fixed <= 1, variable in 0..4). */
+int perk_set_shock_capturing(perk_ctx *ctx, const perk_shock_capturing *sc);
+/* Blending factors of the state U_dev (raw indicator and smoothed) into device arrays of >= n_cells
+ * doubles, canonical leaf order.  Asynchronous; EINVAL if shock capturing is off. */
+int perk_sc_alpha(perk_ctx *ctx, const double *U_dev, double *raw_dev, double *smoothed_dev);
 
 /* ---- introspection (synchronising) ---- */
 int perk_num_cells(perk_ctx *ctx, int64_t *n_cells);

@@ -521,13 +521,18 @@ __host__ __device__ constexpr size_t vol2d_smem_bytes(bool ns)
 // so neither the state gather nor the epilogue reads expose memory latency.  (A first version used
 // cp.async.bulk on mbarriers; issuing the per-element bulk copies through the uniform datapath cost
 // about a quarter of the kernel's issue slots.)
-template <int MODE, bool NS>
+//
+// SC (shock capturing, sc.cuh): the element's inviscid volume part becomes (1 - alpha) V_DG + alpha V_FV,
+// V_FV[a] = (F_{a+1/2} - F_{a-1/2}) / w_a along the line with the subcell fluxes F_{a+1/2} = f*(u_a,
+// u_{a+1}) of the problem's surface flux (F_{-1/2} = F_{N+1/2} = 0), evaluated in line coordinates
+// from the primitives the line already holds; alpha = 0 elements skip it.
+template <int MODE, bool NS, bool SC = false>
 __global__ void __launch_bounds__(vol2d_threads(NS), NS ? (VOL2D_EPB_NS == 8 ? 5 : 3) : 3)
 k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                                                  double *__restrict__ Ubuf, double *__restrict__ K1,
                                                  const double *__restrict__ Fs, const double *__restrict__ Uin,
                                                  double *__restrict__ dU, const double *__restrict__ Gs,
-                                                 double *__restrict__ Wb)
+                                                 double *__restrict__ Wb, const double *__restrict__ alpha)
 {
     constexpr int NF = vol2d_nf(NS);          // rho, v_n/2, v_t/2, p/2, ln rho, beta, ln beta (+ T)
     constexpr int EPB = vol2d_epb(NS), LS = vol2d_ls(NS);
@@ -603,6 +608,7 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
         const size_t eb = (size_t)e * 64;
         const double hcell = md.hf * (double)(1 << (md.max_level - pk_level(pk)));
         double2 pre_un[4], pre_k1[4];          // epilogue operands held in registers (EM == 2)
+        const double al = SC ? __ldg(alpha + e) : 0.0;
 
         // phase 1: nodes q0, q0+1 -> primitives + logs, stored in x-line and y-line layouts
         cp_async_wait<0>();
@@ -717,6 +723,28 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                     acc[b][v] = fma(dba, f[v], acc[b][v]);
                 }
             }
+        }
+        if (SC && al != 0.0) {   // blend with the subcell finite-volume divergence
+            double Fp[3][4];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                double uL[4], uR[4];
+                const LinePrim &A = P[a], &B = P[a + 1];
+                const double vnA = 2.0 * A.hvn, vtA = 2.0 * A.hvt, vnB = 2.0 * B.hvn, vtB = 2.0 * B.hvt;
+                uL[0] = A.rho; uL[1] = A.rho * vnA; uL[2] = A.rho * vtA;
+                uL[3] = 2.0 * A.hp * inv_gm1 + 0.5 * A.rho * (vnA * vnA + vtA * vtA);
+                uR[0] = B.rho; uR[1] = B.rho * vnB; uR[2] = B.rho * vtB;
+                uR[3] = 2.0 * B.hp * inv_gm1 + 0.5 * B.rho * (vnB * vnB + vtB * vtB);
+                numflux2d(uL, uR, 0, g, md.surface, Fp[a]);   // line coordinates: normal first
+            }
+            const double bl = 1.0 - al;
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const double fr = a < 3 ? Fp[a][v] : 0.0, fl = a > 0 ? Fp[a - 1][v] : 0.0;
+                    acc[a][v] = fma(al, (fr - fl) * cB.invw[a], bl * acc[a][v]);
+                }
         }
         // NS: + sum_a Dhat_ia F^v(node a) along the line (BR1 gradients recomputed from Gs)
         if (NS) {

@@ -25,6 +25,7 @@
 #include "step1d.cuh"
 #include "transfer.cuh"
 #include "amr.cuh"
+#include "sc.cuh"
 
 using namespace perk;
 
@@ -49,6 +50,10 @@ struct perk_ctx {
     double *Gs = nullptr, *Vt = nullptr;   // BR1 (Navier-Stokes): central w* and viscous-flux traces
     double *Wb = nullptr;                  // P-ERK3: W = U_n + dt (b_1 K_1 + b_{S-1} K_{S-1})
     bool ns = false;
+    bool sc = false;                       // subcell shock capturing (sc.cuh): per-stage alpha, blended volume
+    ScParams scp{};
+    double *alpha_raw = nullptr, *alpha = nullptr;
+    bool halo_alloc = false;               // BR1 / shock-capturing halo lists allocated
     unsigned long long act[MAXR] = {};     // evaluated stages per member (bit i-1), standard or given
     bool std_pattern = true;
     // non-nested stage patterns (2D): per-stage hot arrays [S][capacity] (elements, interfaces,
@@ -287,7 +292,7 @@ static void build_mesh(perk_ctx *c, cudaStream_t s, const uint8_t *lmap)
             k_set_count<<<1, 1, 0, s>>>(ca + KIND_BD * MAXS + i - 1, c->segtmp, 0);
         }
     }
-    if (c->ns) {   // BR1 halo lists (see MeshDev::halo)
+    if (c->halo_alloc) {   // BR1 / shock-capturing halo lists (see MeshDev::halo)
         k_halo_clear<<<blocks_for(c->cap, 256), 256, 0, s>>>(md);
         k_halo_flags<<<blocks_for(c->cap_faces, 256), 256, 0, s>>>(md);
         partition(c, s, KeyHaloEl{md.halo, md.mem}, md.n + 0, 1, c->cap, R, md.hlist[KIND_EL], nullptr,
@@ -384,17 +389,18 @@ static void launch_volume(perk_ctx *c, cudaStream_t s, const StageParams &sp, do
 {
     const MeshDev md = stage_mesh(c, sp);
     if (c->prob.dim == 2) {
-        if (c->ns) {
-            if (sp.mode == MODE_STAGE)
-                launch_pdl(k_vol2d<MODE_STAGE, true>, c->vol_blocks, vol2d_threads(true), vol2d_smem_bytes(true), s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Gs, c->Wb);
-            else
-                launch_pdl(k_vol2d<MODE_RHS, true>, c->vol_blocks, vol2d_threads(true), vol2d_smem_bytes(true), s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Gs, c->Wb);
-        } else {
-            if (sp.mode == MODE_STAGE)
-                launch_pdl(k_vol2d<MODE_STAGE, false>, c->vol_blocks, 128, vol2d_smem_bytes(false), s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, nullptr, c->Wb);
-            else
-                launch_pdl(k_vol2d<MODE_RHS, false>, c->vol_blocks, 128, vol2d_smem_bytes(false), s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, nullptr, c->Wb);
-        }
+        const double *al = c->alpha;
+        const bool st = sp.mode == MODE_STAGE;
+        const int tn = vol2d_threads(c->ns);
+        const size_t sm = vol2d_smem_bytes(c->ns);
+        if (c->ns && c->sc)
+            launch_pdl(st ? k_vol2d<MODE_STAGE, true, true> : k_vol2d<MODE_RHS, true, true>, c->vol_blocks, tn, sm, s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, (const double *)c->Gs, c->Wb, al);
+        else if (c->ns)
+            launch_pdl(st ? k_vol2d<MODE_STAGE, true> : k_vol2d<MODE_RHS, true>, c->vol_blocks, tn, sm, s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, (const double *)c->Gs, c->Wb, al);
+        else if (c->sc)
+            launch_pdl(st ? k_vol2d<MODE_STAGE, false, true> : k_vol2d<MODE_RHS, false, true>, c->vol_blocks, tn, sm, s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, (const double *)nullptr, c->Wb, al);
+        else
+            launch_pdl(st ? k_vol2d<MODE_STAGE, false> : k_vol2d<MODE_RHS, false>, c->vol_blocks, tn, sm, s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, (const double *)nullptr, c->Wb, al);
     } else if (c->nv == 1) {
         if (sp.mode == MODE_STAGE)
             k_vol1d<1, MODE_STAGE><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Wb);
@@ -406,6 +412,24 @@ static void launch_volume(perk_ctx *c, cudaStream_t s, const StageParams &sp, do
         else
             k_vol1d<3, MODE_RHS><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Wb);
     }
+}
+
+// shock capturing (sc.cuh): blending factors of the stage's elements, then neighbour smoothing
+static void launch_sc(perk_ctx *c, cudaStream_t s, const StageParams &sp, const double *Un, const double *Uin, Prof *p)
+{
+    prof_mark(p, s, 6);
+    if (!((c->kind_mask >> 6) & 1u)) return;
+    const int ga = std::min(blocks_for(c->cap, AMR_T / 16), SM_COUNT_B200 * 8);
+    if (sp.mode == MODE_STAGE)
+        launch_pdl(k_sc_alpha<MODE_STAGE>, ga, AMR_T, 0, s, c->md, sp, c->scp, Un, (const double *)c->Ubuf, (const double *)c->K1, Uin, c->alpha_raw, c->alpha);
+    else
+        launch_pdl(k_sc_alpha<MODE_RHS>, ga, AMR_T, 0, s, c->md, sp, c->scp, Un, (const double *)c->Ubuf, (const double *)c->K1, Uin, c->alpha_raw, c->alpha);
+    if (!c->scp.smooth) return;
+    const int gs = std::min(blocks_for(c->cap_faces, 256), SM_COUNT_B200 * 8);
+    if (sp.mode == MODE_STAGE)
+        launch_pdl(k_sc_smooth<MODE_STAGE>, gs, 256, 0, s, c->md, sp, (const double *)c->alpha_raw, c->alpha);
+    else
+        launch_pdl(k_sc_smooth<MODE_RHS>, gs, 256, 0, s, c->md, sp, (const double *)c->alpha_raw, c->alpha);
 }
 
 // BR1 passes (Navier-Stokes): central gradient traces, then gradients + viscous-flux traces
@@ -439,6 +463,7 @@ static void launch_step(perk_ctx *c, cudaStream_t s, double *U, double dt, Prof 
     }
     for (int i = 1; i <= c->tab.S; ++i) {
         const StageParams sp = stage_params(c, i, dt, MODE_STAGE, 0u);
+        if (c->sc) launch_sc(c, s, sp, U, nullptr, p);
         if (c->ns) launch_br1(c, s, sp, U, nullptr, p);
         prof_mark(p, s, 0);
         if ((c->kind_mask >> 0) & 1u) launch_surface(c, s, sp, U, nullptr);
@@ -446,6 +471,23 @@ static void launch_step(perk_ctx *c, cudaStream_t s, double *U, double dt, Prof 
         if ((c->kind_mask >> 1) & 1u) launch_volume(c, s, sp, U, nullptr, nullptr);
         prof_mark(p, s, -1);
     }
+}
+
+// halo lists (MeshDev::halo): BR1 gradients and shock-capturing blending factors of the neighbours
+// of active elements across mortars
+static int alloc_halo(perk_ctx *c)
+{
+    if (c->halo_alloc) return PERK_OK;
+    MeshDev &md = c->md;
+    CU(dalloc(c, &md.halo, c->cap));
+    CU(dalloc(c, &md.hlist[KIND_EL], c->cap));
+    CU(dalloc(c, &md.hlist[KIND_IF], c->cap_faces));
+    CU(dalloc(c, &md.hlist[KIND_MO], c->cap_faces));
+    CU(dalloc(c, &md.hseg, 3 * (MAXR + 1)));
+    CU(dalloc(c, &md.hrng, 3 * MAXS));
+    CU(dalloc(c, &md.hpk, c->cap));
+    c->halo_alloc = true;
+    return PERK_OK;
 }
 
 static int check_device_err(perk_ctx *c)
@@ -633,13 +675,8 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
     CU(dalloc(c, &c->Fs, (size_t)c->cap * (dim == 1 ? 2 * c->nv : 4 * c->nv * NP)));
     if (tab->S >= 3 && tab->b[tab->S - 2] != 0.0) CU(dalloc(c, &c->Wb, (size_t)c->cap * rowd));   // P-ERK3
     if (c->ns) {
-        CU(dalloc(c, &md.halo, c->cap));
-        CU(dalloc(c, &md.hlist[KIND_EL], c->cap));
-        CU(dalloc(c, &md.hlist[KIND_IF], c->cap_faces));
-        CU(dalloc(c, &md.hlist[KIND_MO], c->cap_faces));
-        CU(dalloc(c, &md.hseg, 3 * (MAXR + 1)));
-        CU(dalloc(c, &md.hrng, 3 * MAXS));
-        CU(dalloc(c, &md.hpk, c->cap));
+        rc = alloc_halo(c);
+        if (rc) { *out = c; return rc; }
         CU(dalloc(c, &c->Gs, (size_t)c->cap * 4 * GV * NP));
         CU(dalloc(c, &c->Vt, (size_t)c->cap * 4 * GV * NP));
     }
@@ -660,6 +697,10 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
         CU(cudaFuncSetAttribute(k_vol2d<MODE_RHS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vol2d_smem_bytes(true)));
         CU(cudaFuncSetAttribute(k_vol2d<MODE_STAGE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vol2d_smem_bytes(false)));
         CU(cudaFuncSetAttribute(k_vol2d<MODE_RHS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vol2d_smem_bytes(false)));
+        CU(cudaFuncSetAttribute(k_vol2d<MODE_STAGE, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vol2d_smem_bytes(true)));
+        CU(cudaFuncSetAttribute(k_vol2d<MODE_RHS, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vol2d_smem_bytes(true)));
+        CU(cudaFuncSetAttribute(k_vol2d<MODE_STAGE, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vol2d_smem_bytes(false)));
+        CU(cudaFuncSetAttribute(k_vol2d<MODE_RHS, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vol2d_smem_bytes(false)));
         if (c->ns) CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vol2d<MODE_STAGE, true>, vol2d_threads(true), vol2d_smem_bytes(true)));
         else CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vol2d<MODE_STAGE, false>, vol2d_threads(false), vol2d_smem_bytes(false)));
         const int want = (c->cap + vol2d_epb(c->ns) - 1) / vol2d_epb(c->ns);
@@ -806,7 +847,7 @@ extern "C" int perk_launches_per_step(perk_ctx *c, int32_t *launches)
 {
     if (!c) return PERK_ENOTINIT;
     if (!launches) return PERK_EINVAL;
-    *launches = c->step1d ? 1 : (c->ns ? 4 : 2) * c->tab.S;
+    *launches = c->step1d ? 1 : ((c->ns ? 4 : 2) + (c->sc ? (c->scp.smooth ? 2 : 1) : 0)) * c->tab.S;
     return PERK_OK;
 }
 
@@ -1005,11 +1046,80 @@ extern "C" int perk_amr_launches(perk_ctx *c, int32_t *launches)
     return PERK_OK;
 }
 
+// ----------------------------------------------------------------------------------------------
+// subcell shock capturing (sc.cuh)
+// ----------------------------------------------------------------------------------------------
+extern "C" int perk_set_shock_capturing(perk_ctx *c, const perk_shock_capturing *sc)
+{
+    if (!c) return PERK_ENOTINIT;
+    if (sc) {
+        if (c->prob.dim != 2 || c->prob.equation == PERK_EQ_ADVECTION)
+            return set_err(c, PERK_EUNSUPPORTED, "shock capturing needs a 2D Euler / Navier-Stokes problem");
+        if (!c->std_pattern)
+            return set_err(c, PERK_EUNSUPPORTED, "shock capturing runs the standard stage pattern only (halo needs nesting)");
+        if (sc->variable < 0 || sc->variable > 4 || !(sc->alpha_min >= 0.0 && sc->alpha_min <= 0.5) ||
+            !(sc->alpha_max >= 0.0 && sc->alpha_max <= 1.0) || !(sc->alpha_fixed <= 1.0))
+            return set_err(c, PERK_EINVAL, "need variable in 0..4, 0 <= alpha_min <= 1/2, 0 <= alpha_max <= 1, alpha_fixed <= 1");
+    }
+    // the captured step and re-mesh graphs change shape: capture again on next use
+    CU(cudaStreamSynchronize(c->stream));
+    if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
+    if (c->rexec) { cudaGraphExecDestroy(c->rexec); c->rexec = nullptr; }
+    if (!sc) { c->sc = false; return PERK_OK; }
+    if (!c->alpha) {
+        CU(dalloc(c, &c->alpha_raw, c->cap));
+        CU(dalloc(c, &c->alpha, c->cap));
+    }
+    if (!c->halo_alloc) {   // halo lists of the current mesh (build_mesh keeps them up to date from now on)
+        int rc = alloc_halo(c);
+        if (rc) return rc;
+        const MeshDev &md = c->md;
+        const int R = c->tab.R;
+        cudaStream_t s = c->stream;
+        k_halo_clear<<<blocks_for(c->cap, 256), 256, 0, s>>>(md);
+        k_halo_flags<<<blocks_for(c->cap_faces, 256), 256, 0, s>>>(md);
+        partition(c, s, KeyHaloEl{md.halo, md.mem}, md.n + 0, 1, c->cap, R, md.hlist[KIND_EL], nullptr,
+                  md.hseg + KIND_EL * (MAXR + 1), nullptr, nullptr);
+        partition(c, s, KeyHaloIf{md.ifc, md.halo}, md.n + 1, 1, c->cap_faces, R, md.hlist[KIND_IF], nullptr,
+                  md.hseg + KIND_IF * (MAXR + 1), nullptr, nullptr);
+        partition(c, s, KeyHaloMo{md.mor, md.halo}, md.n + 2, 1, c->cap_faces, R, md.hlist[KIND_MO], nullptr,
+                  md.hseg + KIND_MO * (MAXR + 1), nullptr, nullptr);
+        k_halo_ranges<<<SM_COUNT_B200, 256, 0, s>>>(md, active_desc(c));
+        CU(cudaGetLastError());
+    }
+    c->scp.variable = sc->variable;
+    c->scp.smooth = sc->smooth ? 1 : 0;
+    c->scp.alpha_max = sc->alpha_max;
+    c->scp.alpha_min = sc->alpha_min;
+    c->scp.alpha_fixed = sc->alpha_fixed;
+    c->scp.hg_T = 0.5 * std::pow(10.0, -1.8 * std::pow((double)NP, 0.25));
+    c->scp.hg_sT = std::log((1.0 - 0.0001) / 0.0001) / c->scp.hg_T;
+    c->sc = true;
+    return PERK_OK;
+}
+
+extern "C" int perk_sc_alpha(perk_ctx *c, const double *U, double *raw, double *smoothed)
+{
+    if (!c) return PERK_ENOTINIT;
+    if (!U || !raw || !smoothed) return set_err(c, PERK_EINVAL, "null pointer");
+    if (!c->sc) return set_err(c, PERK_EINVAL, "shock capturing is off");
+    const StageParams sp = stage_params(c, 1, 0.0, MODE_RHS, ~0u);
+    launch_sc(c, c->stream, sp, nullptr, U, nullptr);
+    int64_t n = 0;
+    int rc = perk_num_cells(c, &n);
+    if (rc) return rc;
+    CU(cudaMemcpyAsync(raw, c->alpha_raw, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, c->stream));
+    CU(cudaMemcpyAsync(smoothed, c->alpha, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, c->stream));
+    CU(cudaGetLastError());
+    return PERK_OK;
+}
+
 extern "C" int rhs_eval(perk_ctx *c, const double *U, uint32_t mask, double *dU)
 {
     if (!c) return PERK_ENOTINIT;
     if (!U || !dU) return set_err(c, PERK_EINVAL, "null pointer");
     const StageParams sp = stage_params(c, 1, 0.0, MODE_RHS, mask);
+    if (c->sc) launch_sc(c, c->stream, sp, nullptr, U, nullptr);
     if (c->ns) launch_br1(c, c->stream, sp, nullptr, U, nullptr);
     launch_surface(c, c->stream, sp, nullptr, U);
     launch_volume(c, c->stream, sp, nullptr, U, dU);

@@ -21,7 +21,8 @@ SURF = {"upwind": 0, "rusanov": 1, "hll": 2}
 KIND = {"elements": 0, "interfaces": 1, "mortars": 2, "boundaries": 3}
 ERRORS = {-1: "EINVAL", -2: "EUNBALANCED", -3: "ECAPACITY", -4: "ECUDA", -5: "ENOTINIT", -6: "EUNSUPPORTED"}
 NP = 4
-NKINDS = 6   # PERK_NUM_KERNEL_KINDS: surface, volume+stage, mesh, transfer, BR1 traces, BR1 gradients
+NKINDS = 7   # PERK_NUM_KERNEL_KINDS: surface, volume+stage, mesh, transfer, BR1 traces, BR1 gradients,
+             # shock-capturing blending factors
 
 
 class PerkError(RuntimeError):
@@ -67,6 +68,23 @@ def amr_params(a: dict) -> perk_amr:
     return s
 
 
+class perk_shock_capturing(C.Structure):
+    _fields_ = [("variable", C.c_int32), ("smooth", C.c_int32), ("alpha_max", C.c_double),
+                ("alpha_min", C.c_double), ("alpha_fixed", C.c_double)]
+
+
+def sc_params(sc: dict) -> perk_shock_capturing:
+    """problem["shock_capturing"]: variable (AMR variable name, default rho_p), alpha_max (0.5), alpha_min
+    (0.001), smooth (True), alpha_fixed (None = the Hennemann-Gassner indicator)"""
+    s = perk_shock_capturing()
+    s.variable = AMR_VARIABLE[sc.get("variable", "rho_p")]
+    s.smooth = int(bool(sc.get("smooth", True)))
+    s.alpha_max, s.alpha_min = sc.get("alpha_max", 0.5), sc.get("alpha_min", 0.001)
+    af = sc.get("alpha_fixed")
+    s.alpha_fixed = -1.0 if af is None else float(af)
+    return s
+
+
 _lib = None
 
 
@@ -107,6 +125,8 @@ def lib():
         L.perk_amr_indicator.argtypes = [P, P, C.POINTER(perk_amr), P]
         L.perk_amr_adapt.argtypes = [P, P, C.POINTER(perk_amr), P]
         L.perk_amr_launches.argtypes = [P, C.POINTER(i32)]
+        L.perk_set_shock_capturing.argtypes = [P, C.POINTER(perk_shock_capturing)]
+        L.perk_sc_alpha.argtypes = [P, P, P, P]
         _lib = L
     return _lib
 
@@ -116,7 +136,8 @@ def exported_symbols():
             "perk_run_host", "perk_repartition", "rhs_eval", "perk_num_cells", "perk_num_faces", "perk_node_coords",
             "perk_get_leaves", "perk_get_faces", "perk_get_list", "perk_get_count_active", "perk_get_counters",
             "perk_sync", "perk_last_error", "perk_profile_step", "perk_time_kernels", "perk_profile_repartition",
-            "perk_launches_per_step", "perk_amr_indicator", "perk_amr_adapt", "perk_amr_launches"]
+            "perk_launches_per_step", "perk_amr_indicator", "perk_amr_adapt", "perk_amr_launches",
+            "perk_set_shock_capturing", "perk_sc_alpha"]
 
 
 def pattern_mask(S: int, E: int, pattern) -> int:
@@ -247,6 +268,21 @@ class Perk:
                 lib().perk_destroy(h)
                 self.h = None
             raise PerkError(rc, msg)
+        if problem.get("shock_capturing") is not None:
+            self.set_shock_capturing(problem["shock_capturing"])
+
+    def set_shock_capturing(self, sc):
+        """sc: dict (see sc_params) or None (off)"""
+        self._sc = None if sc is None else sc_params(sc)
+        _check(self.h, lib().perk_set_shock_capturing(self.h, None if sc is None else C.byref(self._sc)))
+
+    def sc_alpha(self, U):
+        """shock-capturing blending factors of U: (raw, smoothed) device tensors of n_cells doubles"""
+        raw = self.torch.zeros(self.max_cells, dtype=self.torch.float64, device="cuda")
+        sm = self.torch.zeros(self.max_cells, dtype=self.torch.float64, device="cuda")
+        _check(self.h, lib().perk_sc_alpha(self.h, _ptr(U), _ptr(raw), _ptr(sm)))
+        n = self.n_cells
+        return raw[:n], sm[:n]
 
     def _to_dev_u8(self, level_map):
         torch = self.torch

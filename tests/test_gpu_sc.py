@@ -1,0 +1,183 @@
+"""GPU parity of the subcell shock capturing (sc.cuh + k_vol2d<., ., true>) against
+the oracle (perk_oracle.c section 9, pinned by tests/test_oracle_sc.py) on identical seeded states.
+
+* blending factors (raw and smoothed) per leaf, and rhs_eval for every partition mask, Euler and
+  Navier-Stokes, HLL and Rusanov, indicator-driven and fixed alpha (0.5, 1), mortar meshes;
+* P-ERK steps (stage-wise alpha on the lazy / buffered stage states, the halo across mortars)
+  with a contact discontinuity that switches the blending on in a band of elements: cfg-3 and
+  cfg-5 structures, a P-ERK3 family, the full cfg-3 mesh, and repartition cycles;
+* launch counts, on / off switching (off again equals the unblended path bitwise), error codes.
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import oracle as O
+from oracle import tableau as T
+from gpu_util import TOL, build_pair, compare_mesh, gpu_state_numpy, rel_err_per_var
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+SC = W.configs.SHOCK_CAPTURING
+
+
+def _with_sc(w, sc=SC, surface=None):
+    p = dict(w.problem)
+    p["shock_capturing"] = sc
+    if surface:
+        p["surface"] = surface
+    return p
+
+
+def _jump_ic(ic):
+    return W.configs.contact_band(ic)
+
+
+def _pair(w, problem, max_cells=None):
+    return build_pair(w, problem=problem, max_cells=max_cells)
+
+
+def _to_dev(gpu, Uo):
+    Ug = gpu.alloc_state()
+    Ug[: Uo.shape[0]] = torch.from_numpy(np.ascontiguousarray(Uo)).cuda()
+    return Ug
+
+
+def _run_both(w, ora, gpu, steps, ic):
+    Uo = ora.initial_state(ic)
+    Ug = gpu.initial_state(ic)
+    ora.step(Uo, w.dt, steps)
+    gpu.step(Ug, w.dt, steps)
+    torch.cuda.synchronize()
+    return Uo, gpu_state_numpy(gpu, Ug)
+
+
+@pytest.mark.parametrize("cfg,sc,surface", [
+    (3, SC, None), (3, dict(SC, smooth=False), None), (3, dict(SC, alpha_fixed=1.0), None),
+    (3, dict(SC, alpha_fixed=0.5), "rusanov"), (3, dict(SC, variable="rho", alpha_max=1.0), "rusanov"),
+    (5, SC, None), (5, dict(SC, alpha_fixed=1.0), None)])
+def test_alpha_and_rhs_eval_masks(cfg, sc, surface):
+    w = W.make(cfg, n_base=16)
+    ora, gpu = _pair(w, _with_sc(w, sc, surface))
+    assert ora.face_counts()["mortars"] > 0
+    ic = _jump_ic(w.ic)
+    Uo = ora.initial_state(ic)
+    Ug = _to_dev(gpu, Uo)
+    ro, so = ora.sc_alpha(Uo)
+    rg, sg = gpu.sc_alpha(Ug)
+    rg, sg = rg.cpu().numpy(), sg.cpu().numpy()
+    assert np.max(np.abs(rg - ro)) <= 1e-12 and np.max(np.abs(sg - so)) <= 1e-12
+    if sc.get("alpha_fixed") is None:
+        assert 0 < np.count_nonzero(so) < ora.n          # blended and pure-DG elements
+    R = len(w.E)
+    for mask in sorted({(1 << R) - 1, 1, 1 << (R - 1), ((1 << R) - 1) ^ 1}):
+        dUo = ora.rhs(Uo, mask)
+        dUg = gpu.rhs(Ug, mask)
+        torch.cuda.synchronize()
+        assert rel_err_per_var(gpu_state_numpy(gpu, dUg), dUo).max() <= TOL, mask
+
+
+def test_cfg3_structure_steps():
+    w = W.make(3, n_base=16)
+    ora, gpu = _pair(w, _with_sc(w))
+    Uo, Ug = _run_both(w, ora, gpu, 40, _jump_ic(w.ic))
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
+    _, sm = ora.sc_alpha(Uo)
+    assert 0 < np.count_nonzero(sm) < ora.n
+
+
+def test_cfg5_structure_steps():
+    w = W.make(5, n_base=16)
+    ora, gpu = _pair(w, _with_sc(w))
+    Uo, Ug = _run_both(w, ora, gpu, 20, _jump_ic(w.ic))
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
+
+
+def test_perk3_family_steps():
+    from workloads import perk3
+    from paper_2403_05144_b200 import Perk
+    w = W.make(3, n_base=16)
+    fam3 = perk3.family3(16, (4, 8, 16))
+    p = _with_sc(w)
+    ora = O.OracleMesh(p, w.level_map, fam3)
+    gpu = Perk(p, w.level_map, fam3["S"], fam3["E"], family=fam3, max_cells=p["max_cells"])
+    Uo, Ug = _run_both(w, ora, gpu, 20, _jump_ic(w.ic))
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
+
+
+def test_full_cfg3_mesh_steps():
+    """BASELINE cfg-3 mesh (62,932 cells), bench launch configuration, 2 steps"""
+    w = W.make(3)
+    ora, gpu = _pair(w, _with_sc(w))
+    Uo, Ug = _run_both(w, ora, gpu, 2, _jump_ic(w.ic))
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
+
+
+def test_repartition_cycles():
+    w = W.make(4, n_base=16, max_level=3, widths=(0.3, 0.15, 0.06))
+    w.S, w.E = 16, [4, 6, 10, 16]
+    fam = T.family(w.S, w.E, "taylor")
+    p = _with_sc(w)
+    ora, gpu = build_pair(w, problem=p, max_cells=4 * W.configs.count_leaves(w))
+    ic = _jump_ic(w.ic)
+    Uo = ora.initial_state(ic)
+    Ug = gpu.initial_state(ic)
+    for k in range(1, 4):
+        ora.step(Uo, w.dt, 5)
+        gpu.step(Ug, w.dt, 5)
+        lm = w.level_map_seq(k)
+        new = O.OracleMesh(p, lm, fam)
+        Uo = O.transfer(ora, new, Uo)
+        ora = new
+        gpu.repartition(lm, Ug)
+        gpu.sync()
+        compare_mesh(ora, gpu)
+        assert rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo).max() <= TOL
+    ora.step(Uo, w.dt, 5)
+    gpu.step(Ug, w.dt, 5)
+    torch.cuda.synchronize()
+    assert rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo).max() <= TOL
+
+
+def test_switch_on_off_and_launch_counts():
+    w = W.make(3, n_base=8)
+    ora, gpu = build_pair(w)
+    ic = _jump_ic(w.ic)
+    U0 = gpu.initial_state(ic)
+    base = gpu.launches_per_step()
+    a = U0.clone()
+    gpu.step(a, w.dt, 3)
+    gpu.set_shock_capturing(SC)
+    assert gpu.launches_per_step() == base + 2 * w.S
+    gpu.set_shock_capturing(dict(SC, smooth=False))
+    assert gpu.launches_per_step() == base + w.S
+    b = U0.clone()
+    gpu.step(b, w.dt, 3)
+    gpu.set_shock_capturing(None)
+    assert gpu.launches_per_step() == base
+    c = U0.clone()
+    gpu.step(c, w.dt, 3)
+    torch.cuda.synchronize()
+    assert torch.equal(a, c)                 # off again: bitwise the unblended path
+    assert not torch.equal(a, b)
+
+
+def test_error_codes():
+    from paper_2403_05144_b200 import Perk, PerkError
+    w = W.make(3, n_base=8)
+    gpu = Perk(w.problem, w.level_map, w.S, w.E)
+    with pytest.raises(PerkError):
+        gpu.set_shock_capturing(dict(SC, alpha_max=1.5))
+    with pytest.raises(PerkError):
+        gpu.set_shock_capturing(dict(SC, alpha_min=0.7))
+    w1 = W.make(2, n_base=64, w1=16, w2=4, steps=10)
+    g1 = Perk(w1.problem, w1.level_map, w1.S, w1.E)
+    with pytest.raises(PerkError):
+        g1.set_shock_capturing(SC)
+    ga = Perk(w.problem, w.level_map, w.S, w.E, pattern="alternating")
+    with pytest.raises(PerkError):
+        ga.set_shock_capturing(SC)

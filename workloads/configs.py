@@ -377,3 +377,24 @@ def make(cfg: int, seed: int = 0, **kw) -> Workload:
 
 def count_leaves(w: Workload) -> int:
     return _count_leaves(w.level_map, w.problem["max_level"])
+
+
+# ----------------------------------------------------------------------------
+# shock-capturing inputs: a contact discontinuity on top of a workload's IC, so
+# that the Hennemann-Gassner blending switches on in a band of elements (the paper's shock-capturing
+# runs, P:l.1720-1731, start from discontinuous data)
+# ----------------------------------------------------------------------------
+SHOCK_CAPTURING = {"variable": "rho_p", "alpha_max": 0.5, "alpha_min": 0.001, "smooth": True}
+
+
+def contact_band(ic, x0=0.35, width=0.12, factor=2.5, gamma=GAMMA):
+    """2D IC wrapper: density x `factor` where |s - x0| < width, s = the x coordinate rescaled to
+    [0, 1] over the nodes passed in; velocity and pressure unchanged"""
+    def f(x, y):
+        U = np.asarray(ic(x, y), np.float64)
+        rho, vx, vy = U[0], U[1] / U[0], U[2] / U[0]
+        p = (gamma - 1) * (U[3] - 0.5 * rho * (vx * vx + vy * vy))
+        s = (x - x.min()) / (x.max() - x.min())
+        rho = rho * np.where(np.abs(s - x0) < width, factor, 1.0)
+        return np.stack([rho, rho * vx, rho * vy, p / (gamma - 1) + 0.5 * rho * (vx * vx + vy * vy)])
+    return f
