@@ -213,7 +213,8 @@ int perk_amr_launches(perk_ctx *ctx, int32_t *launches);
  * nodes.  alpha = alpha_fixed if alpha_fixed >= 0, else the Hennemann-Gassner indicator of
  * `variable` (PERK_VAR_*) on the element's stage state, 0 below alpha_min, 1 above 1 - alpha_min,
  * clipped to alpha_max; smooth != 0: alpha_e = max(alpha_e, alpha_n / 2) over face neighbours n.
- * Each P-ERK stage then launches 2 more kernels (1 without smoothing) before its surface flux. */
+ * Each P-ERK stage then launches 1 more kernel (the blending factors) before its surface flux, which
+ * also applies the smoothing (env PERK_SC_FUSED=0 at this call: a separate smoothing launch). */
 typedef struct perk_shock_capturing {
     int32_t variable;
     int32_t smooth;

@@ -204,11 +204,19 @@ __device__ __forceinline__ void store_face2d(double *Fs, int e, int face, int k,
 #ifndef SURF2D_MINB
 #define SURF2D_MINB 3
 #endif
-template <int MODE, bool NS>
+// SCS: the shock-capturing neighbour smoothing (sc.cuh) rides along: lane k = 0 of every interface /
+// mortar raises alpha of both sides to half the other side's raw value (k_sc_alpha ran before).
+__device__ __forceinline__ void sc_amax(double *p, double v)
+{
+    atomicMax(reinterpret_cast<unsigned long long *>(p), (unsigned long long)__double_as_longlong(v));
+}
+
+template <int MODE, bool NS, bool SCS = false>
 __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StageParams sp, const double *__restrict__ Un,
                                                const double *__restrict__ Ubuf, const double *__restrict__ K1,
                                                const double *__restrict__ Uin, double *__restrict__ Fs,
-                                               const double *__restrict__ Vt)
+                                               const double *__restrict__ Vt, const double *__restrict__ alpha_raw,
+                                               double *alpha)
 {
     int nif, nmo, nbd;
     if (MODE == MODE_STAGE) {
@@ -255,6 +263,14 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
         store_face2d(Fs, Ia.y, 2 * Ia.z + 1, ka, fa);
         store_face2d(Fs, Ib.x, 2 * Ib.z, kb, fb);
         store_face2d(Fs, Ib.y, 2 * Ib.z + 1, kb, fb);
+        if (SCS && ka == 0) {
+            sc_amax(alpha + Ia.x, 0.5 * __ldg(alpha_raw + Ia.y));
+            sc_amax(alpha + Ia.y, 0.5 * __ldg(alpha_raw + Ia.x));
+        }
+        if (SCS && kb == 0) {
+            sc_amax(alpha + Ib.x, 0.5 * __ldg(alpha_raw + Ib.y));
+            sc_amax(alpha + Ib.y, 0.5 * __ldg(alpha_raw + Ib.x));
+        }
     }
     for (; gt < total; gt += GS) {
         const int item = gt >> 2, k = gt & 3;
@@ -274,6 +290,10 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
             }
             store_face2d(Fs, I.x, 2 * o, k, fl);
             store_face2d(Fs, I.y, 2 * o + 1, k, fl);
+            if (SCS && k == 0) {
+                sc_amax(alpha + I.x, 0.5 * __ldg(alpha_raw + I.y));
+                sc_amax(alpha + I.y, 0.5 * __ldg(alpha_raw + I.x));
+            }
         } else if (item < nif + nmo) {
             const int q = item - nif;
             const int4 M = MODE == MODE_STAGE ? md.mors[q] : md.mor[q];
@@ -339,6 +359,12 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
                 }
             }
             store_face2d(Fs, M.x, lf, k, fl);
+            if (SCS && k == 0) {
+                const double al = 0.5 * __ldg(alpha_raw + M.x);
+                sc_amax(alpha + M.x, 0.5 * fmax(__ldg(alpha_raw + M.y), __ldg(alpha_raw + M.z)));
+                sc_amax(alpha + M.y, al);
+                sc_amax(alpha + M.z, al);
+            }
         } else {
             const int q = item - nif - nmo;
             const int bi = MODE == MODE_STAGE ? md.list[KIND_BD][q] : q;

@@ -54,6 +54,7 @@ struct perk_ctx {
     ScParams scp{};
     double *alpha_raw = nullptr, *alpha = nullptr;
     bool halo_alloc = false;               // BR1 / shock-capturing halo lists allocated
+    bool sc_fused = true;                  // smoothing inside k_surf2d (PERK_SC_FUSED=0: k_sc_smooth launch)
     unsigned long long act[MAXR] = {};     // evaluated stages per member (bit i-1), standard or given
     bool std_pattern = true;
     // non-nested stage patterns (2D): per-stage hot arrays [S][capacity] (elements, interfaces,
@@ -361,17 +362,19 @@ static void launch_surface(perk_ctx *c, cudaStream_t s, const StageParams &sp, c
 {
     const MeshDev md = stage_mesh(c, sp);
     if (c->prob.dim == 2) {
-        if (c->ns) {
-            if (sp.mode == MODE_STAGE)
-                launch_pdl(k_surf2d<MODE_STAGE, true>, c->surf_blocks, 256, 0, s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs, c->Vt);
-            else
-                launch_pdl(k_surf2d<MODE_RHS, true>, c->surf_blocks, 256, 0, s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs, c->Vt);
-        } else {
-            if (sp.mode == MODE_STAGE)
-                launch_pdl(k_surf2d<MODE_STAGE, false>, c->surf_blocks, 256, 0, s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs, nullptr);
-            else
-                launch_pdl(k_surf2d<MODE_RHS, false>, c->surf_blocks, 256, 0, s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs, nullptr);
-        }
+        const bool st = sp.mode == MODE_STAGE;
+        const bool scs = c->sc && c->scp.smooth && c->sc_fused;   // shock-capturing smoothing rides along
+        const double *vt = c->ns ? c->Vt : nullptr;
+        const double *ar = c->alpha_raw;
+        double *al = c->alpha;
+        if (c->ns && scs)
+            launch_pdl(st ? k_surf2d<MODE_STAGE, true, true> : k_surf2d<MODE_RHS, true, true>, c->surf_blocks, 256, 0, s, md, sp, Un, (const double *)c->Ubuf, (const double *)c->K1, Uin, c->Fs, vt, ar, al);
+        else if (c->ns)
+            launch_pdl(st ? k_surf2d<MODE_STAGE, true> : k_surf2d<MODE_RHS, true>, c->surf_blocks, 256, 0, s, md, sp, Un, (const double *)c->Ubuf, (const double *)c->K1, Uin, c->Fs, vt, ar, al);
+        else if (scs)
+            launch_pdl(st ? k_surf2d<MODE_STAGE, false, true> : k_surf2d<MODE_RHS, false, true>, c->surf_blocks, 256, 0, s, md, sp, Un, (const double *)c->Ubuf, (const double *)c->K1, Uin, c->Fs, vt, ar, al);
+        else
+            launch_pdl(st ? k_surf2d<MODE_STAGE, false> : k_surf2d<MODE_RHS, false>, c->surf_blocks, 256, 0, s, md, sp, Un, (const double *)c->Ubuf, (const double *)c->K1, Uin, c->Fs, vt, ar, al);
     } else if (c->nv == 1) {
         if (sp.mode == MODE_STAGE)
             k_surf1d<1, MODE_STAGE><<<c->surf_blocks, 256, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, Uin, c->Fs);
@@ -415,7 +418,8 @@ static void launch_volume(perk_ctx *c, cudaStream_t s, const StageParams &sp, do
 }
 
 // shock capturing (sc.cuh): blending factors of the stage's elements, then neighbour smoothing
-static void launch_sc(perk_ctx *c, cudaStream_t s, const StageParams &sp, const double *Un, const double *Uin, Prof *p)
+static void launch_sc(perk_ctx *c, cudaStream_t s, const StageParams &sp, const double *Un, const double *Uin, Prof *p,
+                      bool smooth_kernel = false)
 {
     prof_mark(p, s, 6);
     if (!((c->kind_mask >> 6) & 1u)) return;
@@ -424,7 +428,7 @@ static void launch_sc(perk_ctx *c, cudaStream_t s, const StageParams &sp, const 
         launch_pdl(k_sc_alpha<MODE_STAGE>, ga, AMR_T, 0, s, c->md, sp, c->scp, Un, (const double *)c->Ubuf, (const double *)c->K1, Uin, c->alpha_raw, c->alpha);
     else
         launch_pdl(k_sc_alpha<MODE_RHS>, ga, AMR_T, 0, s, c->md, sp, c->scp, Un, (const double *)c->Ubuf, (const double *)c->K1, Uin, c->alpha_raw, c->alpha);
-    if (!c->scp.smooth) return;
+    if (!c->scp.smooth || (c->sc_fused && !smooth_kernel)) return;   // fused: k_surf2d smooths
     const int gs = std::min(blocks_for(c->cap_faces, 256), SM_COUNT_B200 * 8);
     if (sp.mode == MODE_STAGE)
         launch_pdl(k_sc_smooth<MODE_STAGE>, gs, 256, 0, s, c->md, sp, (const double *)c->alpha_raw, c->alpha);
@@ -847,7 +851,7 @@ extern "C" int perk_launches_per_step(perk_ctx *c, int32_t *launches)
 {
     if (!c) return PERK_ENOTINIT;
     if (!launches) return PERK_EINVAL;
-    *launches = c->step1d ? 1 : ((c->ns ? 4 : 2) + (c->sc ? (c->scp.smooth ? 2 : 1) : 0)) * c->tab.S;
+    *launches = c->step1d ? 1 : ((c->ns ? 4 : 2) + (c->sc ? ((c->scp.smooth && !c->sc_fused) ? 2 : 1) : 0)) * c->tab.S;
     return PERK_OK;
 }
 
@@ -1087,6 +1091,8 @@ extern "C" int perk_set_shock_capturing(perk_ctx *c, const perk_shock_capturing 
         k_halo_ranges<<<SM_COUNT_B200, 256, 0, s>>>(md, active_desc(c));
         CU(cudaGetLastError());
     }
+    const char *fenv = std::getenv("PERK_SC_FUSED");
+    c->sc_fused = !(fenv && fenv[0] == '0');
     c->scp.variable = sc->variable;
     c->scp.smooth = sc->smooth ? 1 : 0;
     c->scp.alpha_max = sc->alpha_max;
@@ -1104,7 +1110,7 @@ extern "C" int perk_sc_alpha(perk_ctx *c, const double *U, double *raw, double *
     if (!U || !raw || !smoothed) return set_err(c, PERK_EINVAL, "null pointer");
     if (!c->sc) return set_err(c, PERK_EINVAL, "shock capturing is off");
     const StageParams sp = stage_params(c, 1, 0.0, MODE_RHS, ~0u);
-    launch_sc(c, c->stream, sp, nullptr, U, nullptr);
+    launch_sc(c, c->stream, sp, nullptr, U, nullptr, true);
     int64_t n = 0;
     int rc = perk_num_cells(c, &n);
     if (rc) return rc;

@@ -11,9 +11,12 @@
 //                 neighbours across active mortars (the BR1 halo lists, mesh.cuh) -- from the
 //                 element's stage state (U_n, the stage buffer, or U_n + dt c_i K_1 formed on the
 //                 fly); writes alpha_raw and alpha
-//   k_sc_smooth : alpha_e = max(alpha_e, alpha_raw_n / 2) over the stage's active interfaces and
-//                 mortars (atomicMax on the fp64 bit pattern, exact for alpha >= 0); every face of an
-//                 active element is active, so every active element sees all its neighbours
+//   smoothing   : alpha_e = max(alpha_e, alpha_raw_n / 2) over the stage's active interfaces and
+//                 mortars (atomicMax on the fp64 bit pattern, exact for alpha >= 0, so the result does
+//                 not depend on the order); every face of an active element is active, so every
+//                 active element sees all its neighbours.  Done by lane 0 of each face inside
+//                 k_surf2d<., ., true> (no extra launch); k_sc_smooth is the stand-alone version
+//                 (PERK_SC_FUSED=0, used by the tests to cross-check the fused one bitwise)
 #pragma once
 #include "common.cuh"
 #include "amr.cuh"

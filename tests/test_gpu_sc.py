@@ -8,6 +8,8 @@ the oracle (perk_oracle.c section 9, pinned by tests/test_oracle_sc.py) on ident
   cfg-5 structures, a P-ERK3 family, the full cfg-3 mesh, and repartition cycles;
 * launch counts, on / off switching (off again equals the unblended path bitwise), error codes.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -152,11 +154,21 @@ def test_switch_on_off_and_launch_counts():
     a = U0.clone()
     gpu.step(a, w.dt, 3)
     gpu.set_shock_capturing(SC)
-    assert gpu.launches_per_step() == base + 2 * w.S
-    gpu.set_shock_capturing(dict(SC, smooth=False))
-    assert gpu.launches_per_step() == base + w.S
+    assert gpu.launches_per_step() == base + w.S      # blending factors; smoothing inside k_surf2d
     b = U0.clone()
     gpu.step(b, w.dt, 3)
+    os.environ["PERK_SC_FUSED"] = "0"                 # stand-alone smoothing kernel
+    try:
+        gpu.set_shock_capturing(SC)
+    finally:
+        del os.environ["PERK_SC_FUSED"]
+    assert gpu.launches_per_step() == base + 2 * w.S
+    b2 = U0.clone()
+    gpu.step(b2, w.dt, 3)
+    gpu.set_shock_capturing(dict(SC, smooth=False))
+    assert gpu.launches_per_step() == base + w.S
+    torch.cuda.synchronize()
+    assert torch.equal(b, b2)                 # atomicMax smoothing: order-independent, bitwise equal
     gpu.set_shock_capturing(None)
     assert gpu.launches_per_step() == base
     c = U0.clone()

@@ -2,7 +2,7 @@
 cfg 1, 2 (1D, single-CTA step and the two-launch path), cfg 3 structure (2D Euler, mortars), a
 non-periodic 2D variant (boundary faces), cfg 5 structure (BR1), rhs_eval with masks, a cfg-4
 structure with two device re-meshes and device AMR adaptations (three indicators), stage patterns
-(alternating, non-nested), Heun weights and a P-ERK3 family."""
+(alternating, non-nested), Heun weights, a P-ERK3 family and subcell shock capturing."""
 import os
 import sys
 
@@ -54,4 +54,17 @@ run(w3, 2, pattern=[[1, 5, 9, 16], [1, 2, 4, 6, 8, 10, 12, 16], "standard"], c_S
 run(W.make(2, n_base=512), 2, pattern="early")
 from workloads import perk3 as P3  # noqa: E402
 run(w3, 2, family=P3.family3(w3.S, w3.E))
+# subcell shock capturing (fused and stand-alone smoothing), Euler + NS, with re-meshes
+SC = W.configs.SHOCK_CAPTURING
+w3j = W.make(3, n_base=8)
+w3j.ic = W.configs.contact_band(w3j.ic)
+run(w3j, 2, problem=dict(w3j.problem, shock_capturing=SC))
+os.environ["PERK_SC_FUSED"] = "0"
+run(w3j, 2, problem=dict(w3j.problem, shock_capturing=SC))
+del os.environ["PERK_SC_FUSED"]
+w5j = W.make(5, n_base=8)
+w5j.ic = W.configs.contact_band(w5j.ic)
+run(w5j, 2, problem=dict(w5j.problem, shock_capturing=dict(SC, alpha_fixed=1.0)))
+w4.ic = W.configs.contact_band(w4.ic)
+run(w4, 2, problem=dict(w4.problem, shock_capturing=SC), remesh=True)
 print("sanitize run ok")
