@@ -39,7 +39,7 @@
  */
 #include <math.h>
 #include <stdint.h>
-/* Optional OpenMP (oracle.build(omp=True), only for long full-run parity checks): every parallel loop
+/* Optional OpenMP (ORACLE_OMP=1 -> liboracle_omp.so, only for long full-run parity checks): every parallel loop
    below writes disjoint per-element / per-face-slot outputs and has no reduction, so the results are
    bitwise identical for any thread count; the default build has no -fopenmp and runs
    the same loops serially. */

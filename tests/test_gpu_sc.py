@@ -72,7 +72,7 @@ def test_alpha_and_rhs_eval_masks(cfg, sc, surface):
     ro, so = ora.sc_alpha(Uo)
     rg, sg = gpu.sc_alpha(Ug)
     rg, sg = rg.cpu().numpy(), sg.cpu().numpy()
-    assert np.max(np.abs(rg - ro)) <= 1e-12 and np.max(np.abs(sg - so)) <= 1e-12
+    assert np.max(np.abs(rg - ro)) <= TOL and np.max(np.abs(sg - so)) <= TOL
     if sc.get("alpha_fixed") is None:
         assert 0 < np.count_nonzero(so) < ora.n          # blended and pure-DG elements
     R = len(w.E)
