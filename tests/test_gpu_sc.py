@@ -75,12 +75,19 @@ def test_alpha_and_rhs_eval_masks(cfg, sc, surface):
     assert np.max(np.abs(rg - ro)) <= TOL and np.max(np.abs(sg - so)) <= TOL
     if sc.get("alpha_fixed") is None:
         assert 0 < np.count_nonzero(so) < ora.n          # blended and pure-DG elements
+    # masked RHS errors are measured on the scale of the full F per variable: a masked subset can
+    # have a RHS many orders below the terms that cancel in it (cfg 5, finest member only: max |d rho|
+    # 7e-6 against max |F_rho| 463; a 1e-15 relative perturbation of U moves it by 1.6e-6 of its own
+    # maximum in the oracle alone), A8
     R = len(w.E)
+    Fo = ora.rhs(Uo)
+    scale = np.abs(Fo).max(axis=(0, 2))
     for mask in sorted({(1 << R) - 1, 1, 1 << (R - 1), ((1 << R) - 1) ^ 1}):
         dUo = ora.rhs(Uo, mask)
-        dUg = gpu.rhs(Ug, mask)
+        dUg = gpu_state_numpy(gpu, gpu.rhs(Ug, mask))
         torch.cuda.synchronize()
-        assert rel_err_per_var(gpu_state_numpy(gpu, dUg), dUo).max() <= TOL, mask
+        err = np.abs(dUg - dUo).max(axis=(0, 2)) / scale
+        assert err.max() <= TOL, (mask, err)
 
 
 def test_cfg3_structure_steps():

@@ -2,7 +2,7 @@
 contact-band IC, P-ERK step time with and without shock capturing (CUDA events on the context
 stream, L2 flushed between steps), the per-kind split of one eager step, the device time of the
 kernel kinds alone (perk_time_kernels: 1 volume, 0 surface, 6 blending factors), and the fraction
-of blended elements.  `--ncu`: a few steps only (for an ncu launch list / --set full capture)."""
+of blended elements.  `--ncu`: 3 steps with shock capturing on only (for an ncu launch list / --set full capture)."""
 import json
 import os
 import sys
@@ -44,6 +44,8 @@ def main():
         res = {}
         for name, sc in [("off", None), ("on", W.configs.SHOCK_CAPTURING),
                          ("alpha_fixed_1", dict(W.configs.SHOCK_CAPTURING, alpha_fixed=1.0))]:
+            if ncu and name != "on":
+                continue
             prob = dict(w.problem) if sc is None else dict(w.problem, shock_capturing=sc)
             p = Perk(prob, w.level_map, w.S, w.E)
             U = p.initial_state(ic)
