@@ -334,8 +334,9 @@ def run_ours(args):
     # per-kernel device time: CUDA events around graph replays that contain only that kernel kind's
     # launches of a step, launched exactly as perk_step launches them (perk_time_kernels); the eager
     # numbers (events around every individual launch) include ~5 us of launch path per kernel
+    from paper_2403_05144_b200.perk import NKINDS
     prof_steps = 3
-    ms_e = np.zeros(6)
+    ms_e = np.zeros(NKINDS)
     U0 = perk.initial_state(w.ic)
     Up = U0.clone()
     for _ in range(prof_steps):
@@ -343,7 +344,7 @@ def run_ours(args):
         ms_e += np.array(m_)
     ms_e /= prof_steps
     kinds = [0, 1] + ([4, 5] if w.problem["equation"] == "navier_stokes" else [])
-    ms_k = np.zeros(6)
+    ms_k = np.zeros(NKINDS)
     for k in kinds:
         ms_k[k] = perk.time_kernels(U0.clone(), w.dt, [k], reps=10)
     ms_all = perk.time_kernels(U0.clone(), w.dt, kinds, reps=10)

@@ -423,7 +423,7 @@ static void launch_sc(perk_ctx *c, cudaStream_t s, const StageParams &sp, const 
 {
     prof_mark(p, s, 6);
     if (!((c->kind_mask >> 6) & 1u)) return;
-    const int ga = std::min(blocks_for(c->cap, AMR_T / 16), SM_COUNT_B200 * 8);
+    const int ga = std::min(blocks_for(c->cap, AMR_T / 16), SM_COUNT_B200 * 4);   // persistent: 4 CTAs per SM
     if (sp.mode == MODE_STAGE)
         launch_pdl(k_sc_alpha<MODE_STAGE>, ga, AMR_T, 0, s, c->md, sp, c->scp, Un, (const double *)c->Ubuf, (const double *)c->K1, Uin, c->alpha_raw, c->alpha);
     else

@@ -6,8 +6,8 @@
 // in k_vol2d<., ., true> (per node line, from the primitives it already holds in shared memory);
 // this file computes alpha per stage, before the stage's surface and volume launches:
 //
-//   k_sc_alpha  : Hennemann-Gassner indicator (amr.cuh, the same modal energy and logistic as the
-//                 AMR indicator) on the elements the stage needs -- the active elements and their
+//   k_sc_alpha  : Hennemann-Gassner indicator (the modal energy and logistic of the AMR indicator,
+//                 amr.cuh / DESIGN.md A1) on the elements the stage needs -- the active elements and their
 //                 neighbours across active mortars (the BR1 halo lists, mesh.cuh) -- from the
 //                 element's stage state (U_n, the stage buffer, or U_n + dt c_i K_1 formed on the
 //                 fly); writes alpha_raw and alpha
@@ -29,42 +29,48 @@ struct ScParams {
     double hg_T, hg_sT;                         // threshold T and s / T (host-computed, as AmrParams)
 };
 
+// One 16-lane group per element (lane q = node q) forms the indicator variable and its orthonormal
+// Legendre modal coefficients with width-16 shuffles (as k_amr_indicator), reduces the three energy
+// sums, and leaves them in shared memory; the scalar tail (two quotients, the logistic's exp, the
+// clipping) then runs once per element on one lane each -- 16 elements per warp instead of the
+// 16-fold replicated tail of the per-group form.  The next iteration's state (U_n and K_1 raw for a
+// lazy state) is loaded into registers before the current one is processed, so two elements per
+// group are in flight (ncu of the unpipelined form: 1.1 TB/s, 47 % issue-active, latency bound);
+// the Vandermonde rows come from shared memory to leave the registers to the prefetch.
 template <int MODE>
 __global__ void __launch_bounds__(AMR_T) k_sc_alpha(MeshDev md, StageParams sp, ScParams scp,
                                                     const double *__restrict__ Un, const double *__restrict__ Ubuf,
                                                     const double *__restrict__ K1, const double *__restrict__ Uin,
                                                     double *__restrict__ alpha_raw, double *__restrict__ alpha)
 {
+    constexpr int PER = AMR_T / 16;    // elements per CTA and iteration
+    __shared__ double sE[3][PER];      // tot, clip1, clip2 per group
+    __shared__ int sEl[PER];           // element id (-1: no element)
+    __shared__ double sV[NP][NP];      // Vinv
     const int q = threadIdx.x & 15, g = threadIdx.x >> 4;
     const unsigned gm = 0xffffffffu;   // converged full-mask shuffles (width 16), as in k_amr_indicator
-    double Ri[NP], Rj[NP];
-#pragma unroll
-    for (int k = 0; k < NP; ++k) {
-        Ri[k] = cB.Vinv[q & 3][k];
-        Rj[k] = cB.Vinv[q >> 2][k];
-    }
-    AmrParams ap;
-    ap.indicator = IND_HG;
-    ap.variable = scp.variable;
-    ap.base_level = ap.med_level = ap.max_level = 0;
-    ap.med_thr = ap.max_thr = 0.0;
-    ap.alpha_max = scp.alpha_max;
-    ap.alpha_min = scp.alpha_min;
-    ap.hg_T = scp.hg_T;
-    ap.hg_sT = scp.hg_sT;
-    ap.f_wave = 0.0;
+    const int i = q & 3, j = q >> 2;
+    if (threadIdx.x < NP * NP) sV[threadIdx.x >> 2][threadIdx.x & 3] = cB.Vinv[threadIdx.x >> 2][threadIdx.x & 3];
+    __syncthreads();
     pdl_wait();
     // items: [active elements | halo elements of the member below the lowest active one]
     const int n_el_a = MODE == MODE_STAGE ? md.count_active[KIND_EL * MAXS + sp.stage - 1] : md.n[0];
     const int2 hel = MODE == MODE_STAGE ? md.hrng[KIND_EL * MAXS + sp.stage - 1] : make_int2(0, 0);
     const int n_items = n_el_a + hel.y;
-    const StateBufs sb{Un, Ubuf, K1, Uin};
     const double dtc = sp.dt * sp.c_stage;
-    const int per = AMR_T / 16;
-    for (int base = blockIdx.x * per; base < n_items; base += gridDim.x * per) {   // CTA-uniform trip count
-        const int t = base + g;
-        const int tt = t < n_items ? t : base;
-        int e, src;
+    const double gm1 = md.gamma - 1.0;
+    if (scp.alpha_fixed >= 0.0) {
+        for (int t = blockIdx.x * PER + g; t < n_items; t += gridDim.x * PER) {
+            if (q) continue;
+            const int e = MODE == MODE_STAGE ? pk_elem(t < n_el_a ? md.elpk[t] : md.hpk[hel.x + t - n_el_a]) : t;
+            alpha_raw[e] = scp.alpha_fixed;
+            alpha[e] = scp.alpha_fixed;
+        }
+        return;
+    }
+    // element of slot t (clamped into range) and its state source
+    auto element_at = [&](int t, int &e, int &src) {
+        const int tt = t < n_items ? t : n_items - 1;
         if (MODE == MODE_STAGE) {
             const int pk = tt < n_el_a ? md.elpk[tt] : md.hpk[hel.x + tt - n_el_a];
             e = pk_elem(pk);
@@ -74,18 +80,88 @@ __global__ void __launch_bounds__(AMR_T) k_sc_alpha(MeshDev md, StageParams sp, 
             src = SRC_IN;
         }
         PERK_DASSERT(e >= 0 && e < md.n[0]);
-        double a;
-        if (scp.alpha_fixed >= 0.0) {
-            a = scp.alpha_fixed;
-        } else {
-            const size_t b = (size_t)e * 64 + q;
-            const double u0 = load_state(sb, src, dtc, b), u1 = load_state(sb, src, dtc, b + 16);
-            const double u2 = load_state(sb, src, dtc, b + 32), u3 = load_state(sb, src, dtc, b + 48);
-            a = amr_element_indicator<IND_HG>(md, ap, 0, u0, u1, u2, u3, Ri, Rj, gm, q);
+    };
+    // raw loads of one element's node values: a[v] (U_n, stage buffer or U_in), k[v] (K_1, lazy only)
+    auto issue = [&](int e, int src, double a[4], double k[4]) {
+        const size_t b = (size_t)e * 64 + q;
+        const double *base = src == SRC_BUF ? Ubuf : (src == SRC_IN ? Uin : Un);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) a[v] = __ldg(base + b + 16 * v);
+        if (src == SRC_LAZY) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) k[v] = __ldg(K1 + b + 16 * v);
         }
-        if (q == 0 && t < n_items) {
-            alpha_raw[e] = a;
-            alpha[e] = a;
+    };
+    int base = blockIdx.x * PER;
+    if (base >= n_items) return;
+    int e, src;
+    element_at(base + g, e, src);
+    double ca[4], ck[4] = {0.0, 0.0, 0.0, 0.0};
+    issue(e, src, ca, ck);
+    for (; base < n_items; base += gridDim.x * PER) {   // CTA-uniform trip count
+        const int t = base + g;
+        const bool has_next = base + gridDim.x * PER < n_items;
+        int e_n = 0, src_n = SRC_UN;
+        double na[4], nk[4] = {0.0, 0.0, 0.0, 0.0};
+        if (has_next) {
+            element_at(t + gridDim.x * PER, e_n, src_n);
+            issue(e_n, src_n, na, nk);
+        }
+        double u[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) u[v] = src == SRC_LAZY ? fma(dtc, ck[v], ca[v]) : ca[v];
+        const double rho = u[0], mx = u[1], my = u[2], En = u[3];
+        const double irho = rcp64(rho);
+        const double vx = mx * irho, vy = my * irho;
+        const double p = gm1 * (En - 0.5 * rho * (vx * vx + vy * vy));
+        double val;
+        switch (scp.variable) {
+        case 0: val = rho; break;
+        case 1: val = p; break;
+        case 2: val = rho * p; break;
+        case 3: val = vx; break;
+        default: val = vy; break;
+        }
+        // m_kl = sum_ij Vinv[k][i] Vinv[l][j] val_ij; lane (k, l) = (i, j) ends with m_kl
+        double tq = 0.0;
+#pragma unroll
+        for (int a = 0; a < NP; ++a) tq = fma(sV[i][a], __shfl_sync(gm, val, j * 4 + a, 16), tq);
+        double m = 0.0;
+#pragma unroll
+        for (int c = 0; c < NP; ++c) m = fma(sV[j][c], __shfl_sync(gm, tq, c * 4 + i, 16), m);
+        const double mm = m * m;
+        const double tot = sum16(gm, mm);
+        const double c1 = sum16(gm, (i <= NP - 2 && j <= NP - 2) ? mm : 0.0);
+        const double c2 = sum16(gm, (i <= NP - 3 && j <= NP - 3) ? mm : 0.0);
+        if (q == 0) {
+            sE[0][g] = tot;
+            sE[1][g] = c1;
+            sE[2][g] = c2;
+            sEl[g] = t < n_items ? e : -1;
+        }
+        __syncthreads();
+        if (threadIdx.x < PER) {   // tail: one lane per element
+            const int ee = sEl[threadIdx.x];
+            if (ee >= 0) {
+                const double T0 = sE[0][threadIdx.x], T1 = sE[1][threadIdx.x], T2 = sE[2][threadIdx.x];
+                const double e1 = T0 > 0.0 ? (T0 - T1) / T0 : 0.0;
+                const double e2 = T1 > 0.0 ? (T1 - T2) / T1 : 0.0;
+                const double E = fmax(e1, e2);
+                double a = 1.0 / (1.0 + exp(-scp.hg_sT * (E - scp.hg_T)));
+                if (a < scp.alpha_min) a = 0.0;
+                else if (a > 1.0 - scp.alpha_min) a = 1.0;
+                a = fmin(a, scp.alpha_max);
+                alpha_raw[ee] = a;
+                alpha[ee] = a;
+            }
+        }
+        __syncthreads();   // sE / sEl reused by the next iteration
+        e = e_n;
+        src = src_n;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            ca[v] = na[v];
+            ck[v] = nk[v];
         }
     }
 }

@@ -42,7 +42,7 @@ def main():
         sr = Perk(w.problem, w.level_map, w.S, [w.S])
         Us = sr.initial_state(w.ic)
         ms_sr = timed(sr, Us, w.dt)
-        prof = np.zeros(6)
+        prof = np.zeros(7)
         for k in [0, 1, 4, 5]:
             if k >= 4 and w.problem["equation"] != "navier_stokes":
                 continue
