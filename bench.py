@@ -396,7 +396,7 @@ def run_ours(args):
             sc = item.endswith("sc")
             pattern = {"alt": "alternating", "early": "early"}.get(item.lstrip("0123456789"))
             c, order = (int(item[:-2]), 3) if item.endswith("p3") else (int(item.rstrip("ialterysc")), 2)
-            if c == args.config and order == 2 and not amr and not pattern:
+            if c == args.config and order == 2 and not amr and not pattern and not sc:
                 continue
             try:
                 p2, _U, _w, r2 = measure_config(c, max(5, min(args.steps, 20)), args.warmup, timer, torch, dist,
