@@ -31,9 +31,10 @@ struct ScParams {
 
 // One 16-lane group per element (lane q = node q) forms the indicator variable and its orthonormal
 // Legendre modal coefficients with width-16 shuffles (as k_amr_indicator), reduces the three energy
-// sums, and leaves them in shared memory; the scalar tail (two quotients, the logistic's exp, the
-// clipping) then runs once per element on one lane each -- 16 elements per warp instead of the
-// 16-fold replicated tail of the per-group form.  The next iteration's state (U_n and K_1 raw for a
+// sums, and leaves them in a per-warp shared-memory buffer; every 8 iterations (16 elements) the
+// warp runs the scalar tail (two quotients, the logistic's exp, the clipping) once, one lane per
+// element, instead of the 16-fold replicated tail of the per-group form (warp-synchronous: a
+// per-CTA tail behind __syncthreads made barrier waits the top stall).  The next iteration's state (U_n and K_1 raw for a
 // lazy state) is loaded into registers before the current one is processed, so two elements per
 // group are in flight (ncu of the unpipelined form: 1.1 TB/s, 47 % issue-active, latency bound);
 // the Vandermonde rows come from shared memory to leave the registers to the prefetch.
@@ -44,10 +45,13 @@ __global__ void __launch_bounds__(AMR_T) k_sc_alpha(MeshDev md, StageParams sp, 
                                                     double *__restrict__ alpha_raw, double *__restrict__ alpha)
 {
     constexpr int PER = AMR_T / 16;    // elements per CTA and iteration
-    __shared__ double sE[3][PER];      // tot, clip1, clip2 per group
-    __shared__ int sEl[PER];           // element id (-1: no element)
+    constexpr int NW = AMR_T / 32;     // warps per CTA
+    __shared__ double sE[NW][3][16];   // per warp: tot, clip1, clip2 of up to 16 buffered elements
+    __shared__ int sEl[NW][16];        // element id (-1: no element)
     __shared__ double sV[NP][NP];      // Vinv
-    const int q = threadIdx.x & 15, g = threadIdx.x >> 4;
+    const int q = threadIdx.x & 15, g = threadIdx.x >> 4, wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int hg = g & 1;              // group within the warp
+    int nb = 0;                        // elements buffered by this warp (warp-uniform)
     const unsigned gm = 0xffffffffu;   // converged full-mask shuffles (width 16), as in k_amr_indicator
     const int i = q & 3, j = q >> 2;
     if (threadIdx.x < NP * NP) sV[threadIdx.x >> 2][threadIdx.x & 3] = cB.Vinv[threadIdx.x >> 2][threadIdx.x & 3];
@@ -134,28 +138,32 @@ __global__ void __launch_bounds__(AMR_T) k_sc_alpha(MeshDev md, StageParams sp, 
         const double c1 = sum16(gm, (i <= NP - 2 && j <= NP - 2) ? mm : 0.0);
         const double c2 = sum16(gm, (i <= NP - 3 && j <= NP - 3) ? mm : 0.0);
         if (q == 0) {
-            sE[0][g] = tot;
-            sE[1][g] = c1;
-            sE[2][g] = c2;
-            sEl[g] = t < n_items ? e : -1;
+            sE[wi][0][nb + hg] = tot;
+            sE[wi][1][nb + hg] = c1;
+            sE[wi][2][nb + hg] = c2;
+            sEl[wi][nb + hg] = t < n_items ? e : -1;
         }
-        __syncthreads();
-        if (threadIdx.x < PER) {   // tail: one lane per element
-            const int ee = sEl[threadIdx.x];
-            if (ee >= 0) {
-                const double T0 = sE[0][threadIdx.x], T1 = sE[1][threadIdx.x], T2 = sE[2][threadIdx.x];
-                const double e1 = T0 > 0.0 ? (T0 - T1) / T0 : 0.0;
-                const double e2 = T1 > 0.0 ? (T1 - T2) / T1 : 0.0;
-                const double E = fmax(e1, e2);
-                double a = 1.0 / (1.0 + exp(-scp.hg_sT * (E - scp.hg_T)));
-                if (a < scp.alpha_min) a = 0.0;
-                else if (a > 1.0 - scp.alpha_min) a = 1.0;
-                a = fmin(a, scp.alpha_max);
-                alpha_raw[ee] = a;
-                alpha[ee] = a;
+        nb += 2;
+        if (nb == 16 || !has_next) {   // warp-uniform
+            __syncwarp();
+            if (lane < nb) {   // tail: one lane per element
+                const int ee = sEl[wi][lane];
+                if (ee >= 0) {
+                    const double T0 = sE[wi][0][lane], T1 = sE[wi][1][lane], T2 = sE[wi][2][lane];
+                    const double e1 = T0 > 0.0 ? (T0 - T1) / T0 : 0.0;
+                    const double e2 = T1 > 0.0 ? (T1 - T2) / T1 : 0.0;
+                    const double E = fmax(e1, e2);
+                    double a = 1.0 / (1.0 + exp(-scp.hg_sT * (E - scp.hg_T)));
+                    if (a < scp.alpha_min) a = 0.0;
+                    else if (a > 1.0 - scp.alpha_min) a = 1.0;
+                    a = fmin(a, scp.alpha_max);
+                    alpha_raw[ee] = a;
+                    alpha[ee] = a;
+                }
             }
+            __syncwarp();
+            nb = 0;
         }
-        __syncthreads();   // sE / sEl reused by the next iteration
         e = e_n;
         src = src_n;
 #pragma unroll
