@@ -115,6 +115,15 @@ struct StageParams {
                                  // U_{n+1} = U_n + dt (b_1 K_1 + b_S K_S), no W buffer
 };
 
+// Subcell shock capturing parameters (sc.cuh, k_vol2d<., ., true>)
+struct ScParams {
+    int variable, smooth;
+    double alpha_max, alpha_min, alpha_fixed;   // alpha_fixed >= 0: no indicator
+    double hg_T, hg_sT;                         // threshold T and s / T (host-computed, as AmrParams)
+    int epi;                                    // k_vol2d computes the next stage's alpha of the elements
+                                                // whose next stage state its epilogue writes (stages 2..S-1)
+};
+
 // Which buffer holds element e's stage-i state (SURVEY §7 rule):
 //   i == 1: U_n;  i evaluated after an earlier evaluated stage > 1 (standard: i > f(e) = S - E + 2):
 //   Ubuf;  otherwise U_n + dt c_i K_1 (formed on the fly)

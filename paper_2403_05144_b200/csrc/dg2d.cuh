@@ -558,7 +558,8 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                                                  double *__restrict__ Ubuf, double *__restrict__ K1,
                                                  const double *__restrict__ Fs, const double *__restrict__ Uin,
                                                  double *__restrict__ dU, const double *__restrict__ Gs,
-                                                 double *__restrict__ Wb, const double *__restrict__ alpha)
+                                                 double *__restrict__ Wb, double *alpha, double *alpha_raw,
+                                                 ScParams scp)
 {
     constexpr int NF = vol2d_nf(NS);          // rho, v_n/2, v_t/2, p/2, ln rho, beta, ln beta (+ T)
     constexpr int EPB = vol2d_epb(NS), LS = vol2d_ls(NS);
@@ -634,7 +635,7 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
         const size_t eb = (size_t)e * 64;
         const double hcell = md.hf * (double)(1 << (md.max_level - pk_level(pk)));
         double2 pre_un[4], pre_k1[4];          // epilogue operands held in registers (EM == 2)
-        const double al = SC ? __ldg(alpha + e) : 0.0;
+        const double al = SC ? alpha[e] : 0.0;   // read before this element's next-stage alpha is written
 
         // phase 1: nodes q0, q0+1 -> primitives + logs, stored in x-line and y-line layouts
         cp_async_wait<0>();
@@ -801,6 +802,7 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                 acc[0][v] = fma(-Flo[v * 4], cB.invw[0], acc[0][v]);
             }
         }
+        double2 nu[4];   // SC: the next stage state of nodes q0, q0 + 1 written to the stage buffer
         // stage epilogue of one node pair (qq, qq + 1) of variable v (K = the pair's RHS values)
         auto epilogue = [&](int v, int qq, double2 K) {
             const size_t idx = eb + v * 16 + qq;
@@ -825,8 +827,9 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                 const double2 un = EM == 2 ? pre_un[v] : *reinterpret_cast<const double2 *>(EP(EPI_UN) + v * 16 + qq);
                 const double2 k1 = EM == 2 ? pre_k1[v] : *reinterpret_cast<const double2 *>(EP(EPI_K1) + v * 16 + qq);
                 const double a1 = sp.a1_next[m], as = sp.asub_next[m];
-                *reinterpret_cast<double2 *>(Ubuf + idx) =
-                    make_double2(fma(sp.dt, fma(a1, k1.x, as * K.x), un.x), fma(sp.dt, fma(a1, k1.y, as * K.y), un.y));
+                const double2 nxt = make_double2(fma(sp.dt, fma(a1, k1.x, as * K.x), un.x), fma(sp.dt, fma(a1, k1.y, as * K.y), un.y));
+                *reinterpret_cast<double2 *>(Ubuf + idx) = nxt;
+                if (SC) nu[v] = nxt;
                 if (sp.wmode)
                     *reinterpret_cast<double2 *>(Wb + idx) =
                         make_double2(fma(sp.dt, fma(sp.wb1, k1.x, sp.wbS1 * K.x), un.x),
@@ -853,6 +856,59 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                 const double s0 = sx.x + sm[v][1][yo + eoy + 4 * i0 + j0];
                 const double s1 = sx.y + sm[v][1][yo + eoy + 4 * (i0 + 1) + j0];
                 epilogue(v, q0, make_double2(J * s0, J * s1));
+            }
+        }
+        if (SC && MODE == MODE_STAGE && scp.epi && scp.alpha_fixed < 0.0 && sp.stage > 1 && sp.stage < sp.S) {
+            // Hennemann-Gassner indicator of the next stage state just written (the blend factor the
+            // next stage needs; k_sc_alpha skips these elements).  The element's 8 threads hold nodes
+            // (i0, j0), (i0 + 1, j0): the modal transform runs as width-8 shuffles (warp-converged).
+            const int i0 = q0 & 3, j0 = q0 >> 2, par = t8 & 1;
+            double vq[2] = {1.0, 1.0};
+            if (writes) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const double r = h ? nu[0].y : nu[0].x, m1 = h ? nu[1].y : nu[1].x;
+                    const double m2 = h ? nu[2].y : nu[2].x, En = h ? nu[3].y : nu[3].x;
+                    const double ir = rcp64(r), v1 = m1 * ir, v2 = m2 * ir;
+                    const double p = gm1 * (En - 0.5 * r * (v1 * v1 + v2 * v2));
+                    vq[h] = scp.variable == 0 ? r : scp.variable == 1 ? p : scp.variable == 2 ? r * p
+                          : scp.variable == 3 ? v1 : v2;
+                }
+            }
+            const double o0 = __shfl_xor_sync(0xffffffffu, vq[0], 1, 8), o1 = __shfl_xor_sync(0xffffffffu, vq[1], 1, 8);
+            const double row[4] = {par ? o0 : vq[0], par ? o1 : vq[1], par ? vq[0] : o0, par ? vq[1] : o1};
+            double tk0 = 0.0, tk1 = 0.0;   // x transform of row j0, modes k = i0, i0 + 1
+#pragma unroll
+            for (int a = 0; a < NP; ++a) {
+                tk0 = fma(cB.Vinv[i0][a], row[a], tk0);
+                tk1 = fma(cB.Vinv[i0 + 1][a], row[a], tk1);
+            }
+            double m0 = 0.0, m1 = 0.0;     // y transform: modes (i0, j0), (i0 + 1, j0)
+#pragma unroll
+            for (int b = 0; b < NP; ++b) {
+                const double vb = cB.Vinv[j0][b];
+                m0 = fma(vb, __shfl_sync(0xffffffffu, tk0, 2 * b + par, 8), m0);
+                m1 = fma(vb, __shfl_sync(0xffffffffu, tk1, 2 * b + par, 8), m1);
+            }
+            const double mm0 = m0 * m0, mm1 = m1 * m1;
+            double tot = mm0 + mm1;
+            double c1 = (j0 <= NP - 2 ? (i0 <= NP - 2 ? mm0 : 0.0) + (i0 + 1 <= NP - 2 ? mm1 : 0.0) : 0.0);
+            double c2 = (j0 <= NP - 3 ? (i0 <= NP - 3 ? mm0 : 0.0) + (i0 + 1 <= NP - 3 ? mm1 : 0.0) : 0.0);
+#pragma unroll
+            for (int off = 4; off > 0; off >>= 1) {
+                tot += __shfl_xor_sync(0xffffffffu, tot, off, 8);
+                c1 += __shfl_xor_sync(0xffffffffu, c1, off, 8);
+                c2 += __shfl_xor_sync(0xffffffffu, c2, off, 8);
+            }
+            if (writes && t8 == 0) {
+                const double e1 = tot > 0.0 ? (tot - c1) / tot : 0.0;
+                const double e2 = c1 > 0.0 ? (c1 - c2) / c1 : 0.0;
+                double a = 1.0 / (1.0 + exp(-scp.hg_sT * (fmax(e1, e2) - scp.hg_T)));
+                if (a < scp.alpha_min) a = 0.0;
+                else if (a > 1.0 - scp.alpha_min) a = 1.0;
+                a = fmin(a, scp.alpha_max);
+                alpha_raw[e] = a;
+                alpha[e] = a;
             }
         }
         __syncwarp();

@@ -392,18 +392,18 @@ static void launch_volume(perk_ctx *c, cudaStream_t s, const StageParams &sp, do
 {
     const MeshDev md = stage_mesh(c, sp);
     if (c->prob.dim == 2) {
-        const double *al = c->alpha;
+        double *al = c->alpha;
         const bool st = sp.mode == MODE_STAGE;
         const int tn = vol2d_threads(c->ns);
         const size_t sm = vol2d_smem_bytes(c->ns);
         if (c->ns && c->sc)
-            launch_pdl(st ? k_vol2d<MODE_STAGE, true, true> : k_vol2d<MODE_RHS, true, true>, c->vol_blocks, tn, sm, s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, (const double *)c->Gs, c->Wb, al);
+            launch_pdl(st ? k_vol2d<MODE_STAGE, true, true> : k_vol2d<MODE_RHS, true, true>, c->vol_blocks, tn, sm, s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, (const double *)c->Gs, c->Wb, al, c->alpha_raw, c->scp);
         else if (c->ns)
-            launch_pdl(st ? k_vol2d<MODE_STAGE, true> : k_vol2d<MODE_RHS, true>, c->vol_blocks, tn, sm, s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, (const double *)c->Gs, c->Wb, al);
+            launch_pdl(st ? k_vol2d<MODE_STAGE, true> : k_vol2d<MODE_RHS, true>, c->vol_blocks, tn, sm, s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, (const double *)c->Gs, c->Wb, al, c->alpha_raw, c->scp);
         else if (c->sc)
-            launch_pdl(st ? k_vol2d<MODE_STAGE, false, true> : k_vol2d<MODE_RHS, false, true>, c->vol_blocks, tn, sm, s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, (const double *)nullptr, c->Wb, al);
+            launch_pdl(st ? k_vol2d<MODE_STAGE, false, true> : k_vol2d<MODE_RHS, false, true>, c->vol_blocks, tn, sm, s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, (const double *)nullptr, c->Wb, al, c->alpha_raw, c->scp);
         else
-            launch_pdl(st ? k_vol2d<MODE_STAGE, false> : k_vol2d<MODE_RHS, false>, c->vol_blocks, tn, sm, s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, (const double *)nullptr, c->Wb, al);
+            launch_pdl(st ? k_vol2d<MODE_STAGE, false> : k_vol2d<MODE_RHS, false>, c->vol_blocks, tn, sm, s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, (const double *)nullptr, c->Wb, al, c->alpha_raw, c->scp);
     } else if (c->nv == 1) {
         if (sp.mode == MODE_STAGE)
             k_vol1d<1, MODE_STAGE><<<c->vol_blocks, 128, 0, s>>>(md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, c->Wb);
@@ -1093,6 +1093,8 @@ extern "C" int perk_set_shock_capturing(perk_ctx *c, const perk_shock_capturing 
     }
     const char *fenv = std::getenv("PERK_SC_FUSED");
     c->sc_fused = !(fenv && fenv[0] == '0');
+    const char *eenv = std::getenv("PERK_SC_EPI");   // "0": every stage's alpha from k_sc_alpha
+    c->scp.epi = (eenv && eenv[0] == '0') ? 0 : 1;
     c->scp.variable = sc->variable;
     c->scp.smooth = sc->smooth ? 1 : 0;
     c->scp.alpha_max = sc->alpha_max;

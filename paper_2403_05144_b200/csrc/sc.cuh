@@ -23,11 +23,6 @@
 
 namespace perk {
 
-struct ScParams {
-    int variable, smooth;
-    double alpha_max, alpha_min, alpha_fixed;   // alpha_fixed >= 0: no indicator
-    double hg_T, hg_sT;                         // threshold T and s / T (host-computed, as AmrParams)
-};
 
 // One 16-lane group per element (lane q = node q) forms the indicator variable and its orthonormal
 // Legendre modal coefficients with width-16 shuffles (as k_amr_indicator), reduces the three energy
@@ -57,16 +52,22 @@ __global__ void __launch_bounds__(AMR_T) k_sc_alpha(MeshDev md, StageParams sp, 
     if (threadIdx.x < NP * NP) sV[threadIdx.x >> 2][threadIdx.x & 3] = cB.Vinv[threadIdx.x >> 2][threadIdx.x & 3];
     __syncthreads();
     pdl_wait();
-    // items: [active elements | halo elements of the member below the lowest active one]
-    const int n_el_a = MODE == MODE_STAGE ? md.count_active[KIND_EL * MAXS + sp.stage - 1] : md.n[0];
+    // items: [active elements | halo elements of the member below the lowest active one].  With
+    // scp.epi the previous stage's k_vol2d epilogue already wrote alpha for the elements whose stage
+    // state it wrote to the stage buffer -- the elements active at stage i - 1 >= 2, a prefix of the
+    // member-sorted list -- so only the rest (first-time active, lazy states) and the halo remain.
+    const int skip = (MODE == MODE_STAGE && scp.epi && scp.alpha_fixed < 0.0 && sp.stage >= 3)
+                         ? md.count_active[KIND_EL * MAXS + sp.stage - 2] : 0;
+    const int n_el_a = (MODE == MODE_STAGE ? md.count_active[KIND_EL * MAXS + sp.stage - 1] : md.n[0]) - skip;
     const int2 hel = MODE == MODE_STAGE ? md.hrng[KIND_EL * MAXS + sp.stage - 1] : make_int2(0, 0);
     const int n_items = n_el_a + hel.y;
+    const int *elpk = md.elpk + skip;
     const double dtc = sp.dt * sp.c_stage;
     const double gm1 = md.gamma - 1.0;
     if (scp.alpha_fixed >= 0.0) {
         for (int t = blockIdx.x * PER + g; t < n_items; t += gridDim.x * PER) {
             if (q) continue;
-            const int e = MODE == MODE_STAGE ? pk_elem(t < n_el_a ? md.elpk[t] : md.hpk[hel.x + t - n_el_a]) : t;
+            const int e = MODE == MODE_STAGE ? pk_elem(t < n_el_a ? elpk[t] : md.hpk[hel.x + t - n_el_a]) : t;
             alpha_raw[e] = scp.alpha_fixed;
             alpha[e] = scp.alpha_fixed;
         }
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(AMR_T) k_sc_alpha(MeshDev md, StageParams sp, 
     auto element_at = [&](int t, int &e, int &src) {
         const int tt = t < n_items ? t : n_items - 1;
         if (MODE == MODE_STAGE) {
-            const int pk = tt < n_el_a ? md.elpk[tt] : md.hpk[hel.x + tt - n_el_a];
+            const int pk = tt < n_el_a ? elpk[tt] : md.hpk[hel.x + tt - n_el_a];
             e = pk_elem(pk);
             src = state_src(sp, pk_member(pk));
         } else {

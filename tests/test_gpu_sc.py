@@ -90,9 +90,16 @@ def test_alpha_and_rhs_eval_masks(cfg, sc, surface):
         assert err.max() <= TOL, (mask, err)
 
 
-def test_cfg3_structure_steps():
+@pytest.mark.parametrize("epi", ["1", "0"])
+def test_cfg3_structure_steps(epi):
+    """epi 1 (default): the next stage's alpha of buffered elements from the k_vol2d epilogue;
+    epi 0: every stage's alpha from k_sc_alpha"""
     w = W.make(3, n_base=16)
-    ora, gpu = _pair(w, _with_sc(w))
+    os.environ["PERK_SC_EPI"] = epi
+    try:
+        ora, gpu = _pair(w, _with_sc(w))
+    finally:
+        del os.environ["PERK_SC_EPI"]
     Uo, Ug = _run_both(w, ora, gpu, 40, _jump_ic(w.ic))
     assert rel_err_per_var(Ug, Uo).max() <= TOL
     _, sm = ora.sc_alpha(Uo)
