@@ -106,9 +106,15 @@ def test_cfg3_structure_steps(epi):
     assert 0 < np.count_nonzero(sm) < ora.n
 
 
-def test_cfg5_structure_steps():
+@pytest.mark.parametrize("epi", ["default", "1"])
+def test_cfg5_structure_steps(epi):
     w = W.make(5, n_base=16)
-    ora, gpu = _pair(w, _with_sc(w))
+    if epi != "default":
+        os.environ["PERK_SC_EPI"] = epi
+    try:
+        ora, gpu = _pair(w, _with_sc(w))
+    finally:
+        os.environ.pop("PERK_SC_EPI", None)
     Uo, Ug = _run_both(w, ora, gpu, 20, _jump_ic(w.ic))
     assert rel_err_per_var(Ug, Uo).max() <= TOL
 
