@@ -10,7 +10,9 @@
 //                 amr.cuh / DESIGN.md A1) on the elements the stage needs -- the active elements and their
 //                 neighbours across active mortars (the BR1 halo lists, mesh.cuh) -- from the
 //                 element's stage state (U_n, the stage buffer, or U_n + dt c_i K_1 formed on the
-//                 fly); writes alpha_raw and alpha
+//                 fly); writes alpha_raw and alpha.  With ScParams::epi (Euler default) the elements
+//                 whose state the previous stage's k_vol2d wrote to the stage buffer already have
+//                 theirs (computed in that epilogue) and are skipped
 //   smoothing   : alpha_e = max(alpha_e, alpha_raw_n / 2) over the stage's active interfaces and
 //                 mortars (atomicMax on the fp64 bit pattern, exact for alpha >= 0, so the result does
 //                 not depend on the order); every face of an active element is active, so every
