@@ -213,3 +213,47 @@ def test_error_codes():
     ga = Perk(w.problem, w.level_map, w.S, w.E, pattern="alternating")
     with pytest.raises(PerkError):
         ga.set_shock_capturing(SC)
+
+
+@pytest.mark.parametrize("surface", ["hll", "rusanov"])
+def test_nonperiodic_boundary_steps(surface):
+    """weakly imposed Dirichlet faces on a non-periodic x direction (a8) with shock capturing: the
+    boundary faces enter the subcell FV through the unchanged surface term, no smoothing across them"""
+    w = W.make(3, n_base=8)
+    p = dict(_with_sc(w, surface=surface), periodic=(0, 1), bc_state=(1.0, 1.0, 1.0, 1.0 / 0.4 + 1.0))
+    ora, gpu = build_pair(w, problem=p)
+    assert ora.face_counts()["boundaries"] > 0
+    Uo, Ug = _run_both(w, ora, gpu, 30, _jump_ic(w.ic))
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
+
+
+def test_amr_adapt_with_shock_capturing():
+    """device indicator-driven AMR (perk_amr_adapt, f3) cycles with shock capturing on"""
+    w = W.make(4, n_base=16, max_level=3, widths=(0.3, 0.15, 0.06))
+    w.S, w.E = 16, [4, 6, 10, 16]
+    fam = T.family(w.S, w.E, "taylor")
+    p = _with_sc(w)
+    amr = dict(indicator="hennemann_gassner", variable="rho_p", base_level=0, med_level=1, max_level=3,
+               med_threshold=0.01, max_threshold=0.1)
+    ora, gpu = build_pair(w, problem=p)     # capacity: every finest cell a leaf
+    ic = _jump_ic(w.ic)
+    Uo = ora.initial_state(ic)
+    Ug = gpu.initial_state(ic)
+    for _ in range(3):
+        ora.step(Uo, w.dt, 5)
+        gpu.step(Ug, w.dt, 5)
+        torch.cuda.synchronize()
+        assert rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo).max() <= TOL
+        lm_g = gpu.amr_adapt(Ug, amr)
+        lm_o = ora.amr_adapt(Uo, amr)
+        assert np.array_equal(lm_g.cpu().numpy(), lm_o)
+        new = O.OracleMesh(p, lm_o, fam)
+        Uo = O.transfer(ora, new, Uo)
+        ora = new
+        gpu.repartition(lm_g, Ug)
+        gpu.sync()
+        compare_mesh(ora, gpu)
+    ora.step(Uo, w.dt, 5)
+    gpu.step(Ug, w.dt, 5)
+    torch.cuda.synchronize()
+    assert rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo).max() <= TOL
