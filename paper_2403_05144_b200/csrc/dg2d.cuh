@@ -592,6 +592,17 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
     const int stride = gridDim.x * EPB;
 
     int base = blockIdx.x * EPB;
+    // SC epilogue indicator: Vandermonde rows in shared memory (lane-indexed __constant__ reads would
+    // serialise) and a per-warp buffer of the energy sums of up to 16 elements, whose scalar tail
+    // (quotients, exp, clipping) runs once per element on one lane
+    __shared__ double sVv[SC ? NP * NP : 1];
+    __shared__ double sTail[SC ? EPB / 4 : 1][3][SC ? 16 : 1];
+    __shared__ int sTe[SC ? EPB / 4 : 1][SC ? 16 : 1];
+    int nbuf = 0;                                    // elements buffered by this warp (warp-uniform)
+    if (SC) {
+        if (threadIdx.x < NP * NP) sVv[threadIdx.x] = cB.Vinv[threadIdx.x >> 2][threadIdx.x & 3];
+        __syncthreads();
+    }
     // prologue before the dependency wait: indices only (lists are rebuilt by the mesh pipeline,
     // which completed before the step started)
     const int pk0 = base < n_act ? (MODE == MODE_STAGE ? md.elpk[base + le < n_act ? base + le : base] : 0) : 0;
@@ -880,13 +891,13 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
             double tk0 = 0.0, tk1 = 0.0;   // x transform of row j0, modes k = i0, i0 + 1
 #pragma unroll
             for (int a = 0; a < NP; ++a) {
-                tk0 = fma(cB.Vinv[i0][a], row[a], tk0);
-                tk1 = fma(cB.Vinv[i0 + 1][a], row[a], tk1);
+                tk0 = fma(sVv[i0 * NP + a], row[a], tk0);
+                tk1 = fma(sVv[(i0 + 1) * NP + a], row[a], tk1);
             }
             double m0 = 0.0, m1 = 0.0;     // y transform: modes (i0, j0), (i0 + 1, j0)
 #pragma unroll
             for (int b = 0; b < NP; ++b) {
-                const double vb = cB.Vinv[j0][b];
+                const double vb = sVv[j0 * NP + b];
                 m0 = fma(vb, __shfl_sync(0xffffffffu, tk0, 2 * b + par, 8), m0);
                 m1 = fma(vb, __shfl_sync(0xffffffffu, tk1, 2 * b + par, 8), m1);
             }
@@ -900,15 +911,29 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                 c1 += __shfl_xor_sync(0xffffffffu, c1, off, 8);
                 c2 += __shfl_xor_sync(0xffffffffu, c2, off, 8);
             }
-            if (writes && t8 == 0) {
-                const double e1 = tot > 0.0 ? (tot - c1) / tot : 0.0;
-                const double e2 = c1 > 0.0 ? (c1 - c2) / c1 : 0.0;
-                double a = 1.0 / (1.0 + exp(-scp.hg_sT * (fmax(e1, e2) - scp.hg_T)));
-                if (a < scp.alpha_min) a = 0.0;
-                else if (a > 1.0 - scp.alpha_min) a = 1.0;
-                a = fmin(a, scp.alpha_max);
-                alpha_raw[e] = a;
-                alpha[e] = a;
+            const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31, slot = nbuf + (lane >> 3);
+            if (t8 == 0) {
+                sTail[wi][0][slot] = tot;
+                sTail[wi][1][slot] = c1;
+                sTail[wi][2][slot] = c2;
+                sTe[wi][slot] = writes ? e : -1;
+            }
+            nbuf += 4;
+            if (nbuf == 16 || !has_next) {   // CTA-uniform
+                __syncwarp();
+                if (lane < nbuf && sTe[wi][lane] >= 0) {
+                    const double T0 = sTail[wi][0][lane], T1 = sTail[wi][1][lane], T2 = sTail[wi][2][lane];
+                    const double e1 = T0 > 0.0 ? (T0 - T1) / T0 : 0.0;
+                    const double e2 = T1 > 0.0 ? (T1 - T2) / T1 : 0.0;
+                    double a = 1.0 / (1.0 + exp(-scp.hg_sT * (fmax(e1, e2) - scp.hg_T)));
+                    if (a < scp.alpha_min) a = 0.0;
+                    else if (a > 1.0 - scp.alpha_min) a = 1.0;
+                    a = fmin(a, scp.alpha_max);
+                    alpha_raw[sTe[wi][lane]] = a;
+                    alpha[sTe[wi][lane]] = a;
+                }
+                __syncwarp();
+                nbuf = 0;
             }
         }
         __syncwarp();
