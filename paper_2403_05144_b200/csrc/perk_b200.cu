@@ -1093,11 +1093,10 @@ extern "C" int perk_set_shock_capturing(perk_ctx *c, const perk_shock_capturing 
     }
     const char *fenv = std::getenv("PERK_SC_FUSED");
     c->sc_fused = !(fenv && fenv[0] == '0');
-    // next-stage alpha in the k_vol2d epilogue: Euler only by default (cfg 3: 0.764 -> 0.742 ms/step);
-    // the Navier-Stokes volume kernel is at its register limit and slowed down more than the
-    // separate pass costs (cfg 5: 8.65 -> 8.93 ms/step).  PERK_SC_EPI=0 / 1 forces it.
+    // next-stage alpha in the k_vol2d epilogue (cfg 3: 0.764 -> 0.719 ms/step, cfg 5: 8.68 -> 8.54 with
+    // the batched tail; before it, the Navier-Stokes kernel got slower, 8.93).  PERK_SC_EPI=0: off.
     const char *eenv = std::getenv("PERK_SC_EPI");
-    c->scp.epi = eenv && (eenv[0] == '0' || eenv[0] == '1') ? eenv[0] - '0' : (c->ns ? 0 : 1);
+    c->scp.epi = (eenv && eenv[0] == '0') ? 0 : 1;
     c->scp.variable = sc->variable;
     c->scp.smooth = sc->smooth ? 1 : 0;
     c->scp.alpha_max = sc->alpha_max;
