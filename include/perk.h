@@ -224,9 +224,10 @@ typedef struct perk_shock_capturing {
 } perk_shock_capturing;
 
 /* Switch shock capturing on (sc != NULL; parameters copied) or off (sc = NULL) for the following
- * steps and rhs_eval calls; re-mesh keeps it.  Synchronises the context stream.  EUNSUPPORTED for
- * 1D / advection problems and non-standard stage patterns; EINVAL for parameters out of range
- * (0 <= alpha_min <= 1/2, 0 <= alpha_max <= 1, alpha_fixed <= 1, variable in 0..4). */
+ * steps and rhs_eval calls; re-mesh keeps it.  Synchronises the context stream.  Any stage pattern
+ * (non-standard ones evaluate alpha on every element at every stage).  EUNSUPPORTED for 1D /
+ * advection problems; EINVAL for parameters out of range (0 <= alpha_min <= 1/2,
+ * 0 <= alpha_max <= 1, alpha_fixed <= 1, variable in 0..4). */
 int perk_set_shock_capturing(perk_ctx *ctx, const perk_shock_capturing *sc);
 /* Blending factors of the state U_dev (raw indicator and smoothed) into device arrays of >= n_cells
  * doubles, canonical leaf order.  Asynchronous; EINVAL if shock capturing is off. */

@@ -122,6 +122,8 @@ struct ScParams {
     double hg_T, hg_sT;                         // threshold T and s / T (host-computed, as AmrParams)
     int epi;                                    // k_vol2d computes the next stage's alpha of the elements
                                                 // whose next stage state its epilogue writes (stages 2..S-1)
+    int all;                                    // non-standard stage patterns: alpha of every element at
+                                                // every stage (no nested halo lists exist for them)
 };
 
 // Which buffer holds element e's stage-i state (SURVEY §7 rule):

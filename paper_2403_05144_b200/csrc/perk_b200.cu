@@ -1059,8 +1059,6 @@ extern "C" int perk_set_shock_capturing(perk_ctx *c, const perk_shock_capturing 
     if (sc) {
         if (c->prob.dim != 2 || c->prob.equation == PERK_EQ_ADVECTION)
             return set_err(c, PERK_EUNSUPPORTED, "shock capturing needs a 2D Euler / Navier-Stokes problem");
-        if (!c->std_pattern)
-            return set_err(c, PERK_EUNSUPPORTED, "shock capturing runs the standard stage pattern only (halo needs nesting)");
         if (sc->variable < 0 || sc->variable > 4 || !(sc->alpha_min >= 0.0 && sc->alpha_min <= 0.5) ||
             !(sc->alpha_max >= 0.0 && sc->alpha_max <= 1.0) || !(sc->alpha_fixed <= 1.0))
             return set_err(c, PERK_EINVAL, "need variable in 0..4, 0 <= alpha_min <= 1/2, 0 <= alpha_max <= 1, alpha_fixed <= 1");
@@ -1096,7 +1094,8 @@ extern "C" int perk_set_shock_capturing(perk_ctx *c, const perk_shock_capturing 
     // next-stage alpha in the k_vol2d epilogue (cfg 3: 0.764 -> 0.719 ms/step, cfg 5: 8.68 -> 8.54 with
     // the batched tail; before it, the Navier-Stokes kernel got slower, 8.93).  PERK_SC_EPI=0: off.
     const char *eenv = std::getenv("PERK_SC_EPI");
-    c->scp.epi = (eenv && eenv[0] == '0') ? 0 : 1;
+    c->scp.epi = (eenv && eenv[0] == '0') || !c->std_pattern ? 0 : 1;
+    c->scp.all = c->std_pattern ? 0 : 1;   // non-standard patterns: alpha of every element per stage
     c->scp.variable = sc->variable;
     c->scp.smooth = sc->smooth ? 1 : 0;
     c->scp.alpha_max = sc->alpha_max;

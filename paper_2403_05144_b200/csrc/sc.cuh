@@ -58,10 +58,13 @@ __global__ void __launch_bounds__(AMR_T) k_sc_alpha(MeshDev md, StageParams sp, 
     // scp.epi the previous stage's k_vol2d epilogue already wrote alpha for the elements whose stage
     // state it wrote to the stage buffer -- the elements active at stage i - 1 >= 2, a prefix of the
     // member-sorted list -- so only the rest (first-time active, lazy states) and the halo remain.
-    const int skip = (MODE == MODE_STAGE && scp.epi && scp.alpha_fixed < 0.0 && sp.stage >= 3)
+    // Non-standard stage patterns (scp.all): every element, in the member-sorted list (an inactive
+    // member's stage state is the lazy U_n + dt c_i K_1, state_src).
+    const bool part = MODE == MODE_STAGE && !scp.all;
+    const int skip = (part && scp.epi && scp.alpha_fixed < 0.0 && sp.stage >= 3)
                          ? md.count_active[KIND_EL * MAXS + sp.stage - 2] : 0;
-    const int n_el_a = (MODE == MODE_STAGE ? md.count_active[KIND_EL * MAXS + sp.stage - 1] : md.n[0]) - skip;
-    const int2 hel = MODE == MODE_STAGE ? md.hrng[KIND_EL * MAXS + sp.stage - 1] : make_int2(0, 0);
+    const int n_el_a = (part ? md.count_active[KIND_EL * MAXS + sp.stage - 1] : md.n[0]) - skip;
+    const int2 hel = part ? md.hrng[KIND_EL * MAXS + sp.stage - 1] : make_int2(0, 0);
     const int n_items = n_el_a + hel.y;
     const int *elpk = md.elpk + skip;
     const double dtc = sp.dt * sp.c_stage;

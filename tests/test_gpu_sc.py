@@ -210,9 +210,6 @@ def test_error_codes():
     g1 = Perk(w1.problem, w1.level_map, w1.S, w1.E)
     with pytest.raises(PerkError):
         g1.set_shock_capturing(SC)
-    ga = Perk(w.problem, w.level_map, w.S, w.E, pattern="alternating")
-    with pytest.raises(PerkError):
-        ga.set_shock_capturing(SC)
 
 
 @pytest.mark.parametrize("surface", ["hll", "rusanov"])
@@ -257,3 +254,22 @@ def test_amr_adapt_with_shock_capturing():
     gpu.step(Ug, w.dt, 5)
     torch.cuda.synchronize()
     assert rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo).max() <= TOL
+
+
+@pytest.mark.parametrize("pattern,stage_lists", [("alternating", "1"), ("alternating", "0"), ("early", "1"),
+                                                 ([[1, 5, 9, 16], [1, 2, 4, 6, 8, 10, 12, 16], "standard"], "1")])
+def test_stage_patterns_steps(pattern, stage_lists):
+    """non-standard stage patterns (f2) with shock capturing: alpha of every element at every stage
+    (per-stage hot arrays, and the superset-prefix path with PERK_STAGE_LISTS=0)"""
+    from paper_2403_05144_b200 import Perk
+    w = W.make(3, n_base=16)
+    p = _with_sc(w)
+    fam = T.family(w.S, w.E, w.alpha_rule, pattern=pattern)
+    ora = O.OracleMesh(p, w.level_map, fam)
+    os.environ["PERK_STAGE_LISTS"] = stage_lists
+    try:
+        gpu = Perk(p, w.level_map, w.S, w.E, pattern=pattern)
+    finally:
+        del os.environ["PERK_STAGE_LISTS"]
+    Uo, Ug = _run_both(w, ora, gpu, 20, _jump_ic(w.ic))
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
