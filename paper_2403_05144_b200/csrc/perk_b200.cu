@@ -577,8 +577,6 @@ static int validate(perk_ctx *c, const perk_problem *p, const perk_tableau *t)
                 return set_err(c, PERK_EINVAL, "a_sub[r][i-1] != 0 at a stage without an evaluated predecessor > 1");
         }
     }
-    if (any && p->equation == PERK_EQ_NAVIER_STOKES)
-        return set_err(c, PERK_EUNSUPPORTED, "non-standard stage patterns: Euler / advection only (BR1 halo needs nesting)");
     // b_{S-1} != 0 (P-ERK3): W = U_n + dt (b_1 K_1 + b_{S-1} K_{S-1}) is formed in the stage S-1 epilogue;
     // b_1 alone (Heun / Ralston) is added at stage S
     if (t->S >= 3 && t->b[t->S - 2] != 0.0)
@@ -750,7 +748,10 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
         // prefix (correct, surplus members skipped) instead
         const double bytes = (double)tab->S * ((double)c->cap * 4.0 + (double)c->cap_faces * 36.0);
         const char *env = std::getenv("PERK_STAGE_LISTS");   // "0": force the superset path (tests)
-        if (!nested && bytes <= 8.0e9 && !(env && env[0] == '0')) {
+        // Navier-Stokes keeps the superset prefix: its BR1 halo lists (the neighbours of the launch's
+        // members across mortars) are defined for member prefixes; surplus members of the prefix see
+        // their lazy stage state, so their gradients are the definition's
+        if (!nested && bytes <= 8.0e9 && !(env && env[0] == '0') && !c->ns) {
             c->stage_lists = true;
             const size_t S = (size_t)tab->S;
             CU(dalloc(c, &c->st_el, S * c->cap));

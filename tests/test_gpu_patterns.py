@@ -124,13 +124,30 @@ def test_heun_standard_1d_and_2d():
         assert rel_err_per_var(Ug, Uo).max() <= TOL
 
 
-def test_patterns_rejected_for_navier_stokes_and_bad_masks():
-    from paper_2403_05144_b200 import Perk
+@pytest.mark.parametrize("pattern", ["alternating", "early", [[1, 11, 21, 32], [1, 3, 5, 7, 9, 11, 13, 32],
+                                                              "standard", "standard"]], ids=str)
+def test_navier_stokes_patterns(pattern):
+    """Navier-Stokes (BR1) with non-standard stage patterns: the superset member prefix per stage
+    with its halo; surplus members see their lazy stage state"""
+    w = W.make(5, n_base=8)
+    fam, ora, gpu = _pair(w, pattern)
+    Uo = ora.initial_state(w.ic)
+    Ug = gpu.initial_state(w.ic)
+    ora.step(Uo, w.dt, 10)
+    gpu.step(Ug, w.dt, 10)
+    torch.cuda.synchronize()
+    assert rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo).max() <= TOL
+    R = len(w.E)
+    for mask in (1, (1 << R) - 1, 0b0101):
+        dUo = ora.rhs(Uo, mask)
+        dUg = gpu_state_numpy(gpu, gpu.rhs(Ug, mask))
+        torch.cuda.synchronize()
+        scale = np.abs(ora.rhs(Uo)).max(axis=(0, 2))
+        assert (np.abs(dUg - dUo).max(axis=(0, 2)) / scale).max() <= TOL
+
+
+def test_bad_masks_rejected():
     from paper_2403_05144_b200.perk import PerkError, tableau_p2
-    w = W.make(5, n_base=16)
-    with pytest.raises(PerkError) as ei:
-        Perk(w.problem, w.level_map, w.S, w.E, pattern="alternating")
-    assert ei.value.code == -6
     w3 = W.make(3, n_base=8)
     with pytest.raises(PerkError):
         tableau_p2(w3.S, w3.E, pattern=[[1, 2, 16], [1, 2, 4, 5, 6, 7, 8, 16], "standard"])
