@@ -97,7 +97,8 @@ typedef struct perk_problem {
  * c[i-1] = c_i; a_sub[r][i-1] = a_{i,p(i)} of member r, the coefficient of K_{p(i)} in stage i's
  * state, where p(i) is the member's previous evaluated stage > 1 (= i-1 in the standard pattern);
  * it may be nonzero only at evaluated stages that have such a predecessor.  a_{i,1} = c_i - a_sub is
- * derived.  Non-standard patterns: 1D / 2D Euler (not Navier-Stokes).
+ * derived.  Non-standard patterns: 1D / 2D Euler / Navier-Stokes (NS launches the superset member
+ * prefix of each stage).
  * Shared weights b[i-1] = b_i, nonzero only at i = 1, S-1, S:
  *   P-ERK2: b = e_S (P:l.423; perk_tableau_p2 fills it);
  *   P-ERK3: b_1 = b_{S-1} = 1/6, b_S = 4/6 (Shu-Osher base, P:l.870-883), c_{S-1} = 1, c_S = 1/2,
