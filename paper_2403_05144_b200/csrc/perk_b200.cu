@@ -423,13 +423,7 @@ static void launch_sc(perk_ctx *c, cudaStream_t s, const StageParams &sp, const 
 {
     prof_mark(p, s, 6);
     if (!((c->kind_mask >> 6) & 1u)) return;
-    // persistent grid of 4 CTAs per SM; with the epilogue indicator (standard pattern) the stages at
-    // which no member joins only hold the mortar halo (a few hundred elements): one CTA per SM
-    // there (a 592-CTA launch of nearly idle CTAs cost ~7 us per stage, ncu)
-    bool small = sp.mode == MODE_STAGE && c->scp.epi && !c->scp.all && c->scp.alpha_fixed < 0.0 && sp.stage > 2;
-    for (int r = 0; r < c->tab.R && small; ++r)
-        if (sp.stage == c->tab.S - c->tab.E[r] + 2) small = false;   // member r joins at this stage
-    const int ga = std::min(blocks_for(c->cap, AMR_T / 16), SM_COUNT_B200 * (small ? 1 : 4));
+    const int ga = std::min(blocks_for(c->cap, AMR_T / 16), SM_COUNT_B200 * 4);   // persistent: 4 CTAs per SM
     if (sp.mode == MODE_STAGE)
         launch_pdl(k_sc_alpha<MODE_STAGE>, ga, AMR_T, 0, s, c->md, sp, c->scp, Un, (const double *)c->Ubuf, (const double *)c->K1, Uin, c->alpha_raw, c->alpha);
     else
