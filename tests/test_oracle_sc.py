@@ -214,3 +214,26 @@ def test_invalid_parameters():
     p1["shock_capturing"] = {}
     with pytest.raises(ValueError):
         O.OracleMesh(p1, np.zeros(4, np.uint8), FAM1)
+
+
+def test_contact_band_input():
+    """the shock-capturing input (workloads.configs.contact_band): density x 2.5 inside the band,
+    velocity and pressure of the base IC unchanged everywhere"""
+    w = W.make(3, n_base=8)
+    m = O.OracleMesh(w.problem, w.level_map, FAM1)
+    U0 = m.initial_state(w.ic)
+    U1 = m.initial_state(W.configs.contact_band(w.ic))
+    def prim(U):
+        r = U[:, 0]
+        vx, vy = U[:, 1] / r, U[:, 2] / r
+        return r, vx, vy, (G - 1) * (U[:, 3] - 0.5 * r * (vx * vx + vy * vy))
+    r0, vx0, vy0, p0 = prim(U0)
+    r1, vx1, vy1, p1 = prim(U1)
+    ratio = r1 / r0
+    assert np.allclose(vx1, vx0, rtol=1e-13, atol=1e-13) and np.allclose(vy1, vy0, rtol=1e-13, atol=1e-13)
+    assert np.allclose(p1, p0, rtol=1e-12)
+    inside = np.isclose(ratio, 2.5, rtol=1e-14)
+    assert np.all(inside | np.isclose(ratio, 1.0, rtol=1e-14))
+    x = m.node_coords()[:, 0, :]
+    s = (x - x.min()) / (x.max() - x.min())
+    assert np.array_equal(inside, np.abs(s - 0.35) < 0.12)
