@@ -176,22 +176,31 @@ def _neighbours(lv, nf):
 
 
 def test_smoothing_matches_brute_force_neighbours():
+    """4 x 4 base cells, levels 0-2 (64 leaves, interfaces AND mortars between blended and unblended
+    elements, intermediate alpha values)"""
     L = 2
-    lm = _three_level_map()
-    m = O.OracleMesh(_prob(2, L, {"variable": "rho", "alpha_max": 0.8, "alpha_min": 0.001}), lm, FAM1)
-    U = _state(m, seed=5, amp=0.3, jump=True)
+    lm = np.ones((16, 16), np.uint8)
+    lm[0:4, 0:4] = 2
+    lm[8:16, 8:16] = 0
+    p = W.configs._problem(2, "euler", "fluxdiff", "hll", 4, L, 0.0, 1.0, periodic=(1, 1))
+    p["shock_capturing"] = {"variable": "rho", "alpha_max": 0.8, "alpha_min": 0.001}
+    m = O.OracleMesh(p, lm, FAM1)
+    U = _state(m, seed=4, amp=0.2, jump=True)
     raw, sm = m.sc_alpha(U)
     ind = m.amr_indicator(U, {"indicator": "hennemann_gassner", "variable": "rho", "base_level": 0,
                               "med_level": 0, "max_level": L, "med_threshold": 0.1, "max_threshold": 0.5,
                               "alpha_max": 0.8, "alpha_min": 0.001})
     assert np.array_equal(raw, ind)
-    assert 0 < np.count_nonzero(raw) < m.n
-    nbrs = _neighbours(m.leaves(), 2 << L)
+    assert 0 < np.count_nonzero(raw) < m.n and ((raw > 0.01) & (raw < 0.79)).any()
+    f, _ = m.faces("interfaces")
+    assert sum(1 for a, b, o in f if raw[a] != raw[b]) > 10      # interfaces between differing alphas
+    assert m.face_counts()["mortars"] > 0
+    nbrs = _neighbours(m.leaves(), 4 << L)
     exp = np.array([max([raw[e]] + [0.5 * raw[b] for b in nbrs[e]]) for e in range(m.n)])
     assert np.array_equal(sm, exp)
     assert not np.array_equal(sm, raw)                  # the smoothing changed something
-    m2 = O.OracleMesh(_prob(2, L, {"variable": "rho", "alpha_max": 0.8, "smooth": False}), lm, FAM1)
-    raw2, sm2 = m2.sc_alpha(U)
+    p2 = dict(p, shock_capturing={"variable": "rho", "alpha_max": 0.8, "smooth": False})
+    raw2, sm2 = O.OracleMesh(p2, lm, FAM1).sc_alpha(U)
     assert np.array_equal(sm2, raw2) and np.array_equal(raw2, raw)
 
 
