@@ -283,21 +283,25 @@ def test_transfer_polynomial_exact_and_conservative():
     fam = T.family(16, [4, 8, 16], "taylor")
     p = _prob(4, 2, dom=2.0)
     rng = np.random.default_rng(7)
-    lm0 = _random_map(rng, 4, 2)
-    lm1 = lm0.copy()
-    # refine one level-0 block fully and coarsen one level-1 group where possible
-    lm1 = W.balance(np.maximum(lm1, (rng.random(lm1.shape) < 0.05).astype(np.uint8)), 2, (True, True))
-    assert np.abs(lm1.astype(int) - lm0.astype(int)).max() <= 1
+    # 4 x 4 base cells, L = 2 (16 x 16 finest): m0 -> m1 refines base cell (0, 0) from level 0 to 1,
+    # and coarsens base cell (1, 1) from 1 to 0 and a level-2 quadrant of base cell (2, 2) to level 1
+    lm0 = np.ones((16, 16), np.uint8)
+    lm0[0:4, 0:4] = 0
+    lm0[8:10, 8:10] = 2
+    lm1 = np.ones((16, 16), np.uint8)
+    lm1[4:8, 4:8] = 0
     m0 = O.OracleMesh(p, lm0, fam)
     m1 = O.OracleMesh(p, lm1, fam)
+    lv0, lv1 = m0.leaves()["level"], m1.leaves()["level"]
+    assert (lv0 == 0).sum() == 1 and (lv0 == 2).sum() == 4 and (lv1 == 0).sum() == 1 and (lv1 == 2).sum() == 0
 
     def poly(x, y):   # degree <= 3 per direction, one per conserved variable
         return np.stack([1 + x ** 3 - 2 * x * y, y ** 2 * x, 0.5 + y ** 3 * x ** 2, x * x * y * y * y + 2])
 
     U0 = m0.initial_state(poly)
     U1 = O.transfer(m0, m1, U0)
-    assert np.abs(U1 - m1.initial_state(poly)).max() < 1e-12       # refinement + copy exact
-    # coarsen back: projection is exact on the polynomial space too, and conservative
+    assert np.abs(U1 - m1.initial_state(poly)).max() < 1e-12       # refinement, coarsening, copies exact
+    # and back: projection / interpolation exact on the polynomial space, and conservative
     U2 = O.transfer(m1, m0, U1)
     assert np.abs(U2 - U0).max() < 1e-12
     rnd = rng.standard_normal(m1.shape)
