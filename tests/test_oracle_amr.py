@@ -347,3 +347,29 @@ def test_amr_rejects_bad_parameters():
         m.amr_indicator(U, dict(CTRL, max_level=5))
     with pytest.raises(ValueError):
         m.amr_indicator(U, dict(CTRL, med_threshold=20.0))
+
+
+def test_controller_one_level_per_adaptation_from_base():
+    """a base-level leaf whose indicator asks for max_level (2) moves one level only (A4)"""
+    m = _mesh(2, 2, np.zeros((8, 8), np.uint8))
+    t = [0] * m.n
+    t[3] = 2
+    lm = m.amr_adapt(_state_with_targets(m, t), CTRL)
+    lv = m.leaves()
+    blk = lm[lv["fy"][3]:lv["fy"][3] + 4, lv["fx"][3]:lv["fx"][3] + 4]
+    assert np.all(blk == 1)
+    assert int(lm.max()) == 1
+
+
+def test_controller_threshold_is_inclusive():
+    """target = base level if indicator <= med_threshold (A4): a leaf whose indicator EQUALS the
+    threshold coarsens with its siblings; just above it, it keeps the block refined"""
+    m = _mesh(2, 2, np.ones((8, 8), np.uint8))
+    t = [0] * m.n
+    t[0] = 1
+    U = _state_with_targets(m, t)
+    ind = m.amr_indicator(U, CTRL)
+    at = dict(CTRL, med_threshold=float(ind[0]))
+    assert np.all(m.amr_adapt(U, at)[0:4, 0:4] == 0)
+    below = dict(CTRL, med_threshold=float(np.nextafter(ind[0], 0.0)))
+    assert np.all(m.amr_adapt(U, below)[0:4, 0:4] == 1)
