@@ -20,7 +20,7 @@ PLAN = {1: None, 2: None, 3: None, 4: 200, 5: 20}   # None = the BASELINE step c
 
 
 def run(arg):
-    cfg, steps_override = arg
+    cfg, steps_override, variant = arg
     import numpy as np
     import torch
     import workloads as W
@@ -30,9 +30,22 @@ def run(arg):
     from paper_2403_05144_b200 import Perk
     w = W.make(cfg)
     steps = steps_override or PLAN[cfg] or w.steps
-    fam = T.family(w.S, w.E, w.alpha_rule)
+    # variants: p3 = the P-ERK3 family with the config's S, E (f1); alt / early = stage
+    # patterns (f2); sc = subcell shock capturing on the contact-band input (f3)
+    family = pattern = None
+    if variant == "p3":
+        from workloads import perk3 as P3
+        family = fam = P3.family3(w.S, w.E)
+    elif variant in ("alt", "early"):
+        pattern = {"alt": "alternating", "early": "early"}[variant]
+        fam = T.family(w.S, w.E, w.alpha_rule, pattern=pattern)
+    else:
+        fam = T.family(w.S, w.E, w.alpha_rule)
+    if variant == "sc":
+        w.problem = dict(w.problem, shock_capturing=W.configs.SHOCK_CAPTURING)
+        w.ic = W.configs.contact_band(w.ic)
     ora = O.OracleMesh(w.problem, w.level_map, fam)
-    gpu = Perk(w.problem, w.level_map, w.S, w.E)
+    gpu = Perk(w.problem, w.level_map, w.S, w.E, family=family, pattern=pattern)
     Uo = ora.initial_state(w.ic)
     Ug = gpu.initial_state(w.ic)
     t0 = time.time()
@@ -61,21 +74,24 @@ def run(arg):
     err = rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo)
     lo, lg = ora.leaves(), gpu.leaves()
     same_mesh = all(np.array_equal(lo[q], lg[q]) for q in ("fx", "fy", "level", "member"))
-    res = {"workload": w.name, "steps": steps, "baseline_steps": w.steps, "re_meshes": remeshes,
+    res = {"workload": w.name + (f"_{variant}" if variant else ""), "steps": steps, "baseline_steps": w.steps, "re_meshes": remeshes,
            "cells": int(ora.n), "max_rel_err_per_var": [float(x) for x in err], "mesh_identical": same_mesh,
            "pass": bool(err.max() <= 1e-10 and same_mesh), "oracle_seconds": round(time.time() - t0, 1)}
     out = os.path.join(ROOT, "gpurun_out")                # each config's result as soon as it is done
     os.makedirs(out, exist_ok=True)
-    with open(os.path.join(out, f"full_run_parity_cfg{cfg}_{steps}.json"), "w") as f:
+    with open(os.path.join(out, f"full_run_parity_cfg{cfg}{variant}_{steps}.json"), "w") as f:
         json.dump(res, f, indent=1)
-    return cfg, res
+    return f"cfg{cfg}{variant}", res
 
 
 if __name__ == "__main__":
-    # argument: comma list of configs, each optionally "cfg:steps" (e.g. "4:1000,5:200")
+    # argument: comma list of configs, each optionally "cfg[variant]:steps" (e.g. "4:1000,5:200,3p3:500")
     items = [x for x in (sys.argv[1] if len(sys.argv) > 1 else "1,2,3,4,5").split(",") if x]
-    args = [(int(x.split(":")[0]), int(x.split(":")[1]) if ":" in x else None) for x in items]
+    args = []
+    for x in items:
+        head, steps = (x.split(":")[0], int(x.split(":")[1])) if ":" in x else (x, None)
+        args.append((int(head[0]), steps, head[1:]))
     ctx = mp.get_context("spawn")
     with ctx.Pool(len(args)) as pool:
         res = dict(pool.map(run, args))
-    print(json.dumps({"tolerance": 1e-10, "configs": {f"cfg{c}": res[c] for c, _ in args}}, indent=1))
+    print(json.dumps({"tolerance": 1e-10, "configs": res}, indent=1))
