@@ -31,7 +31,8 @@ def run(arg):
     w = W.make(cfg)
     steps = steps_override or PLAN[cfg] or w.steps
     # variants: p3 = the P-ERK3 family with the config's S, E (f1); alt / early = stage
-    # patterns (f2); sc = subcell shock capturing on the contact-band input (f3)
+    # patterns (f2); sc = subcell shock capturing on the contact-band input (f3); i = cfg 4 with the
+    # device AMR indicator + controller instead of the seeded map sequence (f3)
     family = pattern = None
     if variant == "p3":
         from workloads import perk3 as P3
@@ -50,6 +51,7 @@ def run(arg):
     Ug = gpu.initial_state(w.ic)
     t0 = time.time()
     remeshes = 0
+    map_diffs = 0
     if w.remesh_every:
         done = 0
         k = 0
@@ -60,7 +62,12 @@ def run(arg):
             done += n
             if done % w.remesh_every == 0 and done < steps:
                 k += 1
-                lm = w.level_map_seq(k)
+                if variant == "i":   # indicator-driven AMR (f3): both sides adapt; the oracle's map is used
+                    lm = ora.amr_adapt(Uo, w.meta["amr"])
+                    lm_g = gpu.amr_adapt(Ug, w.meta["amr"]).cpu().numpy()
+                    map_diffs += int(not np.array_equal(lm, lm_g))
+                else:
+                    lm = w.level_map_seq(k)
                 new = O.OracleMesh(w.problem, lm, fam)
                 Uo = O.transfer(ora, new, Uo)
                 ora = new
@@ -77,6 +84,8 @@ def run(arg):
     res = {"workload": w.name + (f"_{variant}" if variant else ""), "steps": steps, "baseline_steps": w.steps, "re_meshes": remeshes,
            "cells": int(ora.n), "max_rel_err_per_var": [float(x) for x in err], "mesh_identical": same_mesh,
            "pass": bool(err.max() <= 1e-10 and same_mesh), "oracle_seconds": round(time.time() - t0, 1)}
+    if variant == "i":
+        res["amr_maps_differing"] = map_diffs   # near-threshold ties; 0 = every adapted map bit-exact
     out = os.path.join(ROOT, "gpurun_out")                # each config's result as soon as it is done
     os.makedirs(out, exist_ok=True)
     with open(os.path.join(out, f"full_run_parity_cfg{cfg}{variant}_{steps}.json"), "w") as f:
