@@ -135,11 +135,27 @@ int perk_tableau_p2(int32_t S, int32_t R, const int32_t *E_host, const double *a
 int perk_tableau_p2_ex(int32_t S, int32_t R, const int32_t *E_host, const double *alpha_host,
                        const uint64_t *active_host, double c_S, perk_tableau *out);
 
+/* Host only.  Evaluated-stage set of a member with E evaluations in an S-stage method, as the bit
+ * mask perk_tableau_p2_ex / perk_tableau.active take (bit i-1 = stage i):
+ *   kind PERK_PATTERN_STANDARD    {1} u {S-E+2, ..., S}          (P:l.407-436, eq. PERK_ButcherTableauClassic)
+ *   kind PERK_PATTERN_EARLY       {1, ..., E-1} u {S}            (P:l.683-700: S = 6, E = 4 -> {1,2,3,6})
+ *   kind PERK_PATTERN_ALTERNATING {1} u {S - floor((E-1-k)(S-1)/(E-1) + 1/2) : k = 1..E-1}
+ *                                 (P:l.655-675: S = 6, E = 4 -> {1,3,4,6}; general rule DESIGN.md F1)
+ *   kind PERK_PATTERN_EXPLICIT    the n_stages stage numbers in stages_host (1-based, must hold 1
+ *                                 and S, no duplicates, n_stages == E)
+ * EINVAL on 2 > E, E > S, S > PERK_MAX_STAGES, an unknown kind or an invalid explicit set. */
+enum { PERK_PATTERN_STANDARD = 0, PERK_PATTERN_EARLY = 1, PERK_PATTERN_ALTERNATING = 2, PERK_PATTERN_EXPLICIT = 3 };
+int perk_pattern_mask(int32_t S, int32_t E, int32_t kind, const int32_t *stages_host, int32_t n_stages,
+                      uint64_t *mask_out);
+
 /* Create a context: validates prob/tab (EINVAL, EUNSUPPORTED), uploads the tableau, allocates
  * capacity-sized device buffers and builds the mesh and per-member lists on the device from the
  * finest-grid level map level_map_dev (uint8, (n_base[0] << L) x (n_base[1] << L) entries, x
  * fastest; not retained).  Synchronises once at the end: EUNBALANCED / ECAPACITY are reported here.
- * stream: a cudaStream_t (NULL = legacy stream). */
+ * stream: a cudaStream_t (NULL = legacy stream).
+ * Ownership: unless out / prob / level_map_dev / tab is NULL (EINVAL, *out untouched), *out receives
+ * the context on EVERY return, including errors: read perk_last_error(*out), then release it with
+ * perk_destroy (it frees whatever was allocated before the failure). */
 int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t *level_map_dev, const perk_tableau *tab,
               void *stream);
 int perk_destroy(perk_ctx *ctx);

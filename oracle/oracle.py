@@ -129,6 +129,8 @@ def lib():
         L.ora_amr_indicator.argtypes = [P, dp, C.POINTER(OraAmr), dp]
         L.ora_amr_adapt.restype = C.c_int
         L.ora_amr_adapt.argtypes = [P, dp, C.POINTER(OraAmr), up]
+        L.ora_amr_adapt_ind.restype = C.c_int
+        L.ora_amr_adapt_ind.argtypes = [P, dp, C.POINTER(OraAmr), up]
         L.ora_set_shock_capturing.restype = C.c_int
         L.ora_set_shock_capturing.argtypes = [P, C.POINTER(OraSC)]
         L.ora_sc_alpha.restype = C.c_int
@@ -308,13 +310,20 @@ class OracleMesh:
             raise ValueError(f"amr_indicator: {'unsupported problem' if rc == -2 else 'invalid parameters'}")
         return ind
 
-    def amr_adapt(self, U, amr: dict):
-        """new finest-grid level map (uint8, x fastest) from the controller + 2:1 balance"""
+    def amr_adapt(self, U, amr: dict, indicator=None):
+        """new finest-grid level map (uint8, x fastest) from the controller + 2:1 balance; with
+        `indicator` (per leaf, canonical order) the controller runs on those values instead of the
+        oracle's own indicator of U (U is then unused)"""
         p = self.problem
         nf = [p["n_base"][0] << p["max_level"], p["n_base"][1] << p["max_level"]]
         lmap = np.zeros(nf[0] * nf[1], np.uint8)
         a = amr_struct(amr)
-        rc = lib().ora_amr_adapt(self.h, np.ascontiguousarray(U, np.float64).ravel(), C.byref(a), lmap)
+        if indicator is None:
+            rc = lib().ora_amr_adapt(self.h, np.ascontiguousarray(U, np.float64).ravel(), C.byref(a), lmap)
+        else:
+            ind = np.ascontiguousarray(indicator, np.float64)
+            assert ind.shape == (self.n,)
+            rc = lib().ora_amr_adapt_ind(self.h, ind, C.byref(a), lmap)
         if rc:
             raise ValueError(f"amr_adapt: {'unsupported problem' if rc == -2 else 'invalid parameters'}")
         return lmap.reshape(nf[1], nf[0])

@@ -1411,15 +1411,29 @@ int ora_amr_indicator(void *p, const double *U, const OraAmr *a, double *ind)
       all four wanting to coarsen);
    A6 2:1 face balance (the condition perk_init / perk_repartition check) is restored by refining:
       while some leaf has a face neighbour two or more levels finer, split that leaf. */
+int ora_amr_adapt_ind(void *p, const double *ind, const OraAmr *a, uint8_t *lmap);
+
 int ora_amr_adapt(void *p, const double *U, const OraAmr *a, uint8_t *lmap)
 {
     Ora *o = (Ora *)p;
     int rc = amr_check(o, a);
     if (rc) return rc;
-    int L = o->prob.max_level;
     double *ind = (double *)malloc(sizeof(double) * o->n);
-    int *want = (int *)malloc(sizeof(int) * o->n);
     ora_amr_indicator(p, U, a, ind);
+    rc = ora_amr_adapt_ind(p, ind, a, lmap);
+    free(ind);
+    return rc;
+}
+
+/* the controller + balance alone, on a given per-leaf indicator (tests: the same decisions from
+   another implementation's indicator values) */
+int ora_amr_adapt_ind(void *p, const double *ind, const OraAmr *a, uint8_t *lmap)
+{
+    Ora *o = (Ora *)p;
+    int rc = amr_check(o, a);
+    if (rc) return rc;
+    int L = o->prob.max_level;
+    int *want = (int *)malloc(sizeof(int) * o->n);
     for (int e = 0; e < o->n; ++e) {
         int target = ind[e] <= a->med_threshold ? a->base_level
                    : (ind[e] <= a->max_threshold ? a->med_level : a->max_level);
@@ -1459,7 +1473,6 @@ int ora_amr_adapt(void *p, const double *U, const OraAmr *a, uint8_t *lmap)
                 }
             }
     }
-    free(ind);
     free(want);
     return 0;
 }

@@ -75,6 +75,8 @@ __global__ void k_leaf_flags(MeshDev md, const uint8_t *__restrict__ lmap, long 
     flag[m] = (x % s == 0 && (md.dim == 1 || y % s == 0)) ? 1 : 0;
 }
 
+constexpr int CELL_OVERFLOW = -2;
+
 __global__ void k_check_capacity(MeshDev md)
 {
     if (md.n[0] > md.cap) { atomicOr(md.err, ERR_CAPACITY); md.n[0] = md.cap; }
@@ -104,10 +106,14 @@ __global__ void k_cell_of(MeshDev md, const uint8_t *__restrict__ lmap, const in
     const int x = (int)(c % md.nfx), y = (int)(c / md.nfx);
     const int s = 1 << (md.max_level - lmap[c]);
     const int ox = x - x % s, oy = md.dim == 1 ? 0 : y - y % s;
-    md.cell_of[c] = rank[morton_of(md, ox, oy)];
+    int r = rank[morton_of(md, ox, oy)];
+    // leaves beyond the capacity (md.n[0] was clamped to cap by k_check_capacity) have no storage:
+    // mark them -2 so that no later kernel indexes a cap-sized array with them
+    if (r >= md.n[0]) { atomicOr(md.err, ERR_CAPACITY); r = CELL_OVERFLOW; }
+    md.cell_of[c] = r;
 }
 
-// finest cell (x, y) -> leaf, -1 outside a non-periodic domain
+// finest cell (x, y) -> leaf, -1 outside a non-periodic domain, CELL_OVERFLOW past the capacity
 __device__ __forceinline__ int cell_at(const MeshDev &md, int x, int y)
 {
     if (x < 0 || x >= md.nfx) { if (!md.periodic[0]) return -1; x = wrapi(x, md.nfx); }
@@ -131,6 +137,7 @@ __device__ __forceinline__ SlotInfo classify_slot(const MeshDev &md, int e, int 
     if (orient == 0) { nx = plus ? md.fx[e] + s : md.fx[e] - 1; ny = md.fy[e]; }
     else { nx = md.fx[e]; ny = plus ? md.fy[e] + s : md.fy[e] - 1; }
     const int nb = cell_at(md, nx, ny);
+    if (nb == CELL_OVERFLOW) return r;     // capacity error already latched; no face
     if (nb < 0) { r.cls = SLOT_BND; return r; }
     const int ln = md.lev[nb];
     r.nb = nb;
@@ -147,6 +154,7 @@ __device__ __forceinline__ SlotInfo classify_slot(const MeshDev &md, int e, int 
         else { a0x = md.fx[e]; a0y = ny; a1x = md.fx[e] + h; a1y = ny; }
         r.s0 = cell_at(md, a0x, a0y);
         r.s1 = cell_at(md, a1x, a1y);
+        if (r.s0 < 0 || r.s1 < 0) return r;   // CELL_OVERFLOW (capacity error latched)
         if (md.lev[r.s0] != l + 1 || md.lev[r.s1] != l + 1) {
             if (check) atomicOr(md.err, ERR_UNBALANCED);
             return r;

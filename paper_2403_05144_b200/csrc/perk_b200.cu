@@ -179,6 +179,45 @@ extern "C" int perk_tableau_p2_ex(int32_t S, int32_t R, const int32_t *E, const 
     return PERK_OK;
 }
 
+extern "C" int perk_pattern_mask(int32_t S, int32_t E, int32_t kind, const int32_t *stages, int32_t n_stages,
+                                 uint64_t *mask_out)
+{
+    if (!mask_out || S < 2 || S > PERK_MAX_STAGES || E < 2 || E > S) return PERK_EINVAL;
+    unsigned long long m = 0;
+    switch (kind) {
+    case PERK_PATTERN_STANDARD:
+        m = 1ull;
+        for (int i = S - E + 2; i <= S; ++i) m |= 1ull << (i - 1);
+        break;
+    case PERK_PATTERN_EARLY:
+        for (int i = 1; i <= E - 1; ++i) m |= 1ull << (i - 1);
+        m |= 1ull << (S - 1);
+        break;
+    case PERK_PATTERN_ALTERNATING:
+        // S - floor((E-1-k)(S-1)/(E-1) + 1/2) in integers: floor((2(E-1-k)(S-1) + (E-1)) / (2(E-1)))
+        m = 1ull;
+        for (int k = 1; k <= E - 1; ++k) {
+            const long long num = 2ll * (E - 1 - k) * (S - 1) + (E - 1);
+            m |= 1ull << (S - (int)(num / (2ll * (E - 1))) - 1);
+        }
+        break;
+    case PERK_PATTERN_EXPLICIT:
+        if (!stages || n_stages != E) return PERK_EINVAL;
+        for (int k = 0; k < n_stages; ++k) {
+            const int i = stages[k];
+            if (i < 1 || i > S || ((m >> (i - 1)) & 1ull)) return PERK_EINVAL;
+            m |= 1ull << (i - 1);
+        }
+        if (!(m & 1ull) || !((m >> (S - 1)) & 1ull)) return PERK_EINVAL;
+        break;
+    default:
+        return PERK_EINVAL;
+    }
+    if (__builtin_popcountll(m) != E) return PERK_EINVAL;   // e.g. an alternating rule collision
+    *mask_out = m;
+    return PERK_OK;
+}
+
 extern "C" int perk_tableau_p2(int32_t S, int32_t R, const int32_t *E, const double *alpha, perk_tableau *out)
 {
     return perk_tableau_p2_ex(S, R, E, alpha, nullptr, 0.5, out);
@@ -596,8 +635,11 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
     if (!out || !prob || !level_map_dev || !tab) return PERK_EINVAL;
     *out = nullptr;
     perk_ctx *c = new perk_ctx();
+    // the handle is returned on every path from here on, so that a caller can read perk_last_error
+    // and release the partially built context (streams, device buffers) with perk_destroy
+    *out = c;
     int rc = validate(c, prob, tab);
-    if (rc) { *out = c; return rc; }
+    if (rc) return rc;
     c->prob = *prob;
     c->tab = *tab;
     c->stream = (cudaStream_t)stream;

@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(256) k_transfer2d(MeshDev md, OldMesh om, int 
         const int L = md.max_level, l = md.lev[e], s = 1 << (L - l);
         const int fx = md.fx[e], fy = md.fy[e];
         const int eo = om.cell_of[(size_t)fy * md.nfx + fx];
+        if (eo < 0) { atomicOr(md.err, ERR_CAPACITY); continue; }   // the old mesh had overflowed
         PERK_DASSERT(eo >= 0 && eo < *om.n_old);
         const int lo = om.lev[eo];
         double out[4] = {0.0, 0.0, 0.0, 0.0};
@@ -100,6 +101,7 @@ __global__ void __launch_bounds__(256) k_transfer2d(MeshDev md, OldMesh om, int 
             for (int c = 0; c < 4; ++c) {
                 const int cx = c & 1, cy = c >> 1;
                 const int ec = om.cell_of[(size_t)(fy + cy * h) * md.nfx + fx + cx * h];
+                if (ec < 0) { atomicOr(md.err, ERR_CAPACITY); continue; }
                 PERK_DASSERT(ec >= 0 && ec < *om.n_old);
                 if (om.lev[ec] != l + 1) { atomicOr(md.err, ERR_TRANSFER); continue; }
                 stage(ec);

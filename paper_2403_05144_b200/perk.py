@@ -100,6 +100,7 @@ def lib():
         L.perk_tableau_p2.argtypes = [i32, i32, C.POINTER(i32), C.POINTER(dbl), C.POINTER(perk_tableau)]
         L.perk_tableau_p2_ex.argtypes = [i32, i32, C.POINTER(i32), C.POINTER(dbl), C.POINTER(C.c_uint64), dbl,
                                          C.POINTER(perk_tableau)]
+        L.perk_pattern_mask.argtypes = [i32, i32, i32, C.POINTER(i32), i32, C.POINTER(C.c_uint64)]
         L.perk_init.argtypes = [C.POINTER(P), C.POINTER(perk_problem), P, C.POINTER(perk_tableau), P]
         L.perk_destroy.argtypes = [P]
         L.perk_set_stream.argtypes = [P, P]
@@ -137,26 +138,26 @@ def exported_symbols():
             "perk_get_leaves", "perk_get_faces", "perk_get_list", "perk_get_count_active", "perk_get_counters",
             "perk_sync", "perk_last_error", "perk_profile_step", "perk_time_kernels", "perk_profile_repartition",
             "perk_launches_per_step", "perk_amr_indicator", "perk_amr_adapt", "perk_amr_launches",
-            "perk_set_shock_capturing", "perk_sc_alpha"]
+            "perk_set_shock_capturing", "perk_sc_alpha", "perk_pattern_mask"]
+
+
+PATTERNS = {"standard": 0, "early": 1, "alternating": 2}
 
 
 def pattern_mask(S: int, E: int, pattern) -> int:
-    """Evaluated-stage bitmask (bit i-1 = stage i) of a member with E evaluations: "standard"
-    {1} u {S-E+2..S} (P:l.407-436), "early" {1..E-1} u {S} (P:l.683-700), "alternating"
-    {1} u {S - floor((E-1-k)(S-1)/(E-1) + 1/2) : k = 1..E-1} (P:l.655-675 at S = 6, E = 4; F1),
-    or an explicit iterable of stages."""
-    if pattern == "standard":
-        st = [1] + list(range(S - E + 2, S + 1))
-    elif pattern == "early":
-        st = list(range(1, E)) + [S]
-    elif pattern == "alternating":
-        st = [1] + [S - ((E - 1 - k) * (S - 1) * 2 + (E - 1)) // (2 * (E - 1)) for k in range(1, E)]
+    """Evaluated-stage bitmask (bit i-1 = stage i) of a member with E evaluations, computed by the
+    library (perk_pattern_mask, include/perk.h): "standard", "early", "alternating" or an explicit
+    iterable of stages."""
+    m = C.c_uint64()
+    if isinstance(pattern, str):
+        if pattern not in PATTERNS:
+            raise PerkError(-1, f"unknown stage pattern {pattern!r}")
+        _check(None, lib().perk_pattern_mask(int(S), int(E), PATTERNS[pattern], None, 0, C.byref(m)))
     else:
         st = [int(i) for i in pattern]
-    m = 0
-    for i in st:
-        m |= 1 << (i - 1)
-    return m
+        arr = (C.c_int32 * max(len(st), 1))(*st)
+        _check(None, lib().perk_pattern_mask(int(S), int(E), 3, arr, len(st), C.byref(m)))
+    return int(m.value)
 
 
 def tableau_p2(S: int, E, alpha_rows=None, pattern=None, c_S: float = 0.5) -> perk_tableau:

@@ -111,3 +111,22 @@ def test_invalid_patterns_rejected(lib):
                 [[1, 2, 3, 4], [1, 2, 4, 5, 8], "standard"]):  # stage S missing
         with pytest.raises(lib.PerkError):
             lib.tableau_p2(8, [4, 5, 8], pattern=pat)
+
+
+def test_pattern_mask_behind_the_abi(lib):
+    """perk_pattern_mask (the stage-pattern rule lives in the library, not the binding) against the
+    oracle's stage sets, every S <= 40 and 2 <= E <= S, plus the printed S = 6, E = 4 sets
+    (P:l.655-700: alternating {1,3,4,6}, early-shared {1,2,3,6})"""
+    assert lib.pattern_mask(6, 4, "alternating") == 0b101101
+    assert lib.pattern_mask(6, 4, "early") == 0b100111
+    for S in range(2, 41):
+        for E in range(2, S + 1):
+            for pat in ("standard", "early", "alternating"):
+                want = sum(1 << (i - 1) for i in T.pattern_stages(S, E, pat))
+                assert lib.pattern_mask(S, E, pat) == want, (S, E, pat)
+    assert lib.pattern_mask(8, 4, [1, 3, 6, 8]) == 0b10100101
+    for bad in ([1, 3, 3, 8], [2, 3, 6, 8], [1, 3, 6, 7], [1, 3, 8], [1, 3, 6, 9]):
+        with pytest.raises(lib.PerkError):
+            lib.pattern_mask(8, 4, bad)
+    with pytest.raises(lib.PerkError):
+        lib.pattern_mask(8, 9, "standard")

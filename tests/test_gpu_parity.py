@@ -477,6 +477,32 @@ def test_repartition_errors_latch():
     assert ei.value.code == -2
 
 
+def test_capacity_large_overflow_is_clean():
+    """a large overflow (cap = n/4 on the ~78k-cell cfg-4 mesh, at perk_init and during a
+    device re-mesh) must latch PERK_ECAPACITY without an out-of-bounds access: no sticky CUDA error,
+    so a fresh context on the same device still runs and matches the oracle."""
+    from paper_2403_05144_b200 import Perk, PerkError
+    w = W.make(4)
+    n0 = W.configs.count_leaves(w)
+    with pytest.raises(PerkError) as ei:
+        Perk(w.problem, w.level_map, w.S, w.E, max_cells=n0 // 4)
+    assert ei.value.code == -3
+    coarse = W.make(4, widths=(0.3, 0.15, 0.06, 0.0))       # no level-4 band: fewer cells
+    nc = W.configs.count_leaves(coarse)
+    assert nc < n0
+    gpu = Perk(w.problem, coarse.level_map, w.S, w.E, max_cells=nc)
+    U = gpu.initial_state(w.ic)
+    gpu.repartition(w.level_map, U)                          # needs n0 > cap cells
+    with pytest.raises(PerkError) as ei:
+        gpu.sync()
+    assert ei.value.code == -3
+    torch.cuda.synchronize()                                 # raises on a sticky device error
+    small = W.make(3, n_base=16, steps=3)
+    ora, g2 = build_pair(small)
+    Uo, Ug = _run_both(small, small.steps, ora, g2)
+    assert max(rel_err_per_var(Ug, Uo)) < TOL
+
+
 def test_1d_repartition_unsupported():
     from paper_2403_05144_b200 import Perk, PerkError
     w = W.make(1)

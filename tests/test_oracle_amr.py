@@ -373,3 +373,20 @@ def test_controller_threshold_is_inclusive():
     assert np.all(m.amr_adapt(U, at)[0:4, 0:4] == 0)
     below = dict(CTRL, med_threshold=float(np.nextafter(ind[0], 0.0)))
     assert np.all(m.amr_adapt(U, below)[0:4, 0:4] == 1)
+
+
+def test_controller_on_given_indicator_equals_adapt():
+    """ora_amr_adapt_ind (the controller + balance on given indicator values, used by the GPU map
+    comparison) is ora_amr_adapt without the indicator pass"""
+    m = _mesh(2, 2, np.ones((8, 8), np.uint8))
+    t = [0] * m.n
+    t[5], t[12] = 1, 2
+    U = _state_with_targets(m, t)
+    ind = m.amr_indicator(U, CTRL)
+    assert np.array_equal(m.amr_adapt(None, CTRL, indicator=ind), m.amr_adapt(U, CTRL))
+    flipped = ind.copy()
+    flipped[12] = 0.0                            # leaf 12 wants to coarsen like its siblings
+    lm = m.amr_adapt(None, CTRL, indicator=flipped)
+    lv = m.leaves()
+    assert m.amr_adapt(U, CTRL)[lv["fy"][12], lv["fx"][12]] == 2
+    assert lm[lv["fy"][12], lv["fx"][12]] == 0
