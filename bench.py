@@ -1,24 +1,31 @@
 """bench.py -- P-ERK multirate DGSEM step on B200 (BASELINE.json metric), one JSON line on rank 0.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
 
-Workload (default): BASELINE.json configs[2] = cfg 3, 2D Euler on the seeded 3-level quadtree
-(62,932 cells, 1.007M nodes), P-ERK2 {4, 8, 16}; DESIGN.md §6 says why cfg 3 is the headline.
-A "step" is one full P-ERK step (S = 16 stages: surface-flux + volume/stage kernels per stage).
+Workload (default): BASELINE.json configs[4] = cfg 5, the largest configuration: 2D Navier-Stokes
+(BR1) on the seeded 4-level quadtree (305,827 cells, 4.89M nodes), P-ERK2 {4, 8, 16, 32}; DESIGN.md
+§6 says why cfg 5 is the headline.  A "step" is one full P-ERK step (S = 32 stages: BR1 gradient
+traces + gradients, surface flux, volume/stage kernels per stage).
 `value` = element-RHS evaluations/s (sum_r E_r N_C(r) per step / device time per step), whole job.
 Timing: W warm-up steps, then K steps each bracketed by CUDA events on the launching stream with
 an L2 flush (256 MB write) between timed steps; barrier + synchronize on both sides; max over
-ranks.  N > 1 runs independent replicas of the workload (weak scaling; no data-path collective:
-the multi-GPU domain decomposition of SURVEY §8(e) is not built).
-`other_configs` adds the same measurement for BASELINE cfg 1, 2 (1D, launch-latency bound), cfg 4
-(dynamic AMR: device re-mesh every 5 steps inside the timed steps, repartition time reported
-separately), cfg 5 (Navier-Stokes, BR1) and cfg 3 with the third-order P-ERK3 family (SURVEY §8(f)
-f1), cfg 4 with indicator-driven AMR instead of the seeded map sequence (`4i`: perk_amr_adapt +
-perk_repartition every 5 steps) and cfg 3 with the alternating / early-shared stage
-patterns (`3alt`, `3early`) and cfg 3 / 5 with subcell shock capturing on a contact
-band (`3sc`, `5sc`), so one run shows every config (--extra none skips them).
---impl reference times the oracle (oracle/, plain C, 1 host core) on a bounded sample of the same
-workload (full-mesh P-ERK steps, at most ~120 s of CPU work).
+ranks.  N > 1 decomposes ONE problem over the N GPUs (E-weighted Morton ranges, per-stage ghost exchange
+by NCCL point-to-point; "scaling": "strong"); --replicas runs N independent copies instead.
+Per kernel kind: graph replays holding only that kind's launches of a step, L2 flushed between the
+replays (perk_time_kernels_ex), against its algorithmic bytes (`kernel_bytes_per_step`)
+and, from the committed ncu counts of the same kernels (profiles/r02_kernel_counts_cfg*.json), its
+executed fp64 flops; `roofline` is the dominant kernel's, `roofline_kernels` lists every kind.
+`other_configs` adds the same measurement for BASELINE cfg 3 (with its own per-kernel rooflines) and
+cfg 1, 2 (1D, launch-latency bound), cfg 4 (dynamic AMR: device re-mesh every 5 steps inside the
+timed steps, repartition time reported separately), cfg 3 with the third-order P-ERK3 family
+(SURVEY §8(f) f1), cfg 4 with indicator-driven AMR instead of the seeded map sequence (`4i`:
+perk_amr_adapt + perk_repartition every 5 steps), cfg 3 with the alternating /
+early-shared stage patterns (`3alt`, `3early`) and cfg 3 / 5 with subcell shock
+capturing on a contact band (`3sc`, `5sc`), so one run shows every config
+(--extra none skips them).
+cpu_baseline: the oracle (oracle/, plain C) on this host, all cores (OpenMP build, bitwise the
+serial one) and 1 thread, on bounded samples of the same workload.
+--impl reference times the same oracle on all host cores on a bounded sample (a few minutes at most).
 """
 from __future__ import annotations
 
@@ -42,14 +49,10 @@ import workloads as W  # noqa: E402
 METRIC = "element-RHS evals/s per P-ERK step (fp64)"
 UNIT = "element-RHS/s"
 
-# Executed fp64 work of the hot kernels per element-RHS: counted with ncu
-# (smsp__sass_thread_inst_executed_op_{dfma,dmul,dadd}_pred_on.sum over all 32 launches of one cfg-3
-# step, profiles/r01_fp64_ops_dram_per_step_v13.csv) and divided by the step's 713,596 element-RHS;
-# flops = 2 DFMA + DMUL + DADD.  Cold-cache DRAM bytes of the same launches (ncu, per launch average)
-# give `traffic`.
-VOL_FLOPS_PER_ELEMENT_RHS = 6401.9        # k_vol2d (volume + lift + Jacobian + stage epilogue)
-SURF_FLOPS_PER_ELEMENT_RHS = 947.3        # k_surf2d (HLL interface / mortar fluxes)
-VOL_DRAM_BYTES_PER_LAUNCH = (1335842816.0 + 74005504.0) / 16   # k_vol2d, cold cache (ncu flushes)
+# kernel kinds of perk_time_kernels / perk_profile_step (include/perk.h PERK_NUM_KERNEL_KINDS)
+KIND_NAMES = {0: "surface", 1: "volume_stage", 4: "br1_gradient_traces", 5: "br1_gradients"}
+KERNEL_OF_KIND = {0: "k_surf2d", 1: "k_vol2d", 4: "k_gsurf2d", 5: "k_grad2d"}
+LIB = os.path.join(ROOT, "paper_2403_05144_b200", "lib", "libperk_b200.so")
 
 
 def _peaks():
@@ -130,23 +133,89 @@ def _dist():
     return ws, rank, local
 
 
-def _volume_bytes_per_step(count_el, S):
-    """Algorithmic HBM bytes of the volume/stage kernel per step: per element-stage
-    8 B x 64 doubles for each state-sized vector it must touch:
-      stage 1           : read U_n, Fs; write K_1                      -> 3 x 512 B
-      first active i>1  : read U_n, K_1 (lazy state), Fs; write U^(i+1) -> 4 x 512 B
-      later 1 < i < S   : read U^(i), U_n, K_1, Fs; write U^(i+1)      -> 5 x 512 B
-      stage S           : read U^(S), U_n, Fs; write U_{n+1}            -> 4 x 512 B"""
-    B = 512
-    tot = 3 * B * count_el[0]
-    for i in range(2, S + 1):
-        n = count_el[i - 1]
-        newly = n - (count_el[i - 2] if i > 2 else 0)
-        if i == S:
-            tot += 4 * B * n
-        else:
-            tot += 4 * B * newly + 5 * B * (n - newly)
-    return tot
+def kernel_bytes_per_step(perk, w):
+    """Algorithmic HBM bytes per P-ERK step of every 2D kernel kind, from the device
+    lists (standard stage pattern, P-ERK2): the bytes each kernel must move at least, counting a
+    lazily formed stage state U_n + dt c_i K_1 as two reads.  Units: a state block of an element
+    512 B (16 nodes x 4 variables x 8 B), a face trace 128 B (4 nodes x 4 variables), a face-flux
+    slot 128 B, a BR1 face slice of Gs / Vt 96 B (4 nodes x 3 components).  Member r (E[r]) is
+    active at stage i iff i = 1 or i >= S - E[r] + 2 and its stage state is lazy iff
+    2 <= i <= S - E[r] + 2.
+      k_vol2d   stage 1: U_n + Fs read, K_1 write; 1 < i < S: (U^(i) or lazy U_n, K_1) + U_n + K_1 +
+                Fs read, U^(i+1) write; stage S: state + U_n + Fs read, U_{n+1} write (+ Gs 384 B, NS)
+      k_surf2d  interface: 2 traces + 2 flux slots (+ 2 Vt slices, NS); mortar: 3 traces + 3 slots
+                (+ 3 Vt slices); boundary: 1 trace + 1 slot
+      k_gsurf2d (NS) active + halo interfaces: 2 traces + 2 Gs slices; mortars: 3 traces + 3 slices;
+                halo items are lazy (their member is inactive at the stage)
+      k_grad2d  (NS) active + halo elements: stage state + Gs (384 B) read, Vt (384 B) write"""
+    S, E, R = w.S, list(w.E), len(w.E)
+    ns = w.problem["equation"] == "navier_stokes"
+    segs = {}
+    for kind in ("elements", "interfaces", "mortars", "boundaries"):
+        seg = perk.list(kind)[1]
+        segs[kind] = [int(seg[R - 1 - r + 1] - seg[R - 1 - r]) for r in range(R)]   # per member r
+    halo = perk.halo_counts() if ns else None
+
+    def active(r, i):
+        return i == 1 or i >= S - E[r] + 2
+
+    def lazy(r, i):
+        return 2 <= i <= S - E[r] + 2
+
+    def tr(r, i):
+        return 256 if lazy(r, i) else 128
+
+    out = {"volume_stage": 0, "surface": 0}
+    if ns:
+        out.update(br1_gradient_traces=0, br1_gradients=0)
+    for i in range(1, S + 1):
+        for r in range(R):
+            if not active(r, i):
+                continue
+            ne, ni, nm, nb = (segs[k][r] for k in ("elements", "interfaces", "mortars", "boundaries"))
+            rl = max(r - 1, 0)                     # member of a mortar's large side
+            if i == 1:
+                vb = 1536
+            elif i < S:
+                vb = 2048 if lazy(r, i) else 2560
+            else:
+                vb = 2048
+            out["volume_stage"] += ne * (vb + (384 if ns else 0))
+            out["surface"] += ni * (2 * tr(r, i) + 2 * 128 + (2 * 96 if ns else 0))
+            out["surface"] += nm * (tr(rl, i) + 2 * tr(r, i) + 3 * 128 + (3 * 96 if ns else 0))
+            out["surface"] += nb * (tr(r, i) + 128)
+            if ns:
+                out["br1_gradient_traces"] += ni * (2 * tr(r, i) + 2 * 96) + nm * (tr(rl, i) + 2 * tr(r, i) + 3 * 96)
+                out["br1_gradients"] += ne * ((1024 if lazy(r, i) else 512) + 2 * 384)
+        if ns:
+            out["br1_gradient_traces"] += int(halo["interfaces"][i - 1]) * (2 * 256 + 2 * 96) + \
+                int(halo["mortars"][i - 1]) * (3 * 256 + 3 * 96)
+            out["br1_gradients"] += int(halo["elements"][i - 1]) * (1024 + 2 * 384)
+    return out
+
+
+def _lib_sha():
+    import hashlib
+    try:
+        with open(LIB, "rb") as f:
+            return hashlib.sha256(f.read()).hexdigest()[:16]
+    except OSError:
+        return None
+
+
+def kernel_counts(cfg):
+    """ncu counts of the current kernels (profiles/r02_kernel_counts_cfg<cfg>.json, written by
+    tools/kernel_counts.py from one ncu pass over every launch of one P-ERK step): per kernel kind the
+    executed fp64 flops (2 DFMA + DMUL + DADD) and the cold-cache DRAM bytes per step."""
+    path = os.path.join(ROOT, "profiles", f"r02_kernel_counts_cfg{cfg}.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+    except (OSError, ValueError):
+        return None
+    d["_path"] = os.path.relpath(path, ROOT)
+    d["_current_build"] = d.get("lib_sha16") == _lib_sha()
+    return d
 
 
 class _Timer:
@@ -297,17 +366,130 @@ def measure_config(cfg, K, Wm, timer, torch, dist, ws, dev, with_single=True, or
     return perk, U, w, res
 
 
+def kernel_report(perk, w, cfg, timer, torch, elem_rhs_per_step, fp64, hbm):
+    """Per kernel kind: flushed graph-replay time per step (perk_time_kernels_ex), algorithmic bytes
+    (kernel_bytes_per_step) and executed fp64 flops (committed ncu counts) -> HBM and fp64 roofline
+    fractions; the dominant kernel's larger fraction is the line's `roofline`."""
+    fp64_peak, fp64_src = fp64
+    hbm_peak, hbm_src = hbm
+    ns = w.problem["equation"] == "navier_stokes"
+    kinds = [0, 1] + ([4, 5] if ns else [])
+    U0 = perk.initial_state(w.ic)
+    ms_k = {k: perk.time_kernels(U0.clone(), w.dt, [k], reps=10, flush=timer.flush) for k in kinds}
+    ms_all = perk.time_kernels(U0.clone(), w.dt, kinds, reps=10, flush=timer.flush)
+    nbytes = kernel_bytes_per_step(perk, w)
+    counts = kernel_counts(cfg)
+    S = w.S
+    roofs = {}
+    for k in kinds:
+        name = KIND_NAMES[k]
+        ms = ms_k[k]
+        cnt = (counts or {}).get("kinds", {}).get(name)
+        gbs = nbytes[name] / (ms * 1e-3) / 1e9
+        kname = KERNEL_OF_KIND[k] + ("<MODE_STAGE, NS>" if ns else "<MODE_STAGE>")
+        traffic = round(cnt["dram_bytes_per_step"] / S) if cnt else None
+        r_h = {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+               "frac": round(gbs / hbm_peak, 4), "traffic": traffic, "kernel": kname, "peak_source": hbm_src,
+               "algorithmic_bytes_per_launch": round(nbytes[name] / S), "launches_per_step": S,
+               "kernel_ms_per_launch": round(ms / S, 5), "kernel_ms_per_step": round(ms, 5)}
+        r = {"hbm": r_h}
+        if cnt and cnt.get("fp64_flops_per_step"):
+            tf = cnt["fp64_flops_per_step"] / (ms * 1e-3) / 1e12
+            r["alu"] = {"bound": "alu", "achieved": round(tf, 3), "peak": round(fp64_peak, 2), "unit": "TFLOP/s",
+                        "frac": round(tf / fp64_peak, 4), "traffic": traffic, "kernel": kname,
+                        "peak_source": fp64_src,
+                        "fp64_flops_per_element_rhs": round(cnt["fp64_flops_per_step"] / elem_rhs_per_step, 1)}
+        roofs[name] = r
+    if counts:
+        note = (f"traffic and flops: {counts['_path']} (ncu, one step, cold cache: ncu flushes caches between "
+                f"replays); captured on {'this' if counts['_current_build'] else 'an EARLIER'} build of the library")
+    else:
+        note = "no ncu counts for this config: traffic null, no fp64 roofline"
+    dom = max(kinds, key=lambda k: ms_k[k])
+    rd = roofs[KIND_NAMES[dom]]
+    best = max(rd.values(), key=lambda r: r["frac"])
+    other = [r for r in rd.values() if r is not best]
+    kern = {KIND_NAMES[k]: round(ms_k[k], 5) for k in kinds}
+    kern["all_kinds_graph"] = round(ms_all, 5)
+    kern["timing"] = "graph replays holding only that kind's launches of a step, L2 flushed between replays"
+    return kern, roofs, best, (other[0] if other else None), note
+
+
+def e2e_report(perk, w, U0, args, ws, elem_rhs_per_step, torch):
+    """end to end through the public API with HOST buffers (pinned): perk_run_host copies the step's
+    input state to the device, runs the step and copies the result back, inside the timed region"""
+    n = perk.n_cells
+    npe = 4 ** w.problem["dim"]
+    Uh = U0[:n].cpu().pin_memory()
+    e2e_steps = max(3, min(args.steps, 10))
+    perk.run_host(Uh, w.dt, 1)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        perk.run_host(Uh, w.dt, 1)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    h2d = int(n * w.nv * npe * 8)
+    return {"value": round(ws * elem_rhs_per_step / e2e_s, 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": h2d, "ms_per_step": round(1e3 * e2e_s, 4),
+            "how": "perk_run_host (pinned host state in, step, state out, synchronise), wall clock per call"}
+
+
+def run_decomposed(args, torch, dist, ws, rank, local, dev):
+    """N > 1: ONE problem decomposed over the N GPUs: each rank owns an E-weighted
+    contiguous Morton range of the BASELINE mesh (DistributedPerk: the library's stage launches and
+    pack / unpack kernels, the ghost blocks moved by NCCL point-to-point per stage).  Total work is
+    fixed as N grows ("scaling": "strong"); value = the whole mesh's element-RHS per step / the
+    slowest rank's device time per step."""
+    from paper_2403_05144_b200 import DistributedPerk
+    w = W.make(args.config)
+    timer = _Timer(torch, dev, ws, dist)
+    with ClockSampler(local) as clk:
+        dp = DistributedPerk(w.problem, w.level_map, w.S, w.E, dist)
+        U = dp.initial_state(w.ic)
+        ts = timer.steps(lambda k: dp.step(U, w.dt), args.steps, args.warmup)
+    ms = _max_over_ranks(torch, dist, ws, dev, float(np.mean(ts)))
+    ev, st = dp.counters()
+    t = torch.tensor([ev], dtype=torch.int64, device=dev)
+    dist.all_reduce(t)
+    elem_rhs_per_step = float(t.item()) / max(st, 1)
+    f, c = dp.owned()
+    if rank == 0:
+        n = dp.p.n_cells
+        npe = 4 ** w.problem["dim"]
+        value = elem_rhs_per_step / (ms * 1e-3)
+        line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator workloads/, DESIGN.md §3)",
+                "config": {"workload": w.name, "cells": n, "nodes": n * npe, "S": w.S, "E": w.E,
+                           "element_rhs_per_step": elem_rhs_per_step, "dt": w.dt,
+                           "l2": "flushed between timed steps (256 MB write, outside the events)",
+                           "parallelism": f"domain decomposition x{ws} (E-weighted Morton ranges, NCCL ghost "
+                                          f"exchange per stage)", "rank0_owned_cells": c},
+                "dof_stage_updates_per_s": round(value * npe, 1),
+                "gpu_launches": (dp.p.launches_per_step() + w.S * len(dp.peers) * 2 * (2 if dp.ns else 1)) * args.steps,
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    dp.close()
+    dist.destroy_process_group()
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     ws, rank, local = _dist()
+    if ws > 1 and not args.replicas:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+        return run_decomposed(args, torch, dist, ws, rank, local, torch.device("cuda", local))
     torch.cuda.set_device(local)
     if ws > 1:
         dist.init_process_group("nccl")
     dev = torch.device("cuda", local)
     timer = _Timer(torch, dev, ws, dist)
-    fp64_peak, fp64_src = _fp64_peak()
+    fp64 = _fp64_peak()
+    peaks, src = _peaks()
+    hbm = (float(peaks.get("hbm_gbs", 6650.0)), src)
 
     from paper_2403_05144_b200 import Perk  # noqa: F401  (fails loudly without the CUDA library)
     with ClockSampler(local) as clk:
@@ -318,7 +500,7 @@ def run_ours(args):
         Usoak = soak.initial_state(w0.ic)
         t_soak = time.perf_counter()
         while time.perf_counter() - t_soak < 0.5:
-            for _ in range(50):
+            for _ in range(10):
                 soak.step(Usoak, w0.dt)
             torch.cuda.synchronize()
         soak.close()
@@ -329,63 +511,11 @@ def run_ours(args):
     ms = res["ms_per_step"]
     value = res["value"]
     elem_rhs_per_step = res["element_rhs_per_step"]
-    count_el = [int(x) for x in perk.count_active("elements")]
-
-    # per-kernel device time: CUDA events around graph replays that contain only that kernel kind's
-    # launches of a step, launched exactly as perk_step launches them (perk_time_kernels); the eager
-    # numbers (events around every individual launch) include ~5 us of launch path per kernel
-    from paper_2403_05144_b200.perk import NKINDS
-    prof_steps = 3
-    ms_e = np.zeros(NKINDS)
+    kern = roofs = best = other = note = None
+    if w.problem["dim"] == 2:
+        kern, roofs, best, other, note = kernel_report(perk, w, args.config, timer, torch, elem_rhs_per_step, fp64, hbm)
     U0 = perk.initial_state(w.ic)
-    Up = U0.clone()
-    for _ in range(prof_steps):
-        m_, _l = perk.profile_step(Up, w.dt)
-        ms_e += np.array(m_)
-    ms_e /= prof_steps
-    kinds = [0, 1] + ([4, 5] if w.problem["equation"] == "navier_stokes" else [])
-    ms_k = np.zeros(NKINDS)
-    for k in kinds:
-        ms_k[k] = perk.time_kernels(U0.clone(), w.dt, [k], reps=10)
-    ms_all = perk.time_kernels(U0.clone(), w.dt, kinds, reps=10)
-    kern = {"surface": round(ms_k[0], 5), "volume_stage": round(ms_k[1], 5), "all_kinds_graph": round(ms_all, 5),
-            "eager_launches": {"surface": round(ms_e[0], 5), "volume_stage": round(ms_e[1], 5)}}
-    if w.problem["equation"] == "navier_stokes":
-        kern.update(br1_gradient_traces=round(ms_k[4], 5), br1_gradients=round(ms_k[5], 5))
-    vol_ms = ms_k[1]
-    peaks, src = _peaks()
-    hbm = float(peaks.get("hbm_gbs", 6650.0))
-    line_roof = None
-    if w.problem["dim"] == 2 and w.problem["equation"] == "euler":
-        vol_bytes = _volume_bytes_per_step(count_el, w.S)
-        launches = w.S
-        achieved_gbs = vol_bytes / (vol_ms * 1e-3) / 1e9
-        achieved_tf = elem_rhs_per_step * VOL_FLOPS_PER_ELEMENT_RHS / (vol_ms * 1e-3) / 1e12
-        kname = "k_vol2d<MODE_STAGE> (volume + surface lift + Jacobian + stage epilogue)"
-        roof_hbm = {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": hbm, "unit": "GB/s",
-                    "frac": round(achieved_gbs / hbm, 4), "traffic": round(VOL_DRAM_BYTES_PER_LAUNCH),
-                    "kernel": kname, "peak_source": src,
-                    "algorithmic_bytes_per_launch": round(vol_bytes / launches),
-                    "kernel_ms_per_launch": round(vol_ms / launches, 5),
-                    "traffic_note": "ncu dram bytes per launch, cold cache (ncu flushes caches between replays)"}
-        roof_alu = {"bound": "alu", "achieved": round(achieved_tf, 3), "peak": round(fp64_peak, 2),
-                    "unit": "TFLOP/s", "frac": round(achieved_tf / fp64_peak, 4), "traffic": roof_hbm["traffic"],
-                    "kernel": kname, "peak_source": fp64_src,
-                    "flops_per_element_rhs": VOL_FLOPS_PER_ELEMENT_RHS}
-        roof = roof_alu if roof_alu["frac"] >= roof_hbm["frac"] else roof_hbm
-        line_roof = (roof, roof_hbm if roof is roof_alu else roof_alu)
-
-    # end to end through the public API with HOST buffers (pinned), copies inside the timed region
-    Uh = U0[:n].cpu().pin_memory()
-    e2e_steps = max(3, min(args.steps, 20))
-    perk.run_host(Uh, w.dt, 1)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        perk.run_host(Uh, w.dt, 1)
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
-    e2e_val = ws * elem_rhs_per_step / e2e_s
-    h2d = int(n * w.nv * npe * 8)
+    e2e = e2e_report(perk, w, U0, args, ws, elem_rhs_per_step, torch)
     launches = perk.launches_per_step()
     perk.close()
 
@@ -399,10 +529,18 @@ def run_ours(args):
             if c == args.config and order == 2 and not amr and not pattern and not sc:
                 continue
             try:
-                p2, _U, _w, r2 = measure_config(c, max(5, min(args.steps, 20)), args.warmup, timer, torch, dist,
-                                                 ws, dev, order=order, amr=amr, pattern=pattern, sc=sc)
+                Ko = max(5, min(args.steps, 20))
+                p2, _U, _w, r2 = measure_config(c, Ko, args.warmup, timer, torch, dist, ws, dev, order=order, amr=amr,
+                                                 pattern=pattern, sc=sc)
                 r2["dof_stage_updates_per_s"] = round(r2["value"] * 4 ** _w.problem["dim"], 1)
                 r2["gpu_launches_per_step"] = p2.launches_per_step()
+                if order == 2 and not amr and not pattern and not sc and _w.problem["dim"] == 2 and not _w.remesh_every:
+                    # a static 2D configuration: the full per-kernel report, like the headline's
+                    k2, ro2, b2, o2, n2 = kernel_report(p2, _w, c, timer, torch, r2["element_rhs_per_step"], fp64, hbm)
+                    r2.update(kernel_ms_per_step=k2, roofline=b2, roofline_other=o2, roofline_kernels=ro2,
+                              roofline_note=n2,
+                              e2e=e2e_report(p2, _w, p2.initial_state(_w.ic), args, ws, r2["element_rhs_per_step"],
+                                             torch))
                 p2.close()
                 others[f"cfg{item}"] = r2
             except Exception as ex:       # report, do not hide: the line records the failure
@@ -410,7 +548,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(w, budget_s=args.cpu_budget)
+        cpu = cpu_baseline(args.config, budget_s=args.cpu_budget)
 
     if rank == 0:
         clocks = clk.summary()
@@ -428,12 +566,15 @@ def run_ours(args):
             "multirate_speedup": res.get("multirate_speedup"),
             "ideal_multirate_speedup": res.get("ideal_multirate_speedup"),
             "kernel_ms_per_step": kern,
-            "e2e": {"value": round(e2e_val, 1), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": h2d},
+            "e2e": e2e,
             "gpu_launches": launches * args.steps,
             "clocks": clocks,
         }
-        if line_roof:
-            line["roofline"], line["roofline_other"] = line_roof
+        if best:
+            line["roofline"] = best
+            line["roofline_other"] = other
+            line["roofline_kernels"] = roofs
+            line["roofline_note"] = note
         if others:
             line["other_configs"] = others
         if cpu is not None:
@@ -443,25 +584,89 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def cpu_baseline(w, budget_s=20.0):
-    """The oracle as it stands (plain C, single thread) on a bounded sample: whole P-ERK steps of the
-    same mesh, as many as fit in ~budget_s (at least one)."""
+def _cpu_model():
+    try:
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                return l.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def _cells_per_member(m, R):
+    mem = m.leaves()["member"]
+    return [int((mem == r).sum()) for r in range(R)]
+
+
+def oracle_sample(cfg, budget_s, threads):
+    """The oracle as it stands on a bounded sample of BASELINE config `cfg`: whole P-ERK steps of the
+    full mesh (restricted mode) while they fit the budget; if one step would not, the stage RHS
+    evaluations of one P-ERK step in stage order (each F restricted to the members active at that
+    stage, as in the step; the stage combinations, a few axpys, are left out), until the budget is
+    spent.  Runs in this process; `threads` only labels the result (the caller sets ORACLE_OMP /
+    OMP_NUM_THREADS)."""
     from oracle import oracle as O
     from oracle import tableau as T
+    w = W.make(cfg)
     fam = T.family(w.S, w.E, w.alpha_rule)
     m = O.OracleMesh(w.problem, w.level_map, fam)
     U = m.initial_state(w.ic)
+    R = len(w.E)
+    cpm = _cells_per_member(m, R)
     t0 = time.perf_counter()
-    ev = m.step(U, w.dt, 1)
-    dt1 = time.perf_counter() - t0
-    k = max(0, int(budget_s / max(dt1, 1e-9)) - 1)
-    t1 = time.perf_counter()
-    ev2 = m.step(U, w.dt, k) if k > 0 else 0
-    dt2 = time.perf_counter() - t1
-    total_ev, total_t = (ev2, dt2) if k > 0 else (ev, dt1)
-    return {"value": round(total_ev / total_t, 1), "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{k if k > 0 else 1} full P-ERK step(s) of {w.name} ({m.n} cells), restricted mode, 1 thread",
-            "seconds": round(total_t, 2)}
+    m.rhs(U, (1 << R) - 1, 1)           # one full F: sizes the sample
+    t_full = time.perf_counter() - t0
+    ev_step = sum(e * c for e, c in zip(w.E, cpm))
+    est_step = t_full * ev_step / m.n
+    if est_step <= budget_s / 2:
+        k = max(1, int(budget_s / max(est_step, 1e-9)))
+        t1 = time.perf_counter()
+        ev = m.step(U, w.dt, k)
+        dt = time.perf_counter() - t1
+        sample = f"{k} full P-ERK step(s) of {w.name} ({m.n} cells), restricted mode"
+    else:
+        ev, dt, nst = 0, 0.0, 0
+        for i in range(1, w.S + 1):
+            mask = sum(1 << r for r in range(R) if i == 1 or i >= w.S - w.E[r] + 2)
+            t1 = time.perf_counter()
+            m.rhs(U, mask, 1)
+            dt += time.perf_counter() - t1
+            ev += sum(c for r, c in enumerate(cpm) if (mask >> r) & 1)
+            nst += 1
+            if dt >= budget_s:
+                break
+        sample = (f"stage RHS evaluations 1..{nst} of one P-ERK step of {w.name} ({m.n} cells; each F restricted "
+                  f"to the stage's active members, stage combinations omitted)")
+    return {"value": round(ev / dt, 1), "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
+            "seconds": round(dt, 2), "element_rhs": int(ev)}
+
+
+def _oracle_subprocess(cfg, budget_s, threads):
+    env = dict(os.environ, OMP_NUM_THREADS=str(threads), OMP_PROC_BIND="spread", OMP_PLACES="cores")
+    env.pop("ORACLE_OMP", None)
+    if threads > 1:
+        env["ORACLE_OMP"] = "1"
+    out = subprocess.run([sys.executable, os.path.abspath(__file__), "--oracle-worker", f"{cfg},{budget_s},{threads}"],
+                         capture_output=True, text=True, env=env, timeout=30 * budget_s + 600)
+    if out.returncode != 0:
+        return {"error": out.stderr[-300:]}
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def cpu_baseline(cfg, budget_s=20.0):
+    """The oracle (plain C) on this host: all cores (OpenMP build, bitwise the serial results) and one
+    thread, each on a bounded sample of the same workload (oracle_sample); `value` / `cores` are the
+    all-core run's."""
+    nproc = os.cpu_count() or 1
+    allc = _oracle_subprocess(cfg, budget_s, nproc)
+    one = _oracle_subprocess(cfg, budget_s, 1)
+    res = dict(allc) if "value" in allc else {"value": None, "unit": UNIT, "cores": nproc, "kind": "oracle",
+                                               "sample": None, "error": allc.get("error")}
+    res["cpu_model"] = _cpu_model()
+    res["nproc"] = nproc
+    res["single_thread"] = one
+    return res
 
 
 def run_profile_only(args):
@@ -478,35 +683,54 @@ def run_profile_only(args):
                       "launches_per_step": perk.launches_per_step()}))
 
 
-def run_reference(args):
-    ws, rank, _ = _dist()
-    if rank != 0:
-        return
-    w = W.make(args.config)
+def reference_steps(cfg, K, Wm, cap_s):
+    """--impl reference worker: the oracle (OpenMP build on all cores when ORACLE_OMP=1) runs Wm
+    warm-up and then up to K whole P-ERK steps of the full mesh, stopping early once cap_s seconds
+    of timed steps are spent (a bounded sample)."""
     from oracle import oracle as O
     from oracle import tableau as T
+    w = W.make(cfg)
     fam = T.family(w.S, w.E, w.alpha_rule)
     m = O.OracleMesh(w.problem, w.level_map, fam)
     U = m.initial_state(w.ic)
-    Wm = max(1, min(args.warmup, 3))               # warm-up steps (no JIT; the last one sizes the sample)
+    ev = 0
     for _ in range(Wm):
-        t0 = time.perf_counter()
         ev = m.step(U, w.dt, 1)
-        t_step = time.perf_counter() - t0
-    K = max(1, min(args.steps, int(120.0 / max(t_step, 1e-9))))
-    t1 = time.perf_counter()
-    tot = m.step(U, w.dt, K)
-    dt = time.perf_counter() - t1
-    value = tot / dt
-    line = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": ws, "steps": K,
-            "warmup": Wm, "ms_per_step": round(1e3 * dt / K, 3), "higher_is_better": True, "scaling": "weak",
+    tot, dt, k = 0, 0.0, 0
+    while k < K and dt < cap_s:
+        t1 = time.perf_counter()
+        tot += m.step(U, w.dt, 1)
+        dt += time.perf_counter() - t1
+        k += 1
+    return {"value": round(tot / dt, 1), "steps": k, "seconds": round(dt, 2), "ms_per_step": round(1e3 * dt / k, 3),
+            "cells": m.n, "element_rhs_per_step": int(ev), "workload": w.name}
+
+
+def run_reference(args):
+    """The reference arm (tier framing): the oracle as it stands, on the box's host cores (OpenMP build,
+    all cores), whole P-ERK steps of the same workload; rank 0 only."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    nproc = os.cpu_count() or 1
+    env = dict(os.environ, ORACLE_OMP="1", OMP_NUM_THREADS=str(nproc), OMP_PROC_BIND="spread", OMP_PLACES="cores")
+    cap = 150.0
+    out = subprocess.run([sys.executable, os.path.abspath(__file__), "--reference-worker",
+                          f"{args.config},{args.steps},{args.warmup},{cap}"], capture_output=True, text=True, env=env)
+    if out.returncode != 0:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle run failed: " + out.stderr[-200:]}), flush=True)
+        return
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    sample = (f"{r['steps']} full P-ERK step(s) of {r['workload']} ({r['cells']} cells), restricted mode, "
+              f"{nproc} OpenMP threads (requested --steps {args.steps}; stops after ~{cap:.0f} s of timed steps)")
+    line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": ws, "steps": r["steps"],
+            "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator workloads/)",
-            "config": {"workload": w.name, "cells": m.n, "element_rhs_per_step": int(ev)},
+            "config": {"workload": r["workload"], "cells": r["cells"], "element_rhs_per_step": r["element_rhs_per_step"]},
             "impl": "reference",
-            "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{K} full P-ERK step(s) of {w.name}, restricted mode, 1 thread "
-                                       f"(requested --steps {args.steps}, capped at ~120 s)"},
-            "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": nproc, "kind": "oracle", "sample": sample,
+                             "cpu_model": _cpu_model()},
+            "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -515,19 +739,29 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--extra", default="1,2,4,4i,5,3p3,3alt,3early,3sc,5sc",
+    ap.add_argument("--extra", default="3,1,2,4,4i,3p3,3alt,3early,3sc,5sc",
                     help="other BASELINE configs measured into other_configs (comma list, 'Np3' = config N "
                          "with the P-ERK3 family, 'Ni' = config N with indicator-driven AMR, "
                          "'Nalt' / 'Nearly' = config N with the alternating / early-shared stage pattern, or 'none')")
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: N independent replicas of the workload instead of one decomposed problem")
     ap.add_argument("--profile-only", action="store_true",
                     help="build the workload and run warmup+steps P-ERK steps only (short ncu target)")
+    ap.add_argument("--oracle-worker", default=None, help=argparse.SUPPRESS)      # cfg,budget_s,threads
+    ap.add_argument("--reference-worker", default=None, help=argparse.SUPPRESS)   # cfg,K,W,cap_s
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
-    if args.profile_only:
+    if args.oracle_worker:
+        c, b, t = args.oracle_worker.split(",")
+        print(json.dumps(oracle_sample(int(c), float(b), int(t))), flush=True)
+    elif args.reference_worker:
+        c, k, wm, cap = args.reference_worker.split(",")
+        print(json.dumps(reference_steps(int(c), int(k), int(wm), float(cap))), flush=True)
+    elif args.profile_only:
         run_profile_only(args)
     elif args.impl == "reference":
         run_reference(args)

@@ -266,6 +266,11 @@ int perk_get_faces(perk_ctx *ctx, int32_t kind, int32_t *rec_host, int32_t *memb
 int perk_get_list(perk_ctx *ctx, int32_t kind, int32_t *list_host, int64_t cap, int64_t *seg_host);
 /* count_active_host[i-1] = number of `kind` items evaluated at stage i, i = 1..S */
 int perk_get_count_active(perk_ctx *ctx, int32_t kind, int32_t *count_active_host);
+/* BR1 / shock-capturing halo per stage (Navier-Stokes or shock capturing contexts; zeros otherwise):
+ * halo_host[kind][i-1] for kind 0 elements, 1 interfaces, 2 mortars, i = 1..S = number of halo
+ * items the stage-i BR1 / indicator launches process besides the active ones (the large elements of
+ * the active mortars whose fine side is another member, and their faces; D7).  Synchronising. */
+int perk_get_halo_counts(perk_ctx *ctx, int32_t *halo_host);
 /* element-RHS evaluations (sum over steps of sum_r E_r N_C(r), P:l.1282-1289) and steps taken */
 int perk_get_counters(perk_ctx *ctx, int64_t *elem_rhs_evals, int64_t *steps);
 int perk_sync(perk_ctx *ctx);
@@ -280,11 +285,69 @@ int perk_profile_step(perk_ctx *ctx, double *U_dev, double dt, float *ms_host, i
  * left out of the graph, so the state is NOT a valid P-ERK evolution afterwards (timing only).
  * Synchronising. */
 int perk_time_kernels(perk_ctx *ctx, double *U_dev, double dt, uint32_t kind_mask, int32_t reps, float *ms_per_step);
+/* perk_time_kernels with an L2 flush between replays: before each of the reps replays (outside its
+ * event pair) flush_bytes of the caller's device buffer flush_dev are overwritten (use more than the
+ * 126 MB L2); ms_per_step = mean of the per-replay event times.  flush_bytes = 0: no flush. */
+int perk_time_kernels_ex(perk_ctx *ctx, double *U_dev, double dt, uint32_t kind_mask, int32_t reps,
+                         void *flush_dev, int64_t flush_bytes, float *ms_per_step);
 /* Same for one repartition (kinds 2 and 3). */
 int perk_profile_repartition(perk_ctx *ctx, const uint8_t *level_map_dev, double *U_dev, float *ms_host,
                              int32_t *launches_host);
 /* Number of kernel launches one perk_step performs (graph nodes). */
 int perk_launches_per_step(perk_ctx *ctx, int32_t *launches);
+
+/* ------------------------------------------------------------------------------------------------
+ * Spatial domain decomposition over ranks.  The paper's
+ * partitioning is by level only and "no additional data exchange is required compared to standard
+ * Runge-Kutta methods" (P:l.1258-1263, §6.3): across GPUs each rank owns a contiguous Morton range of
+ * leaves, balanced in the per-step work sum_leaves E_member (the E-weighted split below), keeps its
+ * owned elements and the faces with an owned side, and receives per stage the blocks its ghost cells
+ * (face neighbours owned elsewhere) changed.  2D, standard stage pattern, no shock capturing.
+ * ------------------------------------------------------------------------------------------------ */
+
+/* Host only.  The E-weighted split of n leaves in Morton order with per-leaf weights w_k (the stage
+ * evaluations E of the leaf's member): owner_k = min(P-1, floor(P (2 prefix_k + w_k) / (2 W))),
+ * prefix_k = sum_{j<k} w_j, W = sum w (all owners 0 when W = 0).  Owners are non-decreasing in k
+ * (contiguous ranges); the device mesh pipeline computes the same owners.  EINVAL on n < 0,
+ * NULL arrays with n > 0, negative weights, nranks outside 1..8. */
+int perk_dd_split(int64_t n, const int32_t *weights_host, int32_t nranks, int32_t *owner_host);
+
+/* Create sub-domain `rank` of an nranks-way decomposition: like perk_init (every rank passes the same
+ * problem, level map and tableau and builds the same global mesh), then keeps the owned part.  The
+ * state U_dev is still [max_cells][nv][npe] in global cell order: rows of owned cells are this rank's,
+ * rows of its ghost cells are kept current by the exchange, other rows are not used.  nranks = 1 is
+ * perk_init.  EINVAL on rank / nranks, EUNSUPPORTED for 1D or a non-standard stage pattern.  A
+ * sub-domain context does not take perk_step (EUNSUPPORTED); perk_repartition and perk_amr_* need the
+ * complete state on every rank (gather the owned ranges first, perk_dd_info). */
+int perk_init_dd(perk_ctx **out, const perk_problem *prob, const uint8_t *level_map_dev, const perk_tableau *tab,
+                 void *stream, int32_t rank, int32_t nranks);
+/* rank, nranks and the owned cells [first, first + count) of the current mesh (synchronising) */
+int perk_dd_info(perk_ctx *ctx, int32_t *rank, int32_t *nranks, int64_t *first, int64_t *count);
+/* Per stage i = 1..S, the number of cell blocks this rank sends to / receives from `peer` for
+ * `what` (0: state blocks, 1: Navier-Stokes viscous-flux traces; see perk_dd_pack).  Synchronising. */
+int perk_dd_counts(perk_ctx *ctx, int32_t peer, int32_t what, int32_t *send_host, int32_t *recv_host);
+/* The send (dir 0: owned cells that are ghosts of peer) or receive (dir 1: peer's cells that are ghosts
+ * here) list, member-sorted by descending E; synchronising. */
+int perk_dd_get_list(perk_ctx *ctx, int32_t peer, int32_t dir, int32_t *list_host, int64_t cap, int64_t *len);
+/* Asynchronous stage launches of a sub-domain: part 0 = the BR1 passes of stage `stage`
+ * (Navier-Stokes; nothing otherwise), part 1 = surface flux + volume / stage epilogue.  A stage is
+ * part 0, exchange what = 1, part 1, exchange what = 0. */
+int perk_dd_stage(perk_ctx *ctx, double *U_dev, double dt, int32_t stage, int32_t part);
+/* Asynchronous, on the context stream: gather (pack) into buf_dev / scatter (unpack) from buf_dev the
+ * blocks of stage `stage` exchanged with `peer`, in list order: what 0 = the blocks the stage's volume
+ * epilogue wrote (K_1 at stage 1, the next stage state at 1 < i < S, U_{n+1} = U_dev at stage S;
+ * nv * (N+1)^2 doubles per cell) of the cells active at the stage; what 1 = Vt (48 doubles per cell)
+ * of the active cells and of the member below (the BR1 halo).  buf_dev holds the perk_dd_counts
+ * number of blocks; the transport between ranks (NCCL send / recv) is the caller's. */
+int perk_dd_pack(perk_ctx *ctx, double *U_dev, int32_t stage, int32_t what, int32_t peer, double *buf_dev);
+int perk_dd_unpack(perk_ctx *ctx, double *U_dev, int32_t stage, int32_t what, int32_t peer, const double *buf_dev);
+/* In-process exchange between two sub-domains of one split (on one device, or on devices with peer
+ * access): src's blocks for dst go straight into the same rows of dst's arrays, one kernel on src's
+ * stream (the caller orders dst's stream after it). */
+int perk_dd_exchange(perk_ctx *src, perk_ctx *dst, double *U_src_dev, double *U_dst_dev, int32_t stage, int32_t what);
+/* One P-ERK step of all n sub-domains of a split held by this process (ctxs[p] = rank p, sharing one
+ * stream): per stage the parts and exchanges above, in order.  Asynchronous. */
+int perk_dd_group_step(perk_ctx **ctxs, int32_t n, double **U_dev, double dt);
 
 #ifdef __cplusplus
 }

@@ -3,4 +3,4 @@
 The product is libperk_b200.so (C ABI in include/perk.h); `perk.Perk` is its thin ctypes
 binding.  See DESIGN.md.
 """
-from .perk import Perk, PerkError, tableau_p2, lib, LIB_PATH  # noqa: F401
+from .perk import Perk, PerkError, DomainGroup, DistributedPerk, dd_split, tableau_p2, lib, LIB_PATH  # noqa: F401

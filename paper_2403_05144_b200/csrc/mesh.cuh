@@ -215,15 +215,16 @@ __global__ void k_face_records(MeshDev md, const int *__restrict__ slot_list, co
 
 // physical node coordinates [n][dim][npe]
 // hot-path copies in list order: packed element entries, interface and mortar records
-__global__ void k_hot_lists(MeshDev md)
+// (list lengths = the partition totals seg[kind][R]: all items, or the owned ones of a sub-domain)
+__global__ void k_hot_lists(MeshDev md, int R)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < md.n[0]) {
+    if (t < md.seg[KIND_EL * (MAXR + 1) + R]) {
         const int e = md.list[KIND_EL][t];
         md.elpk[t] = e | ((int)md.mem[e] << PK_EBITS) | ((int)md.lev[e] << (PK_EBITS + 3));
     }
-    if (t < md.n[1]) md.ifcs[t] = md.ifc[md.list[KIND_IF][t]];
-    if (t < md.n[2]) md.mors[t] = md.mor[md.list[KIND_MO][t]];
+    if (t < md.seg[KIND_IF * (MAXR + 1) + R]) md.ifcs[t] = md.ifc[md.list[KIND_IF][t]];
+    if (t < md.seg[KIND_MO * (MAXR + 1) + R]) md.mors[t] = md.mor[md.list[KIND_MO][t]];
 }
 
 // BR1 halo flags: the large side of a mortar whose fine side belongs to another member

@@ -26,6 +26,7 @@
 #include "transfer.cuh"
 #include "amr.cuh"
 #include "sc.cuh"
+#include "dd.cuh"
 
 using namespace perk;
 
@@ -81,6 +82,15 @@ struct perk_ctx {
     double *rU = nullptr;
     double *gU = nullptr;
     double gdt = 0.0;
+    // spatial domain decomposition (dd.cuh): this context is sub-domain dd_rank of
+    // dd_P; dd_P == 1 is the undecomposed path
+    int dd_rank = 0, dd_P = 1;
+    uint8_t *dd_owner = nullptr, *dd_flags = nullptr;  // owner rank per leaf; [2P][cap] send / ghost flags
+    long long *dd_bsum = nullptr;                       // per-block weight sums (E-weighted split)
+    int *dd_range = nullptr;                            // owned cells [first, first + count)
+    int *dd_list[DD_MAXP][2] = {};                      // per peer: send (owned ghosts of the peer), recv lists
+    int *dd_seg[DD_MAXP][2] = {};                       // their member segments
+    int *dd_cnt[DD_MAXP][2] = {};                       // [2][MAXS] per-stage prefix counts (k_dd_counts)
     std::vector<void *> allocs;
     std::string err;
 };
@@ -297,20 +307,53 @@ static void build_mesh(perk_ctx *c, cudaStream_t s, const uint8_t *lmap)
     k_check_capacity<<<1, 1, 0, s>>>(md);
     k_leaf_fill<<<blocks_for(c->cap, 256), 256, 0, s>>>(md, lmap, c->items, R);
     k_cell_of<<<blocks_for((long long)c->nf, 256), 256, 0, s>>>(md, lmap, c->rank);
+    const bool dd = c->dd_P > 1;
+    const int ddr = c->dd_rank;
+    if (dd) {   // E-weighted contiguous Morton ranges (dd.cuh)
+        const int nb = blocks_for(c->cap, DD_SCAN_T);
+        k_dd_block_sums<<<nb, DD_SCAN_T, 0, s>>>(md, active_desc(c), c->dd_bsum);
+        k_dd_scan_blocks<<<1, DD_SCAN_T, 0, s>>>(md.n, c->dd_bsum);
+        k_dd_range_init<<<1, 1, 0, s>>>(md.n, c->dd_range);
+        k_dd_owner<<<nb, DD_SCAN_T, 0, s>>>(md, active_desc(c), c->dd_bsum, c->dd_P, ddr, c->dd_owner, c->dd_range);
+    }
     k_classify<<<blocks_for((long long)c->nd * c->cap, 256), 256, 0, s>>>(md, c->keys);
     partition(c, s, KeyU8{c->keys}, md.n, c->nd, (long long)c->nd * c->cap, 4, c->items, nullptr, c->segtmp, nullptr,
               nullptr);
     k_face_counts<<<1, 1, 0, s>>>(md, c->segtmp, c->cap_faces);
     k_face_records<<<blocks_for((long long)c->nd * c->cap, 256), 256, 0, s>>>(md, c->items, c->segtmp, R);
-    partition(c, s, KeyU8{md.mem}, md.n + 0, 1, c->cap, R, md.list[KIND_EL], nullptr, md.seg + 0 * (MAXR + 1), nullptr,
-              md.count_active + KIND_EL * MAXS, md.evals + 2);
-    partition(c, s, KeyIfc{md.ifc}, md.n + 1, 1, c->cap_faces, R, md.list[KIND_IF], nullptr, md.seg + 1 * (MAXR + 1),
-              nullptr, md.count_active + KIND_IF * MAXS);
-    partition(c, s, KeyMor{md.mor}, md.n + 2, 1, c->cap_faces, R, md.list[KIND_MO], nullptr, md.seg + 2 * (MAXR + 1),
-              nullptr, md.count_active + KIND_MO * MAXS);
-    partition(c, s, KeyBnd{md.bnd}, md.n + 3, 1, c->cap_faces, R, md.list[KIND_BD], nullptr, md.seg + 3 * (MAXR + 1),
-              nullptr, md.count_active + KIND_BD * MAXS);
-    k_hot_lists<<<blocks_for(c->cap_faces, 256), 256, 0, s>>>(md);
+    if (dd) {   // a sub-domain keeps its owned elements and the faces with an owned side
+        const uint8_t *ow = c->dd_owner;
+        partition(c, s, KeyOwnEl{md.mem, ow, ddr}, md.n + 0, 1, c->cap, R, md.list[KIND_EL], nullptr,
+                  md.seg + 0 * (MAXR + 1), nullptr, md.count_active + KIND_EL * MAXS, md.evals + 2);
+        partition(c, s, KeyOwnIfc{md.ifc, ow, ddr}, md.n + 1, 1, c->cap_faces, R, md.list[KIND_IF], nullptr,
+                  md.seg + 1 * (MAXR + 1), nullptr, md.count_active + KIND_IF * MAXS);
+        partition(c, s, KeyOwnMor{md.mor, ow, ddr}, md.n + 2, 1, c->cap_faces, R, md.list[KIND_MO], nullptr,
+                  md.seg + 2 * (MAXR + 1), nullptr, md.count_active + KIND_MO * MAXS);
+        partition(c, s, KeyOwnBnd{md.bnd, ow, ddr}, md.n + 3, 1, c->cap_faces, R, md.list[KIND_BD], nullptr,
+                  md.seg + 3 * (MAXR + 1), nullptr, md.count_active + KIND_BD * MAXS);
+    } else {
+        partition(c, s, KeyU8{md.mem}, md.n + 0, 1, c->cap, R, md.list[KIND_EL], nullptr, md.seg + 0 * (MAXR + 1),
+                  nullptr, md.count_active + KIND_EL * MAXS, md.evals + 2);
+        partition(c, s, KeyIfc{md.ifc}, md.n + 1, 1, c->cap_faces, R, md.list[KIND_IF], nullptr,
+                  md.seg + 1 * (MAXR + 1), nullptr, md.count_active + KIND_IF * MAXS);
+        partition(c, s, KeyMor{md.mor}, md.n + 2, 1, c->cap_faces, R, md.list[KIND_MO], nullptr,
+                  md.seg + 2 * (MAXR + 1), nullptr, md.count_active + KIND_MO * MAXS);
+        partition(c, s, KeyBnd{md.bnd}, md.n + 3, 1, c->cap_faces, R, md.list[KIND_BD], nullptr,
+                  md.seg + 3 * (MAXR + 1), nullptr, md.count_active + KIND_BD * MAXS);
+    }
+    k_hot_lists<<<blocks_for(c->cap_faces, 256), 256, 0, s>>>(md, R);
+    if (dd) {   // ghost layers: per peer the owned cells it reads (send) and its cells read here (recv)
+        cudaMemsetAsync(c->dd_flags, 0, (size_t)2 * c->dd_P * c->cap, s);
+        k_dd_flags<<<SM_COUNT_B200 * 4, 256, 0, s>>>(md, c->dd_owner, ddr, c->dd_flags);
+        for (int q = 0; q < c->dd_P; ++q) {
+            if (q == ddr) continue;
+            for (int d = 0; d < 2; ++d) {
+                partition(c, s, KeyFlagMem{c->dd_flags + (size_t)(2 * q + d) * c->cap, md.mem}, md.n + 0, 1, c->cap, R,
+                          c->dd_list[q][d], nullptr, c->dd_seg[q][d], nullptr, nullptr);
+                k_dd_counts<<<1, MAXS, 0, s>>>(c->dd_seg[q][d], active_desc(c), c->dd_cnt[q][d]);
+            }
+        }
+    }
     if (c->stage_lists) {   // per-stage lists (non-nested patterns): stable compaction per (stage, kind)
         for (int i = 1; i <= c->tab.S; ++i) {
             unsigned mask = 0;
@@ -335,12 +378,21 @@ static void build_mesh(perk_ctx *c, cudaStream_t s, const uint8_t *lmap)
     if (c->halo_alloc) {   // BR1 / shock-capturing halo lists (see MeshDev::halo)
         k_halo_clear<<<blocks_for(c->cap, 256), 256, 0, s>>>(md);
         k_halo_flags<<<blocks_for(c->cap_faces, 256), 256, 0, s>>>(md);
-        partition(c, s, KeyHaloEl{md.halo, md.mem}, md.n + 0, 1, c->cap, R, md.hlist[KIND_EL], nullptr,
-                  md.hseg + KIND_EL * (MAXR + 1), nullptr, nullptr);
-        partition(c, s, KeyHaloIf{md.ifc, md.halo}, md.n + 1, 1, c->cap_faces, R, md.hlist[KIND_IF], nullptr,
-                  md.hseg + KIND_IF * (MAXR + 1), nullptr, nullptr);
-        partition(c, s, KeyHaloMo{md.mor, md.halo}, md.n + 2, 1, c->cap_faces, R, md.hlist[KIND_MO], nullptr,
-                  md.hseg + KIND_MO * (MAXR + 1), nullptr, nullptr);
+        if (dd) {   // the halo elements this sub-domain owns (others' gradients arrive with Vt)
+            partition(c, s, KeyOwnHaloEl{md.halo, md.mem, c->dd_owner, ddr}, md.n + 0, 1, c->cap, R, md.hlist[KIND_EL],
+                      nullptr, md.hseg + KIND_EL * (MAXR + 1), nullptr, nullptr);
+            partition(c, s, KeyOwnHaloIf{md.ifc, md.halo, c->dd_owner, ddr}, md.n + 1, 1, c->cap_faces, R,
+                      md.hlist[KIND_IF], nullptr, md.hseg + KIND_IF * (MAXR + 1), nullptr, nullptr);
+            partition(c, s, KeyOwnHaloMo{md.mor, md.halo, c->dd_owner, ddr}, md.n + 2, 1, c->cap_faces, R,
+                      md.hlist[KIND_MO], nullptr, md.hseg + KIND_MO * (MAXR + 1), nullptr, nullptr);
+        } else {
+            partition(c, s, KeyHaloEl{md.halo, md.mem}, md.n + 0, 1, c->cap, R, md.hlist[KIND_EL], nullptr,
+                      md.hseg + KIND_EL * (MAXR + 1), nullptr, nullptr);
+            partition(c, s, KeyHaloIf{md.ifc, md.halo}, md.n + 1, 1, c->cap_faces, R, md.hlist[KIND_IF], nullptr,
+                      md.hseg + KIND_IF * (MAXR + 1), nullptr, nullptr);
+            partition(c, s, KeyHaloMo{md.mor, md.halo}, md.n + 2, 1, c->cap_faces, R, md.hlist[KIND_MO], nullptr,
+                      md.hseg + KIND_MO * (MAXR + 1), nullptr, nullptr);
+        }
         k_halo_ranges<<<SM_COUNT_B200, 256, 0, s>>>(md, active_desc(c));
     }
 }
@@ -632,6 +684,12 @@ static int validate(perk_ctx *c, const perk_problem *p, const perk_tableau *t)
 extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t *level_map_dev, const perk_tableau *tab,
                          void *stream)
 {
+    return perk_init_dd(out, prob, level_map_dev, tab, stream, 0, 1);
+}
+
+extern "C" int perk_init_dd(perk_ctx **out, const perk_problem *prob, const uint8_t *level_map_dev,
+                            const perk_tableau *tab, void *stream, int32_t rank, int32_t nranks)
+{
     if (!out || !prob || !level_map_dev || !tab) return PERK_EINVAL;
     *out = nullptr;
     perk_ctx *c = new perk_ctx();
@@ -640,6 +698,12 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
     *out = c;
     int rc = validate(c, prob, tab);
     if (rc) return rc;
+    if (nranks < 1 || nranks > DD_MAXP || rank < 0 || rank >= nranks)
+        return set_err(c, PERK_EINVAL, "need 1 <= nranks <= 8 and 0 <= rank < nranks");
+    if (nranks > 1 && (prob->dim != 2 || !c->std_pattern))
+        return set_err(c, PERK_EUNSUPPORTED, "domain decomposition: 2D problems with the standard stage pattern");
+    c->dd_rank = rank;
+    c->dd_P = nranks;
     c->prob = *prob;
     c->tab = *tab;
     c->stream = (cudaStream_t)stream;
@@ -732,6 +796,20 @@ extern "C" int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t
     CU(dalloc(c, &c->blockoff, (size_t)nb_max * MAXR));
     CU(dalloc(c, &c->segtmp, 16));
     CU(dalloc(c, &c->dconst, 4));
+    if (c->dd_P > 1) {
+        CU(dalloc(c, &c->dd_owner, c->cap));
+        CU(dalloc(c, &c->dd_flags, (size_t)2 * c->dd_P * c->cap));
+        CU(dalloc(c, &c->dd_bsum, (size_t)blocks_for(c->cap, DD_SCAN_T) + 1));
+        CU(dalloc(c, &c->dd_range, 2));
+        for (int q = 0; q < c->dd_P; ++q) {
+            if (q == c->dd_rank) continue;
+            for (int d = 0; d < 2; ++d) {
+                CU(dalloc(c, &c->dd_list[q][d], c->cap));
+                CU(dalloc(c, &c->dd_seg[q][d], MAXR + 1));
+                CU(dalloc(c, &c->dd_cnt[q][d], 2 * MAXS));
+            }
+        }
+    }
     int h_const[4] = {(int)c->nmorton, 0, 0, 0};
     CU(cudaMemcpy(c->dconst, h_const, sizeof(h_const), cudaMemcpyHostToDevice));
 
@@ -884,6 +962,8 @@ extern "C" int perk_step(perk_ctx *c, double *U, double dt)
 {
     if (!c) return PERK_ENOTINIT;
     if (!U) return set_err(c, PERK_EINVAL, "U_dev is null");
+    if (c->dd_P > 1)
+        return set_err(c, PERK_EUNSUPPORTED, "a sub-domain steps with perk_dd_group_step or perk_dd_stage + exchange");
     int rc = ensure_graph(c, U, dt);
     if (rc) return rc;
     CU(cudaGraphLaunch(c->gexec, c->stream));
@@ -1099,6 +1179,7 @@ extern "C" int perk_amr_launches(perk_ctx *c, int32_t *launches)
 extern "C" int perk_set_shock_capturing(perk_ctx *c, const perk_shock_capturing *sc)
 {
     if (!c) return PERK_ENOTINIT;
+    if (sc && c->dd_P > 1) return set_err(c, PERK_EUNSUPPORTED, "shock capturing with domain decomposition");
     if (sc) {
         if (c->prob.dim != 2 || c->prob.equation == PERK_EQ_ADVECTION)
             return set_err(c, PERK_EUNSUPPORTED, "shock capturing needs a 2D Euler / Navier-Stokes problem");
@@ -1262,6 +1343,22 @@ extern "C" int perk_get_count_active(perk_ctx *c, int32_t kind, int32_t *out)
     return PERK_OK;
 }
 
+extern "C" int perk_get_halo_counts(perk_ctx *c, int32_t *out)
+{
+    if (!c) return PERK_ENOTINIT;
+    if (!out) return set_err(c, PERK_EINVAL, "null pointer");
+    int rc = check_device_err(c);
+    if (rc) return rc;
+    const int S = c->tab.S;
+    for (int k = 0; k < 3 * S; ++k) out[k] = 0;
+    if (!c->halo_alloc) return PERK_OK;
+    std::vector<int2> h((size_t)3 * MAXS);
+    CU(cudaMemcpy(h.data(), c->md.hrng, sizeof(int2) * 3 * MAXS, cudaMemcpyDeviceToHost));
+    for (int kind = 0; kind < 3; ++kind)
+        for (int i = 0; i < S; ++i) out[kind * S + i] = h[(size_t)kind * MAXS + i].y;
+    return PERK_OK;
+}
+
 extern "C" int perk_get_counters(perk_ctx *c, int64_t *evals, int64_t *steps)
 {
     if (!c) return PERK_ENOTINIT;
@@ -1312,10 +1409,12 @@ extern "C" int perk_profile_step(perk_ctx *c, double *U, double dt, float *ms, i
     return finish_prof(c, p, ms, launches);
 }
 
-extern "C" int perk_time_kernels(perk_ctx *c, double *U, double dt, uint32_t kind_mask, int32_t reps, float *ms_per_step)
+extern "C" int perk_time_kernels_ex(perk_ctx *c, double *U, double dt, uint32_t kind_mask, int32_t reps,
+                                    void *flush_dev, int64_t flush_bytes, float *ms_per_step)
 {
     if (!c) return PERK_ENOTINIT;
-    if (!U || !ms_per_step || reps < 1) return set_err(c, PERK_EINVAL, "U_dev / ms / reps");
+    if (!U || !ms_per_step || reps < 1 || reps > 1000 || (flush_bytes > 0 && !flush_dev))
+        return set_err(c, PERK_EINVAL, "U_dev / ms / reps / flush buffer");
     cudaGraph_t g;
     cudaGraphExec_t ge;
     c->kind_mask = kind_mask;
@@ -1328,21 +1427,33 @@ extern "C" int perk_time_kernels(perk_ctx *c, double *U, double dt, uint32_t kin
     if (ce != cudaSuccess) return set_err(c, PERK_ECUDA, std::string("capture: ") + cudaGetErrorString(ce));
     CU(cudaGraphInstantiate(&ge, g, 0));
     cudaGraphDestroy(g);
-    cudaEvent_t a, b;
-    CU(cudaEventCreate(&a));
-    CU(cudaEventCreate(&b));
+    std::vector<cudaEvent_t> ev(2 * (size_t)reps);
+    for (auto &e : ev) CU(cudaEventCreate(&e));
     CU(cudaGraphLaunch(ge, c->stream));   // warm-up
-    CU(cudaEventRecord(a, c->stream));
-    for (int r = 0; r < reps; ++r) CU(cudaGraphLaunch(ge, c->stream));
-    CU(cudaEventRecord(b, c->stream));
-    CU(cudaEventSynchronize(b));
-    float t = 0.f;
-    CU(cudaEventElapsedTime(&t, a, b));
-    *ms_per_step = t / reps;
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
+    for (int r = 0; r < reps; ++r) {
+        // L2 flush between replays (outside the events): the replays then see the cache state of a
+        // step inside a timed P-ERK run, not the previous replay's leftovers
+        if (flush_bytes > 0) CU(cudaMemsetAsync(flush_dev, r & 0xff, (size_t)flush_bytes, c->stream));
+        CU(cudaEventRecord(ev[2 * r], c->stream));
+        CU(cudaGraphLaunch(ge, c->stream));
+        CU(cudaEventRecord(ev[2 * r + 1], c->stream));
+    }
+    CU(cudaEventSynchronize(ev.back()));
+    float tot = 0.f;
+    for (int r = 0; r < reps; ++r) {
+        float t = 0.f;
+        CU(cudaEventElapsedTime(&t, ev[2 * r], ev[2 * r + 1]));
+        tot += t;
+    }
+    *ms_per_step = tot / reps;
+    for (auto &e : ev) cudaEventDestroy(e);
     cudaGraphExecDestroy(ge);
     return check_device_err(c);
+}
+
+extern "C" int perk_time_kernels(perk_ctx *c, double *U, double dt, uint32_t kind_mask, int32_t reps, float *ms_per_step)
+{
+    return perk_time_kernels_ex(c, U, dt, kind_mask, reps, nullptr, 0, ms_per_step);
 }
 
 extern "C" int perk_profile_repartition(perk_ctx *c, const uint8_t *lmap, double *U, float *ms, int32_t *launches)
@@ -1353,4 +1464,202 @@ extern "C" int perk_profile_repartition(perk_ctx *c, const uint8_t *lmap, double
     int rc = do_repartition(c, lmap, U, &p);
     if (rc) return rc;
     return finish_prof(c, p, ms, launches);
+}
+
+// ----------------------------------------------------------------------------------------------
+// spatial domain decomposition (dd.cuh)
+// ----------------------------------------------------------------------------------------------
+extern "C" int perk_dd_split(int64_t n, const int32_t *weights, int32_t nranks, int32_t *owner)
+{
+    if (n < 0 || (n > 0 && (!weights || !owner)) || nranks < 1 || nranks > DD_MAXP) return PERK_EINVAL;
+    long long W = 0;
+    for (int64_t k = 0; k < n; ++k) {
+        if (weights[k] < 0) return PERK_EINVAL;
+        W += weights[k];
+    }
+    long long pre = 0;
+    for (int64_t k = 0; k < n; ++k) {
+        long long o = W > 0 ? ((long long)nranks * (2 * pre + weights[k])) / (2 * W) : 0;
+        owner[k] = (int32_t)(o > nranks - 1 ? nranks - 1 : o);
+        pre += weights[k];
+    }
+    return PERK_OK;
+}
+
+static int dd_check(perk_ctx *c)
+{
+    if (!c) return PERK_ENOTINIT;
+    if (c->dd_P < 2) return set_err(c, PERK_EINVAL, "not a sub-domain context (perk_init_dd with nranks > 1)");
+    return PERK_OK;
+}
+
+extern "C" int perk_dd_info(perk_ctx *c, int32_t *rank, int32_t *nranks, int64_t *first, int64_t *count)
+{
+    if (!c) return PERK_ENOTINIT;
+    if (!rank || !nranks || !first || !count) return set_err(c, PERK_EINVAL, "null pointer");
+    *rank = c->dd_rank;
+    *nranks = c->dd_P;
+    int rc = check_device_err(c);
+    if (rc) return rc;
+    if (c->dd_P < 2) {
+        int n = 0;
+        CU(cudaMemcpy(&n, c->md.n, sizeof(int), cudaMemcpyDeviceToHost));
+        *first = 0;
+        *count = n;
+        return PERK_OK;
+    }
+    int h[2];
+    CU(cudaMemcpy(h, c->dd_range, sizeof(h), cudaMemcpyDeviceToHost));
+    *first = h[1] > 0 ? h[0] : 0;
+    *count = h[1];
+    return PERK_OK;
+}
+
+extern "C" int perk_dd_counts(perk_ctx *c, int32_t peer, int32_t what, int32_t *send_host, int32_t *recv_host)
+{
+    int rc = dd_check(c);
+    if (rc) return rc;
+    if (peer < 0 || peer >= c->dd_P || peer == c->dd_rank || what < 0 || what > 1 || !send_host || !recv_host)
+        return set_err(c, PERK_EINVAL, "peer / what / null pointer");
+    rc = check_device_err(c);
+    if (rc) return rc;
+    const int S = c->tab.S;
+    CU(cudaMemcpy(send_host, c->dd_cnt[peer][0] + what * MAXS, S * sizeof(int), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(recv_host, c->dd_cnt[peer][1] + what * MAXS, S * sizeof(int), cudaMemcpyDeviceToHost));
+    return PERK_OK;
+}
+
+extern "C" int perk_dd_get_list(perk_ctx *c, int32_t peer, int32_t dir, int32_t *list_host, int64_t cap, int64_t *len)
+{
+    int rc = dd_check(c);
+    if (rc) return rc;
+    if (peer < 0 || peer >= c->dd_P || peer == c->dd_rank || dir < 0 || dir > 1 || !len)
+        return set_err(c, PERK_EINVAL, "peer / dir / null pointer");
+    rc = check_device_err(c);
+    if (rc) return rc;
+    int seg[MAXR + 1];
+    CU(cudaMemcpy(seg, c->dd_seg[peer][dir], sizeof(seg), cudaMemcpyDeviceToHost));
+    *len = seg[c->tab.R];
+    if (!list_host || cap < *len) return set_err(c, PERK_EINVAL, "host array too small");
+    CU(cudaMemcpy(list_host, c->dd_list[peer][dir], (size_t)*len * sizeof(int), cudaMemcpyDeviceToHost));
+    return PERK_OK;
+}
+
+// the array a stage's exchange carries (what 0: the blocks the stage-i volume epilogue wrote; 1: Vt)
+static double *dd_array(perk_ctx *c, double *U, int stage, int what, int &row)
+{
+    if (what == 1) {
+        row = 4 * GV * NP;
+        return c->Vt;
+    }
+    row = c->nv * c->npe;
+    return stage == 1 ? c->K1 : (stage == c->tab.S ? U : c->Ubuf);
+}
+
+static int dd_args(perk_ctx *c, double *U, int32_t stage, int32_t what)
+{
+    int rc = dd_check(c);
+    if (rc) return rc;
+    if (!U || stage < 1 || stage > c->tab.S || what < 0 || what > 1) return set_err(c, PERK_EINVAL, "U / stage / what");
+    if (what == 1 && !c->ns) return set_err(c, PERK_EINVAL, "Vt exchange needs a Navier-Stokes context");
+    return PERK_OK;
+}
+
+extern "C" int perk_dd_stage(perk_ctx *c, double *U, double dt, int32_t stage, int32_t part)
+{
+    int rc = dd_check(c);
+    if (rc) return rc;
+    if (!U || stage < 1 || stage > c->tab.S || part < 0 || part > 1) return set_err(c, PERK_EINVAL, "U / stage / part");
+    const StageParams sp = stage_params(c, stage, dt, MODE_STAGE, 0u);
+    if (part == 0) {
+        if (c->ns) launch_br1(c, c->stream, sp, U, nullptr, nullptr);
+    } else {
+        launch_surface(c, c->stream, sp, U, nullptr);
+        launch_volume(c, c->stream, sp, U, nullptr, nullptr);
+    }
+    CU(cudaGetLastError());
+    return PERK_OK;
+}
+
+extern "C" int perk_dd_pack(perk_ctx *c, double *U, int32_t stage, int32_t what, int32_t peer, double *buf)
+{
+    int rc = dd_args(c, U, stage, what);
+    if (rc) return rc;
+    if (peer < 0 || peer >= c->dd_P || peer == c->dd_rank || !buf) return set_err(c, PERK_EINVAL, "peer / buffer");
+    int row;
+    const double *a = dd_array(c, U, stage, what, row);
+    k_dd_pack<<<SM_COUNT_B200 * 2, 256, 0, c->stream>>>(c->dd_list[peer][0], c->dd_cnt[peer][0] + what * MAXS + stage - 1,
+                                                       row, a, buf);
+    CU(cudaGetLastError());
+    return PERK_OK;
+}
+
+extern "C" int perk_dd_unpack(perk_ctx *c, double *U, int32_t stage, int32_t what, int32_t peer, const double *buf)
+{
+    int rc = dd_args(c, U, stage, what);
+    if (rc) return rc;
+    if (peer < 0 || peer >= c->dd_P || peer == c->dd_rank || !buf) return set_err(c, PERK_EINVAL, "peer / buffer");
+    int row;
+    double *a = dd_array(c, U, stage, what, row);
+    k_dd_unpack<<<SM_COUNT_B200 * 2, 256, 0, c->stream>>>(c->dd_list[peer][1], c->dd_cnt[peer][1] + what * MAXS + stage - 1,
+                                                         row, buf, a);
+    CU(cudaGetLastError());
+    return PERK_OK;
+}
+
+extern "C" int perk_dd_exchange(perk_ctx *src, perk_ctx *dst, double *U_src, double *U_dst, int32_t stage, int32_t what)
+{
+    int rc = dd_args(src, U_src, stage, what);
+    if (rc) return rc;
+    rc = dd_args(dst, U_dst, stage, what);
+    if (rc) return rc;
+    if (src->dd_P != dst->dd_P || src->dd_rank == dst->dd_rank) return set_err(src, PERK_EINVAL, "not two sub-domains of one split");
+    perk_ctx *c = src;
+    int row;
+    const double *a = dd_array(src, U_src, stage, what, row);
+    double *b = dd_array(dst, U_dst, stage, what, row);
+    k_dd_copy<<<SM_COUNT_B200 * 2, 256, 0, src->stream>>>(src->dd_list[dst->dd_rank][0],
+                                                         src->dd_cnt[dst->dd_rank][0] + what * MAXS + stage - 1, row, a, b);
+    CU(cudaGetLastError());
+    return PERK_OK;
+}
+
+extern "C" int perk_dd_group_step(perk_ctx **ctxs, int32_t n, double **U, double dt)
+{
+    if (!ctxs || !U || n < 2 || n > DD_MAXP) return PERK_EINVAL;
+    for (int p = 0; p < n; ++p) {
+        int rc = dd_check(ctxs[p]);
+        if (rc) return rc;
+        if (ctxs[p]->dd_P != n || ctxs[p]->dd_rank != p || !U[p])
+            return set_err(ctxs[p], PERK_EINVAL, "ctxs[p] must be sub-domain p of an n-way split, U[p] non-null");
+        if (ctxs[p]->stream != ctxs[0]->stream || ctxs[p]->tab.S != ctxs[0]->tab.S)
+            return set_err(ctxs[p], PERK_EINVAL, "the sub-domains of a group share one stream and one tableau");
+    }
+    const int S = ctxs[0]->tab.S;
+    const bool ns = ctxs[0]->ns;
+    for (int i = 1; i <= S; ++i) {
+        if (ns) {
+            for (int p = 0; p < n; ++p) {
+                int rc = perk_dd_stage(ctxs[p], U[p], dt, i, 0);
+                if (rc) return rc;
+            }
+            for (int p = 0; p < n; ++p)
+                for (int q = 0; q < n; ++q)
+                    if (q != p) {
+                        int rc = perk_dd_exchange(ctxs[p], ctxs[q], U[p], U[q], i, 1);
+                        if (rc) return rc;
+                    }
+        }
+        for (int p = 0; p < n; ++p) {
+            int rc = perk_dd_stage(ctxs[p], U[p], dt, i, 1);
+            if (rc) return rc;
+        }
+        for (int p = 0; p < n; ++p)
+            for (int q = 0; q < n; ++q)
+                if (q != p) {
+                    int rc = perk_dd_exchange(ctxs[p], ctxs[q], U[p], U[q], i, 0);
+                    if (rc) return rc;
+                }
+    }
+    return PERK_OK;
 }

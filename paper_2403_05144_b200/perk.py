@@ -102,6 +102,16 @@ def lib():
                                          C.POINTER(perk_tableau)]
         L.perk_pattern_mask.argtypes = [i32, i32, i32, C.POINTER(i32), i32, C.POINTER(C.c_uint64)]
         L.perk_init.argtypes = [C.POINTER(P), C.POINTER(perk_problem), P, C.POINTER(perk_tableau), P]
+        L.perk_init_dd.argtypes = [C.POINTER(P), C.POINTER(perk_problem), P, C.POINTER(perk_tableau), P, i32, i32]
+        L.perk_dd_split.argtypes = [i64, P, i32, P]
+        L.perk_dd_info.argtypes = [P, C.POINTER(i32), C.POINTER(i32), C.POINTER(i64), C.POINTER(i64)]
+        L.perk_dd_counts.argtypes = [P, i32, i32, P, P]
+        L.perk_dd_get_list.argtypes = [P, i32, i32, P, i64, C.POINTER(i64)]
+        L.perk_dd_stage.argtypes = [P, P, dbl, i32, i32]
+        L.perk_dd_pack.argtypes = [P, P, i32, i32, i32, P]
+        L.perk_dd_unpack.argtypes = [P, P, i32, i32, i32, P]
+        L.perk_dd_exchange.argtypes = [P, P, P, P, i32, i32]
+        L.perk_dd_group_step.argtypes = [P, i32, P, dbl]
         L.perk_destroy.argtypes = [P]
         L.perk_set_stream.argtypes = [P, P]
         L.perk_step.argtypes = [P, P, dbl]
@@ -115,12 +125,14 @@ def lib():
         L.perk_get_faces.argtypes = [P, i32, P, P, i64, C.POINTER(i64)]
         L.perk_get_list.argtypes = [P, i32, P, i64, P]
         L.perk_get_count_active.argtypes = [P, i32, P]
+        L.perk_get_halo_counts.argtypes = [P, P]
         L.perk_get_counters.argtypes = [P, C.POINTER(i64), C.POINTER(i64)]
         L.perk_sync.argtypes = [P]
         L.perk_last_error.argtypes = [P]
         L.perk_last_error.restype = C.c_char_p
         L.perk_profile_step.argtypes = [P, P, dbl, P, P]
         L.perk_time_kernels.argtypes = [P, P, dbl, C.c_uint32, i32, C.POINTER(C.c_float)]
+        L.perk_time_kernels_ex.argtypes = [P, P, dbl, C.c_uint32, i32, P, i64, C.POINTER(C.c_float)]
         L.perk_profile_repartition.argtypes = [P, P, P, P, P]
         L.perk_launches_per_step.argtypes = [P, C.POINTER(i32)]
         L.perk_amr_indicator.argtypes = [P, P, C.POINTER(perk_amr), P]
@@ -138,7 +150,9 @@ def exported_symbols():
             "perk_get_leaves", "perk_get_faces", "perk_get_list", "perk_get_count_active", "perk_get_counters",
             "perk_sync", "perk_last_error", "perk_profile_step", "perk_time_kernels", "perk_profile_repartition",
             "perk_launches_per_step", "perk_amr_indicator", "perk_amr_adapt", "perk_amr_launches",
-            "perk_set_shock_capturing", "perk_sc_alpha", "perk_pattern_mask"]
+            "perk_set_shock_capturing", "perk_sc_alpha", "perk_pattern_mask", "perk_get_halo_counts", "perk_time_kernels_ex",
+            "perk_init_dd", "perk_dd_split", "perk_dd_info", "perk_dd_counts", "perk_dd_get_list", "perk_dd_stage",
+            "perk_dd_pack", "perk_dd_unpack", "perk_dd_exchange", "perk_dd_group_step"]
 
 
 PATTERNS = {"standard": 0, "early": 1, "alternating": 2}
@@ -242,7 +256,7 @@ class Perk:
     """One P-ERK multirate DGSEM context on the current CUDA device (all work on the current stream)."""
 
     def __init__(self, problem: dict, level_map, S: int, E, alpha_rows=None, max_cells=None, stream=None,
-                 family=None, pattern=None, c_S: float = 0.5):
+                 family=None, pattern=None, c_S: float = 0.5, rank: int = 0, nranks: int = 1):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("CUDA device required: libperk_b200 has no CPU path")
@@ -260,8 +274,9 @@ class Perk:
         lm = self._to_dev_u8(level_map)
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         h = C.c_void_p()
-        rc = lib().perk_init(C.byref(h), C.byref(self._prob), _ptr(lm), C.byref(self._tab),
-                             C.c_void_p(self.stream.cuda_stream))
+        self.rank, self.nranks = int(rank), int(nranks)
+        rc = lib().perk_init_dd(C.byref(h), C.byref(self._prob), _ptr(lm), C.byref(self._tab),
+                                C.c_void_p(self.stream.cuda_stream), self.rank, self.nranks)
         self.h = h
         if rc != 0:
             msg = lib().perk_last_error(h).decode() if h else ""
@@ -407,12 +422,18 @@ class Perk:
         lst = np.zeros(max(n, 1), np.int32)
         seg = np.zeros(self.R + 1, np.int64)
         _check(self.h, lib().perk_get_list(self.h, k, lst.ctypes.data, max(n, 1), seg.ctypes.data))
-        return lst[:n], seg
+        return lst[: int(seg[-1])], seg      # a sub-domain's lists hold only its owned items
 
     def count_active(self, kind: str):
         out = np.zeros(self.S, np.int32)
         _check(self.h, lib().perk_get_count_active(self.h, KIND[kind], out.ctypes.data))
         return out
+
+    def halo_counts(self):
+        """BR1 / shock-capturing halo items per stage: dict kind -> array of S counts"""
+        out = np.zeros(3 * self.S, np.int32)
+        _check(self.h, lib().perk_get_halo_counts(self.h, out.ctypes.data))
+        return {"elements": out[: self.S], "interfaces": out[self.S: 2 * self.S], "mortars": out[2 * self.S:]}
 
     def counters(self):
         ev, st = C.c_int64(), C.c_int64()
@@ -430,14 +451,20 @@ class Perk:
         _check(self.h, lib().perk_profile_step(self.h, _ptr(U), float(dt), ms, nl))
         return list(ms), list(nl)
 
-    def time_kernels(self, U, dt, kinds, reps=10):
+    def time_kernels(self, U, dt, kinds, reps=10, flush=None):
         """device ms per step of only the kernels of `kinds` (0 surface, 1 volume+stage, 4/5 BR1),
-        launched as perk_step does (graph + programmatic launches); timing only, U is garbage after"""
+        launched as perk_step does (graph + programmatic launches); timing only, U is garbage after.
+        flush: a device tensor overwritten between the replays (L2 flush), or None"""
         mask = 0
         for k in kinds:
             mask |= 1 << k
         ms = C.c_float()
-        _check(self.h, lib().perk_time_kernels(self.h, _ptr(U), float(dt), mask, int(reps), C.byref(ms)))
+        if flush is None:
+            _check(self.h, lib().perk_time_kernels(self.h, _ptr(U), float(dt), mask, int(reps), C.byref(ms)))
+        else:
+            nbytes = flush.numel() * flush.element_size()
+            _check(self.h, lib().perk_time_kernels_ex(self.h, _ptr(U), float(dt), mask, int(reps), _ptr(flush),
+                                                      int(nbytes), C.byref(ms)))
         return ms.value
 
     def profile_repartition(self, level_map, U):
@@ -452,3 +479,209 @@ class Perk:
         t = self._tab
         return dict(S=t.S, R=t.R, E=list(t.E[: t.R]), c=list(t.c[: t.S]),
                     a_sub=[list(t.a_sub[r][: t.S]) for r in range(t.R)])
+
+
+# ------------------------------------------------------------------------------------------------
+# spatial domain decomposition (include/perk.h perk_dd_*) -- marshalling only
+# ------------------------------------------------------------------------------------------------
+def dd_split(weights, nranks: int):
+    """the library's E-weighted contiguous split (host function perk_dd_split): owner rank per leaf"""
+    w = np.ascontiguousarray(np.asarray(weights, dtype=np.int32))
+    out = np.zeros(max(len(w), 1), np.int32)
+    _check(None, lib().perk_dd_split(len(w), w.ctypes.data, int(nranks), out.ctypes.data))
+    return out[: len(w)]
+
+
+def _dd_info(p):
+    r, n, f, c = C.c_int32(), C.c_int32(), C.c_int64(), C.c_int64()
+    _check(p.h, lib().perk_dd_info(p.h, C.byref(r), C.byref(n), C.byref(f), C.byref(c)))
+    return r.value, n.value, f.value, c.value
+
+
+def _dd_counts(p, peer, what):
+    snd = np.zeros(p.S, np.int32)
+    rcv = np.zeros(p.S, np.int32)
+    _check(p.h, lib().perk_dd_counts(p.h, int(peer), int(what), snd.ctypes.data, rcv.ctypes.data))
+    return snd, rcv
+
+
+def _dd_list(p, peer, direction):
+    n = C.c_int64()
+    buf = np.zeros(max(p.max_cells, 1), np.int32)
+    _check(p.h, lib().perk_dd_get_list(p.h, int(peer), int(direction), buf.ctypes.data, len(buf), C.byref(n)))
+    return buf[: n.value]
+
+
+Perk.dd_info = lambda self: _dd_info(self)
+Perk.dd_counts = lambda self, peer, what: _dd_counts(self, peer, what)
+Perk.dd_list = lambda self, peer, direction: _dd_list(self, peer, direction)
+
+
+class DomainGroup:
+    """All sub-domains of an nranks-way split held by this process on the current device and stream
+    (perk_init_dd + perk_dd_group_step): the in-process form of the multi-GPU decomposition, used to
+    prove it on one GPU.  Every sub-domain keeps a full-size state whose owned rows are its own."""
+
+    def __init__(self, problem: dict, level_map, S: int, E, nranks: int, **kw):
+        self.parts = [Perk(problem, level_map, S, E, rank=p, nranks=nranks, **kw) for p in range(nranks)]
+        self.nranks = nranks
+        self.torch = self.parts[0].torch
+
+    def initial_state(self, ic):
+        return [p.initial_state(ic) for p in self.parts]
+
+    def step(self, Us, dt, nsteps: int = 1):
+        arr = (C.c_void_p * self.nranks)(*[u.data_ptr() for u in Us])
+        hs = (C.c_void_p * self.nranks)(*[p.h.value for p in self.parts])
+        for _ in range(nsteps):
+            _check(self.parts[0].h, lib().perk_dd_group_step(hs, self.nranks, arr, float(dt)))
+
+    def ranges(self):
+        return [_dd_info(p)[2:] for p in self.parts]
+
+    def gather(self, Us):
+        """the global state: each sub-domain's owned rows (numpy)"""
+        n = self.parts[0].n_cells
+        out = np.zeros((n,) + tuple(Us[0].shape[1:]))
+        for p, U in zip(self.parts, Us):
+            f, c = _dd_info(p)[2:]
+            out[f:f + c] = U[f:f + c].cpu().numpy()
+        return out
+
+    def allgather(self, Us):
+        """make every sub-domain's state complete (before perk_repartition / perk_amr_*)"""
+        for p, U in zip(self.parts, Us):
+            f, c = _dd_info(p)[2:]
+            for V in Us:
+                if V is not U:
+                    V[f:f + c].copy_(U[f:f + c])
+
+    def repartition(self, level_map, Us):
+        self.allgather(Us)
+        for p, U in zip(self.parts, Us):
+            p.repartition(level_map, U)
+
+    def counters(self):
+        ev = st = 0
+        for p in self.parts:
+            e, s_ = p.counters()
+            ev += e
+            st = max(st, s_)
+        return ev, st
+
+    def sync(self):
+        for p in self.parts:
+            p.sync()
+
+    def close(self):
+        for p in self.parts:
+            p.close()
+
+
+class DistributedPerk:
+    """One sub-domain per process (rank = torch.distributed rank): per stage the library's stage
+    launches and pack / unpack kernels, with the blocks moved by torch.distributed point-to-point
+    (NCCL on GPUs; with the gloo backend the buffers are staged through host memory, which is how
+    the path is exercised with several processes on one GPU)."""
+
+    def __init__(self, problem: dict, level_map, S: int, E, dist, **kw):
+        self.dist = dist
+        self.rank, self.nranks = dist.get_rank(), dist.get_world_size()
+        self.p = Perk(problem, level_map, S, E, rank=self.rank, nranks=self.nranks, **kw)
+        self.torch = self.p.torch
+        self.ns = problem["equation"] == "navier_stokes"
+        self.host_staged = dist.get_backend() != "nccl"
+        self._setup()
+
+    def _setup(self):
+        """per peer and exchange kind: per-stage block counts (synchronising; once per mesh)"""
+        p = self.p
+        self.row = {0: p.nv * p.npe, 1: 48}
+        self.cnt = {}
+        self.peers = []
+        for q in range(self.nranks):
+            if q == self.rank:
+                continue
+            c0 = _dd_counts(p, q, 0)
+            if c0[0].max() > 0 or c0[1].max() > 0:
+                self.peers.append(q)
+            self.cnt[(q, 0)] = c0
+            if self.ns:
+                self.cnt[(q, 1)] = _dd_counts(p, q, 1)
+        nmax = max([int(max(c[0].max(), c[1].max())) for c in self.cnt.values()] + [1])
+        T = self.torch
+        self.sbuf = {q: T.empty(nmax * 64, dtype=T.float64, device="cuda") for q in self.peers}
+        self.rbuf = {q: T.empty(nmax * 64, dtype=T.float64, device="cuda") for q in self.peers}
+
+    def initial_state(self, ic):
+        return self.p.initial_state(ic)
+
+    def _exchange(self, U, i, what):
+        T, dist, p = self.torch, self.dist, self.p
+        lib_ = lib()
+        for q in self.peers:
+            _check(p.h, lib_.perk_dd_pack(p.h, _ptr(U), i, what, q, _ptr(self.sbuf[q])))
+        ops, host = [], {}
+        for q in self.peers:
+            ns_, nr_ = int(self.cnt[(q, what)][0][i - 1]), int(self.cnt[(q, what)][1][i - 1])
+            sb = self.sbuf[q][: ns_ * self.row[what]]
+            rb = self.rbuf[q][: nr_ * self.row[what]]
+            if self.host_staged:
+                sb, rb_h = sb.cpu(), T.empty(rb.numel(), dtype=T.float64)
+                host[q] = rb_h
+                rb = rb_h
+            if ns_:
+                ops.append(dist.P2POp(dist.isend, sb, q))
+            if nr_:
+                ops.append(dist.P2POp(dist.irecv, rb, q))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        for q in self.peers:
+            nr_ = int(self.cnt[(q, what)][1][i - 1])
+            if not nr_:
+                continue
+            if self.host_staged:
+                self.rbuf[q][: nr_ * self.row[what]].copy_(host[q])
+            _check(p.h, lib_.perk_dd_unpack(p.h, _ptr(U), i, what, q, _ptr(self.rbuf[q])))
+
+    def step(self, U, dt, nsteps: int = 1):
+        p = self.p
+        lib_ = lib()
+        for _ in range(nsteps):
+            for i in range(1, p.S + 1):
+                if self.ns:
+                    _check(p.h, lib_.perk_dd_stage(p.h, _ptr(U), float(dt), i, 0))
+                    self._exchange(U, i, 1)
+                _check(p.h, lib_.perk_dd_stage(p.h, _ptr(U), float(dt), i, 1))
+                self._exchange(U, i, 0)
+
+    def owned(self):
+        return _dd_info(self.p)[2:]
+
+    def allgather(self, U):
+        """complete state on every rank (before perk_repartition / perk_amr_*): owned row ranges"""
+        T, dist = self.torch, self.dist
+        f, c = self.owned()
+        meta = T.tensor([f, c], dtype=T.int64, device="cuda" if not self.host_staged else "cpu")
+        allm = [T.zeros_like(meta) for _ in range(self.nranks)]
+        dist.all_gather(allm, meta)
+        for q, m in enumerate(allm):
+            fq, cq = int(m[0]), int(m[1])
+            blk = U[fq:fq + cq].contiguous()
+            if self.host_staged:
+                blk = blk.cpu()
+            dist.broadcast(blk, src=q)
+            if q != self.rank:
+                U[fq:fq + cq].copy_(blk)
+
+    def repartition(self, level_map, U):
+        self.allgather(U)
+        self.p.repartition(level_map, U)
+        self._setup()
+
+    def counters(self):
+        return self.p.counters()
+
+    def close(self):
+        self.p.close()

@@ -26,7 +26,7 @@ def run(arg):
     import workloads as W
     from oracle import oracle as O
     from oracle import tableau as T
-    from gpu_util import gpu_state_numpy, rel_err_per_var
+    from gpu_util import compare_mesh, gpu_state_numpy, rel_err_per_var
     from paper_2403_05144_b200 import Perk
     w = W.make(cfg)
     steps = steps_override or PLAN[cfg] or w.steps
@@ -81,9 +81,15 @@ def run(arg):
     err = rel_err_per_var(gpu_state_numpy(gpu, Ug), Uo)
     lo, lg = ora.leaves(), gpu.leaves()
     same_mesh = all(np.array_equal(lo[q], lg[q]) for q in ("fx", "fy", "level", "member"))
+    try:                                   # faces, per-member lists and stage prefix tables, bitwise
+        compare_mesh(ora, gpu)
+        same_lists = True
+    except AssertionError:
+        same_lists = False
     res = {"workload": w.name + (f"_{variant}" if variant else ""), "steps": steps, "baseline_steps": w.steps, "re_meshes": remeshes,
            "cells": int(ora.n), "max_rel_err_per_var": [float(x) for x in err], "mesh_identical": same_mesh,
-           "pass": bool(err.max() <= 1e-10 and same_mesh and map_diffs == 0), "oracle_seconds": round(time.time() - t0, 1)}
+           "lists_identical": same_lists,
+           "pass": bool(err.max() <= 1e-10 and same_mesh and same_lists and map_diffs == 0), "oracle_seconds": round(time.time() - t0, 1)}
     if variant == "i":
         res["amr_maps_differing"] = map_diffs   # near-threshold ties; 0 = every adapted map bit-exact
     out = os.path.join(ROOT, "gpurun_out")                # each config's result as soon as it is done
