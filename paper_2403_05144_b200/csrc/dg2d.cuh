@@ -211,8 +211,9 @@ __device__ __forceinline__ void sc_amax(double *p, double v)
     atomicMax(reinterpret_cast<unsigned long long *>(p), (unsigned long long)__double_as_longlong(v));
 }
 
+// (Navier-Stokes with the shock-capturing smoothing: 2 CTAs per SM, the 80-register budget of 3 spilled)
 template <int MODE, bool NS, bool SCS = false>
-__global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StageParams sp, const double *__restrict__ Un,
+__global__ void __launch_bounds__(256, (NS && SCS) ? 2 : SURF2D_MINB) k_surf2d(MeshDev md, StageParams sp, const double *__restrict__ Un,
                                                const double *__restrict__ Ubuf, const double *__restrict__ K1,
                                                const double *__restrict__ Uin, double *__restrict__ Fs,
                                                const double *__restrict__ Vt, const double *__restrict__ alpha_raw,
@@ -553,7 +554,8 @@ __host__ __device__ constexpr size_t vol2d_smem_bytes(bool ns)
 // u_{a+1}) of the problem's surface flux (F_{-1/2} = F_{N+1/2} = 0), evaluated in line coordinates
 // from the primitives the line already holds; alpha = 0 elements skip it.
 template <int MODE, bool NS, bool SC = false>
-__global__ void __launch_bounds__(vol2d_threads(NS), NS ? (VOL2D_EPB_NS == 8 ? 5 : 3) : 3)
+// (Navier-Stokes + shock capturing: 2 CTAs per SM -- at 3 the 168-register budget spilled 44 B)
+__global__ void __launch_bounds__(vol2d_threads(NS), NS ? (VOL2D_EPB_NS == 8 ? 5 : (SC ? 2 : 3)) : 3)
 k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                                                  double *__restrict__ Ubuf, double *__restrict__ K1,
                                                  const double *__restrict__ Fs, const double *__restrict__ Uin,

@@ -72,7 +72,7 @@ struct perk_ctx {
     uint8_t *amr_want = nullptr, *amr_newlev = nullptr;  // ping-pong finest-grid maps of the balance
     uint8_t *amr_map[2] = {nullptr, nullptr};
     int *amr_flags = nullptr;                            // balance: iteration k changed a cell
-    int vol_blocks = 0, surf_blocks = 0, grad_blocks = 0;
+    int vol_blocks = 0, vol_blocks_sc = 0, surf_blocks = 0, surf_blocks_nssc = 0, grad_blocks = 0;
     unsigned kind_mask = ~0u;              // kernel kinds launch_step issues (perk_time_kernels)
     bool step1d = false;                   // small 1D mesh: whole step in one single-CTA launch
     StepTab1D *tb1d = nullptr;
@@ -459,7 +459,7 @@ static void launch_surface(perk_ctx *c, cudaStream_t s, const StageParams &sp, c
         const double *ar = c->alpha_raw;
         double *al = c->alpha;
         if (c->ns && scs)
-            launch_pdl(st ? k_surf2d<MODE_STAGE, true, true> : k_surf2d<MODE_RHS, true, true>, c->surf_blocks, 256, 0, s, md, sp, Un, (const double *)c->Ubuf, (const double *)c->K1, Uin, c->Fs, vt, ar, al);
+            launch_pdl(st ? k_surf2d<MODE_STAGE, true, true> : k_surf2d<MODE_RHS, true, true>, c->surf_blocks_nssc, 256, 0, s, md, sp, Un, (const double *)c->Ubuf, (const double *)c->K1, Uin, c->Fs, vt, ar, al);
         else if (c->ns)
             launch_pdl(st ? k_surf2d<MODE_STAGE, true> : k_surf2d<MODE_RHS, true>, c->surf_blocks, 256, 0, s, md, sp, Un, (const double *)c->Ubuf, (const double *)c->K1, Uin, c->Fs, vt, ar, al);
         else if (scs)
@@ -488,11 +488,11 @@ static void launch_volume(perk_ctx *c, cudaStream_t s, const StageParams &sp, do
         const int tn = vol2d_threads(c->ns);
         const size_t sm = vol2d_smem_bytes(c->ns);
         if (c->ns && c->sc)
-            launch_pdl(st ? k_vol2d<MODE_STAGE, true, true> : k_vol2d<MODE_RHS, true, true>, c->vol_blocks, tn, sm, s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, (const double *)c->Gs, c->Wb, al, c->alpha_raw, c->scp);
+            launch_pdl(st ? k_vol2d<MODE_STAGE, true, true> : k_vol2d<MODE_RHS, true, true>, c->vol_blocks_sc, tn, sm, s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, (const double *)c->Gs, c->Wb, al, c->alpha_raw, c->scp);
         else if (c->ns)
             launch_pdl(st ? k_vol2d<MODE_STAGE, true> : k_vol2d<MODE_RHS, true>, c->vol_blocks, tn, sm, s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, (const double *)c->Gs, c->Wb, al, c->alpha_raw, c->scp);
         else if (c->sc)
-            launch_pdl(st ? k_vol2d<MODE_STAGE, false, true> : k_vol2d<MODE_RHS, false, true>, c->vol_blocks, tn, sm, s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, (const double *)nullptr, c->Wb, al, c->alpha_raw, c->scp);
+            launch_pdl(st ? k_vol2d<MODE_STAGE, false, true> : k_vol2d<MODE_RHS, false, true>, c->vol_blocks_sc, tn, sm, s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, (const double *)nullptr, c->Wb, al, c->alpha_raw, c->scp);
         else
             launch_pdl(st ? k_vol2d<MODE_STAGE, false> : k_vol2d<MODE_RHS, false>, c->vol_blocks, tn, sm, s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, (const double *)nullptr, c->Wb, al, c->alpha_raw, c->scp);
     } else if (c->nv == 1) {
@@ -827,6 +827,10 @@ extern "C" int perk_init_dd(perk_ctx **out, const perk_problem *prob, const uint
         else CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vol2d<MODE_STAGE, false>, vol2d_threads(false), vol2d_smem_bytes(false)));
         const int want = (c->cap + vol2d_epb(c->ns) - 1) / vol2d_epb(c->ns);
         c->vol_blocks = std::min(want, SM_COUNT_B200 * std::max(occ, 1));
+        int occ_sc = 0;   // the shock-capturing variant has its own register budget (NS: 2 CTAs per SM)
+        if (c->ns) CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sc, k_vol2d<MODE_STAGE, true, true>, vol2d_threads(true), vol2d_smem_bytes(true)));
+        else CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sc, k_vol2d<MODE_STAGE, false, true>, vol2d_threads(false), vol2d_smem_bytes(false)));
+        c->vol_blocks_sc = std::min(want, SM_COUNT_B200 * std::max(occ_sc, 1));
         int occg = 0;
         CU(cudaFuncSetAttribute(k_grad2d<MODE_STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grad2d_smem_bytes()));
         CU(cudaFuncSetAttribute(k_grad2d<MODE_RHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grad2d_smem_bytes()));
@@ -835,6 +839,9 @@ extern "C" int perk_init_dd(perk_ctx **out, const perk_problem *prob, const uint
         int occf = 0;
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occf, k_surf2d<MODE_STAGE, false>, 256, 0));
         c->surf_blocks = std::min(blocks_for(4ll * c->cap_faces, 256), SM_COUNT_B200 * std::max(occf, 1));
+        int occfs = 0;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occfs, k_surf2d<MODE_STAGE, true, true>, 256, 0));
+        c->surf_blocks_nssc = std::min(blocks_for(4ll * c->cap_faces, 256), SM_COUNT_B200 * std::max(occfs, 1));
         // re-mesh (transfer double buffer, old-mesh copy) and AMR scratch, allocated up front so that
         // no cudaMalloc / memset lands inside a timed re-mesh
         CU(dalloc(c, &c->Utmp, (size_t)c->cap * c->nv * c->npe));
