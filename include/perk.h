@@ -295,6 +295,11 @@ int perk_profile_repartition(perk_ctx *ctx, const uint8_t *level_map_dev, double
                              int32_t *launches_host);
 /* Number of kernel launches one perk_step performs (graph nodes). */
 int perk_launches_per_step(perk_ctx *ctx, int32_t *launches);
+/* Race exposure, debug library only (libperk_debug.so, -DPERK_DEBUG; EUNSUPPORTED otherwise): seed != 0
+ * makes every thread of the staged kernels (k_vol2d, k_grad2d) sleep a pseudo-random 0..4 us at
+ * each warp barrier / asynchronous-copy wait, for all contexts of the current device; seed 0 turns it
+ * off.  Results must be bitwise those of an unjittered run (tests/test_gpu_races.py). */
+int perk_debug_jitter(uint32_t seed);
 
 /* ------------------------------------------------------------------------------------------------
  * Spatial domain decomposition over ranks.  The paper's

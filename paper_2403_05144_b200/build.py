@@ -46,11 +46,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return OUT
 
 
-def build_debug() -> str:
-    """lib/libperk_debug.so: the same library with the device-side bounds checks (PERK_DASSERT) on;
-    run the GPU tests against it with PERK_LIB_PATH=<that path> (compute-sanitizer is not available on
-    the GPU pool)."""
+def build_debug(force: bool = True) -> str:
+    """lib/libperk_debug.so: the same library with the device-side bounds checks (PERK_DASSERT) and the
+    race-exposure jitter (perk_debug_jitter) on; run the GPU tests against it with
+    PERK_LIB_PATH=<that path> (compute-sanitizer is not available on the GPU pool)."""
     out = os.path.join(HERE, "lib", "libperk_debug.so")
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(s) for s in sources()):
+        return out
     cmd = [NVCC] + [f for f in FLAGS if f not in ("-Xptxas", "-v")] + ["-DPERK_DEBUG", "-I", os.path.join(ROOT, "include"),
                                                                       "-o", out, SRC]
     res = subprocess.run(cmd, capture_output=True, text=True)

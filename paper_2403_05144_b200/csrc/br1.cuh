@@ -172,8 +172,10 @@ __global__ void __launch_bounds__(128, 4) k_grad2d(MeshDev md, StageParams sp, c
         PERK_DASSERT(e >= 0 && e < md.n[0]);
         const int src = state_src(sp, pk_member(pk));
         const double hcell = md.hf * (double)(1 << (md.max_level - pk_level(pk)));
+        PERK_JITTER(11);
         cp_async_wait<0>();
         __syncwarp();
+        PERK_JITTER(12);
         {
             double2 u[4];
 #pragma unroll
@@ -198,6 +200,7 @@ __global__ void __launch_bounds__(128, 4) k_grad2d(MeshDev md, StageParams sp, c
                 sm[G_V1 + c][1][yo + eoy + 4 * (i0 + 1) + j0] = w[1][c];
             }
         }
+        PERK_JITTER(13);
         __syncwarp();
         if (has_next) issue_state(pk_next);       // stg consumed
         cp_async_commit();
@@ -211,6 +214,7 @@ __global__ void __launch_bounds__(128, 4) k_grad2d(MeshDev md, StageParams sp, c
             *reinterpret_cast<double2 *>(&sm[G_Q + c][o][lo]) = make_double2(q[c][0], q[c][1]);
             *reinterpret_cast<double2 *>(&sm[G_Q + c][o][lo + 2]) = make_double2(q[c][2], q[c][3]);
         }
+        PERK_JITTER(14);
         __syncwarp();
         if (has_next) issue_gs(pk_next);          // gst consumed
         cp_async_commit();

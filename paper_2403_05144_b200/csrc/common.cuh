@@ -29,6 +29,31 @@
 
 namespace perk {
 
+// Race exposure (debug builds only; compute-sanitizer's racecheck is closed on this GPU pool): with
+// perk_debug_jitter(seed != 0) every thread sleeps a pseudo-random 0..4 us at the marked points of
+// the staged kernels (before each warp barrier / wait and before reading staged data), so threads of
+// a warp drift apart.  A missing __syncwarp / cp.async wait then reads stale shared memory and the
+// result differs from the unjittered run (tests/test_gpu_races.py compares them bitwise).
+#ifdef PERK_DEBUG
+__device__ unsigned g_jitter_seed;
+__device__ __forceinline__ void perk_jitter(unsigned site)
+{
+    const unsigned s = g_jitter_seed;
+    if (!s) return;
+    unsigned h = s ^ (blockIdx.x * 0x9E3779B9u) ^ (threadIdx.x * 0x85EBCA6Bu) ^ (site * 0xC2B2AE35u) ^
+                 (unsigned)clock();
+    h ^= h >> 16;
+    h *= 0x7FEB352Du;
+    h ^= h >> 15;
+    __nanosleep(h & 4095u);
+}
+#define PERK_JITTER(site) perk_jitter(site)
+#else
+#define PERK_JITTER(site) \
+    do {                  \
+    } while (0)
+#endif
+
 constexpr int NP = 4;          // N + 1 LGL nodes per direction (N = 3)
 constexpr int MAXV = 4;
 constexpr int MAXS = 64;

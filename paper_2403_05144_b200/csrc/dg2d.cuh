@@ -444,6 +444,7 @@ __device__ __forceinline__ void line_gradient(const double (*sm)[2][LS], int o, 
             q[c][a] = (Jq * sc[c]) * t;
         }
     }
+    PERK_JITTER(8);
 }
 
 // NS volume contribution (MODE_STAGE and MODE_RHS): adds sum_a Dhat_ia F^v_o(node a) to acc (in line
@@ -651,8 +652,10 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
         const double al = SC ? alpha[e] : 0.0;   // read before this element's next-stage alpha is written
 
         // phase 1: nodes q0, q0+1 -> primitives + logs, stored in x-line and y-line layouts
+        PERK_JITTER(1);
         cp_async_wait<0>();
         __syncwarp();
+        PERK_JITTER(2);
         {
             double2 u[4];
 #pragma unroll
@@ -693,6 +696,7 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                 sm[k][1][yo + eoy + 4 * (i0 + 1) + j0] = fy[1][k];
             }
         }
+        PERK_JITTER(3);
         __syncwarp();   // the warp has read stg: refill it (next group) and stage this group's epilogue operands
         {
             const bool need_un = MODE == MODE_STAGE && sp.stage > 1;
@@ -788,6 +792,7 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
         }
         // NS: + sum_a Dhat_ia F^v(node a) along the line (BR1 gradients recomputed from Gs)
         if (NS) {
+            PERK_JITTER(4);
             if (has_next) cp_async_wait<1>();
             else cp_async_wait<0>();
             __syncwarp();
@@ -803,6 +808,7 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                 acc[a][2] = t;
             }
         }
+        PERK_JITTER(5);
         if (has_next) cp_async_wait<1>();    // this group's epilogue operands (the next state may still fly)
         else cp_async_wait<0>();
         __syncwarp();
@@ -852,12 +858,14 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
         // members in the launch's prefix that do not evaluate this stage (non-standard patterns) write nothing
         const bool writes = valid && (MODE == MODE_RHS || ((sp.actmask >> m) & 1u));
         const double J = -2.0 / hcell;
+        PERK_JITTER(6);
         __syncwarp();   // all primitives consumed: reuse sm[v][o] as the accumulator arrays
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
             *reinterpret_cast<double2 *>(&sm[v][o][lo]) = make_double2(acc[0][v], acc[1][v]);
             *reinterpret_cast<double2 *>(&sm[v][o][lo + 2]) = make_double2(acc[2][v], acc[3][v]);
         }
+        PERK_JITTER(7);
         __syncwarp();
 
         // phase 3: K = -(2/h) (x + y contributions), stage epilogue for nodes q0, q0+1

@@ -827,21 +827,30 @@ extern "C" int perk_init_dd(perk_ctx **out, const perk_problem *prob, const uint
         else CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_vol2d<MODE_STAGE, false>, vol2d_threads(false), vol2d_smem_bytes(false)));
         const int want = (c->cap + vol2d_epb(c->ns) - 1) / vol2d_epb(c->ns);
         c->vol_blocks = std::min(want, SM_COUNT_B200 * std::max(occ, 1));
+        // test hooks: PERK_VOL_BLOCKS / PERK_GRAD_BLOCKS / PERK_SURF_BLOCKS cap the persistent grids (a grid
+        // of 1 CTA sends every element group through one CTA's staging rings; results must not change)
+        auto cap_env = [](const char *name, int v) {
+            const char *e = std::getenv(name);
+            const int k = e ? std::atoi(e) : 0;
+            return k > 0 ? std::min(v, k) : v;
+        };
+        c->vol_blocks = cap_env("PERK_VOL_BLOCKS", c->vol_blocks);
         int occ_sc = 0;   // the shock-capturing variant has its own register budget (NS: 2 CTAs per SM)
         if (c->ns) CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sc, k_vol2d<MODE_STAGE, true, true>, vol2d_threads(true), vol2d_smem_bytes(true)));
         else CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sc, k_vol2d<MODE_STAGE, false, true>, vol2d_threads(false), vol2d_smem_bytes(false)));
-        c->vol_blocks_sc = std::min(want, SM_COUNT_B200 * std::max(occ_sc, 1));
+        c->vol_blocks_sc = cap_env("PERK_VOL_BLOCKS", std::min(want, SM_COUNT_B200 * std::max(occ_sc, 1)));
         int occg = 0;
         CU(cudaFuncSetAttribute(k_grad2d<MODE_STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grad2d_smem_bytes()));
         CU(cudaFuncSetAttribute(k_grad2d<MODE_RHS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)grad2d_smem_bytes()));
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occg, k_grad2d<MODE_STAGE>, 128, grad2d_smem_bytes()));
-        c->grad_blocks = std::min(want, SM_COUNT_B200 * std::max(occg, 1));
+        c->grad_blocks = cap_env("PERK_GRAD_BLOCKS", std::min(want, SM_COUNT_B200 * std::max(occg, 1)));
         int occf = 0;
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occf, k_surf2d<MODE_STAGE, false>, 256, 0));
         c->surf_blocks = std::min(blocks_for(4ll * c->cap_faces, 256), SM_COUNT_B200 * std::max(occf, 1));
         int occfs = 0;
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occfs, k_surf2d<MODE_STAGE, true, true>, 256, 0));
-        c->surf_blocks_nssc = std::min(blocks_for(4ll * c->cap_faces, 256), SM_COUNT_B200 * std::max(occfs, 1));
+        c->surf_blocks_nssc = cap_env("PERK_SURF_BLOCKS", std::min(blocks_for(4ll * c->cap_faces, 256), SM_COUNT_B200 * std::max(occfs, 1)));
+        c->surf_blocks = cap_env("PERK_SURF_BLOCKS", c->surf_blocks);
         // re-mesh (transfer double buffer, old-mesh copy) and AMR scratch, allocated up front so that
         // no cudaMalloc / memset lands inside a timed re-mesh
         CU(dalloc(c, &c->Utmp, (size_t)c->cap * c->nv * c->npe));
@@ -1669,4 +1678,20 @@ extern "C" int perk_dd_group_step(perk_ctx **ctxs, int32_t n, double **U, double
                 }
     }
     return PERK_OK;
+}
+
+// ----------------------------------------------------------------------------------------------
+// race exposure (debug builds)
+// ----------------------------------------------------------------------------------------------
+extern "C" int perk_debug_jitter(uint32_t seed)
+{
+#ifdef PERK_DEBUG
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return PERK_ECUDA;
+    if (cudaMemcpyToSymbol(g_jitter_seed, &seed, sizeof(seed)) != cudaSuccess) return PERK_ECUDA;
+    return PERK_OK;
+#else
+    (void)seed;
+    return PERK_EUNSUPPORTED;
+#endif
 }

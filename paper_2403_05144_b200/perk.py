@@ -112,6 +112,7 @@ def lib():
         L.perk_dd_unpack.argtypes = [P, P, i32, i32, i32, P]
         L.perk_dd_exchange.argtypes = [P, P, P, P, i32, i32]
         L.perk_dd_group_step.argtypes = [P, i32, P, dbl]
+        L.perk_debug_jitter.argtypes = [C.c_uint32]
         L.perk_destroy.argtypes = [P]
         L.perk_set_stream.argtypes = [P, P]
         L.perk_step.argtypes = [P, P, dbl]
@@ -152,7 +153,7 @@ def exported_symbols():
             "perk_launches_per_step", "perk_amr_indicator", "perk_amr_adapt", "perk_amr_launches",
             "perk_set_shock_capturing", "perk_sc_alpha", "perk_pattern_mask", "perk_get_halo_counts", "perk_time_kernels_ex",
             "perk_init_dd", "perk_dd_split", "perk_dd_info", "perk_dd_counts", "perk_dd_get_list", "perk_dd_stage",
-            "perk_dd_pack", "perk_dd_unpack", "perk_dd_exchange", "perk_dd_group_step"]
+            "perk_dd_pack", "perk_dd_unpack", "perk_dd_exchange", "perk_dd_group_step", "perk_debug_jitter"]
 
 
 PATTERNS = {"standard": 0, "early": 1, "alternating": 2}
