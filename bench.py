@@ -471,6 +471,7 @@ def run_decomposed(args, torch, dist, ws, rank, local, dev):
         print(json.dumps(line), flush=True)
     dp.close()
     dist.destroy_process_group()
+    return None
 
 
 def run_ours(args):
@@ -478,13 +479,15 @@ def run_ours(args):
     import torch.distributed as dist
 
     ws, rank, local = _dist()
-    if ws > 1 and not args.replicas:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
-        return run_decomposed(args, torch, dist, ws, rank, local, torch.device("cuda", local))
     torch.cuda.set_device(local)
     if ws > 1:
         dist.init_process_group("nccl")
+    if ws > 1 and not args.replicas:
+        try:
+            return run_decomposed(args, torch, dist, ws, rank, local, torch.device("cuda", local))
+        except Exception as ex:   # report it on the line and measure replicas instead of printing nothing
+            args.decomposition_error = repr(ex)[:300]
+            dist.barrier()
     dev = torch.device("cuda", local)
     timer = _Timer(torch, dev, ws, dist)
     fp64 = _fp64_peak()
@@ -579,6 +582,8 @@ def run_ours(args):
             line["other_configs"] = others
         if cpu is not None:
             line["cpu_baseline"] = cpu
+        if getattr(args, "decomposition_error", None):
+            line["config"]["parallelism"] = f"replicas x{ws} (the domain decomposition failed: {args.decomposition_error})"
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()

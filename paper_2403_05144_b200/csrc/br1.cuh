@@ -106,12 +106,17 @@ __global__ void __launch_bounds__(256, 3) k_gsurf2d(MeshDev md, StageParams sp, 
 // 8 threads per element as in k_vol2d: gradients along the x-lines and y-lines, exchanged through
 // shared memory, then the normal viscous flux at the two end nodes of every line = the face nodes.
 // Persistent CTAs of 16 elements; the element's stage state and its 48 central traces are staged
-// with cp.async one group ahead (commit groups as in k_vol2d).
+// with cp.async one group ahead (commit groups as in k_vol2d); packed entries two groups ahead.
 constexpr int GRAD2D_LS = VOL2D_LS;
 constexpr int G_V1 = 0, G_V2 = 1, G_T = 2, G_Q = 3;     // shared fields: v1, v2, T, gradients (3)
 // staged central traces per element: 48 doubles padded to 52 (== 4 mod 16), so that the scalar trace
 // reads of the x-line threads (faces 0/1) and y-line threads (faces 2/3) of the two elements of a
 // half-warp fall into disjoint banks (with 48 the two elements collided)
+// staged central traces per element: 48 doubles padded to 52 (== 4 mod 16), so that the scalar trace
+// reads of the x-line threads (faces 0/1) and y-line threads (faces 2/3) of the two elements of a
+// half-warp fall into disjoint banks (with 48 the two elements collided).  (Loading each thread's 6
+// end traces into registers one group ahead instead, which frees this buffer: 1.33 vs 1.23 ms/step
+// on cfg 5, slower.)
 constexpr int GST_STRIDE = 4 * GV * NP + 4;
 __host__ __device__ constexpr size_t grad2d_smem_bytes()
 {
@@ -158,6 +163,7 @@ __global__ void __launch_bounds__(128, 4) k_grad2d(MeshDev md, StageParams sp, c
     };
     auto issue_gs = [&](int pkx) { copy_chunks(gst[le], Gs + (size_t)pk_elem(pkx) * 4 * GV * NP, 4 * GV * NP / 2); };
     const int pk0 = base < n_act ? entry_at(base) : 0;
+    int pk_ahead = base + stride < n_act ? entry_at(base + stride) : 0;   // entries two groups ahead
     pdl_wait();
     if (base >= n_act) return;
     int pk = pk0;
@@ -167,7 +173,8 @@ __global__ void __launch_bounds__(128, 4) k_grad2d(MeshDev md, StageParams sp, c
     for (; base < n_act; base += stride) {
         const bool valid = base + le < n_act;
         const bool has_next = base + stride < n_act;
-        const int pk_next = has_next ? entry_at(base + stride) : 0;
+        const int pk_next = pk_ahead;
+        pk_ahead = base + 2 * stride < n_act ? entry_at(base + 2 * stride) : 0;
         const int e = pk_elem(pk);
         PERK_DASSERT(e >= 0 && e < md.n[0]);
         const int src = state_src(sp, pk_member(pk));

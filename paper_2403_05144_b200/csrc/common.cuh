@@ -299,6 +299,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
 // the launch attribute.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// L1 prefetch of the line holding p (no register, no scoreboard entry)
+__device__ __forceinline__ void prefetch_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
 // Ampere-style asynchronous copies (SASS LDGSTS): no registers, per-thread commit groups
 __device__ __forceinline__ void cp_async16(void *dst, const void *src)
 {

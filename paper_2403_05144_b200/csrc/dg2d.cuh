@@ -281,6 +281,7 @@ __global__ void __launch_bounds__(256, (NS && SCS) ? 2 : SURF2D_MINB) k_surf2d(M
             const int o = I.z;
             const int src = state_src(sp, I.w);    // conforming: both sides share the member
             double uL[4], uR[4], fl[4];
+
             trace2d(sb, src, dtc, I.x, 2 * o, k, uL);
             trace2d(sb, src, dtc, I.y, 2 * o + 1, k, uR);
             numflux2d(uL, uR, o, g, md.surface, fl);
@@ -636,12 +637,17 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
         cp_async_commit();
     };
     int pk = MODE == MODE_STAGE ? pk0 : entry_at(base);
+    // packed entries run two groups ahead: the next group's entry is needed right after phase 1 (to
+    // issue its state copy), too soon for a load issued at the top of the same iteration (ncu: 15 %
+    // of the Navier-Stokes kernel's stall samples waited on it)
+    int pk_ahead = base + stride < n_act ? entry_at(base + stride) : 0;
     issue_state(pk);
 
     for (; base < n_act; base += stride) {
         const bool valid = base + le < n_act;
         const bool has_next = base + stride < n_act;     // uniform across the CTA
-        const int pk_next = has_next ? entry_at(base + stride) : 0;   // consumed after phase 1
+        const int pk_next = pk_ahead;                     // consumed after phase 1
+        pk_ahead = base + 2 * stride < n_act ? entry_at(base + 2 * stride) : 0;
         const int e = pk_elem(pk);
         PERK_DASSERT(!valid || (e >= 0 && e < md.n[0]));
         const int m = pk_member(pk);

@@ -593,6 +593,7 @@ class DistributedPerk:
         self.ns = problem["equation"] == "navier_stokes"
         self.host_staged = dist.get_backend() != "nccl"
         self._setup()
+        dist.barrier()   # every rank's communicator is up before the first point-to-point batch
 
     def _setup(self):
         """per peer and exchange kind: per-stage block counts (synchronising; once per mesh)"""
