@@ -213,7 +213,10 @@ __device__ __forceinline__ void sc_amax(double *p, double v)
 
 // (Navier-Stokes with the shock-capturing smoothing: 2 CTAs per SM, the 80-register budget of 3 spilled)
 template <int MODE, bool NS, bool SCS = false>
-__global__ void __launch_bounds__(256, (NS && SCS) ? 2 : SURF2D_MINB) k_surf2d(MeshDev md, StageParams sp, const double *__restrict__ Un,
+#ifndef NSSC_MINB
+#define NSSC_MINB 2
+#endif
+__global__ void __launch_bounds__(256, (NS && SCS) ? NSSC_MINB : SURF2D_MINB) k_surf2d(MeshDev md, StageParams sp, const double *__restrict__ Un,
                                                const double *__restrict__ Ubuf, const double *__restrict__ K1,
                                                const double *__restrict__ Uin, double *__restrict__ Fs,
                                                const double *__restrict__ Vt, const double *__restrict__ alpha_raw,
@@ -557,7 +560,7 @@ __host__ __device__ constexpr size_t vol2d_smem_bytes(bool ns)
 // from the primitives the line already holds; alpha = 0 elements skip it.
 template <int MODE, bool NS, bool SC = false>
 // (Navier-Stokes + shock capturing: 2 CTAs per SM -- at 3 the 168-register budget spilled 44 B)
-__global__ void __launch_bounds__(vol2d_threads(NS), NS ? (VOL2D_EPB_NS == 8 ? 5 : (SC ? 2 : 3)) : 3)
+__global__ void __launch_bounds__(vol2d_threads(NS), NS ? (VOL2D_EPB_NS == 8 ? 5 : (SC ? NSSC_MINB : 3)) : 3)
 k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                                                  double *__restrict__ Ubuf, double *__restrict__ K1,
                                                  const double *__restrict__ Fs, const double *__restrict__ Uin,
