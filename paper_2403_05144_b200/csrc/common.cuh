@@ -299,6 +299,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
 // the launch attribute.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// a load the compiler cannot merge with an earlier one (re-reading a value instead of keeping it live)
+__device__ __forceinline__ int ld_volatile(const int *p) { return *reinterpret_cast<const volatile int *>(p); }
+
 // L1 prefetch of the line holding p (no register, no scoreboard entry)
 __device__ __forceinline__ void prefetch_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 

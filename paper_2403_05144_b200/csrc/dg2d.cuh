@@ -204,19 +204,16 @@ __device__ __forceinline__ void store_face2d(double *Fs, int e, int face, int k,
 #ifndef SURF2D_MINB
 #define SURF2D_MINB 3
 #endif
-// SCS: the shock-capturing neighbour smoothing (sc.cuh) rides along: lane k = 0 of every interface /
+// SCS: the shock-capturing neighbour smoothing (sc.cuh) rides along, in a pass over the faces after the
+// fluxes (one thread per interface / mortar) -- formerly lane k = 0 of every interface /
 // mortar raises alpha of both sides to half the other side's raw value (k_sc_alpha ran before).
 __device__ __forceinline__ void sc_amax(double *p, double v)
 {
     atomicMax(reinterpret_cast<unsigned long long *>(p), (unsigned long long)__double_as_longlong(v));
 }
 
-// (Navier-Stokes with the shock-capturing smoothing: 2 CTAs per SM, the 80-register budget of 3 spilled)
 template <int MODE, bool NS, bool SCS = false>
-#ifndef NSSC_MINB
-#define NSSC_MINB 2
-#endif
-__global__ void __launch_bounds__(256, (NS && SCS) ? NSSC_MINB : SURF2D_MINB) k_surf2d(MeshDev md, StageParams sp, const double *__restrict__ Un,
+__global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StageParams sp, const double *__restrict__ Un,
                                                const double *__restrict__ Ubuf, const double *__restrict__ K1,
                                                const double *__restrict__ Uin, double *__restrict__ Fs,
                                                const double *__restrict__ Vt, const double *__restrict__ alpha_raw,
@@ -267,14 +264,6 @@ __global__ void __launch_bounds__(256, (NS && SCS) ? NSSC_MINB : SURF2D_MINB) k_
         store_face2d(Fs, Ia.y, 2 * Ia.z + 1, ka, fa);
         store_face2d(Fs, Ib.x, 2 * Ib.z, kb, fb);
         store_face2d(Fs, Ib.y, 2 * Ib.z + 1, kb, fb);
-        if (SCS && ka == 0) {
-            sc_amax(alpha + Ia.x, 0.5 * __ldg(alpha_raw + Ia.y));
-            sc_amax(alpha + Ia.y, 0.5 * __ldg(alpha_raw + Ia.x));
-        }
-        if (SCS && kb == 0) {
-            sc_amax(alpha + Ib.x, 0.5 * __ldg(alpha_raw + Ib.y));
-            sc_amax(alpha + Ib.y, 0.5 * __ldg(alpha_raw + Ib.x));
-        }
     }
     for (; gt < total; gt += GS) {
         const int item = gt >> 2, k = gt & 3;
@@ -295,10 +284,6 @@ __global__ void __launch_bounds__(256, (NS && SCS) ? NSSC_MINB : SURF2D_MINB) k_
             }
             store_face2d(Fs, I.x, 2 * o, k, fl);
             store_face2d(Fs, I.y, 2 * o + 1, k, fl);
-            if (SCS && k == 0) {
-                sc_amax(alpha + I.x, 0.5 * __ldg(alpha_raw + I.y));
-                sc_amax(alpha + I.y, 0.5 * __ldg(alpha_raw + I.x));
-            }
         } else if (item < nif + nmo) {
             const int q = item - nif;
             const int4 M = MODE == MODE_STAGE ? md.mors[q] : md.mor[q];
@@ -364,12 +349,6 @@ __global__ void __launch_bounds__(256, (NS && SCS) ? NSSC_MINB : SURF2D_MINB) k_
                 }
             }
             store_face2d(Fs, M.x, lf, k, fl);
-            if (SCS && k == 0) {
-                const double al = 0.5 * __ldg(alpha_raw + M.x);
-                sc_amax(alpha + M.x, 0.5 * fmax(__ldg(alpha_raw + M.y), __ldg(alpha_raw + M.z)));
-                sc_amax(alpha + M.y, al);
-                sc_amax(alpha + M.z, al);
-            }
         } else {
             const int q = item - nif - nmo;
             const int bi = MODE == MODE_STAGE ? md.list[KIND_BD][q] : q;
@@ -382,6 +361,24 @@ __global__ void __launch_bounds__(256, (NS && SCS) ? NSSC_MINB : SURF2D_MINB) k_
             if ((face & 1) == 0) numflux2d(u, md.bc, o, g, md.surface, fl);
             else numflux2d(md.bc, u, o, g, md.surface, fl);
             store_face2d(Fs, B.x, face, k, fl);
+        }
+    }
+    if (SCS) {   // shock-capturing smoothing: one thread per face after the fluxes (kept out of the flux
+                 // loops, whose 80-register budget of 3 CTAs per SM it would exceed); counts re-read
+        const int nif2 = MODE == MODE_STAGE ? ld_volatile(md.count_active + KIND_IF * MAXS + sp.stage - 1) : md.n[1];
+        const int nmo2 = MODE == MODE_STAGE ? ld_volatile(md.count_active + KIND_MO * MAXS + sp.stage - 1) : md.n[2];
+        for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nif2 + nmo2; t += gridDim.x * blockDim.x) {
+            if (t < nif2) {
+                const int4 I = MODE == MODE_STAGE ? md.ifcs[t] : md.ifc[t];
+                sc_amax(alpha + I.x, 0.5 * __ldg(alpha_raw + I.y));
+                sc_amax(alpha + I.y, 0.5 * __ldg(alpha_raw + I.x));
+            } else {
+                const int4 M = MODE == MODE_STAGE ? md.mors[t - nif2] : md.mor[t - nif2];
+                const double al = 0.5 * __ldg(alpha_raw + M.x);
+                sc_amax(alpha + M.x, 0.5 * fmax(__ldg(alpha_raw + M.y), __ldg(alpha_raw + M.z)));
+                sc_amax(alpha + M.y, al);
+                sc_amax(alpha + M.z, al);
+            }
         }
     }
 }
@@ -470,7 +467,17 @@ __device__ __forceinline__ void visc_volume(double (*sm)[2][LS], int o, int lo, 
         *reinterpret_cast<double2 *>(&sm[4 + c][o][lo + 2]) = make_double2(q[c][2], q[c][3]);
     }
     __syncwarp();
-    double fv[NP][GV];
+    // the line's own half velocities: contiguous, two 16 B loads per field (scalar reads of the x layout
+    // were 2-way bank conflicts between the two elements of a half-warp)
+    double hv1[NP], hv2[NP];
+    {
+        const double2 a01 = *reinterpret_cast<const double2 *>(&sm[fld[0]][o][lo]);
+        const double2 a23 = *reinterpret_cast<const double2 *>(&sm[fld[0]][o][lo + 2]);
+        const double2 b01 = *reinterpret_cast<const double2 *>(&sm[fld[1]][o][lo]);
+        const double2 b23 = *reinterpret_cast<const double2 *>(&sm[fld[1]][o][lo + 2]);
+        hv1[0] = a01.x; hv1[1] = a01.y; hv1[2] = a23.x; hv1[3] = a23.y;
+        hv2[0] = b01.x; hv2[1] = b01.y; hv2[2] = b23.x; hv2[3] = b23.y;
+    }
 #pragma unroll
     for (int a = 0; a < NP; ++a) {
         // the other direction's gradient at this node: node (a, ln) of an x-line lives at y-layout
@@ -482,21 +489,19 @@ __device__ __forceinline__ void visc_volume(double (*sm)[2][LS], int o, int lo, 
             qs[c] = q[c][a];
             qo[c] = sm[4 + c][1 - o][oi];
         }
-        const double v1 = 2.0 * sm[fld[0]][o][lo + a], v2 = 2.0 * sm[fld[1]][o][lo + a];
+        const double v1 = 2.0 * hv1[a], v2 = 2.0 * hv2[a];
         double f[GV];
         if (o == 0) visc_flux2d(v1, v2, qs, qo, 0, mu, kappa, f);
         else visc_flux2d(v1, v2, qo, qs, 1, mu, kappa, f);
-        // (momentum x, momentum y, energy) -> line coordinates (normal, tangential, energy)
-        fv[a][0] = o == 0 ? f[0] : f[1];
-        fv[a][1] = o == 0 ? f[1] : f[0];
-        fv[a][2] = f[2];
+        // (momentum x, momentum y, energy) -> line coordinates (normal, tangential, energy), applied to
+        // every node at once (same per-node summation order over a as a separate contraction, without
+        // holding the 12 fluxes of the line)
+        const double fl[GV] = {o == 0 ? f[0] : f[1], o == 0 ? f[1] : f[0], f[2]};
+#pragma unroll
+        for (int i = 0; i < NP; ++i)
+#pragma unroll
+            for (int c = 0; c < GV; ++c) acc[i][1 + c] = fma(cB.Dhat[i][a], fl[c], acc[i][1 + c]);
     }
-#pragma unroll
-    for (int i = 0; i < NP; ++i)
-#pragma unroll
-        for (int a = 0; a < NP; ++a)
-#pragma unroll
-            for (int c = 0; c < GV; ++c) acc[i][1 + c] = fma(cB.Dhat[i][a], fv[a][c], acc[i][1 + c]);
 }
 
 // Dynamic shared memory of k_vol2d (bytes): field arrays, own-state staging, epilogue staging.
@@ -505,6 +510,11 @@ __host__ __device__ constexpr int vol2d_nf(bool ns) { return ns ? 8 : 7; }
 // 2 = loaded into registers before the two-point-flux loop.  Measured (cfg 3 / cfg 5 volume ms/step):
 // Euler 1: 0.361, 2: 0.378; Navier-Stokes 1: 3.60, 2: 3.52 (its 16 KB smaller footprint fits 3
 // instead of 2 CTAs per SM); read from global memory in the epilogue instead: Euler 0.406
+// Navier-Stokes, mode 2: issue the register loads of U_n / K_1 after the two-point fluxes (in flight
+// during the BR1 part) instead of before them, so they do not occupy 32 registers across the flux loop
+#ifndef VOL2D_PRELOAD_LATE
+#define VOL2D_PRELOAD_LATE 0
+#endif
 #ifndef VOL2D_EPI_MODE_EULER
 #define VOL2D_EPI_MODE_EULER 1
 #endif
@@ -559,7 +569,11 @@ __host__ __device__ constexpr size_t vol2d_smem_bytes(bool ns)
 // u_{a+1}) of the problem's surface flux (F_{-1/2} = F_{N+1/2} = 0), evaluated in line coordinates
 // from the primitives the line already holds; alpha = 0 elements skip it.
 template <int MODE, bool NS, bool SC = false>
-// (Navier-Stokes + shock capturing: 2 CTAs per SM -- at 3 the 168-register budget spilled 44 B)
+// (Navier-Stokes + shock capturing: 2 CTAs per SM -- at 3 the 168-register budget spilled 44 B and the
+//  kernel was slower, cfg 5 SC volume 4.48 vs 4.18 ms/step; NSSC_MINB=3 builds that variant)
+#ifndef NSSC_MINB
+#define NSSC_MINB 2
+#endif
 __global__ void __launch_bounds__(vol2d_threads(NS), NS ? (VOL2D_EPB_NS == 8 ? 5 : (SC ? NSSC_MINB : 3)) : 3)
 k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                                                  double *__restrict__ Ubuf, double *__restrict__ K1,
@@ -718,7 +732,7 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
             }
             // stage S combines with W (P-ERK3) or U_n
             if (EM == 2) {
-                if (valid) {
+                if (valid && !(NS && VOL2D_PRELOAD_LATE)) {
                     const double *usrc = (Wb && sp.stage == sp.S) ? Wb : Un;
 #pragma unroll
                     for (int v = 0; v < 4; ++v) {
@@ -800,6 +814,16 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                 }
         }
         // NS: + sum_a Dhat_ia F^v(node a) along the line (BR1 gradients recomputed from Gs)
+        if (NS && EM == 2 && VOL2D_PRELOAD_LATE && valid) {   // the epilogue operands, in flight during the BR1 part
+            const bool need_un = MODE == MODE_STAGE && sp.stage > 1;
+            const bool need_k1 = MODE == MODE_STAGE && sp.stage > 1 && (sp.stage < sp.S || sp.fin_k1);
+            const double *usrc = (Wb && sp.stage == sp.S) ? Wb : Un;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                if (need_un) pre_un[v] = __ldg(reinterpret_cast<const double2 *>(usrc + eb + v * 16 + q0));
+                if (need_k1) pre_k1[v] = __ldg(reinterpret_cast<const double2 *>(K1 + eb + v * 16 + q0));
+            }
+        }
         if (NS) {
             PERK_JITTER(4);
             if (has_next) cp_async_wait<1>();

@@ -72,7 +72,7 @@ struct perk_ctx {
     uint8_t *amr_want = nullptr, *amr_newlev = nullptr;  // ping-pong finest-grid maps of the balance
     uint8_t *amr_map[2] = {nullptr, nullptr};
     int *amr_flags = nullptr;                            // balance: iteration k changed a cell
-    int vol_blocks = 0, vol_blocks_sc = 0, surf_blocks = 0, surf_blocks_nssc = 0, grad_blocks = 0;
+    int vol_blocks = 0, vol_blocks_sc = 0, surf_blocks = 0, grad_blocks = 0;
     unsigned kind_mask = ~0u;              // kernel kinds launch_step issues (perk_time_kernels)
     bool step1d = false;                   // small 1D mesh: whole step in one single-CTA launch
     StepTab1D *tb1d = nullptr;
@@ -458,9 +458,7 @@ static void launch_surface(perk_ctx *c, cudaStream_t s, const StageParams &sp, c
         const double *vt = c->ns ? c->Vt : nullptr;
         const double *ar = c->alpha_raw;
         double *al = c->alpha;
-        if (c->ns && scs)
-            launch_pdl(st ? k_surf2d<MODE_STAGE, true, true> : k_surf2d<MODE_RHS, true, true>, c->surf_blocks_nssc, 256, 0, s, md, sp, Un, (const double *)c->Ubuf, (const double *)c->K1, Uin, c->Fs, vt, ar, al);
-        else if (c->ns)
+        if (c->ns)   // (Navier-Stokes smooths in k_sc_smooth: fused, the 80-register budget spilled)
             launch_pdl(st ? k_surf2d<MODE_STAGE, true> : k_surf2d<MODE_RHS, true>, c->surf_blocks, 256, 0, s, md, sp, Un, (const double *)c->Ubuf, (const double *)c->K1, Uin, c->Fs, vt, ar, al);
         else if (scs)
             launch_pdl(st ? k_surf2d<MODE_STAGE, false, true> : k_surf2d<MODE_RHS, false, true>, c->surf_blocks, 256, 0, s, md, sp, Un, (const double *)c->Ubuf, (const double *)c->K1, Uin, c->Fs, vt, ar, al);
@@ -847,9 +845,6 @@ extern "C" int perk_init_dd(perk_ctx **out, const perk_problem *prob, const uint
         int occf = 0;
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occf, k_surf2d<MODE_STAGE, false>, 256, 0));
         c->surf_blocks = std::min(blocks_for(4ll * c->cap_faces, 256), SM_COUNT_B200 * std::max(occf, 1));
-        int occfs = 0;
-        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occfs, k_surf2d<MODE_STAGE, true, true>, 256, 0));
-        c->surf_blocks_nssc = cap_env("PERK_SURF_BLOCKS", std::min(blocks_for(4ll * c->cap_faces, 256), SM_COUNT_B200 * std::max(occfs, 1)));
         c->surf_blocks = cap_env("PERK_SURF_BLOCKS", c->surf_blocks);
         // re-mesh (transfer double buffer, old-mesh copy) and AMR scratch, allocated up front so that
         // no cudaMalloc / memset lands inside a timed re-mesh
@@ -1230,7 +1225,10 @@ extern "C" int perk_set_shock_capturing(perk_ctx *c, const perk_shock_capturing 
         CU(cudaGetLastError());
     }
     const char *fenv = std::getenv("PERK_SC_FUSED");
-    c->sc_fused = !(fenv && fenv[0] == '0');
+    // fused smoothing (a pass over the faces at the end of k_surf2d) for Euler; Navier-Stokes uses the
+    // separate k_sc_smooth launch (A/B on one box, cfg 5 SC: 8.29 vs 8.31 ms/step fused, whose variant of
+    // the Navier-Stokes surface kernel spilled at the 80-register budget of 3 CTAs per SM)
+    c->sc_fused = !(fenv && fenv[0] == '0') && !c->ns;
     // next-stage alpha in the k_vol2d epilogue (cfg 3: 0.764 -> 0.719 ms/step, cfg 5: 8.68 -> 8.54 with
     // the batched tail; before it, the Navier-Stokes kernel got slower, 8.93).  PERK_SC_EPI=0: off.
     const char *eenv = std::getenv("PERK_SC_EPI");

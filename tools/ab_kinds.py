@@ -1,7 +1,8 @@
 """A/B of library builds on one box (development aid): per kernel kind the flushed graph-replay time
 (perk_time_kernels_ex, L2 flushed before each replay) and the flushed step time, each library in its
 own process, alternating for several rounds; prints the per-variant median over rounds.
-  python tools/ab_kinds.py 5,3 A B [rounds]     (libraries paper_2403_05144_b200/lib/libperk_<X>.so)"""
+  python tools/ab_kinds.py 5,3 A B [rounds]     (libraries paper_2403_05144_b200/lib/libperk_<X>.so;
+  a variant "X:NAME=VALUE" runs library X with that environment variable set)"""
 import json
 import os
 import statistics
@@ -52,7 +53,11 @@ def main():
     res = {v: [] for v in variants}
     for _ in range(rounds):
         for v in variants:
-            env = dict(os.environ, PERK_LIB_PATH=os.path.join(ROOT, "paper_2403_05144_b200", "lib", f"libperk_{v}.so"))
+            lib, _, extra = v.partition(":")       # variant "X" or "X:NAME=VALUE" (an environment knob)
+            env = dict(os.environ, PERK_LIB_PATH=os.path.join(ROOT, "paper_2403_05144_b200", "lib", f"libperk_{lib}.so"))
+            if extra:
+                k_, _, v_ = extra.partition("=")
+                env[k_] = v_
             o = subprocess.run([sys.executable, "-c", WORKER.format(root=ROOT), cfgs], capture_output=True, text=True,
                                env=env)
             if o.returncode:
