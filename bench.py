@@ -142,12 +142,13 @@ def kernel_bytes_per_step(perk, w):
     active at stage i iff i = 1 or i >= S - E[r] + 2 and its stage state is lazy iff
     2 <= i <= S - E[r] + 2.
       k_vol2d   stage 1: U_n + Fs read, K_1 write; 1 < i < S: (U^(i) or lazy U_n, K_1) + U_n + K_1 +
-                Fs read, U^(i+1) write; stage S: state + U_n + Fs read, U_{n+1} write (+ Gs 384 B, NS)
+                Fs read, U^(i+1) write; stage S: state + U_n + Fs read, U_{n+1} write (+ Dv 384 B, NS)
       k_surf2d  interface: 2 traces + 2 flux slots (+ 2 Vt slices, NS); mortar: 3 traces + 3 slots
                 (+ 3 Vt slices); boundary: 1 trace + 1 slot
       k_gsurf2d (NS) active + halo interfaces: 2 traces + 2 Gs slices; mortars: 3 traces + 3 slices;
                 halo items are lazy (their member is inactive at the stage)
-      k_grad2d  (NS) active + halo elements: stage state + Gs (384 B) read, Vt (384 B) write"""
+      k_grad2d  (NS) active + halo elements: stage state + Gs (384 B) read, Vt (384 B) write; active
+                elements also write their viscous volume term Dv (384 B, read by k_vol2d instead of Gs)"""
     S, E, R = w.S, list(w.E), len(w.E)
     ns = w.problem["equation"] == "navier_stokes"
     segs = {}
@@ -186,7 +187,7 @@ def kernel_bytes_per_step(perk, w):
             out["surface"] += nb * (tr(r, i) + 128)
             if ns:
                 out["br1_gradient_traces"] += ni * (2 * tr(r, i) + 2 * 96) + nm * (tr(rl, i) + 2 * tr(r, i) + 3 * 96)
-                out["br1_gradients"] += ne * ((1024 if lazy(r, i) else 512) + 2 * 384)
+                out["br1_gradients"] += ne * ((1024 if lazy(r, i) else 512) + 3 * 384)   # + the Dv write
         if ns:
             out["br1_gradient_traces"] += int(halo["interfaces"][i - 1]) * (2 * 256 + 2 * 96) + \
                 int(halo["mortars"][i - 1]) * (3 * 256 + 3 * 96)

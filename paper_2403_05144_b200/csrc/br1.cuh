@@ -127,7 +127,7 @@ template <int MODE>
 __global__ void __launch_bounds__(128, 4) k_grad2d(MeshDev md, StageParams sp, const double *__restrict__ Un,
                                                    const double *__restrict__ Ubuf, const double *__restrict__ K1,
                                                    const double *__restrict__ Uin, const double *__restrict__ Gs,
-                                                   double *__restrict__ Vt)
+                                                   double *__restrict__ Vt, double *__restrict__ Dv)
 {
     extern __shared__ __align__(16) unsigned char smraw[];
     double (*sm)[2][GRAD2D_LS] = reinterpret_cast<double (*)[2][GRAD2D_LS]>(smraw);
@@ -225,7 +225,58 @@ __global__ void __launch_bounds__(128, 4) k_grad2d(MeshDev md, StageParams sp, c
         __syncwarp();
         if (has_next) issue_gs(pk_next);          // gst consumed
         cp_async_commit();
-        if (valid) {
+        if (BR1_DV) {
+            // viscous flux in direction o at the line's 4 nodes: the end nodes' go to Vt (face traces),
+            // all four into dv[i] = sum_a Dhat_ia F^v_o(node a); x + y lines summed through shared memory
+            // (fields v1, v2, T, free once every thread has read its line's velocities) -> Dv = -(2/h) dv
+            double dv[NP][GV];
+#pragma unroll
+            for (int i = 0; i < NP; ++i)
+#pragma unroll
+                for (int c = 0; c < GV; ++c) dv[i][c] = 0.0;
+#pragma unroll
+            for (int a = 0; a < NP; ++a) {
+                const int oi = o == 0 ? yo + eoy + 4 * a + ln : eox + 4 * a + ln;
+                double qo[GV], qs[GV], fv[GV];
+#pragma unroll
+                for (int c = 0; c < GV; ++c) {
+                    qs[c] = q[c][a];
+                    qo[c] = sm[G_Q + c][1 - o][oi];
+                }
+                const double v1 = sm[G_V1][o][lo + a], v2 = sm[G_V2][o][lo + a];
+                if (o == 0) visc_flux2d(v1, v2, qs, qo, 0, md.mu, md.kappa, fv);
+                else visc_flux2d(v1, v2, qo, qs, 1, md.mu, md.kappa, fv);
+                if (valid && (a == 0 || a == NP - 1)) {
+                    const int face = 2 * o + (a == NP - 1 ? 0 : 1);   // a = N: +o face, a = 0: -o face
+#pragma unroll
+                    for (int c = 0; c < GV; ++c) Vt[gidx2d(e, face, c, ln)] = fv[c];
+                }
+#pragma unroll
+                for (int i = 0; i < NP; ++i)
+#pragma unroll
+                    for (int c = 0; c < GV; ++c) dv[i][c] = fma(cB.Dhat[i][a], fv[c], dv[i][c]);
+            }
+            PERK_JITTER(15);
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < GV; ++c) {
+                *reinterpret_cast<double2 *>(&sm[G_V1 + c][o][lo]) = make_double2(dv[0][c], dv[1][c]);
+                *reinterpret_cast<double2 *>(&sm[G_V1 + c][o][lo + 2]) = make_double2(dv[2][c], dv[3][c]);
+            }
+            PERK_JITTER(16);
+            __syncwarp();
+            if (valid && base + le < n_el_a) {   // halo elements (their member is inactive) need no Dv
+                const int i0 = q0 & 3, j0 = q0 >> 2;
+                const double J = -2.0 / hcell;
+#pragma unroll
+                for (int c = 0; c < GV; ++c) {
+                    const double2 sx = *reinterpret_cast<const double2 *>(&sm[G_V1 + c][0][eox + q0]);
+                    const double s0 = sx.x + sm[G_V1 + c][1][yo + eoy + 4 * i0 + j0];
+                    const double s1 = sx.y + sm[G_V1 + c][1][yo + eoy + 4 * (i0 + 1) + j0];
+                    *reinterpret_cast<double2 *>(Dv + (size_t)e * (GV * 16) + c * 16 + q0) = make_double2(J * s0, J * s1);
+                }
+            }
+        } else if (valid) {
 #pragma unroll
             for (int end = 0; end < 2; ++end) {
                 const int a = end ? NP - 1 : 0;

@@ -504,8 +504,17 @@ __device__ __forceinline__ void visc_volume(double (*sm)[2][LS], int o, int lo, 
     }
 }
 
+// BR1_DV = 1: k_grad2d, which holds the element's gradients anyway, also forms the viscous volume
+// term Dv = -(2/h) sum_a Dhat_ia F^v(node a) (x + y lines, 384 B per element) and the volume kernel
+// adds it in its epilogue instead of recomputing the gradients from Gs (same bytes staged: Dv instead
+// of Gs; the Navier-Stokes volume kernel becomes the Euler one plus one 16 B shared load per variable).
+// BR1_DV = 0: the volume kernel recomputes q from the state and Gs (visc_volume).
+#ifndef BR1_DV
+#define BR1_DV 1
+#endif
+
 // Dynamic shared memory of k_vol2d (bytes): field arrays, own-state staging, epilogue staging.
-__host__ __device__ constexpr int vol2d_nf(bool ns) { return ns ? 8 : 7; }
+__host__ __device__ constexpr int vol2d_nf(bool ns) { return ns && !BR1_DV ? 8 : 7; }
 // U_n / K_1 operands of the stage epilogue: 1 = staged in shared memory with the Fs fluxes,
 // 2 = loaded into registers before the two-point-flux loop.  Measured (cfg 3 / cfg 5 volume ms/step):
 // Euler 1: 0.361, 2: 0.378; Navier-Stokes 1: 3.60, 2: 3.52 (its 16 KB smaller footprint fits 3
@@ -744,7 +753,7 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                 if (need_un) copy_block(EP(EPI_UN), (Wb && sp.stage == sp.S ? Wb : Un) + eb);
                 if (need_k1) copy_block(EP(EPI_K1), K1 + eb);
             }
-            if (NS) {   // the element's 48 BR1 central traces (384 B = 24 chunks of 16 B)
+            if (NS) {   // the element's 48 BR1 central traces, or (BR1_DV) its viscous volume term (384 B = 24 chunks)
 #pragma unroll
                 for (int r = 0; r < 3; ++r)
                     cp_async16(EP(EPI_GS) + 2 * (t8 + 8 * r), Gs + (size_t)e * 4 * GV * NP + 2 * (t8 + 8 * r));
@@ -824,7 +833,7 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                 if (need_k1) pre_k1[v] = __ldg(reinterpret_cast<const double2 *>(K1 + eb + v * 16 + q0));
             }
         }
-        if (NS) {
+        if (NS && !BR1_DV) {
             PERK_JITTER(4);
             if (has_next) cp_async_wait<1>();
             else cp_async_wait<0>();
@@ -909,7 +918,12 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                 const double2 sx = *reinterpret_cast<const double2 *>(&sm[v][0][eox + q0]);
                 const double s0 = sx.x + sm[v][1][yo + eoy + 4 * i0 + j0];
                 const double s1 = sx.y + sm[v][1][yo + eoy + 4 * (i0 + 1) + j0];
-                epilogue(v, q0, make_double2(J * s0, J * s1));
+                double2 K = make_double2(J * s0, J * s1);
+                if (NS && BR1_DV && v > 0) {   // + the viscous volume term of k_grad2d (staged in the Gs slot)
+                    const double2 d = *reinterpret_cast<const double2 *>(EP(EPI_GS) + (v - 1) * 16 + q0);
+                    K = make_double2(K.x + d.x, K.y + d.y);
+                }
+                epilogue(v, q0, K);
             }
         }
         if (SC && MODE == MODE_STAGE && scp.epi && scp.alpha_fixed < 0.0 && sp.stage > 1 && sp.stage < sp.S) {

@@ -49,6 +49,7 @@ struct perk_ctx {
     cudaStream_t cap_stream = nullptr;
     double *K1 = nullptr, *Ubuf = nullptr, *Fs = nullptr, *Utmp = nullptr, *Uhost_dev = nullptr;
     double *Gs = nullptr, *Vt = nullptr;   // BR1 (Navier-Stokes): central w* and viscous-flux traces
+    double *Dv = nullptr;                  // BR1_DV: viscous volume term of k_grad2d, read by k_vol2d
     double *Wb = nullptr;                  // P-ERK3: W = U_n + dt (b_1 K_1 + b_{S-1} K_{S-1})
     bool ns = false;
     bool sc = false;                       // subcell shock capturing (sc.cuh): per-stage alpha, blended volume
@@ -486,9 +487,9 @@ static void launch_volume(perk_ctx *c, cudaStream_t s, const StageParams &sp, do
         const int tn = vol2d_threads(c->ns);
         const size_t sm = vol2d_smem_bytes(c->ns);
         if (c->ns && c->sc)
-            launch_pdl(st ? k_vol2d<MODE_STAGE, true, true> : k_vol2d<MODE_RHS, true, true>, c->vol_blocks_sc, tn, sm, s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, (const double *)c->Gs, c->Wb, al, c->alpha_raw, c->scp);
+            launch_pdl(st ? k_vol2d<MODE_STAGE, true, true> : k_vol2d<MODE_RHS, true, true>, c->vol_blocks_sc, tn, sm, s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, (const double *)(BR1_DV ? c->Dv : c->Gs), c->Wb, al, c->alpha_raw, c->scp);
         else if (c->ns)
-            launch_pdl(st ? k_vol2d<MODE_STAGE, true> : k_vol2d<MODE_RHS, true>, c->vol_blocks, tn, sm, s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, (const double *)c->Gs, c->Wb, al, c->alpha_raw, c->scp);
+            launch_pdl(st ? k_vol2d<MODE_STAGE, true> : k_vol2d<MODE_RHS, true>, c->vol_blocks, tn, sm, s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, (const double *)(BR1_DV ? c->Dv : c->Gs), c->Wb, al, c->alpha_raw, c->scp);
         else if (c->sc)
             launch_pdl(st ? k_vol2d<MODE_STAGE, false, true> : k_vol2d<MODE_RHS, false, true>, c->vol_blocks_sc, tn, sm, s, md, sp, Un, c->Ubuf, c->K1, c->Fs, Uin, dU, (const double *)nullptr, c->Wb, al, c->alpha_raw, c->scp);
         else
@@ -538,9 +539,9 @@ static void launch_br1(perk_ctx *c, cudaStream_t s, const StageParams &sp, const
     prof_mark(p, s, 5);
     if (!((c->kind_mask >> 5) & 1u)) {
     } else if (sp.mode == MODE_STAGE)
-        launch_pdl(k_grad2d<MODE_STAGE>, c->grad_blocks, 128, grad2d_smem_bytes(), s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs, c->Vt);
+        launch_pdl(k_grad2d<MODE_STAGE>, c->grad_blocks, 128, grad2d_smem_bytes(), s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs, c->Vt, c->Dv);
     else
-        launch_pdl(k_grad2d<MODE_RHS>, c->grad_blocks, 128, grad2d_smem_bytes(), s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs, c->Vt);
+        launch_pdl(k_grad2d<MODE_RHS>, c->grad_blocks, 128, grad2d_smem_bytes(), s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs, c->Vt, c->Dv);
 }
 
 static void launch_step(perk_ctx *c, cudaStream_t s, double *U, double dt, Prof *p)
@@ -785,6 +786,7 @@ extern "C" int perk_init_dd(perk_ctx **out, const perk_problem *prob, const uint
         if (rc) { *out = c; return rc; }
         CU(dalloc(c, &c->Gs, (size_t)c->cap * 4 * GV * NP));
         CU(dalloc(c, &c->Vt, (size_t)c->cap * 4 * GV * NP));
+        if (BR1_DV) CU(dalloc(c, &c->Dv, (size_t)c->cap * GV * 16));
     }
     CU(dalloc(c, &c->lmap, c->nf));
     CU(dalloc(c, &c->keys, (size_t)max_items));

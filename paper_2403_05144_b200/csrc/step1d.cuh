@@ -48,6 +48,7 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
 {
     extern __shared__ __align__(16) double sh[];
     __shared__ StepTab1D T;
+    __shared__ int sCnt[3][MAXS];   // active interfaces / boundaries / elements per stage (no global load per stage)
     const int n = md.n[0];
     const int rowd = NV * NP;
     double *sUn = sh, *sK1 = sUn + (size_t)n * rowd, *sUb = sK1 + (size_t)n * rowd;
@@ -73,6 +74,10 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
             sIf[k] = make_int2(I.x, I.y);
         }
         for (int k = tid; k < nbd_all && k < 2; k += nt) sBd[k] = md.bnd[md.list[KIND_BD][k]];
+        for (int k = tid; k < 3 * MAXS; k += nt) {
+            const int kind = k / MAXS == 0 ? KIND_IF : (k / MAXS == 1 ? KIND_BD : KIND_EL);
+            sCnt[k / MAXS][k % MAXS] = md.count_active[kind * MAXS + k % MAXS];
+        }
         for (int k = tid; k < n; k += nt) {
             sEl[k] = md.list[KIND_EL][k];
             sMem[k] = md.mem[k];
@@ -82,9 +87,7 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
     __syncthreads();
     const int S = T.S;
     for (int i = 1; i <= S; ++i) {
-        const int nif = md.count_active[KIND_IF * MAXS + i - 1];
-        const int nbd = md.count_active[KIND_BD * MAXS + i - 1];
-        const int nel = md.count_active[KIND_EL * MAXS + i - 1];
+        const int nif = sCnt[0][i - 1], nbd = sCnt[1][i - 1], nel = sCnt[2][i - 1];
         const double dtc = dt * T.c[i - 1];
         // the stage-i state of element e (member m), variable v, node j (SURVEY §7 rule)
         auto state = [&](int e, int m, int v, int j) {

@@ -1,0 +1,9 @@
+# full GPU suite, ncu counts per kind (cfg 5, cfg 3), --set full of the four cfg-5 kernels at stage 30, bench
+sha256sum paper_2403_05144_b200/lib/libperk_b200.so | cut -c1-16 > gpurun_out/lib_sha16.txt
+timeout 1500 python -m pytest tests -m gpu -x -q --durations=10 > gpurun_out/gputests.log 2>&1; echo tests=$? >> gpurun_out/status.txt
+timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench=$? >> gpurun_out/status.txt
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum
+for c in 5 3; do
+timeout 900 ncu --metrics $M --clock-control none --csv --log-file gpurun_out/counts_cfg$c.csv python bench.py --profile-only --config $c --steps 1 --warmup 3 > gpurun_out/ncu_counts$c.log 2>&1; echo counts$c=$? >> gpurun_out/status.txt
+done
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_(vol|surf|gsurf|grad)2d" --launch-skip 116 --launch-count 4 -o gpurun_out/full_cfg5_s30 python bench.py --profile-only --config 5 --steps 1 --warmup 0 > gpurun_out/ncu_full.log 2>&1; echo full=$? >> gpurun_out/status.txt
