@@ -166,9 +166,12 @@ def kernel_bytes_per_step(perk, w):
     def tr(r, i):
         return 256 if lazy(r, i) else 128
 
+    fused = ns and br1_fused()
     out = {"volume_stage": 0, "surface": 0}
     if ns:
-        out.update(br1_gradient_traces=0, br1_gradients=0)
+        out.update(br1_gradients=0)
+        if not fused:
+            out.update(br1_gradient_traces=0)
     for i in range(1, S + 1):
         for r in range(R):
             if not active(r, i):
@@ -186,13 +189,28 @@ def kernel_bytes_per_step(perk, w):
             out["surface"] += nm * (tr(rl, i) + 2 * tr(r, i) + 3 * 128 + (3 * 96 if ns else 0))
             out["surface"] += nb * (tr(r, i) + 128)
             if ns:
-                out["br1_gradient_traces"] += ni * (2 * tr(r, i) + 2 * 96) + nm * (tr(rl, i) + 2 * tr(r, i) + 3 * 96)
-                out["br1_gradients"] += ne * ((1024 if lazy(r, i) else 512) + 3 * 384)   # + the Dv write
-        if ns:
+                if fused:   # own state, the face neighbours' traces, Vt and Dv writes
+                    out["br1_gradients"] += ne * ((1024 if lazy(r, i) else 512) + 2 * 384) + ni * 2 * tr(r, i) + \
+                        nm * 2 * tr(rl, i) + (nm * 2 * tr(r, i) if active(rl, i) else 0)
+                else:
+                    out["br1_gradient_traces"] += ni * (2 * tr(r, i) + 2 * 96) + nm * (tr(rl, i) + 2 * tr(r, i) + 3 * 96)
+                    out["br1_gradients"] += ne * ((1024 if lazy(r, i) else 512) + 3 * 384)   # + the Dv write
+        if ns and fused:   # halo elements: lazy state, 4 lazy neighbour traces, Vt
+            out["br1_gradients"] += int(halo["elements"][i - 1]) * (1024 + 4 * 256 + 384)
+        elif ns:
             out["br1_gradient_traces"] += int(halo["interfaces"][i - 1]) * (2 * 256 + 2 * 96) + \
                 int(halo["mortars"][i - 1]) * (3 * 256 + 3 * 96)
             out["br1_gradients"] += int(halo["elements"][i - 1]) * (1024 + 2 * 384)
     return out
+
+
+def br1_fused():
+    """the library forms the BR1 central traces inside k_grad2d (no k_gsurf2d launches, perk_build_flags)"""
+    try:
+        from paper_2403_05144_b200 import perk as _P
+        return _P.build_flags()["br1_fused"]
+    except Exception:
+        return False
 
 
 def _lib_sha():
@@ -374,7 +392,7 @@ def kernel_report(perk, w, cfg, timer, torch, elem_rhs_per_step, fp64, hbm):
     fp64_peak, fp64_src = fp64
     hbm_peak, hbm_src = hbm
     ns = w.problem["equation"] == "navier_stokes"
-    kinds = [0, 1] + ([4, 5] if ns else [])
+    kinds = [0, 1] + (([5] if br1_fused() else [4, 5]) if ns else [])
     U0 = perk.initial_state(w.ic)
     ms_k = {k: perk.time_kernels(U0.clone(), w.dt, [k], reps=10, flush=timer.flush) for k in kinds}
     ms_all = perk.time_kernels(U0.clone(), w.dt, kinds, reps=10, flush=timer.flush)

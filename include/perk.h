@@ -293,6 +293,10 @@ int perk_time_kernels_ex(perk_ctx *ctx, double *U_dev, double dt, uint32_t kind_
 /* Same for one repartition (kinds 2 and 3). */
 int perk_profile_repartition(perk_ctx *ctx, const uint8_t *level_map_dev, double *U_dev, float *ms_host,
                              int32_t *launches_host);
+/* Build configuration of the library (no context): bit 0 = BR1_DV (k_grad2d forms the viscous volume
+ * term), bit 1 = BR1_FUSED (k_grad2d forms the BR1 central traces from the face neighbours: kernel
+ * kind 4, k_gsurf2d, is never launched).  Pure, never fails. */
+int perk_build_flags(void);
 /* Number of kernel launches one perk_step performs (graph nodes). */
 int perk_launches_per_step(perk_ctx *ctx, int32_t *launches);
 /* Race exposure, debug library only (libperk_debug.so, -DPERK_DEBUG; EUNSUPPORTED otherwise): seed != 0

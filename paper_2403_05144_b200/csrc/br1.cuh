@@ -105,42 +105,61 @@ __global__ void __launch_bounds__(256, 3) k_gsurf2d(MeshDev md, StageParams sp, 
 
 // 8 threads per element as in k_vol2d: gradients along the x-lines and y-lines, exchanged through
 // shared memory, then the normal viscous flux at the two end nodes of every line = the face nodes.
-// Persistent CTAs of 16 elements; the element's stage state and its 48 central traces are staged
-// with cp.async one group ahead (commit groups as in k_vol2d); packed entries two groups ahead.
+// Persistent CTAs of 16 elements; the element's stage state (and, unfused, its 48 central traces) is
+// staged with cp.async one group ahead (commit groups as in k_vol2d); packed entries two groups ahead.
+//
+// BR1_FUSED = 1: no k_gsurf2d pass and no Gs array -- each element forms the central traces w* of its
+// own faces from the face neighbours' stage-state traces (MeshDev::fnb), gathered at the top of the
+// iteration while its own state is turned into primitives: conforming 1/2 (w + w_nb); small side of a
+// mortar 1/2 (P w_large + w); large side R_lo 1/2 (P_lo w + w_s0) + R_up 1/2 (P_up w + w_s1), the
+// interpolations / projections as 4-lane shuffles over the face's nodes, in exactly k_gsurf2d's
+// operation order (so w* is bitwise the same number on both sides of every face).  Saves the Gs write
+// and read (768 B per element-stage) and one launch per stage; the trace gathers move here.
+#ifndef BR1_FUSED
+#define BR1_FUSED 1
+#endif
+static_assert(!BR1_FUSED || BR1_DV, "the fused BR1 gradient kernel leaves no Gs for the volume kernel");
 constexpr int GRAD2D_LS = VOL2D_LS;
 constexpr int G_V1 = 0, G_V2 = 1, G_T = 2, G_Q = 3;     // shared fields: v1, v2, T, gradients (3)
-// staged central traces per element: 48 doubles padded to 52 (== 4 mod 16), so that the scalar trace
-// reads of the x-line threads (faces 0/1) and y-line threads (faces 2/3) of the two elements of a
-// half-warp fall into disjoint banks (with 48 the two elements collided)
-// staged central traces per element: 48 doubles padded to 52 (== 4 mod 16), so that the scalar trace
-// reads of the x-line threads (faces 0/1) and y-line threads (faces 2/3) of the two elements of a
-// half-warp fall into disjoint banks (with 48 the two elements collided).  (Loading each thread's 6
-// end traces into registers one group ahead instead, which frees this buffer: 1.33 vs 1.23 ms/step
-// on cfg 5, slower.)
+// staged central traces per element (unfused): 48 doubles padded to 52 (== 4 mod 16), so that the
+// scalar trace reads of the x-line threads (faces 0/1) and y-line threads (faces 2/3) of the two
+// elements of a half-warp fall into disjoint banks (with 48 the two elements collided).  (Loading each
+// thread's 6 end traces into registers one group ahead instead, which frees this buffer: 1.33 vs
+// 1.23 ms/step on cfg 5, slower.)
 constexpr int GST_STRIDE = 4 * GV * NP + 4;
 __host__ __device__ constexpr size_t grad2d_smem_bytes()
 {
-    return sizeof(double) * ((size_t)6 * 2 * GRAD2D_LS + VOL2D_EPB * 2 * 64 + VOL2D_EPB * GST_STRIDE);
+    return sizeof(double) * ((size_t)6 * 2 * GRAD2D_LS + VOL2D_EPB * 2 * 64 + (BR1_FUSED ? 0 : VOL2D_EPB * GST_STRIDE));
 }
+#ifndef GRAD2D_MINB
+#define GRAD2D_MINB 4
+#endif
+#ifndef GRAD2D_SKEW
+#define GRAD2D_SKEW 0
+#endif
 
 template <int MODE>
-__global__ void __launch_bounds__(128, 4) k_grad2d(MeshDev md, StageParams sp, const double *__restrict__ Un,
+__global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StageParams sp, const double *__restrict__ Un,
                                                    const double *__restrict__ Ubuf, const double *__restrict__ K1,
                                                    const double *__restrict__ Uin, const double *__restrict__ Gs,
                                                    double *__restrict__ Vt, double *__restrict__ Dv)
 {
+    constexpr bool FUSED = BR1_FUSED;
     extern __shared__ __align__(16) unsigned char smraw[];
     double (*sm)[2][GRAD2D_LS] = reinterpret_cast<double (*)[2][GRAD2D_LS]>(smraw);
     double (*stg)[2][64] = reinterpret_cast<double (*)[2][64]>(smraw + sizeof(double) * 6 * 2 * GRAD2D_LS);
     double (*gst)[GST_STRIDE] = reinterpret_cast<double (*)[GST_STRIDE]>(reinterpret_cast<unsigned char *>(stg) +
                                                                          sizeof(double) * VOL2D_EPB * 2 * 64);
     const int t8 = threadIdx.x & 7, le = threadIdx.x >> 3;
+    const int lane = threadIdx.x & 31;
+    const unsigned gmask = 0xFu << (lane & ~3);      // the 4 lanes of one line direction of one element
     // items: [active elements | halo elements of the member below the lowest active one]
     const int n_el_a = MODE == MODE_STAGE ? md.count_active[KIND_EL * MAXS + sp.stage - 1] : md.n[0];
     const int2 hel = MODE == MODE_STAGE ? md.hrng[KIND_EL * MAXS + sp.stage - 1] : make_int2(0, 0);
     const int n_act = n_el_a + hel.y;
     const double gm1 = md.gamma - 1.0;
     const double dtc = sp.dt * sp.c_stage;
+    const StateBufs sb{Un, Ubuf, K1, Uin};
     const int q0 = 2 * t8;
     const int o = t8 >> 2, ln = t8 & 3;
     const int eox = le * 16, eoy = le * 20, yo = 2 - 2 * VOL2D_EPB;   // field layout as in k_vol2d
@@ -162,13 +181,21 @@ __global__ void __launch_bounds__(128, 4) k_grad2d(MeshDev md, StageParams sp, c
         if (srce == SRC_LAZY) copy_chunks(stg[le][1], K1 + off, 32);
     };
     auto issue_gs = [&](int pkx) { copy_chunks(gst[le], Gs + (size_t)pk_elem(pkx) * 4 * GV * NP, 4 * GV * NP / 2); };
+    // face-neighbour entries of this thread's two faces (2o: the line's a = N end, 2o + 1: a = 0)
+    auto faces_of = [&](int pkx, int2 f[2]) {
+        const int2 *F = md.fnb + (size_t)pk_elem(pkx) * 4 + 2 * o;
+        f[0] = F[0];
+        f[1] = F[1];
+    };
     const int pk0 = base < n_act ? entry_at(base) : 0;
     int pk_ahead = base + stride < n_act ? entry_at(base + stride) : 0;   // entries two groups ahead
     pdl_wait();
     if (base >= n_act) return;
     int pk = pk0;
+    int2 fn[2] = {make_int2(-1, FNB_NONE), make_int2(-1, FNB_NONE)};
+    if (FUSED) faces_of(pk, fn);
     issue_state(pk);
-    issue_gs(pk);
+    if (!FUSED) issue_gs(pk);
     cp_async_commit();
     for (; base < n_act; base += stride) {
         const bool valid = base + le < n_act;
@@ -179,6 +206,42 @@ __global__ void __launch_bounds__(128, 4) k_grad2d(MeshDev md, StageParams sp, c
         PERK_DASSERT(e >= 0 && e < md.n[0]);
         const int src = state_src(sp, pk_member(pk));
         const double hcell = md.hf * (double)(1 << (md.max_level - pk_level(pk)));
+        // fused: the neighbours' traces at this thread's two face nodes (a large side needs both smalls),
+        // every load issued before any is used; lazy states formed after the loads
+        double un[2][2][4];
+        if (FUSED) {
+            int xe[2][2], xs[2][2];
+#pragma unroll
+            for (int f = 0; f < 2; ++f) {
+                const int p0 = fn[f].x >= 0 ? fn[f].x : pk;
+                const int p1 = fn[f].y >= 0 ? fn[f].y : p0;
+                xe[f][0] = pk_elem(p0);
+                xe[f][1] = pk_elem(p1);
+                xs[f][0] = state_src(sp, pk_member(p0));
+                xs[f][1] = state_src(sp, pk_member(p1));
+            }
+#pragma unroll
+            for (int f = 0; f < 2; ++f)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (h == 1 && fn[f].y < 0) continue;
+                    const double *P = state_base(sb, xs[f][h]) + (size_t)xe[f][h] * 64 + face_node2d((2 * o + f) ^ 1, ln);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) un[f][h][v] = __ldg(P + v * 16);
+                }
+#pragma unroll
+            for (int f = 0; f < 2; ++f)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if ((h == 1 && fn[f].y < 0) || xs[f][h] != SRC_LAZY) continue;
+                    const double *P = K1 + (size_t)xe[f][h] * 64 + face_node2d((2 * o + f) ^ 1, ln);
+                    double kk[4];
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) kk[v] = __ldg(P + v * 16);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) un[f][h][v] = fma(dtc, kk[v], un[f][h][v]);
+                }
+        }
         PERK_JITTER(11);
         cp_async_wait<0>();
         __syncwarp();
@@ -215,7 +278,61 @@ __global__ void __launch_bounds__(128, 4) k_grad2d(MeshDev md, StageParams sp, c
         double q[GV][NP];
         const int fld[GV] = {G_V1, G_V2, G_T};
         const double sc[GV] = {1.0, 1.0, 1.0};
-        line_gradient<GRAD2D_LS>(sm, o, lo, ln, gst[le], 2.0 / hcell, fld, sc, q);
+        if (FUSED) {
+            // central traces w* at this thread's nodes of faces 2o (g[0]) and 2o + 1 (g[1])
+            double g[2][GV];
+#pragma unroll
+            for (int f = 0; f < 2; ++f) {
+                const int a = f == 0 ? NP - 1 : 0;
+                double wo[GV], wn[GV];
+#pragma unroll
+                for (int c = 0; c < GV; ++c) wo[c] = sm[G_V1 + c][o][lo + a];
+                prim_vT(un[f][0], gm1, wn);
+                const int ty = fn[f].y;
+                if (ty == FNB_CONF) {
+#pragma unroll
+                    for (int c = 0; c < GV; ++c) g[f][c] = 0.5 * (wo[c] + wn[c]);
+                } else if (ty == FNB_SMALL_LO || ty == FNB_SMALL_HI) {   // wn: the large side's node ln
+#pragma unroll
+                    for (int c = 0; c < GV; ++c) {
+                        double il = 0.0;
+#pragma unroll
+                        for (int j = 0; j < NP; ++j) {
+                            const double wj = __shfl_sync(gmask, wn[c], j, 4);
+                            il = fma(ty == FNB_SMALL_LO ? cB.Plo[ln][j] : cB.Pup[ln][j], wj, il);
+                        }
+                        g[f][c] = 0.5 * (il + wo[c]);
+                    }
+                } else if (ty >= 0) {                                     // large side: wn, wn1 the smalls
+                    double wn1[GV];
+                    prim_vT(un[f][1], gm1, wn1);
+#pragma unroll
+                    for (int c = 0; c < GV; ++c) {
+                        double il = 0.0, ih = 0.0;
+#pragma unroll
+                        for (int j = 0; j < NP; ++j) {
+                            const double wj = __shfl_sync(gmask, wo[c], j, 4);
+                            il = fma(cB.Plo[ln][j], wj, il);
+                            ih = fma(cB.Pup[ln][j], wj, ih);
+                        }
+                        const double clo = 0.5 * (il + wn[c]), chi = 0.5 * (ih + wn1[c]);
+                        double s = 0.0;
+#pragma unroll
+                        for (int j = 0; j < NP; ++j) {
+                            s = fma(cB.Rlo[ln][j], __shfl_sync(gmask, clo, j, 4), s);
+                            s = fma(cB.Rup[ln][j], __shfl_sync(gmask, chi, j, 4), s);
+                        }
+                        g[f][c] = s;
+                    }
+                } else {                                                  // no neighbour (unsupported for BR1)
+#pragma unroll
+                    for (int c = 0; c < GV; ++c) g[f][c] = wo[c];
+                }
+            }
+            line_gradient_g<GRAD2D_LS>(sm, o, lo, g[0], g[1], 2.0 / hcell, fld, q);
+        } else {
+            line_gradient<GRAD2D_LS>(sm, o, lo, ln, gst[le], 2.0 / hcell, fld, sc, q);
+        }
 #pragma unroll
         for (int c = 0; c < GV; ++c) {   // the line is contiguous and 16 B aligned: two 16 B stores
             *reinterpret_cast<double2 *>(&sm[G_Q + c][o][lo]) = make_double2(q[c][0], q[c][1]);
@@ -223,8 +340,9 @@ __global__ void __launch_bounds__(128, 4) k_grad2d(MeshDev md, StageParams sp, c
         }
         PERK_JITTER(14);
         __syncwarp();
-        if (has_next) issue_gs(pk_next);          // gst consumed
+        if (!FUSED && has_next) issue_gs(pk_next);          // gst consumed
         cp_async_commit();
+        if (FUSED && has_next) faces_of(pk_next, fn);       // the next group's face entries (used at its top)
         if (BR1_DV) {
             // viscous flux in direction o at the line's 4 nodes: the end nodes' go to Vt (face traces),
             // all four into dv[i] = sum_a Dhat_ia F^v_o(node a); x + y lines summed through shared memory
@@ -234,16 +352,44 @@ __global__ void __launch_bounds__(128, 4) k_grad2d(MeshDev md, StageParams sp, c
             for (int i = 0; i < NP; ++i)
 #pragma unroll
                 for (int c = 0; c < GV; ++c) dv[i][c] = 0.0;
+            // the line's own velocities: contiguous, two 16 B loads per field (conflict-free, as the
+            // line loads); the other direction's gradients: scalar cross-layout reads (2-way conflicts)
+            double lv1[NP], lv2[NP];
+            {
+                const double2 a01 = *reinterpret_cast<const double2 *>(&sm[G_V1][o][lo]);
+                const double2 a23 = *reinterpret_cast<const double2 *>(&sm[G_V1][o][lo + 2]);
+                const double2 b01 = *reinterpret_cast<const double2 *>(&sm[G_V2][o][lo]);
+                const double2 b23 = *reinterpret_cast<const double2 *>(&sm[G_V2][o][lo + 2]);
+                lv1[0] = a01.x; lv1[1] = a01.y; lv1[2] = a23.x; lv1[3] = a23.y;
+                lv2[0] = b01.x; lv2[1] = b01.y; lv2[2] = b23.x; lv2[3] = b23.y;
+            }
+#if GRAD2D_SKEW
+            // cross reads in a skewed node order: the y-line threads of odd element slots read node
+            // (k + 1) & 3 at read k, which takes the half-warp's 16 reads from 3 to 2 wavefronts (the
+            // floor with the two layouts' 2 mod 4 offset); the arithmetic order below is unchanged
+            const int sk = (o == 1 && (le & 1)) ? 1 : 0;
+            double qv[NP][GV];
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+                const int a = (k + sk) & 3;
+                const int oi = o == 0 ? yo + eoy + 4 * a + ln : eox + 4 * a + ln;
+#pragma unroll
+                for (int c = 0; c < GV; ++c) qv[k][c] = sm[G_Q + c][1 - o][oi];
+            }
+#endif
 #pragma unroll
             for (int a = 0; a < NP; ++a) {
-                const int oi = o == 0 ? yo + eoy + 4 * a + ln : eox + 4 * a + ln;
                 double qo[GV], qs[GV], fv[GV];
 #pragma unroll
                 for (int c = 0; c < GV; ++c) {
                     qs[c] = q[c][a];
-                    qo[c] = sm[G_Q + c][1 - o][oi];
+#if GRAD2D_SKEW
+                    qo[c] = sk ? qv[(a + 3) & 3][c] : qv[a][c];
+#else
+                    qo[c] = sm[G_Q + c][1 - o][o == 0 ? yo + eoy + 4 * a + ln : eox + 4 * a + ln];
+#endif
                 }
-                const double v1 = sm[G_V1][o][lo + a], v2 = sm[G_V2][o][lo + a];
+                const double v1 = lv1[a], v2 = lv2[a];
                 if (o == 0) visc_flux2d(v1, v2, qs, qo, 0, md.mu, md.kappa, fv);
                 else visc_flux2d(v1, v2, qo, qs, 1, md.mu, md.kappa, fv);
                 if (valid && (a == 0 || a == NP - 1)) {

@@ -111,7 +111,13 @@ struct MeshDev {
     int *hseg;                   // [3][MAXR + 1]
     int2 *hrng;                  // [3][MAXS]
     int *hpk;                    // packed entries of hlist[KIND_EL]
+    // per element and face (+x, -x, +y, -y), the face neighbours (Navier-Stokes, the fused BR1 gradient
+    // kernel; rebuilt with the face records): {x, y} with x, y packed (cell | member << 24):
+    // conforming {nb, FNB_CONF}; small side of a mortar {large, FNB_SMALL_LO / FNB_SMALL_HI};
+    // large side {small_lo, small_hi}; no neighbour (boundary) {-1, FNB_NONE}
+    int2 *fnb;
 };
+constexpr int FNB_CONF = -1, FNB_SMALL_LO = -2, FNB_SMALL_HI = -3, FNB_NONE = -4;
 
 // packed element entry of md.elpk (cells < 2^24, members < 8, levels < 16)
 constexpr int PK_EBITS = 24;

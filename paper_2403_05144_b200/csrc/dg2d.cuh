@@ -204,6 +204,9 @@ __device__ __forceinline__ void store_face2d(double *Fs, int e, int face, int k,
 #ifndef SURF2D_MINB
 #define SURF2D_MINB 3
 #endif
+#ifndef SURF2D_PREFETCH
+#define SURF2D_PREFETCH 0
+#endif
 // SCS: the shock-capturing neighbour smoothing (sc.cuh) rides along, in a pass over the faces after the
 // fluxes (one thread per interface / mortar) -- formerly lane k = 0 of every interface /
 // mortar raises alpha of both sides to half the other side's raw value (k_sc_alpha ran before).
@@ -233,16 +236,46 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
     const double g = md.gamma;
     const int lane = threadIdx.x & 31;
     const unsigned gmask = 0xFu << (lane & ~3);
-    pdl_wait();
     const int GS = gridDim.x * blockDim.x;
     const int nI = 4 * nif;
     int gt = blockIdx.x * blockDim.x + threadIdx.x;
+    const int4 *__restrict__ IR = MODE == MODE_STAGE ? md.ifcs : md.ifc;
+    // the first records are mesh data (rebuilt by the re-mesh pipeline before the step): pull them into
+    // L1 before the dependency wait, while the previous kernel drains
+    if (SURF2D_PREFETCH >= 2 && gt + GS < nI) {
+        prefetch_l1(IR + (gt >> 2));
+        prefetch_l1(IR + ((gt + GS) >> 2));
+    }
+    pdl_wait();
     // two interface face nodes per iteration while both are interfaces: twice the loads in flight
-    // per thread (the kernel is bound by the latency of the record -> trace gathers)
+    // per thread (the kernel is bound by the latency of the record -> trace gathers).  SURF2D_PREFETCH:
+    // the records of the next iteration are loaded before this iteration's traces are used, so an
+    // iteration after the first waits on one round trip (traces) instead of two (record, traces)
+#if SURF2D_PREFETCH == 1
+    int4 nIa = make_int4(0, 0, 0, 0), nIb = nIa;
+    if (gt + GS < nI) {
+        nIa = IR[gt >> 2];
+        nIb = IR[(gt + GS) >> 2];
+    }
+#endif
     for (; gt + GS < nI; gt += 2 * GS) {
         const int ka = gt & 3, kb = (gt + GS) & 3;
-        const int4 Ia = MODE == MODE_STAGE ? md.ifcs[gt >> 2] : md.ifc[gt >> 2];
-        const int4 Ib = MODE == MODE_STAGE ? md.ifcs[(gt + GS) >> 2] : md.ifc[(gt + GS) >> 2];
+#if SURF2D_PREFETCH == 1
+        const int4 Ia = nIa, Ib = nIb;
+        if (gt + 3 * GS < nI) {
+            nIa = IR[(gt + 2 * GS) >> 2];
+            nIb = IR[(gt + 3 * GS) >> 2];
+        }
+#else
+#if SURF2D_PREFETCH == 2   // L1 prefetch of the next iteration's records (no registers held)
+        if (gt + 3 * GS < nI) {
+            prefetch_l1(IR + ((gt + 2 * GS) >> 2));
+            prefetch_l1(IR + ((gt + 3 * GS) >> 2));
+        }
+#endif
+        const int4 Ia = IR[gt >> 2];
+        const int4 Ib = IR[(gt + GS) >> 2];
+#endif
         PERK_DASSERT(Ia.x >= 0 && Ia.x < md.n[0] && Ia.y >= 0 && Ia.y < md.n[0] && Ib.x >= 0 && Ib.x < md.n[0] &&
                      Ib.y >= 0 && Ib.y < md.n[0]);
         const int srca = state_src(sp, Ia.w), srcb = state_src(sp, Ib.w);
@@ -443,6 +476,33 @@ __device__ __forceinline__ void line_gradient(const double (*sm)[2][LS], int o, 
             if (a == NP - 1) t = fma(ghi, cB.invw[NP - 1], t);
             if (a == 0) t = fma(-glo, cB.invw[0], t);
             q[c][a] = (Jq * sc[c]) * t;
+        }
+    }
+    PERK_JITTER(8);
+}
+
+// the same gradient with the two end traces given in registers (fused BR1 gradient kernel; sc = 1):
+// ghi[c] = w*_c at the +o face node of the line, glo[c] at the -o face node
+template <int LS>
+__device__ __forceinline__ void line_gradient_g(const double (*sm)[2][LS], int o, int lo, const double ghi[GV],
+                                                const double glo[GV], double Jq, const int fld[GV], double q[GV][NP])
+{
+#pragma unroll
+    for (int c = 0; c < GV; ++c) {
+        double w[NP];
+        {
+            const double2 w01 = *reinterpret_cast<const double2 *>(&sm[fld[c]][o][lo]);
+            const double2 w23 = *reinterpret_cast<const double2 *>(&sm[fld[c]][o][lo + 2]);
+            w[0] = w01.x; w[1] = w01.y; w[2] = w23.x; w[3] = w23.y;
+        }
+#pragma unroll
+        for (int a = 0; a < NP; ++a) {
+            double t = 0.0;
+#pragma unroll
+            for (int k = 0; k < NP; ++k) t = fma(-cB.Dhat[a][k], w[k], t);
+            if (a == NP - 1) t = fma(ghi[c], cB.invw[NP - 1], t);
+            if (a == 0) t = fma(-glo[c], cB.invw[0], t);
+            q[c][a] = Jq * t;
         }
     }
     PERK_JITTER(8);

@@ -322,6 +322,7 @@ static void build_mesh(perk_ctx *c, cudaStream_t s, const uint8_t *lmap)
               nullptr);
     k_face_counts<<<1, 1, 0, s>>>(md, c->segtmp, c->cap_faces);
     k_face_records<<<blocks_for((long long)c->nd * c->cap, 256), 256, 0, s>>>(md, c->items, c->segtmp, R);
+    if (md.fnb) k_face_table<<<blocks_for(c->cap_faces, 256), 256, 0, s>>>(md);   // fused BR1 (Navier-Stokes)
     if (dd) {   // a sub-domain keeps its owned elements and the faces with an owned side
         const uint8_t *ow = c->dd_owner;
         partition(c, s, KeyOwnEl{md.mem, ow, ddr}, md.n + 0, 1, c->cap, R, md.list[KIND_EL], nullptr,
@@ -531,7 +532,7 @@ static void launch_br1(perk_ctx *c, cudaStream_t s, const StageParams &sp, const
 {
     const MeshDev &md = c->md;
     prof_mark(p, s, 4);
-    if (!((c->kind_mask >> 4) & 1u)) {
+    if (BR1_FUSED || !((c->kind_mask >> 4) & 1u)) {   // fused: k_grad2d forms the central traces itself
     } else if (sp.mode == MODE_STAGE)
         launch_pdl(k_gsurf2d<MODE_STAGE>, c->surf_blocks, 256, 0, s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs);
     else
@@ -784,7 +785,8 @@ extern "C" int perk_init_dd(perk_ctx **out, const perk_problem *prob, const uint
     if (c->ns) {
         rc = alloc_halo(c);
         if (rc) { *out = c; return rc; }
-        CU(dalloc(c, &c->Gs, (size_t)c->cap * 4 * GV * NP));
+        if (!BR1_FUSED) CU(dalloc(c, &c->Gs, (size_t)c->cap * 4 * GV * NP));
+        else CU(dalloc(c, &c->md.fnb, (size_t)c->cap * 4));
         CU(dalloc(c, &c->Vt, (size_t)c->cap * 4 * GV * NP));
         if (BR1_DV) CU(dalloc(c, &c->Dv, (size_t)c->cap * GV * 16));
     }
@@ -1471,6 +1473,8 @@ extern "C" int perk_time_kernels(perk_ctx *c, double *U, double dt, uint32_t kin
 {
     return perk_time_kernels_ex(c, U, dt, kind_mask, reps, nullptr, 0, ms_per_step);
 }
+
+extern "C" int perk_build_flags(void) { return (BR1_DV ? 1 : 0) | (BR1_FUSED ? 2 : 0); }
 
 extern "C" int perk_profile_repartition(perk_ctx *c, const uint8_t *lmap, double *U, float *ms, int32_t *launches)
 {

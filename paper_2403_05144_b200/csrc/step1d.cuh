@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
     extern __shared__ __align__(16) double sh[];
     __shared__ StepTab1D T;
     __shared__ int sCnt[3][MAXS];   // active interfaces / boundaries / elements per stage (no global load per stage)
+    __shared__ double sD[NP][NP];   // Dhat: row j = the node's lane-dependent index (__constant__ reads would serialise)
     const int n = md.n[0];
     const int rowd = NV * NP;
     double *sUn = sh, *sK1 = sUn + (size_t)n * rowd, *sUb = sK1 + (size_t)n * rowd;
@@ -74,6 +75,7 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
             sIf[k] = make_int2(I.x, I.y);
         }
         for (int k = tid; k < nbd_all && k < 2; k += nt) sBd[k] = md.bnd[md.list[KIND_BD][k]];
+        if (tid < NP * NP) sD[tid / NP][tid % NP] = cB.Dhat[tid / NP][tid % NP];
         for (int k = tid; k < 3 * MAXS; k += nt) {
             const int kind = k / MAXS == 0 ? KIND_IF : (k / MAXS == 1 ? KIND_BD : KIND_EL);
             sCnt[k / MAXS][k % MAXS] = md.count_active[kind * MAXS + k % MAXS];
@@ -159,7 +161,7 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
                 for (int v = 0; v < NV; ++v) {
                     double s = 0.0;
 #pragma unroll
-                    for (int k = 0; k < NP; ++k) s = fma(cB.Dhat[j][k], f[k][v], s);
+                    for (int k = 0; k < NP; ++k) s = fma(sD[j][k], f[k][v], s);
                     if (j == 0) s = fma(sFs[((size_t)e * 2 + 1) * NV + v], cB.invw[0], s);
                     if (j == NP - 1) s = fma(-sFs[((size_t)e * 2 + 0) * NV + v], cB.invw[NP - 1], s);
                     K[v] = J * s;

@@ -145,6 +145,12 @@ def lib():
     return _lib
 
 
+def build_flags() -> dict:
+    """the library's build configuration (perk_build_flags): BR1 variants"""
+    f = int(lib().perk_build_flags())
+    return {"br1_dv": bool(f & 1), "br1_fused": bool(f & 2)}
+
+
 def exported_symbols():
     return ["perk_alpha_taylor", "perk_tableau_p2", "perk_tableau_p2_ex", "perk_init", "perk_destroy", "perk_set_stream", "perk_step",
             "perk_run_host", "perk_repartition", "rhs_eval", "perk_num_cells", "perk_num_faces", "perk_node_coords",
@@ -153,7 +159,8 @@ def exported_symbols():
             "perk_launches_per_step", "perk_amr_indicator", "perk_amr_adapt", "perk_amr_launches",
             "perk_set_shock_capturing", "perk_sc_alpha", "perk_pattern_mask", "perk_get_halo_counts", "perk_time_kernels_ex",
             "perk_init_dd", "perk_dd_split", "perk_dd_info", "perk_dd_counts", "perk_dd_get_list", "perk_dd_stage",
-            "perk_dd_pack", "perk_dd_unpack", "perk_dd_exchange", "perk_dd_group_step", "perk_debug_jitter"]
+            "perk_dd_pack", "perk_dd_unpack", "perk_dd_exchange", "perk_dd_group_step", "perk_debug_jitter",
+            "perk_build_flags"]
 
 
 PATTERNS = {"standard": 0, "early": 1, "alternating": 2}

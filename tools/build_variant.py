@@ -14,5 +14,12 @@ cmd = [B.NVCC] + B.FLAGS + defs + ["-I", os.path.join(ROOT, "include"), "-o", ou
 res = subprocess.run(cmd, capture_output=True, text=True)
 if res.returncode != 0:
     sys.exit(res.stdout + res.stderr)
-spills = [l for l in res.stderr.splitlines() if "spill" in l and not l.strip().startswith("0 bytes") and " 0 bytes spill stores" not in l]
-print(out, "spill lines:", len(spills))
+fn, spills = None, []
+for l in res.stderr.splitlines():
+    if "Compiling entry function" in l:
+        fn = l.split("'")[1]
+    elif "spill" in l and " 0 bytes spill stores" not in l:
+        spills.append((fn, l.strip()))
+print(out, "spilling kernels:", len(spills))
+for f, l in spills:
+    print("  ", f[:90], l)

@@ -35,7 +35,7 @@ def main():
         p = Perk(w.problem, w.level_map, w.S, w.E)
         U = p.initial_state(w.ic)
         ns = w.problem["equation"] == "navier_stokes"
-        kinds = [0, 1] + ([4, 5] if ns else [])
+        kinds = [0, 1] + (([5] if bench.br1_fused() else [4, 5]) if ns else [])
         nb = bench.kernel_bytes_per_step(p, w)
         out = {"variant": name, "cells": p.n_cells}
         for k in kinds:
