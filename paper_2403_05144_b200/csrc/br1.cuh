@@ -2,16 +2,18 @@
 //
 // The paper cites BR1 (P:l.1419-1420) without defining it.  Per stage, before the inviscid+viscous
 // surface kernel (k_surf2d<.., NS>) and the volume kernel (k_vol2d<.., NS>):
-//   k_gsurf2d : central traces w* = (w_L + w_R)/2 of the gradient variables w = (v1, v2, T) on the
-//               active interfaces and mortars PLUS the faces of the halo (the large elements of the
-//               active mortars, which belong to the next coarser member and whose gradients the
-//               active viscous face fluxes need; MeshDev::halo); mortars: halves
-//               (P w_large + w_small)/2, the large side gets R_lower w*_lo + R_upper w*_hi.
-//   k_grad2d  : on the active elements and the halo, q = grad w (weak form with w*), then the
-//               normal viscous flux F^v_n(u, q) at the 12 face nodes -> Vt, read by k_surf2d.
+//   k_grad2d  : on the active elements and the halo (the large elements of the active mortars, which
+//               belong to the next coarser member and whose gradients the active viscous face fluxes
+//               need; MeshDev::halo): the central traces w* = (w_L + w_R)/2 of the gradient variables
+//               w = (v1, v2, T) on the element's own faces, formed from the face neighbours' traces
+//               (BR1_FUSED, MeshDev::fnb; mortars: halves (P w_large + w_small)/2, the large side
+//               R_lower w*_lo + R_upper w*_hi), q = grad w (weak form with w*), then the viscous flux at
+//               the line nodes: the normal one at the 12 face nodes -> Vt, read by k_surf2d, and the
+//               viscous volume term Dv = -(2/h) sum_a Dhat_ia F^v(node a) (BR1_DV), read by k_vol2d.
+//   k_gsurf2d : (BR1_FUSED = 0 only) the central traces as a separate pass over the active interfaces /
+//               mortars and the halo faces -> Gs, staged by k_grad2d.
 // (The oracle evaluates gradients on the whole next coarser member instead; both give the same
 // gradients on every element whose viscous face flux is used.)
-// The volume kernel recomputes q from the state and w* (cheaper than storing 16 x 6 gradients).
 #pragma once
 #include "dg2d.cuh"
 
@@ -134,9 +136,6 @@ __host__ __device__ constexpr size_t grad2d_smem_bytes()
 #ifndef GRAD2D_MINB
 #define GRAD2D_MINB 4
 #endif
-#ifndef GRAD2D_SKEW
-#define GRAD2D_SKEW 0
-#endif
 
 template <int MODE>
 __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StageParams sp, const double *__restrict__ Un,
@@ -207,7 +206,11 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
         const int src = state_src(sp, pk_member(pk));
         const double hcell = md.hf * (double)(1 << (md.max_level - pk_level(pk)));
         // fused: the neighbours' traces at this thread's two face nodes (a large side needs both smalls),
-        // every load issued before any is used; lazy states formed after the loads
+        // every load issued before any is used; lazy states formed after the loads.  (Tried and slower,
+        // cfg 5 gradients ms/step: the line's own velocities as 16 B loads 2.11 -> 2.12; the cross reads
+        // in a skewed node order (3 -> 2 wavefronts per half-warp on paper) 2.16; the first neighbour's
+        // traces staged one group ahead by 8 B cp.async, face entries two groups ahead, 2.62 -- the
+        // entry -> face-table chain stalled every iteration and shared-memory conflicts doubled)
         double un[2][2][4];
         if (FUSED) {
             int xe[2][2], xs[2][2];
@@ -352,44 +355,16 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
             for (int i = 0; i < NP; ++i)
 #pragma unroll
                 for (int c = 0; c < GV; ++c) dv[i][c] = 0.0;
-            // the line's own velocities: contiguous, two 16 B loads per field (conflict-free, as the
-            // line loads); the other direction's gradients: scalar cross-layout reads (2-way conflicts)
-            double lv1[NP], lv2[NP];
-            {
-                const double2 a01 = *reinterpret_cast<const double2 *>(&sm[G_V1][o][lo]);
-                const double2 a23 = *reinterpret_cast<const double2 *>(&sm[G_V1][o][lo + 2]);
-                const double2 b01 = *reinterpret_cast<const double2 *>(&sm[G_V2][o][lo]);
-                const double2 b23 = *reinterpret_cast<const double2 *>(&sm[G_V2][o][lo + 2]);
-                lv1[0] = a01.x; lv1[1] = a01.y; lv1[2] = a23.x; lv1[3] = a23.y;
-                lv2[0] = b01.x; lv2[1] = b01.y; lv2[2] = b23.x; lv2[3] = b23.y;
-            }
-#if GRAD2D_SKEW
-            // cross reads in a skewed node order: the y-line threads of odd element slots read node
-            // (k + 1) & 3 at read k, which takes the half-warp's 16 reads from 3 to 2 wavefronts (the
-            // floor with the two layouts' 2 mod 4 offset); the arithmetic order below is unchanged
-            const int sk = (o == 1 && (le & 1)) ? 1 : 0;
-            double qv[NP][GV];
-#pragma unroll
-            for (int k = 0; k < NP; ++k) {
-                const int a = (k + sk) & 3;
-                const int oi = o == 0 ? yo + eoy + 4 * a + ln : eox + 4 * a + ln;
-#pragma unroll
-                for (int c = 0; c < GV; ++c) qv[k][c] = sm[G_Q + c][1 - o][oi];
-            }
-#endif
 #pragma unroll
             for (int a = 0; a < NP; ++a) {
+                const int oi = o == 0 ? yo + eoy + 4 * a + ln : eox + 4 * a + ln;
                 double qo[GV], qs[GV], fv[GV];
 #pragma unroll
                 for (int c = 0; c < GV; ++c) {
                     qs[c] = q[c][a];
-#if GRAD2D_SKEW
-                    qo[c] = sk ? qv[(a + 3) & 3][c] : qv[a][c];
-#else
-                    qo[c] = sm[G_Q + c][1 - o][o == 0 ? yo + eoy + 4 * a + ln : eox + 4 * a + ln];
-#endif
+                    qo[c] = sm[G_Q + c][1 - o][oi];
                 }
-                const double v1 = lv1[a], v2 = lv2[a];
+                const double v1 = sm[G_V1][o][lo + a], v2 = sm[G_V2][o][lo + a];
                 if (o == 0) visc_flux2d(v1, v2, qs, qo, 0, md.mu, md.kappa, fv);
                 else visc_flux2d(v1, v2, qo, qs, 1, md.mu, md.kappa, fv);
                 if (valid && (a == 0 || a == NP - 1)) {

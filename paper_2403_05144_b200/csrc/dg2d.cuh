@@ -204,9 +204,6 @@ __device__ __forceinline__ void store_face2d(double *Fs, int e, int face, int k,
 #ifndef SURF2D_MINB
 #define SURF2D_MINB 3
 #endif
-#ifndef SURF2D_PREFETCH
-#define SURF2D_PREFETCH 0
-#endif
 // SCS: the shock-capturing neighbour smoothing (sc.cuh) rides along, in a pass over the faces after the
 // fluxes (one thread per interface / mortar) -- formerly lane k = 0 of every interface /
 // mortar raises alpha of both sides to half the other side's raw value (k_sc_alpha ran before).
@@ -240,42 +237,15 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
     const int nI = 4 * nif;
     int gt = blockIdx.x * blockDim.x + threadIdx.x;
     const int4 *__restrict__ IR = MODE == MODE_STAGE ? md.ifcs : md.ifc;
-    // the first records are mesh data (rebuilt by the re-mesh pipeline before the step): pull them into
-    // L1 before the dependency wait, while the previous kernel drains
-    if (SURF2D_PREFETCH >= 2 && gt + GS < nI) {
-        prefetch_l1(IR + (gt >> 2));
-        prefetch_l1(IR + ((gt + GS) >> 2));
-    }
     pdl_wait();
     // two interface face nodes per iteration while both are interfaces: twice the loads in flight
-    // per thread (the kernel is bound by the latency of the record -> trace gathers).  SURF2D_PREFETCH:
-    // the records of the next iteration are loaded before this iteration's traces are used, so an
-    // iteration after the first waits on one round trip (traces) instead of two (record, traces)
-#if SURF2D_PREFETCH == 1
-    int4 nIa = make_int4(0, 0, 0, 0), nIb = nIa;
-    if (gt + GS < nI) {
-        nIa = IR[gt >> 2];
-        nIb = IR[(gt + GS) >> 2];
-    }
-#endif
+    // per thread (the kernel is bound by the latency of the record -> trace gathers).  (Tried: the next
+    // iteration's records prefetched into registers (spills at 80 registers), into L1, or the first
+    // records into L1 before the dependency wait: cfg 3 surface 0.1847 -> 0.1854 / 0.1838 ms/step, noise)
     for (; gt + GS < nI; gt += 2 * GS) {
         const int ka = gt & 3, kb = (gt + GS) & 3;
-#if SURF2D_PREFETCH == 1
-        const int4 Ia = nIa, Ib = nIb;
-        if (gt + 3 * GS < nI) {
-            nIa = IR[(gt + 2 * GS) >> 2];
-            nIb = IR[(gt + 3 * GS) >> 2];
-        }
-#else
-#if SURF2D_PREFETCH == 2   // L1 prefetch of the next iteration's records (no registers held)
-        if (gt + 3 * GS < nI) {
-            prefetch_l1(IR + ((gt + 2 * GS) >> 2));
-            prefetch_l1(IR + ((gt + 3 * GS) >> 2));
-        }
-#endif
         const int4 Ia = IR[gt >> 2];
         const int4 Ib = IR[(gt + GS) >> 2];
-#endif
         PERK_DASSERT(Ia.x >= 0 && Ia.x < md.n[0] && Ia.y >= 0 && Ia.y < md.n[0] && Ib.x >= 0 && Ib.x < md.n[0] &&
                      Ib.y >= 0 && Ib.y < md.n[0]);
         const int srca = state_src(sp, Ia.w), srcb = state_src(sp, Ib.w);

@@ -34,12 +34,12 @@ struct StepTab1D {
 __host__ __device__ constexpr int step1d_threads(int nv) { return nv == 1 ? STEP1D_T1 : STEP1D_T3; }
 
 // state (U_n, K_1, stage buffer, K_i, W) + face fluxes, then the step's read-only mesh data staged once
-// per step so the per-stage loops never wait on global memory: interface pairs (list order, <= n),
-// boundaries (<= 2), the element list, member and level per element
+// per step so the per-stage loops never wait on global memory: 2/h per element, interface pairs packed
+// with their members (list order, <= n), boundaries (<= 2), the element list packed with the members
 __host__ __device__ inline size_t step1d_smem_bytes(int n, int nv, bool use_w)
 {
-    return sizeof(double) * ((size_t)n * nv * NP * (use_w ? 4 : 3) + (size_t)n * 2 * nv) +
-           (size_t)n * 8 + 16 + (size_t)n * 4 + (size_t)n * 2;
+    return sizeof(double) * ((size_t)n * nv * NP * (use_w ? 4 : 3) + (size_t)n * 2 * nv + (size_t)n) +
+           (size_t)n * 8 + 16 + (size_t)n * 4;
 }
 
 template <int NV>
@@ -55,11 +55,10 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
     double *sUn = sh, *sK1 = sUn + (size_t)n * rowd, *sUb = sK1 + (size_t)n * rowd;
     double *sW = sUb + (size_t)n * rowd;
     double *sFs = use_w ? sW + (size_t)n * rowd : sW;
-    int2 *sIf = reinterpret_cast<int2 *>(sFs + (size_t)n * 2 * NV);
+    double *sJ = sFs + (size_t)n * 2 * NV;                       // 2 / h per element (no division per stage)
+    int2 *sIf = reinterpret_cast<int2 *>(sJ + n);                // interface sides packed with their members
     int2 *sBd = sIf + n;
-    int *sEl = reinterpret_cast<int *>(sBd + 2);
-    uint8_t *sMem = reinterpret_cast<uint8_t *>(sEl + n);
-    uint8_t *sLev = sMem + n;
+    int *sEl = reinterpret_cast<int *>(sBd + 2);                 // element list packed with the members
     const int tid = threadIdx.x, nt = blockDim.x;
     {
         const int *src = reinterpret_cast<const int *>(tb);
@@ -72,7 +71,7 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
         for (int k = tid; k < nif_all; k += nt) {
             const int4 I = md.ifcs[k];
             PERK_DASSERT(I.x >= 0 && I.x < n && I.y >= 0 && I.y < n);
-            sIf[k] = make_int2(I.x, I.y);
+            sIf[k] = make_int2(I.x | ((int)md.mem[I.x] << PK_EBITS), I.y | ((int)md.mem[I.y] << PK_EBITS));
         }
         for (int k = tid; k < nbd_all && k < 2; k += nt) sBd[k] = md.bnd[md.list[KIND_BD][k]];
         if (tid < NP * NP) sD[tid / NP][tid % NP] = cB.Dhat[tid / NP][tid % NP];
@@ -81,9 +80,9 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
             sCnt[k / MAXS][k % MAXS] = md.count_active[kind * MAXS + k % MAXS];
         }
         for (int k = tid; k < n; k += nt) {
-            sEl[k] = md.list[KIND_EL][k];
-            sMem[k] = md.mem[k];
-            sLev[k] = md.lev[k];
+            const int e = md.list[KIND_EL][k];
+            sEl[k] = e | ((int)md.mem[e] << PK_EBITS);
+            sJ[k] = 2.0 / (md.hf * (double)(1 << (md.max_level - md.lev[k])));
         }
     }
     __syncthreads();
@@ -91,11 +90,12 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
     for (int i = 1; i <= S; ++i) {
         const int nif = sCnt[0][i - 1], nbd = sCnt[1][i - 1], nel = sCnt[2][i - 1];
         const double dtc = dt * T.c[i - 1];
+        const unsigned bufm = T.bufmask[i - 1];
         // the stage-i state of element e (member m), variable v, node j (SURVEY §7 rule)
         auto state = [&](int e, int m, int v, int j) {
             const size_t x = ((size_t)e * NV + v) * NP + j;
             if (i == 1) return sUn[x];
-            if ((T.bufmask[i - 1] >> m) & 1u) return sUb[x];
+            if ((bufm >> m) & 1u) return sUb[x];
             return fma(dtc, sK1[x], sUn[x]);
         };
         // surface fluxes over the active interfaces and boundaries
@@ -103,17 +103,17 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
             double uL[NV], uR[NV], f[NV];
             if (t < nif) {
                 const int2 I = sIf[t];
-                const int mL = sMem[I.x], mR = sMem[I.y];
+                const int eL = pk_elem(I.x), eR = pk_elem(I.y), mL = I.x >> PK_EBITS, mR = I.y >> PK_EBITS;
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
-                    uL[v] = state(I.x, mL, v, NP - 1);
-                    uR[v] = state(I.y, mR, v, 0);
+                    uL[v] = state(eL, mL, v, NP - 1);
+                    uR[v] = state(eR, mR, v, 0);
                 }
                 numflux1d<NV>(uL, uR, md.gamma, md.adv, f);
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
-                    sFs[((size_t)I.x * 2 + 0) * NV + v] = f[v];
-                    sFs[((size_t)I.y * 2 + 1) * NV + v] = f[v];
+                    sFs[((size_t)eL * 2 + 0) * NV + v] = f[v];
+                    sFs[((size_t)eR * 2 + 1) * NV + v] = f[v];
                 }
             } else {
                 const int2 B = sBd[t - nif];
@@ -141,9 +141,10 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
             bool on = t < tot;
             int e = 0, j = 0, m = 0;
             if (on) {
-                e = sEl[t / NP];
+                const int pe = sEl[t / NP];
+                e = pk_elem(pe);
                 j = t % NP;
-                m = sMem[e];
+                m = pe >> PK_EBITS;
                 on = (act >> m) & 1u;
             }
             double K[NV];
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(step1d_threads(NV)) k_step1d(MeshDev md, const
                     for (int v = 0; v < NV; ++v) u[v] = state(e, m, v, k);
                     phys_flux1d<NV>(u, md.gamma, md.adv, f[k]);
                 }
-                const double J = 2.0 / (md.hf * (double)(1 << (md.max_level - sLev[e])));
+                const double J = sJ[e];
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
                     double s = 0.0;

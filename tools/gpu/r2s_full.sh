@@ -6,4 +6,4 @@ M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__sass_t
 for c in 5 3; do
 timeout 900 ncu --metrics $M --clock-control none --csv --log-file gpurun_out/counts_cfg$c.csv python bench.py --profile-only --config $c --steps 1 --warmup 3 > gpurun_out/ncu_counts$c.log 2>&1; echo counts$c=$? >> gpurun_out/status.txt
 done
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_(vol|surf|gsurf|grad)2d" --launch-skip 116 --launch-count 4 -o gpurun_out/full_cfg5_s30 python bench.py --profile-only --config 5 --steps 1 --warmup 0 > gpurun_out/ncu_full.log 2>&1; echo full=$? >> gpurun_out/status.txt
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_(vol|surf|grad)2d" --launch-skip 87 --launch-count 3 -o gpurun_out/full_cfg5_s30 python bench.py --profile-only --config 5 --steps 1 --warmup 0 > gpurun_out/ncu_full.log 2>&1; echo full=$? >> gpurun_out/status.txt
