@@ -120,6 +120,9 @@ __global__ void __launch_bounds__(256, 3) k_gsurf2d(MeshDev md, StageParams sp, 
 #ifndef BR1_FUSED
 #define BR1_FUSED 1
 #endif
+#ifndef GRAD2D_PF
+#define GRAD2D_PF 0
+#endif
 static_assert(!BR1_FUSED || BR1_DV, "the fused BR1 gradient kernel leaves no Gs for the volume kernel");
 constexpr int GRAD2D_LS = VOL2D_LS;
 constexpr int G_V1 = 0, G_V2 = 1, G_T = 2, G_Q = 3;     // shared fields: v1, v2, T, gradients (3)
@@ -201,6 +204,10 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
         const bool has_next = base + stride < n_act;
         const int pk_next = pk_ahead;
         pk_ahead = base + 2 * stride < n_act ? entry_at(base + 2 * stride) : 0;
+#if GRAD2D_PF
+        int2 fn_nx[2] = {make_int2(-1, FNB_NONE), make_int2(-1, FNB_NONE)};
+        if (FUSED && has_next) faces_of(pk_next, fn_nx);   // needed mid-iteration (prefetch) and next
+#endif
         const int e = pk_elem(pk);
         PERK_DASSERT(e >= 0 && e < md.n[0]);
         const int src = state_src(sp, pk_member(pk));
@@ -333,6 +340,31 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
                 }
             }
             line_gradient_g<GRAD2D_LS>(sm, o, lo, g[0], g[1], 2.0 / hcell, fld, q);
+#if GRAD2D_PF
+            // prefetch the next group's neighbour traces (no registers held): they are gathered at the
+            // top of the next iteration, after this group's viscous fluxes and Dv
+            if (has_next) {
+#pragma unroll
+                for (int f = 0; f < 2; ++f)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int px = h == 0 ? fn_nx[f].x : fn_nx[f].y;
+                        if (px < 0) continue;
+                        const int sx = state_src(sp, pk_member(px));
+                        const size_t b = (size_t)pk_elem(px) * 64 + face_node2d((2 * o + f) ^ 1, ln);
+                        const double *P = state_base(sb, sx) + b;
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) {
+                            if (GRAD2D_PF == 1) prefetch_l2(P + v * 16);
+                            else prefetch_l1(P + v * 16);
+                            if (sx == SRC_LAZY) {
+                                if (GRAD2D_PF == 1) prefetch_l2(K1 + b + v * 16);
+                                else prefetch_l1(K1 + b + v * 16);
+                            }
+                        }
+                    }
+            }
+#endif
         } else {
             line_gradient<GRAD2D_LS>(sm, o, lo, ln, gst[le], 2.0 / hcell, fld, sc, q);
         }
@@ -345,7 +377,14 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
         __syncwarp();
         if (!FUSED && has_next) issue_gs(pk_next);          // gst consumed
         cp_async_commit();
-        if (FUSED && has_next) faces_of(pk_next, fn);       // the next group's face entries (used at its top)
+        if (FUSED && has_next) {
+#if GRAD2D_PF
+            fn[0] = fn_nx[0];
+            fn[1] = fn_nx[1];
+#else
+            faces_of(pk_next, fn);       // the next group's face entries (used at its top)
+#endif
+        }
         if (BR1_DV) {
             // viscous flux in direction o at the line's 4 nodes: the end nodes' go to Vt (face traces),
             // all four into dv[i] = sum_a Dhat_ia F^v_o(node a); x + y lines summed through shared memory

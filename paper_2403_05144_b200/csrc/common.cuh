@@ -310,6 +310,7 @@ __device__ __forceinline__ int ld_volatile(const int *p) { return *reinterpret_c
 
 // L1 prefetch of the line holding p (no register, no scoreboard entry)
 __device__ __forceinline__ void prefetch_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
 // Ampere-style asynchronous copies (SASS LDGSTS): no registers, per-thread commit groups
 __device__ __forceinline__ void cp_async16(void *dst, const void *src)
