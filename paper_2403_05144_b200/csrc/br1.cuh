@@ -120,8 +120,11 @@ __global__ void __launch_bounds__(256, 3) k_gsurf2d(MeshDev md, StageParams sp, 
 #ifndef BR1_FUSED
 #define BR1_FUSED 1
 #endif
-#ifndef GRAD2D_PF
-#define GRAD2D_PF 0
+// 2/h by a division (1) or by the exact power-of-two scaling of common.cuh two_over_h (0): without the
+// division's call the kernel's allocation exceeds 128 registers and spills (cfg 5 gradients 2.07 vs
+// 2.25 ms/step); the volume kernel uses two_over_h (NS volume 2.375 -> 2.348)
+#ifndef GRAD2D_DIV
+#define GRAD2D_DIV 1
 #endif
 static_assert(!BR1_FUSED || BR1_DV, "the fused BR1 gradient kernel leaves no Gs for the volume kernel");
 constexpr int GRAD2D_LS = VOL2D_LS;
@@ -161,6 +164,7 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
     const int n_act = n_el_a + hel.y;
     const double gm1 = md.gamma - 1.0;
     const double dtc = sp.dt * sp.c_stage;
+    const double two_hf = 2.0 / md.hf;
     const StateBufs sb{Un, Ubuf, K1, Uin};
     const int q0 = 2 * t8;
     const int o = t8 >> 2, ln = t8 & 3;
@@ -204,20 +208,21 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
         const bool has_next = base + stride < n_act;
         const int pk_next = pk_ahead;
         pk_ahead = base + 2 * stride < n_act ? entry_at(base + 2 * stride) : 0;
-#if GRAD2D_PF
-        int2 fn_nx[2] = {make_int2(-1, FNB_NONE), make_int2(-1, FNB_NONE)};
-        if (FUSED && has_next) faces_of(pk_next, fn_nx);   // needed mid-iteration (prefetch) and next
-#endif
         const int e = pk_elem(pk);
         PERK_DASSERT(e >= 0 && e < md.n[0]);
         const int src = state_src(sp, pk_member(pk));
-        const double hcell = md.hf * (double)(1 << (md.max_level - pk_level(pk)));
+#if GRAD2D_DIV
+        const double j2h = 2.0 / (md.hf * (double)(1 << (md.max_level - pk_level(pk))));
+#else
+        const double j2h = two_over_h(two_hf, pk_level(pk), md.max_level);   // 2 / h
+#endif
         // fused: the neighbours' traces at this thread's two face nodes (a large side needs both smalls),
         // every load issued before any is used; lazy states formed after the loads.  (Tried and slower,
         // cfg 5 gradients ms/step: the line's own velocities as 16 B loads 2.11 -> 2.12; the cross reads
         // in a skewed node order (3 -> 2 wavefronts per half-warp on paper) 2.16; the first neighbour's
         // traces staged one group ahead by 8 B cp.async, face entries two groups ahead, 2.62 -- the
-        // entry -> face-table chain stalled every iteration and shared-memory conflicts doubled)
+        // entry -> face-table chain stalled every iteration and shared-memory conflicts doubled; the next
+        // group's neighbour traces prefetched into L2 / L1 after the gradients, 2.42; 3 CTAs/SM, 2.19)
         double un[2][2][4];
         if (FUSED) {
             int xe[2][2], xs[2][2];
@@ -339,34 +344,9 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
                     for (int c = 0; c < GV; ++c) g[f][c] = wo[c];
                 }
             }
-            line_gradient_g<GRAD2D_LS>(sm, o, lo, g[0], g[1], 2.0 / hcell, fld, q);
-#if GRAD2D_PF
-            // prefetch the next group's neighbour traces (no registers held): they are gathered at the
-            // top of the next iteration, after this group's viscous fluxes and Dv
-            if (has_next) {
-#pragma unroll
-                for (int f = 0; f < 2; ++f)
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int px = h == 0 ? fn_nx[f].x : fn_nx[f].y;
-                        if (px < 0) continue;
-                        const int sx = state_src(sp, pk_member(px));
-                        const size_t b = (size_t)pk_elem(px) * 64 + face_node2d((2 * o + f) ^ 1, ln);
-                        const double *P = state_base(sb, sx) + b;
-#pragma unroll
-                        for (int v = 0; v < 4; ++v) {
-                            if (GRAD2D_PF == 1) prefetch_l2(P + v * 16);
-                            else prefetch_l1(P + v * 16);
-                            if (sx == SRC_LAZY) {
-                                if (GRAD2D_PF == 1) prefetch_l2(K1 + b + v * 16);
-                                else prefetch_l1(K1 + b + v * 16);
-                            }
-                        }
-                    }
-            }
-#endif
+            line_gradient_g<GRAD2D_LS>(sm, o, lo, g[0], g[1], j2h, fld, q);
         } else {
-            line_gradient<GRAD2D_LS>(sm, o, lo, ln, gst[le], 2.0 / hcell, fld, sc, q);
+            line_gradient<GRAD2D_LS>(sm, o, lo, ln, gst[le], j2h, fld, sc, q);
         }
 #pragma unroll
         for (int c = 0; c < GV; ++c) {   // the line is contiguous and 16 B aligned: two 16 B stores
@@ -377,14 +357,7 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
         __syncwarp();
         if (!FUSED && has_next) issue_gs(pk_next);          // gst consumed
         cp_async_commit();
-        if (FUSED && has_next) {
-#if GRAD2D_PF
-            fn[0] = fn_nx[0];
-            fn[1] = fn_nx[1];
-#else
-            faces_of(pk_next, fn);       // the next group's face entries (used at its top)
-#endif
-        }
+        if (FUSED && has_next) faces_of(pk_next, fn);       // the next group's face entries (used at its top)
         if (BR1_DV) {
             // viscous flux in direction o at the line's 4 nodes: the end nodes' go to Vt (face traces),
             // all four into dv[i] = sum_a Dhat_ia F^v_o(node a); x + y lines summed through shared memory
@@ -427,7 +400,7 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
             __syncwarp();
             if (valid && base + le < n_el_a) {   // halo elements (their member is inactive) need no Dv
                 const int i0 = q0 & 3, j0 = q0 >> 2;
-                const double J = -2.0 / hcell;
+                const double J = -j2h;
 #pragma unroll
                 for (int c = 0; c < GV; ++c) {
                     const double2 sx = *reinterpret_cast<const double2 *>(&sm[G_V1 + c][0][eox + q0]);

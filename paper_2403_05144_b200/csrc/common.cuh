@@ -119,6 +119,14 @@ struct MeshDev {
 };
 constexpr int FNB_CONF = -1, FNB_SMALL_LO = -2, FNB_SMALL_HI = -3, FNB_NONE = -4;
 
+// 2/h of a cell at level lev without a division per element: 2 / (hf 2^(L - lev)) = (2 / hf) 2^(lev - L),
+// and the power-of-two scaling is exact, so this is bitwise 2.0 / (hf * (1 << (L - lev))) (two_over_hf =
+// 2.0 / md.hf, formed once per thread)
+__device__ __forceinline__ double two_over_h(double two_over_hf, int lev, int max_level)
+{
+    return two_over_hf * __hiloint2double((1023 + lev - max_level) << 20, 0);
+}
+
 // packed element entry of md.elpk (cells < 2^24, members < 8, levels < 16)
 constexpr int PK_EBITS = 24;
 __device__ __forceinline__ int pk_elem(int pk) { return pk & ((1 << PK_EBITS) - 1); }

@@ -639,6 +639,7 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
     const int n_act = MODE == MODE_STAGE ? md.count_active[KIND_EL * MAXS + sp.stage - 1] : md.n[0];
     const double g = md.gamma, gm1 = g - 1.0, inv_gm1 = 1.0 / gm1;
     const double dtc = sp.dt * sp.c_stage;
+    const double two_hf = 2.0 / md.hf;
     const int q0 = 2 * t8;
     const int o = t8 >> 2, ln = t8 & 3;
     // element offsets: x layout 16 per element, y layout 20 per element starting 2 doubles into the
@@ -709,7 +710,7 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
         const int m = pk_member(pk);
         const int src = state_src(sp, m);
         const size_t eb = (size_t)e * 64;
-        const double hcell = md.hf * (double)(1 << (md.max_level - pk_level(pk)));
+        const double j2h = two_over_h(two_hf, pk_level(pk), md.max_level);   // 2 / h
         double2 pre_un[4], pre_k1[4];          // epilogue operands held in registers (EM == 2)
         const double al = SC ? alpha[e] : 0.0;   // read before this element's next-stage alpha is written
 
@@ -868,7 +869,7 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
             if (has_next) cp_async_wait<1>();
             else cp_async_wait<0>();
             __syncwarp();
-            visc_volume<LS>(sm, o, lo, eox, eoy, yo, ln, EP(EPI_GS), 2.0 / hcell, md.mu, md.kappa, acc);
+            visc_volume<LS>(sm, o, lo, eox, eoy, yo, ln, EP(EPI_GS), j2h, md.mu, md.kappa, acc);
         }
         // surface lift: + f*_hi / w_N at the last node, - f*_lo / w_0 at the first node
         // line coordinates (normal, tangential) -> (momentum x, momentum y)
@@ -929,7 +930,7 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
         };
         // members in the launch's prefix that do not evaluate this stage (non-standard patterns) write nothing
         const bool writes = valid && (MODE == MODE_RHS || ((sp.actmask >> m) & 1u));
-        const double J = -2.0 / hcell;
+        const double J = -j2h;
         PERK_JITTER(6);
         __syncwarp();   // all primitives consumed: reuse sm[v][o] as the accumulator arrays
 #pragma unroll
