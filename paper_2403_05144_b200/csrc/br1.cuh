@@ -222,7 +222,9 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
         // in a skewed node order (3 -> 2 wavefronts per half-warp on paper) 2.16; the first neighbour's
         // traces staged one group ahead by 8 B cp.async, face entries two groups ahead, 2.62 -- the
         // entry -> face-table chain stalled every iteration and shared-memory conflicts doubled; the next
-        // group's neighbour traces prefetched into L2 / L1 after the gradients, 2.42; 3 CTAs/SM, 2.19)
+        // group's neighbour traces prefetched into L2 / L1 after the gradients, 2.42; 3 CTAs/SM, 2.19;
+        // the next group's first-neighbour traces loaded into registers after this group's phase 1
+        // (entries three groups ahead, 3 CTAs/SM for the registers), 2.14 vs 2.07)
         double un[2][2][4];
         if (FUSED) {
             int xe[2][2], xs[2][2];
