@@ -271,6 +271,12 @@ int perk_get_count_active(perk_ctx *ctx, int32_t kind, int32_t *count_active_hos
  * items the stage-i BR1 / indicator launches process besides the active ones (the large elements of
  * the active mortars whose fine side is another member, and their faces; D7).  Synchronising. */
 int perk_get_halo_counts(perk_ctx *ctx, int32_t *halo_host);
+/* per element face neighbours of the fused BR1 gradient pass (Navier-Stokes contexts built with
+ * BR1_FUSED; EUNSUPPORTED otherwise): table_host[e][face][2], face 0 +x, 1 -x, 2 +y, 3 -y:
+ * conforming {nb, -1}; small side of a mortar {large, -2 (lower half) / -3 (upper half)}; large side
+ * {small_lo, small_hi}; boundary {-1, -4}.  Cells only (the member bits of the device table are
+ * stripped).  cap >= 8 n_cells entries.  Synchronising. */
+int perk_get_face_table(perk_ctx *ctx, int32_t *table_host, int64_t cap);
 /* element-RHS evaluations (sum over steps of sum_r E_r N_C(r), P:l.1282-1289) and steps taken */
 int perk_get_counters(perk_ctx *ctx, int64_t *elem_rhs_evals, int64_t *steps);
 int perk_sync(perk_ctx *ctx);

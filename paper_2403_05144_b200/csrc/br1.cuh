@@ -123,6 +123,9 @@ __global__ void __launch_bounds__(256, 3) k_gsurf2d(MeshDev md, StageParams sp, 
 // 2/h by a division (1) or by the exact power-of-two scaling of common.cuh two_over_h (0): without the
 // division's call the kernel's allocation exceeds 128 registers and spills (cfg 5 gradients 2.07 vs
 // 2.25 ms/step); the volume kernel uses two_over_h (NS volume 2.375 -> 2.348)
+#ifndef VISC_LINE
+#define VISC_LINE 1
+#endif
 #ifndef GRAD2D_DIV
 #define GRAD2D_DIV 1
 #endif
@@ -379,8 +382,12 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
                     qo[c] = sm[G_Q + c][1 - o][oi];
                 }
                 const double v1 = sm[G_V1][o][lo + a], v2 = sm[G_V2][o][lo + a];
+#if VISC_LINE
+                visc_flux2d_line(o, v1, v2, qs, qo, md.mu, md.kappa, fv);
+#else
                 if (o == 0) visc_flux2d(v1, v2, qs, qo, 0, md.mu, md.kappa, fv);
                 else visc_flux2d(v1, v2, qo, qs, 1, md.mu, md.kappa, fv);
+#endif
                 if (valid && (a == 0 || a == NP - 1)) {
                     const int face = 2 * o + (a == NP - 1 ? 0 : 1);   // a = N: +o face, a = 0: -o face
 #pragma unroll
@@ -423,8 +430,12 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
                     qo[c] = sm[G_Q + c][1 - o][oi];
                 }
                 const double v1 = sm[G_V1][o][lo + a], v2 = sm[G_V2][o][lo + a];
+#if VISC_LINE
+                visc_flux2d_line(o, v1, v2, qs, qo, md.mu, md.kappa, fv);
+#else
                 if (o == 0) visc_flux2d(v1, v2, qs, qo, 0, md.mu, md.kappa, fv);
                 else visc_flux2d(v1, v2, qo, qs, 1, md.mu, md.kappa, fv);
+#endif
                 const int face = 2 * o + (end ? 0 : 1);      // a = N: +o face, a = 0: -o face
 #pragma unroll
                 for (int c = 0; c < GV; ++c) Vt[gidx2d(e, face, c, ln)] = fv[c];

@@ -164,6 +164,25 @@ __device__ __forceinline__ void visc_flux2d(double v1, double v2, const double q
     }
 }
 
+// the same flux for a line thread of direction o without a branch on o (the x- and y-line threads of an
+// element share a warp, so `if (o == 0)` ran both bodies): qs = the gradient along the line (direction
+// o), qo = along the other direction; components swapped into line coordinates (normal, tangential),
+// the o = 0 formula, swapped back to (momentum x, momentum y, energy)
+__device__ __forceinline__ void visc_flux2d_line(int o, double v1, double v2, const double qs[GV], const double qo[GV],
+                                                 double mu, double kappa, double f[GV])
+{
+    const bool y = o != 0;
+    const double vn = y ? v2 : v1, vt = y ? v1 : v2;
+    const double sn = y ? qs[1] : qs[0], st = y ? qs[0] : qs[1];   // d v_n / d n, d v_t / d n
+    const double on = y ? qo[1] : qo[0], ot = y ? qo[0] : qo[1];   // d v_n / d t, d v_t / d t
+    const double tnn = mu * ((4.0 / 3.0) * sn - (2.0 / 3.0) * ot);
+    const double tnt = mu * (on + st);
+    const double fe = fma(vn, tnn, fma(vt, tnt, kappa * qs[2]));
+    f[0] = y ? tnt : tnn;
+    f[1] = y ? tnn : tnt;
+    f[2] = fe;
+}
+
 // BR1 face arrays Gs (central w*), Vt (normal viscous flux trace): [cell][face][GV][k]
 __device__ __forceinline__ size_t gidx2d(int e, int face, int c, int k) { return (((size_t)e * 4 + face) * GV + c) * NP + k; }
 

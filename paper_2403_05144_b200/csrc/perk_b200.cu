@@ -1361,6 +1361,25 @@ extern "C" int perk_get_count_active(perk_ctx *c, int32_t kind, int32_t *out)
     return PERK_OK;
 }
 
+extern "C" int perk_get_face_table(perk_ctx *c, int32_t *table, int64_t cap)
+{
+    if (!c) return PERK_ENOTINIT;
+    if (!c->md.fnb) return set_err(c, PERK_EUNSUPPORTED, "no face table (Navier-Stokes with BR1_FUSED only)");
+    int rc = check_device_err(c);
+    if (rc) return rc;
+    int n = 0;
+    CU(cudaMemcpy(&n, c->md.n, sizeof(int), cudaMemcpyDeviceToHost));
+    if (!table || cap < 8 * (int64_t)n) return set_err(c, PERK_EINVAL, "host array too small");
+    std::vector<int2> h((size_t)4 * n);
+    CU(cudaMemcpy(h.data(), c->md.fnb, sizeof(int2) * 4 * (size_t)n, cudaMemcpyDeviceToHost));
+    const int mask = (1 << PK_EBITS) - 1;
+    for (size_t k = 0; k < h.size(); ++k) {
+        table[2 * k] = h[k].x >= 0 ? (h[k].x & mask) : h[k].x;
+        table[2 * k + 1] = h[k].y >= 0 ? (h[k].y & mask) : h[k].y;
+    }
+    return PERK_OK;
+}
+
 extern "C" int perk_get_halo_counts(perk_ctx *c, int32_t *out)
 {
     if (!c) return PERK_ENOTINIT;

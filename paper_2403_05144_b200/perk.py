@@ -127,6 +127,7 @@ def lib():
         L.perk_get_list.argtypes = [P, i32, P, i64, P]
         L.perk_get_count_active.argtypes = [P, i32, P]
         L.perk_get_halo_counts.argtypes = [P, P]
+        L.perk_get_face_table.argtypes = [P, P, i64]
         L.perk_get_counters.argtypes = [P, C.POINTER(i64), C.POINTER(i64)]
         L.perk_sync.argtypes = [P]
         L.perk_last_error.argtypes = [P]
@@ -160,7 +161,7 @@ def exported_symbols():
             "perk_set_shock_capturing", "perk_sc_alpha", "perk_pattern_mask", "perk_get_halo_counts", "perk_time_kernels_ex",
             "perk_init_dd", "perk_dd_split", "perk_dd_info", "perk_dd_counts", "perk_dd_get_list", "perk_dd_stage",
             "perk_dd_pack", "perk_dd_unpack", "perk_dd_exchange", "perk_dd_group_step", "perk_debug_jitter",
-            "perk_build_flags"]
+            "perk_build_flags", "perk_get_face_table"]
 
 
 PATTERNS = {"standard": 0, "early": 1, "alternating": 2}
@@ -436,6 +437,12 @@ class Perk:
         out = np.zeros(self.S, np.int32)
         _check(self.h, lib().perk_get_count_active(self.h, KIND[kind], out.ctypes.data))
         return out
+
+    def face_table(self):
+        """per element face neighbours of the fused BR1 pass: int32 [n_cells][4][2] (include/perk.h)"""
+        out = np.zeros(8 * max(self.n_cells, 1), np.int32)
+        _check(self.h, lib().perk_get_face_table(self.h, out.ctypes.data, out.size))
+        return out[: 8 * self.n_cells].reshape(self.n_cells, 4, 2)
 
     def halo_counts(self):
         """BR1 / shock-capturing halo items per stage: dict kind -> array of S counts"""

@@ -47,3 +47,28 @@ def compare_mesh(ora, gpu, kinds=("elements", "interfaces", "mortars", "boundari
 def gpu_state_numpy(gpu, U):
     n = gpu.n_cells
     return U[:n].cpu().numpy()
+
+
+def expected_face_table(ora):
+    """the fused BR1 pass's per element face neighbours (include/perk.h perk_get_face_table), written
+    out from the oracle's face records: conforming {nb, -1}, small side {large, -2 / -3 (lower / upper
+    half)}, large side {small_lo, small_hi}, boundary {-1, -4}; every face slot exactly once"""
+    n = ora.n
+    t = np.zeros((n, 4, 2), np.int32)
+    seen = np.zeros((n, 4), np.int32)
+
+    def put(e, f, a, b):
+        t[e, f] = (a, b)
+        seen[e, f] += 1
+
+    for lo, hi, o in ora.faces("interfaces")[0]:
+        put(lo, 2 * o, hi, -1)
+        put(hi, 2 * o + 1, lo, -1)
+    for large, s0, s1, o, side in ora.faces("mortars")[0]:
+        put(large, 2 * o + side, s0, s1)
+        put(s0, 2 * o + 1 - side, large, -2)
+        put(s1, 2 * o + 1 - side, large, -3)
+    for e, f in ora.faces("boundaries")[0]:
+        put(e, f, -1, -4)
+    assert (seen == 1).all(), "oracle face records do not cover every face slot once"
+    return t

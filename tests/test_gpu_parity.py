@@ -9,7 +9,7 @@ import pytest
 import workloads as W
 from oracle import oracle as O
 from oracle import tableau as T
-from gpu_util import TOL, build_pair, compare_mesh, gpu_state_numpy, rel_err_per_var
+from gpu_util import TOL, build_pair, compare_mesh, expected_face_table, gpu_state_numpy, rel_err_per_var
 
 pytestmark = pytest.mark.gpu
 
@@ -256,6 +256,26 @@ def test_ns_rhs_eval_masks(n_base):
             assert np.abs(dUg[:, v] - dUo[:, v]).max() <= tol, (mask, v)
 
 
+@pytest.mark.parametrize("n_base", [8, 256])
+def test_ns_face_table(n_base):
+    """the fused BR1 pass's device-built face-neighbour table (an index structure: bit-exact) against
+    the table written out from the oracle's face records; 256 = the BASELINE cfg-5 mesh"""
+    from paper_2403_05144_b200 import perk as P
+    w = W.make(5, n_base=n_base)
+    ora, gpu = build_pair(w)
+    if not P.build_flags()["br1_fused"]:
+        pytest.skip("library built without BR1_FUSED")
+    assert np.array_equal(gpu.face_table(), expected_face_table(ora))
+
+
+def test_face_table_unsupported_for_euler():
+    w = W.make(3, n_base=8)
+    ora, gpu = build_pair(w)
+    with pytest.raises(Exception) as ei:
+        gpu.face_table()
+    assert ei.value.code == -6
+
+
 def test_cfg5_small_full_run():
     """cfg-5 structure (4 levels, {4, 8, 16, 32}, BR1) on an 8^2 base, the full 200 steps"""
     w = W.make(5, n_base=8)
@@ -436,6 +456,9 @@ def test_ns_repartition(order):
         gpu.repartition(lm, Ug)
         gpu.sync()
         compare_mesh(ora, gpu)
+        from paper_2403_05144_b200 import perk as P
+        if P.build_flags()["br1_fused"]:
+            assert np.array_equal(gpu.face_table(), expected_face_table(ora))
     ora.step(Uo, w.dt, 5)
     gpu.step(Ug, w.dt, 5)
     torch.cuda.synchronize()
