@@ -213,27 +213,30 @@ __global__ void k_face_records(MeshDev md, const int *__restrict__ slot_list, co
     }
 }
 
-// per element face neighbours (MeshDev::fnb) from the face records: one thread per interface / mortar
+// per element face neighbours (MeshDev::fnb) from the face records (grid-stride over all records)
 __global__ void k_face_table(MeshDev md)
 {
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
     const int nif = md.n[1], nmo = md.n[2], nbd = md.n[3];
-    if (p >= nif + nmo + nbd) return;
     auto pkn = [&](int e) { return e | ((int)md.mem[e] << PK_EBITS); };
-    if (p >= nif + nmo) {
-        const int2 B = md.bnd[p - nif - nmo];
-        md.fnb[(size_t)B.x * 4 + (B.y & 7)] = make_int2(-1, FNB_NONE);
-    } else if (p < nif) {
-        const int4 I = md.ifc[p];                      // low side's face 2o, high side's face 2o + 1
-        md.fnb[(size_t)I.x * 4 + 2 * I.z] = make_int2(pkn(I.y), FNB_CONF);
-        md.fnb[(size_t)I.y * 4 + 2 * I.z + 1] = make_int2(pkn(I.x), FNB_CONF);
-    } else {
-        const int4 M = md.mor[p - nif];
-        const int o = M.w & 1, side = (M.w >> 1) & 1;
-        const int lf = 2 * o + side, sf = 2 * o + 1 - side;
-        md.fnb[(size_t)M.x * 4 + lf] = make_int2(pkn(M.y), pkn(M.z));
-        md.fnb[(size_t)M.y * 4 + sf] = make_int2(pkn(M.x), FNB_SMALL_LO);
-        md.fnb[(size_t)M.z * 4 + sf] = make_int2(pkn(M.x), FNB_SMALL_HI);
+    auto ok = [&](int e) { return e >= 0 && e < md.cap; };   // (a latched capacity error leaves no valid mesh)
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < nif + nmo + nbd; p += gridDim.x * blockDim.x) {
+        if (p >= nif + nmo) {
+            const int2 B = md.bnd[p - nif - nmo];
+            if (ok(B.x)) md.fnb[(size_t)B.x * 4 + (B.y & 7)] = make_int2(-1, FNB_NONE);
+        } else if (p < nif) {
+            const int4 I = md.ifc[p];                      // low side's face 2o, high side's face 2o + 1
+            if (!ok(I.x) || !ok(I.y)) continue;
+            md.fnb[(size_t)I.x * 4 + 2 * I.z] = make_int2(pkn(I.y), FNB_CONF);
+            md.fnb[(size_t)I.y * 4 + 2 * I.z + 1] = make_int2(pkn(I.x), FNB_CONF);
+        } else {
+            const int4 M = md.mor[p - nif];
+            if (!ok(M.x) || !ok(M.y) || !ok(M.z)) continue;
+            const int o = M.w & 1, side = (M.w >> 1) & 1;
+            const int lf = 2 * o + side, sf = 2 * o + 1 - side;
+            md.fnb[(size_t)M.x * 4 + lf] = make_int2(pkn(M.y), pkn(M.z));
+            md.fnb[(size_t)M.y * 4 + sf] = make_int2(pkn(M.x), FNB_SMALL_LO);
+            md.fnb[(size_t)M.z * 4 + sf] = make_int2(pkn(M.x), FNB_SMALL_HI);
+        }
     }
 }
 

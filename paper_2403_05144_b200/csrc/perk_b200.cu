@@ -322,7 +322,7 @@ static void build_mesh(perk_ctx *c, cudaStream_t s, const uint8_t *lmap)
               nullptr);
     k_face_counts<<<1, 1, 0, s>>>(md, c->segtmp, c->cap_faces);
     k_face_records<<<blocks_for((long long)c->nd * c->cap, 256), 256, 0, s>>>(md, c->items, c->segtmp, R);
-    if (md.fnb) k_face_table<<<blocks_for(c->cap_faces, 256), 256, 0, s>>>(md);   // fused BR1 (Navier-Stokes)
+    if (md.fnb) k_face_table<<<SM_COUNT_B200 * 8, 256, 0, s>>>(md);   // fused BR1 (Navier-Stokes)
     if (dd) {   // a sub-domain keeps its owned elements and the faces with an owned side
         const uint8_t *ow = c->dd_owner;
         partition(c, s, KeyOwnEl{md.mem, ow, ddr}, md.n + 0, 1, c->cap, R, md.list[KIND_EL], nullptr,
