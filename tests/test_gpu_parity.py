@@ -534,3 +534,19 @@ def test_1d_repartition_unsupported():
     with pytest.raises(PerkError) as ei:
         gpu.repartition(w.level_map, U)
     assert ei.value.code == -6
+
+
+def test_capacity_large_overflow_ns_is_clean():
+    """the same for a Navier-Stokes context, whose re-mesh also builds the fused BR1 face table from the
+    (overflowed) face records: a latched PERK_ECAPACITY, no sticky device error"""
+    from paper_2403_05144_b200 import Perk, PerkError
+    w = W.make(5, n_base=64)
+    n0 = W.configs.count_leaves(w)
+    with pytest.raises(PerkError) as ei:
+        Perk(w.problem, w.level_map, w.S, w.E, max_cells=n0 // 4)
+    assert ei.value.code == -3
+    torch.cuda.synchronize()
+    small = W.make(5, n_base=8, steps=2)
+    ora, g2 = build_pair(small)
+    Uo, Ug = _run_both(small, small.steps, ora, g2)
+    assert rel_err_per_var(Ug, Uo).max() <= TOL
