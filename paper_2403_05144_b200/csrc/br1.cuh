@@ -138,9 +138,15 @@ constexpr int G_V1 = 0, G_V2 = 1, G_T = 2, G_Q = 3;     // shared fields: v1, v2
 // thread's 6 end traces into registers one group ahead instead, which frees this buffer: 1.33 vs
 // 1.23 ms/step on cfg 5, slower.)
 constexpr int GST_STRIDE = 4 * GV * NP + 4;
+// staging slots per element: 2 = the state and, for a lazily formed state, K_1 (cp.async one group
+// ahead); 1 = the state only, K_1 of a lazy state read directly (8 KB less shared memory per CTA, so
+// more L1 for the neighbour gathers: cfg 5 gradients 2.046 -> 2.019 ms/step)
+#ifndef GRAD2D_STG
+#define GRAD2D_STG 1
+#endif
 __host__ __device__ constexpr size_t grad2d_smem_bytes()
 {
-    return sizeof(double) * ((size_t)6 * 2 * GRAD2D_LS + VOL2D_EPB * 2 * 64 + (BR1_FUSED ? 0 : VOL2D_EPB * GST_STRIDE));
+    return sizeof(double) * ((size_t)6 * 2 * GRAD2D_LS + VOL2D_EPB * GRAD2D_STG * 64 + (BR1_FUSED ? 0 : VOL2D_EPB * GST_STRIDE));
 }
 #ifndef GRAD2D_MINB
 #define GRAD2D_MINB 4
@@ -155,9 +161,9 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
     constexpr bool FUSED = BR1_FUSED;
     extern __shared__ __align__(16) unsigned char smraw[];
     double (*sm)[2][GRAD2D_LS] = reinterpret_cast<double (*)[2][GRAD2D_LS]>(smraw);
-    double (*stg)[2][64] = reinterpret_cast<double (*)[2][64]>(smraw + sizeof(double) * 6 * 2 * GRAD2D_LS);
+    double (*stg)[GRAD2D_STG][64] = reinterpret_cast<double (*)[GRAD2D_STG][64]>(smraw + sizeof(double) * 6 * 2 * GRAD2D_LS);
     double (*gst)[GST_STRIDE] = reinterpret_cast<double (*)[GST_STRIDE]>(reinterpret_cast<unsigned char *>(stg) +
-                                                                         sizeof(double) * VOL2D_EPB * 2 * 64);
+                                                                         sizeof(double) * VOL2D_EPB * GRAD2D_STG * 64);
     const int t8 = threadIdx.x & 7, le = threadIdx.x >> 3;
     const int lane = threadIdx.x & 31;
     const unsigned gmask = 0xFu << (lane & ~3);      // the 4 lanes of one line direction of one element
@@ -187,7 +193,7 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
         const size_t off = (size_t)pk_elem(pkx) * 64;
         const int srce = state_src(sp, pk_member(pkx));
         copy_chunks(stg[le][0], (srce == SRC_UN || srce == SRC_LAZY ? Un : (srce == SRC_BUF ? Ubuf : Uin)) + off, 32);
-        if (srce == SRC_LAZY) copy_chunks(stg[le][1], K1 + off, 32);
+        if (GRAD2D_STG == 2 && srce == SRC_LAZY) copy_chunks(stg[le][GRAD2D_STG - 1], K1 + off, 32);
     };
     auto issue_gs = [&](int pkx) { copy_chunks(gst[le], Gs + (size_t)pk_elem(pkx) * 4 * GV * NP, 4 * GV * NP / 2); };
     // face-neighbour entries of this thread's two faces (2o: the line's a = N end, 2o + 1: a = 0)
@@ -272,7 +278,8 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
             for (int v = 0; v < 4; ++v) {
                 u[v] = *reinterpret_cast<const double2 *>(&stg[le][0][v * 16 + q0]);
                 if (src == SRC_LAZY) {
-                    const double2 k = *reinterpret_cast<const double2 *>(&stg[le][1][v * 16 + q0]);
+                    const double2 k = GRAD2D_STG == 2 ? *reinterpret_cast<const double2 *>(&stg[le][GRAD2D_STG - 1][v * 16 + q0])
+                                                      : __ldg(reinterpret_cast<const double2 *>(K1 + (size_t)e * 64 + v * 16 + q0));
                     u[v] = make_double2(fma(dtc, k.x, u[v].x), fma(dtc, k.y, u[v].y));
                 }
             }

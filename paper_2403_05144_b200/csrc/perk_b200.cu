@@ -520,6 +520,7 @@ static void launch_sc(perk_ctx *c, cudaStream_t s, const StageParams &sp, const 
     else
         launch_pdl(k_sc_alpha<MODE_RHS>, ga, AMR_T, 0, s, c->md, sp, c->scp, Un, (const double *)c->Ubuf, (const double *)c->K1, Uin, c->alpha_raw, c->alpha);
     if (!c->scp.smooth || (c->sc_fused && !smooth_kernel)) return;   // fused: k_surf2d smooths
+    prof_mark(p, s, 6);                   // the smoothing kernel: its own segment (one launch each)
     const int gs = std::min(blocks_for(c->cap_faces, 256), SM_COUNT_B200 * 8);
     if (sp.mode == MODE_STAGE)
         launch_pdl(k_sc_smooth<MODE_STAGE>, gs, 256, 0, s, c->md, sp, (const double *)c->alpha_raw, c->alpha);
@@ -531,7 +532,7 @@ static void launch_sc(perk_ctx *c, cudaStream_t s, const StageParams &sp, const 
 static void launch_br1(perk_ctx *c, cudaStream_t s, const StageParams &sp, const double *Un, const double *Uin, Prof *p)
 {
     const MeshDev &md = c->md;
-    prof_mark(p, s, 4);
+    if (!BR1_FUSED) prof_mark(p, s, 4);   // (the profile counts one launch per marked segment)
     if (BR1_FUSED || !((c->kind_mask >> 4) & 1u)) {   // fused: k_grad2d forms the central traces itself
     } else if (sp.mode == MODE_STAGE)
         launch_pdl(k_gsurf2d<MODE_STAGE>, c->surf_blocks, 256, 0, s, md, sp, Un, c->Ubuf, c->K1, Uin, c->Gs);
@@ -989,7 +990,8 @@ extern "C" int perk_launches_per_step(perk_ctx *c, int32_t *launches)
 {
     if (!c) return PERK_ENOTINIT;
     if (!launches) return PERK_EINVAL;
-    *launches = c->step1d ? 1 : ((c->ns ? 4 : 2) + (c->sc ? ((c->scp.smooth && !c->sc_fused) ? 2 : 1) : 0)) * c->tab.S;
+    // per stage: surface + volume (+ the BR1 pass(es): k_grad2d, and k_gsurf2d unless fused) (+ shock capturing)
+    *launches = c->step1d ? 1 : ((c->ns ? (BR1_FUSED ? 3 : 4) : 2) + (c->sc ? ((c->scp.smooth && !c->sc_fused) ? 2 : 1) : 0)) * c->tab.S;
     return PERK_OK;
 }
 

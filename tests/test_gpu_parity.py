@@ -550,3 +550,15 @@ def test_capacity_large_overflow_ns_is_clean():
     ora, g2 = build_pair(small)
     Uo, Ug = _run_both(small, small.steps, ora, g2)
     assert rel_err_per_var(Ug, Uo).max() <= TOL
+
+
+@pytest.mark.parametrize("cfg,sc", [(3, False), (5, False), (5, True), (3, True)])
+def test_launches_per_step_matches_profile(cfg, sc):
+    """perk_launches_per_step (bench.py's gpu_launches) equals the kernels one eager profiled step launches"""
+    from paper_2403_05144_b200 import Perk
+    w = W.make(cfg, n_base=8)
+    prob = dict(w.problem, shock_capturing=W.configs.SHOCK_CAPTURING) if sc else w.problem
+    gpu = Perk(prob, w.level_map, w.S, w.E)
+    U = gpu.initial_state(w.ic)
+    _, nl = gpu.profile_step(U, w.dt)
+    assert sum(nl) == gpu.launches_per_step()
