@@ -120,18 +120,30 @@ __global__ void __launch_bounds__(256, 3) k_gsurf2d(MeshDev md, StageParams sp, 
 #ifndef BR1_FUSED
 #define BR1_FUSED 1
 #endif
-// 2/h by a division (1) or by the exact power-of-two scaling of common.cuh two_over_h (0): without the
-// division's call the kernel's allocation exceeds 128 registers and spills (cfg 5 gradients 2.07 vs
-// 2.25 ms/step); the volume kernel uses two_over_h (NS volume 2.375 -> 2.348)
+// 2/h by the exact power-of-two scaling of common.cuh two_over_h (0) or by a division (1).  The division
+// (inline reciprocal iteration + guarded slow-path call, ~25 issued instructions per warp and group in a
+// kernel that is issue-bound) costs cfg 5 gradients 1.89 vs 1.77 ms/step (profiles/r02_ab_grad_l1.json);
+// before GRAD2D_LG freed registers the scaling variant spilled at the 128-register cap (2.25).
 #ifndef VISC_LINE
 #define VISC_LINE 1
 #endif
 #ifndef GRAD2D_DIV
-#define GRAD2D_DIV 1
+#define GRAD2D_DIV 0
 #endif
 static_assert(!BR1_FUSED || BR1_DV, "the fused BR1 gradient kernel leaves no Gs for the volume kernel");
-constexpr int GRAD2D_LS = VOL2D_LS;
-constexpr int G_V1 = 0, G_V2 = 1, G_T = 2, G_Q = 3;     // shared fields: v1, v2, T, gradients (3)
+// shared-memory field layout.  GRAD2D_SX = 16: k_vol2d's (x part 16 le + 4j + i, y part 258 + 20 le + 4i + j);
+// the cross-direction gradient reads (scalar, fixed node a: the y-line threads read 16 le + 4a + ln) then
+// hit the same banks for all four elements of a warp (ncu: 6 instead of 2 wavefronts per load, 22 % of
+// the kernel's shared-memory wavefronts; bank conflicts per stage-30 launch 4.7M -> 1.3M, cfg 5
+// gradients 1.80 -> 1.77 ms/step).  20: both parts with element stride 20 (x part 20 le + 4j + i,
+// y part 318 + 20 le + 4i + j): (4 le + 4a + ln) mod 16 is distinct over the warp's 16 lanes of either
+// direction, the two directions 14 apart; line loads / stores stay conflict-free (4 (le + ln) mod 16).
+#ifndef GRAD2D_SX
+#define GRAD2D_SX 20
+#endif
+constexpr int GRAD2D_LS = GRAD2D_SX == 16 ? VOL2D_LS : 320;
+constexpr int GRAD2D_NF = 5;   // fields: v1, v2, T, d v1, d v2 (the T gradient stays in registers)
+constexpr int G_V1 = 0, G_V2 = 1, G_T = 2, G_Q = 3;     // shared fields: v1, v2, T, velocity gradients (2)
 // staged central traces per element (unfused): 48 doubles padded to 52 (== 4 mod 16), so that the
 // scalar trace reads of the x-line threads (faces 0/1) and y-line threads (faces 2/3) of the two
 // elements of a half-warp fall into disjoint banks (with 48 the two elements collided).  (Loading each
@@ -140,20 +152,45 @@ constexpr int G_V1 = 0, G_V2 = 1, G_T = 2, G_Q = 3;     // shared fields: v1, v2
 constexpr int GST_STRIDE = 4 * GV * NP + 4;
 // staging slots per element: 2 = the state and, for a lazily formed state, K_1 (cp.async one group
 // ahead); 1 = the state only, K_1 of a lazy state read directly (8 KB less shared memory per CTA, so
-// more L1 for the neighbour gathers: cfg 5 gradients 2.046 -> 2.019 ms/step)
+// more L1 for the neighbour gathers: cfg 5 gradients 2.046 -> 2.019 ms/step); 0 (default, fused only) = no
+// staging: the thread's two nodes (and K_1 of a lazy state) are loaded into registers together with the
+// neighbour gathers, whose latency the iteration waits for anyway -- no cp.async address loop, no staging
+// round trip through shared memory (cfg 5 step 6.07 -> 5.99 ms; gradients alone 1.82 -> 1.77)
 #ifndef GRAD2D_STG
-#define GRAD2D_STG 1
+#define GRAD2D_STG 0
 #endif
+static_assert(GRAD2D_STG > 0 || BR1_FUSED, "unstaged state loads are written for the fused kernel");
 __host__ __device__ constexpr size_t grad2d_smem_bytes()
 {
-    return sizeof(double) * ((size_t)6 * 2 * GRAD2D_LS + VOL2D_EPB * GRAD2D_STG * 64 + (BR1_FUSED ? 0 : VOL2D_EPB * GST_STRIDE));
+    return sizeof(double) * ((size_t)GRAD2D_NF * 2 * GRAD2D_LS + VOL2D_EPB * GRAD2D_STG * 64 + (BR1_FUSED ? 0 : VOL2D_EPB * GST_STRIDE));
 }
 #ifndef GRAD2D_MINB
 #define GRAD2D_MINB 4
 #endif
+// the line's own (v1, v2, T) loaded once into registers (ncu: l1tex throughput 92 %, 218 shared-memory
+// wavefronts per warp and group): 1 = its end nodes serve as the own face traces (6 scalar shared loads
+// less per thread), 2 = also the velocities of the viscous flux (cfg 5 gradients 1.81 -> 1.77 ms/step)
+#ifndef GRAD2D_WREG
+#define GRAD2D_WREG 2
+#endif
+// 1 = the whole warp skips the (if-converted) lazy-state K_1 loads when no lane has a lazy state: measured
+// slower than the predicated code (1.94 vs 1.89 ms/step), off
+#ifndef GRAD2D_LAZYVOTE
+#define GRAD2D_LAZYVOTE 0
+#endif
+// 1 = only the x-line threads finalise Dv (half the shared-memory traffic of the x + y sum, idle y-line
+// threads): slower (1.99 vs 1.95 ms/step), off
+#ifndef GRAD2D_DVX
+#define GRAD2D_DVX 0
+#endif
+// 1 = the second small element of a large mortar side is gathered inside the large-side branch (below)
+#ifndef GRAD2D_LG
+#define GRAD2D_LG 1
+#endif
 
+// (the rhs_eval instantiation, off the hot path, takes 3 CTAs per SM: at 4 it spilled 12 B)
 template <int MODE>
-__global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StageParams sp, const double *__restrict__ Un,
+__global__ void __launch_bounds__(128, MODE == MODE_RHS ? 3 : GRAD2D_MINB) k_grad2d(MeshDev md, StageParams sp, const double *__restrict__ Un,
                                                    const double *__restrict__ Ubuf, const double *__restrict__ K1,
                                                    const double *__restrict__ Uin, const double *__restrict__ Gs,
                                                    double *__restrict__ Vt, double *__restrict__ Dv)
@@ -161,7 +198,7 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
     constexpr bool FUSED = BR1_FUSED;
     extern __shared__ __align__(16) unsigned char smraw[];
     double (*sm)[2][GRAD2D_LS] = reinterpret_cast<double (*)[2][GRAD2D_LS]>(smraw);
-    double (*stg)[GRAD2D_STG][64] = reinterpret_cast<double (*)[GRAD2D_STG][64]>(smraw + sizeof(double) * 6 * 2 * GRAD2D_LS);
+    double (*stg)[GRAD2D_STG ? GRAD2D_STG : 1][64] = reinterpret_cast<double (*)[GRAD2D_STG ? GRAD2D_STG : 1][64]>(smraw + sizeof(double) * GRAD2D_NF * 2 * GRAD2D_LS);
     double (*gst)[GST_STRIDE] = reinterpret_cast<double (*)[GST_STRIDE]>(reinterpret_cast<unsigned char *>(stg) +
                                                                          sizeof(double) * VOL2D_EPB * GRAD2D_STG * 64);
     const int t8 = threadIdx.x & 7, le = threadIdx.x >> 3;
@@ -177,12 +214,12 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
     const StateBufs sb{Un, Ubuf, K1, Uin};
     const int q0 = 2 * t8;
     const int o = t8 >> 2, ln = t8 & 3;
-    const int eox = le * 16, eoy = le * 20, yo = 2 - 2 * VOL2D_EPB;   // field layout as in k_vol2d
+    const int eox = le * GRAD2D_SX, eoy = le * 20, yo = GRAD2D_SX == 16 ? 2 - 2 * VOL2D_EPB : -2;
     const int stride = gridDim.x * VOL2D_EPB;
     int base = blockIdx.x * VOL2D_EPB;
     auto entry_at = [&](int b) {
         const int t = b + le;
-        const int tt = t < n_act ? t : b;
+        const int tt = sweep_idx(sp, t < n_act ? t : b, n_act);
         if (MODE == MODE_STAGE) return tt < n_el_a ? md.elpk[tt] : md.hpk[hel.x + tt - n_el_a];
         return tt | ((int)md.mem[tt] << PK_EBITS) | ((int)md.lev[tt] << (PK_EBITS + 3));
     };
@@ -190,10 +227,11 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
         for (int c = t8; c < nchunks; c += 8) cp_async16(dst + 2 * c, src + 2 * c);
     };
     auto issue_state = [&](int pkx) {
+        if (GRAD2D_STG == 0) return;
         const size_t off = (size_t)pk_elem(pkx) * 64;
         const int srce = state_src(sp, pk_member(pkx));
         copy_chunks(stg[le][0], (srce == SRC_UN || srce == SRC_LAZY ? Un : (srce == SRC_BUF ? Ubuf : Uin)) + off, 32);
-        if (GRAD2D_STG == 2 && srce == SRC_LAZY) copy_chunks(stg[le][GRAD2D_STG - 1], K1 + off, 32);
+        if (GRAD2D_STG == 2 && srce == SRC_LAZY) copy_chunks(stg[le][GRAD2D_STG ? GRAD2D_STG - 1 : 0], K1 + off, 32);
     };
     auto issue_gs = [&](int pkx) { copy_chunks(gst[le], Gs + (size_t)pk_elem(pkx) * 4 * GV * NP, 4 * GV * NP / 2); };
     // face-neighbour entries of this thread's two faces (2o: the line's a = N end, 2o + 1: a = 0)
@@ -234,51 +272,84 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
         // group's neighbour traces prefetched into L2 / L1 after the gradients, 2.42; 3 CTAs/SM, 2.19;
         // the next group's first-neighbour traces loaded into registers after this group's phase 1
         // (entries three groups ahead, 3 CTAs/SM for the registers), 2.14 vs 2.07)
+#if GRAD2D_LG
+        // the second small element of a large mortar side (rare: 1-2 % of the elements have such a face) is
+        // gathered inside the large-side branch below, not here: 16 registers less at the top
+        double un[2][1][4];
+        constexpr int NH = 1;
+#else
         double un[2][2][4];
+        constexpr int NH = 2;
+#endif
         if (FUSED) {
-            int xe[2][2], xs[2][2];
+            int xe[2][NH], xs[2][NH];
 #pragma unroll
             for (int f = 0; f < 2; ++f) {
                 const int p0 = fn[f].x >= 0 ? fn[f].x : pk;
-                const int p1 = fn[f].y >= 0 ? fn[f].y : p0;
                 xe[f][0] = pk_elem(p0);
-                xe[f][1] = pk_elem(p1);
                 xs[f][0] = state_src(sp, pk_member(p0));
-                xs[f][1] = state_src(sp, pk_member(p1));
+                if (NH == 2) {
+                    const int p1 = fn[f].y >= 0 ? fn[f].y : p0;
+                    xe[f][NH - 1] = pk_elem(p1);
+                    xs[f][NH - 1] = state_src(sp, pk_member(p1));
+                }
             }
 #pragma unroll
             for (int f = 0; f < 2; ++f)
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < NH; ++h) {
                     if (h == 1 && fn[f].y < 0) continue;
                     const double *P = state_base(sb, xs[f][h]) + (size_t)xe[f][h] * 64 + face_node2d((2 * o + f) ^ 1, ln);
 #pragma unroll
                     for (int v = 0; v < 4; ++v) un[f][h][v] = __ldg(P + v * 16);
                 }
+            // lazily formed neighbour states: skipped by the whole warp when none of its lanes has one (the
+            // if-converted K_1 loads and FMAs were ~9 % of the kernel's issued instructions at the stages
+            // where no state is lazy); the warp is converged here
+            bool nlazy = false;
 #pragma unroll
             for (int f = 0; f < 2; ++f)
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    if ((h == 1 && fn[f].y < 0) || xs[f][h] != SRC_LAZY) continue;
-                    const double *P = K1 + (size_t)xe[f][h] * 64 + face_node2d((2 * o + f) ^ 1, ln);
-                    double kk[4];
+                for (int h = 0; h < NH; ++h) nlazy |= !(h == 1 && fn[f].y < 0) && xs[f][h] == SRC_LAZY;
+            if (!GRAD2D_LAZYVOTE || __any_sync(0xffffffffu, nlazy)) {
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) kk[v] = __ldg(P + v * 16);
+                for (int f = 0; f < 2; ++f)
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) un[f][h][v] = fma(dtc, kk[v], un[f][h][v]);
-                }
+                    for (int h = 0; h < NH; ++h) {
+                        if ((h == 1 && fn[f].y < 0) || xs[f][h] != SRC_LAZY) continue;
+                        const double *P = K1 + (size_t)xe[f][h] * 64 + face_node2d((2 * o + f) ^ 1, ln);
+                        double kk[4];
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) kk[v] = __ldg(P + v * 16);
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) un[f][h][v] = fma(dtc, kk[v], un[f][h][v]);
+                    }
+            }
+        }
+        double2 u[4];
+        const bool olazy_any = !GRAD2D_LAZYVOTE || __any_sync(0xffffffffu, src == SRC_LAZY);
+        if (GRAD2D_STG == 0) {   // the element's own two nodes, issued with the neighbour gathers
+            const double *Ps = state_base(sb, src) + (size_t)e * 64 + q0;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) u[v] = __ldg(reinterpret_cast<const double2 *>(Ps + v * 16));
+            if (olazy_any && src == SRC_LAZY) {
+                double2 k[4];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) k[v] = __ldg(reinterpret_cast<const double2 *>(K1 + (size_t)e * 64 + v * 16 + q0));
+#pragma unroll
+                for (int v = 0; v < 4; ++v) u[v] = make_double2(fma(dtc, k[v].x, u[v].x), fma(dtc, k[v].y, u[v].y));
+            }
         }
         PERK_JITTER(11);
         cp_async_wait<0>();
         __syncwarp();
         PERK_JITTER(12);
         {
-            double2 u[4];
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
-                u[v] = *reinterpret_cast<const double2 *>(&stg[le][0][v * 16 + q0]);
-                if (src == SRC_LAZY) {
-                    const double2 k = GRAD2D_STG == 2 ? *reinterpret_cast<const double2 *>(&stg[le][GRAD2D_STG - 1][v * 16 + q0])
+                if (GRAD2D_STG) u[v] = *reinterpret_cast<const double2 *>(&stg[le][0][v * 16 + q0]);
+                if (GRAD2D_STG && olazy_any && src == SRC_LAZY) {
+                    const double2 k = GRAD2D_STG == 2 ? *reinterpret_cast<const double2 *>(&stg[le][GRAD2D_STG ? GRAD2D_STG - 1 : 0][v * 16 + q0])
                                                       : __ldg(reinterpret_cast<const double2 *>(K1 + (size_t)e * 64 + v * 16 + q0));
                     u[v] = make_double2(fma(dtc, k.x, u[v].x), fma(dtc, k.y, u[v].y));
                 }
@@ -305,6 +376,15 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
         double q[GV][NP];
         const int fld[GV] = {G_V1, G_V2, G_T};
         const double sc[GV] = {1.0, 1.0, 1.0};
+#if GRAD2D_WREG
+        double wl[GV][NP];   // the line's own (v1, v2, T): its end nodes are the own face traces
+#pragma unroll
+        for (int c = 0; c < GV; ++c) {
+            const double2 w01 = *reinterpret_cast<const double2 *>(&sm[G_V1 + c][o][lo]);
+            const double2 w23 = *reinterpret_cast<const double2 *>(&sm[G_V1 + c][o][lo + 2]);
+            wl[c][0] = w01.x; wl[c][1] = w01.y; wl[c][2] = w23.x; wl[c][3] = w23.y;
+        }
+#endif
         if (FUSED) {
             // central traces w* at this thread's nodes of faces 2o (g[0]) and 2o + 1 (g[1])
             double g[2][GV];
@@ -313,7 +393,13 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
                 const int a = f == 0 ? NP - 1 : 0;
                 double wo[GV], wn[GV];
 #pragma unroll
-                for (int c = 0; c < GV; ++c) wo[c] = sm[G_V1 + c][o][lo + a];
+                for (int c = 0; c < GV; ++c) {
+#if GRAD2D_WREG
+                    wo[c] = wl[c][a];
+#else
+                    wo[c] = sm[G_V1 + c][o][lo + a];
+#endif
+                }
                 prim_vT(un[f][0], gm1, wn);
                 const int ty = fn[f].y;
                 if (ty == FNB_CONF) {
@@ -332,7 +418,15 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
                     }
                 } else if (ty >= 0) {                                     // large side: wn, wn1 the smalls
                     double wn1[GV];
+#if GRAD2D_LG
+                    {
+                        double u1[4];
+                        trace2d(sb, state_src(sp, pk_member(ty)), dtc, pk_elem(ty), (2 * o + f) ^ 1, ln, u1);
+                        prim_vT(u1, gm1, wn1);
+                    }
+#else
                     prim_vT(un[f][1], gm1, wn1);
+#endif
 #pragma unroll
                     for (int c = 0; c < GV; ++c) {
                         double il = 0.0, ih = 0.0;
@@ -356,12 +450,17 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
                     for (int c = 0; c < GV; ++c) g[f][c] = wo[c];
                 }
             }
+#if GRAD2D_WREG
+            line_gradient_w(wl, g[0], g[1], j2h, q);
+#else
             line_gradient_g<GRAD2D_LS>(sm, o, lo, g[0], g[1], j2h, fld, q);
+#endif
         } else {
             line_gradient<GRAD2D_LS>(sm, o, lo, ln, gst[le], j2h, fld, sc, q);
         }
 #pragma unroll
-        for (int c = 0; c < GV; ++c) {   // the line is contiguous and 16 B aligned: two 16 B stores
+        for (int c = 0; c < 2; ++c) {    // the line is contiguous and 16 B aligned: two 16 B stores; only the
+                                         // velocity gradients cross directions (the flux takes T's along its line)
             *reinterpret_cast<double2 *>(&sm[G_Q + c][o][lo]) = make_double2(q[c][0], q[c][1]);
             *reinterpret_cast<double2 *>(&sm[G_Q + c][o][lo + 2]) = make_double2(q[c][2], q[c][3]);
         }
@@ -386,9 +485,13 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
 #pragma unroll
                 for (int c = 0; c < GV; ++c) {
                     qs[c] = q[c][a];
-                    qo[c] = sm[G_Q + c][1 - o][oi];
+                    qo[c] = c < 2 ? sm[G_Q + c][1 - o][oi] : 0.0;   // T's cross gradient is not used
                 }
+#if GRAD2D_WREG == 2
+                const double v1 = wl[0][a], v2 = wl[1][a];
+#else
                 const double v1 = sm[G_V1][o][lo + a], v2 = sm[G_V2][o][lo + a];
+#endif
 #if VISC_LINE
                 visc_flux2d_line(o, v1, v2, qs, qo, md.mu, md.kappa, fv);
 #else
@@ -398,7 +501,7 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
                 if (valid && (a == 0 || a == NP - 1)) {
                     const int face = 2 * o + (a == NP - 1 ? 0 : 1);   // a = N: +o face, a = 0: -o face
 #pragma unroll
-                    for (int c = 0; c < GV; ++c) Vt[gidx2d(e, face, c, ln)] = fv[c];
+                    for (int c = 0; c < GV; ++c) Vt[vidx2d(e, face, c, ln)] = fv[c];
                 }
 #pragma unroll
                 for (int i = 0; i < NP; ++i)
@@ -407,6 +510,32 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
             }
             PERK_JITTER(15);
             __syncwarp();
+#if GRAD2D_DVX
+            // the y-line threads hand their sums over in the y layout; the x-line threads add their own
+            // (x + y, as before) and write their line's 4 nodes (half the shared-memory traffic of both
+            // directions storing and every thread summing two nodes)
+            if (o == 1) {
+#pragma unroll
+                for (int c = 0; c < GV; ++c) {
+                    *reinterpret_cast<double2 *>(&sm[G_V1 + c][1][lo]) = make_double2(dv[0][c], dv[1][c]);
+                    *reinterpret_cast<double2 *>(&sm[G_V1 + c][1][lo + 2]) = make_double2(dv[2][c], dv[3][c]);
+                }
+            }
+            PERK_JITTER(16);
+            __syncwarp();
+            if (o == 0 && valid && sweep_idx(sp, base + le, n_act) < n_el_a) {   // halo elements (their member is inactive) need no Dv
+                const double J = -j2h;
+#pragma unroll
+                for (int c = 0; c < GV; ++c) {
+                    double s4[NP];
+#pragma unroll
+                    for (int a = 0; a < NP; ++a) s4[a] = J * (dv[a][c] + sm[G_V1 + c][1][yo + eoy + 4 * a + ln]);
+                    double *D = Dv + (size_t)e * (GV * 16) + c * 16 + 4 * ln;
+                    *reinterpret_cast<double2 *>(D) = make_double2(s4[0], s4[1]);
+                    *reinterpret_cast<double2 *>(D + 2) = make_double2(s4[2], s4[3]);
+                }
+            }
+#else
 #pragma unroll
             for (int c = 0; c < GV; ++c) {
                 *reinterpret_cast<double2 *>(&sm[G_V1 + c][o][lo]) = make_double2(dv[0][c], dv[1][c]);
@@ -414,7 +543,7 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
             }
             PERK_JITTER(16);
             __syncwarp();
-            if (valid && base + le < n_el_a) {   // halo elements (their member is inactive) need no Dv
+            if (valid && sweep_idx(sp, base + le, n_act) < n_el_a) {   // halo elements (their member is inactive) need no Dv
                 const int i0 = q0 & 3, j0 = q0 >> 2;
                 const double J = -j2h;
 #pragma unroll
@@ -425,6 +554,7 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
                     *reinterpret_cast<double2 *>(Dv + (size_t)e * (GV * 16) + c * 16 + q0) = make_double2(J * s0, J * s1);
                 }
             }
+#endif
         } else if (valid) {
 #pragma unroll
             for (int end = 0; end < 2; ++end) {
@@ -434,7 +564,7 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
 #pragma unroll
                 for (int c = 0; c < GV; ++c) {
                     qs[c] = q[c][a];
-                    qo[c] = sm[G_Q + c][1 - o][oi];
+                    qo[c] = c < 2 ? sm[G_Q + c][1 - o][oi] : 0.0;   // T's cross gradient is not used
                 }
                 const double v1 = sm[G_V1][o][lo + a], v2 = sm[G_V2][o][lo + a];
 #if VISC_LINE
@@ -445,7 +575,7 @@ __global__ void __launch_bounds__(128, GRAD2D_MINB) k_grad2d(MeshDev md, StagePa
 #endif
                 const int face = 2 * o + (end ? 0 : 1);      // a = N: +o face, a = 0: -o face
 #pragma unroll
-                for (int c = 0; c < GV; ++c) Vt[gidx2d(e, face, c, ln)] = fv[c];
+                for (int c = 0; c < GV; ++c) Vt[vidx2d(e, face, c, ln)] = fv[c];
             }
         }
         __syncwarp();

@@ -152,7 +152,12 @@ struct StageParams {
     int wmode;                   // ... written by the stage S-1 epilogue when wmode = 1 (P-ERK3)
     int fin_k1;                  // stage S with b_1 != 0 and b_{S-1} = 0 (Heun / Ralston weights, P:l.439-442):
                                  // U_{n+1} = U_n + dt (b_1 K_1 + b_S K_S), no W buffer
+    int rev;                     // 1: this launch walks its lists from the end (the stage kernels of a step
+                                 // alternate direction, so a launch starts on the data its predecessor
+                                 // touched last, which is what the L2 still holds; results do not depend on it)
 };
+// list position of the t-th item of a launch over n items
+__device__ __forceinline__ int sweep_idx(const StageParams &sp, int t, int n) { return sp.rev ? n - 1 - t : t; }
 
 // Subcell shock capturing parameters (sc.cuh, k_vol2d<., ., true>)
 struct ScParams {

@@ -185,7 +185,17 @@ __device__ __forceinline__ void visc_flux2d_line(int o, double v1, double v2, co
 
 // BR1 face arrays Gs (central w*), Vt (normal viscous flux trace): [cell][face][GV][k]
 __device__ __forceinline__ size_t gidx2d(int e, int face, int c, int k) { return (((size_t)e * 4 + face) * GV + c) * NP + k; }
-
+// Vt with VT_CF = 1: [cell][GV][face][k] -- a component's four face traces share one 128 B line, so a
+// warp-wide trace store of k_grad2d (fixed c and line end; the x- and y-line threads of an element write
+// faces {0, 2} or {1, 3}) touches one line per element instead of two.  Time-neutral on cfg 5 (gradients
+// 1.989 vs 1.992 ms/step); kept because k_grad2d's allocation then fits its 128 registers without a spill.
+#ifndef VT_CF
+#define VT_CF 1
+#endif
+__device__ __forceinline__ size_t vidx2d(int e, int face, int c, int k)
+{
+    return VT_CF ? (((size_t)e * GV + c) * 4 + face) * NP + k : gidx2d(e, face, c, k);
+}
 // ---------------------------------------------------------------------------------------------
 // surface kernel
 // ---------------------------------------------------------------------------------------------
@@ -263,8 +273,8 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
     // records into L1 before the dependency wait: cfg 3 surface 0.1847 -> 0.1854 / 0.1838 ms/step, noise)
     for (; gt + GS < nI; gt += 2 * GS) {
         const int ka = gt & 3, kb = (gt + GS) & 3;
-        const int4 Ia = IR[gt >> 2];
-        const int4 Ib = IR[(gt + GS) >> 2];
+        const int4 Ia = IR[sweep_idx(sp, gt >> 2, nif)];
+        const int4 Ib = IR[sweep_idx(sp, (gt + GS) >> 2, nif)];
         PERK_DASSERT(Ia.x >= 0 && Ia.x < md.n[0] && Ia.y >= 0 && Ia.y < md.n[0] && Ib.x >= 0 && Ib.x < md.n[0] &&
                      Ib.y >= 0 && Ib.y < md.n[0]);
         const int srca = state_src(sp, Ia.w), srcb = state_src(sp, Ib.w);
@@ -278,8 +288,8 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
         if (NS) {
 #pragma unroll
             for (int c = 0; c < GV; ++c) {
-                fa[1 + c] -= 0.5 * (__ldg(Vt + gidx2d(Ia.x, 2 * Ia.z, c, ka)) + __ldg(Vt + gidx2d(Ia.y, 2 * Ia.z + 1, c, ka)));
-                fb[1 + c] -= 0.5 * (__ldg(Vt + gidx2d(Ib.x, 2 * Ib.z, c, kb)) + __ldg(Vt + gidx2d(Ib.y, 2 * Ib.z + 1, c, kb)));
+                fa[1 + c] -= 0.5 * (__ldg(Vt + vidx2d(Ia.x, 2 * Ia.z, c, ka)) + __ldg(Vt + vidx2d(Ia.y, 2 * Ia.z + 1, c, ka)));
+                fb[1 + c] -= 0.5 * (__ldg(Vt + vidx2d(Ib.x, 2 * Ib.z, c, kb)) + __ldg(Vt + vidx2d(Ib.y, 2 * Ib.z + 1, c, kb)));
             }
         }
         store_face2d(Fs, Ia.x, 2 * Ia.z, ka, fa);
@@ -290,7 +300,7 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
     for (; gt < total; gt += GS) {
         const int item = gt >> 2, k = gt & 3;
         if (item < nif) {
-            const int4 I = MODE == MODE_STAGE ? md.ifcs[item] : md.ifc[item];
+            const int4 I = IR[sweep_idx(sp, item, nif)];
             PERK_DASSERT(I.x >= 0 && I.x < md.n[0] && I.y >= 0 && I.y < md.n[0]);
             const int o = I.z;
             const int src = state_src(sp, I.w);    // conforming: both sides share the member
@@ -302,12 +312,12 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
             if (NS) {
 #pragma unroll
                 for (int c = 0; c < GV; ++c)
-                    fl[1 + c] -= 0.5 * (__ldg(Vt + gidx2d(I.x, 2 * o, c, k)) + __ldg(Vt + gidx2d(I.y, 2 * o + 1, c, k)));
+                    fl[1 + c] -= 0.5 * (__ldg(Vt + vidx2d(I.x, 2 * o, c, k)) + __ldg(Vt + vidx2d(I.y, 2 * o + 1, c, k)));
             }
             store_face2d(Fs, I.x, 2 * o, k, fl);
             store_face2d(Fs, I.y, 2 * o + 1, k, fl);
         } else if (item < nif + nmo) {
-            const int q = item - nif;
+            const int q = sweep_idx(sp, item - nif, nmo);
             const int4 M = MODE == MODE_STAGE ? md.mors[q] : md.mor[q];
             PERK_DASSERT(M.x >= 0 && M.x < md.n[0] && M.y >= 0 && M.y < md.n[0] && M.z >= 0 && M.z < md.n[0]);
             const int o = M.w & 1, side = (M.w >> 1) & 1, mfine = M.w >> 8;
@@ -343,7 +353,7 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
             if (NS) {   // central viscous flux on each half: (P F^v_large + F^v_small) / 2
                 double vl[GV];
 #pragma unroll
-                for (int c = 0; c < GV; ++c) vl[c] = __ldg(Vt + gidx2d(M.x, lf, c, k));
+                for (int c = 0; c < GV; ++c) vl[c] = __ldg(Vt + vidx2d(M.x, lf, c, k));
 #pragma unroll
                 for (int c = 0; c < GV; ++c) {
                     double il = 0.0, ih = 0.0;
@@ -353,8 +363,8 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
                         il = fma(cB.Plo[k][j], vj, il);
                         ih = fma(cB.Pup[k][j], vj, ih);
                     }
-                    flo[1 + c] -= 0.5 * (il + __ldg(Vt + gidx2d(M.y, sf, c, k)));
-                    fhi[1 + c] -= 0.5 * (ih + __ldg(Vt + gidx2d(M.z, sf, c, k)));
+                    flo[1 + c] -= 0.5 * (il + __ldg(Vt + vidx2d(M.y, sf, c, k)));
+                    fhi[1 + c] -= 0.5 * (ih + __ldg(Vt + vidx2d(M.z, sf, c, k)));
                 }
             }
             store_face2d(Fs, M.y, sf, k, flo);
@@ -489,6 +499,25 @@ __device__ __forceinline__ void line_gradient_g(const double (*sm)[2][LS], int o
             double t = 0.0;
 #pragma unroll
             for (int k = 0; k < NP; ++k) t = fma(-cB.Dhat[a][k], w[k], t);
+            if (a == NP - 1) t = fma(ghi[c], cB.invw[NP - 1], t);
+            if (a == 0) t = fma(-glo[c], cB.invw[0], t);
+            q[c][a] = Jq * t;
+        }
+    }
+    PERK_JITTER(8);
+}
+
+// the same with the line's values in registers
+__device__ __forceinline__ void line_gradient_w(const double w[GV][NP], const double ghi[GV], const double glo[GV],
+                                                double Jq, double q[GV][NP])
+{
+#pragma unroll
+    for (int c = 0; c < GV; ++c) {
+#pragma unroll
+        for (int a = 0; a < NP; ++a) {
+            double t = 0.0;
+#pragma unroll
+            for (int k = 0; k < NP; ++k) t = fma(-cB.Dhat[a][k], w[c][k], t);
             if (a == NP - 1) t = fma(ghi[c], cB.invw[NP - 1], t);
             if (a == 0) t = fma(-glo[c], cB.invw[0], t);
             q[c][a] = Jq * t;
@@ -685,7 +714,7 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
     }
     // prologue before the dependency wait: indices only (lists are rebuilt by the mesh pipeline,
     // which completed before the step started)
-    const int pk0 = base < n_act ? (MODE == MODE_STAGE ? md.elpk[base + le < n_act ? base + le : base] : 0) : 0;
+    const int pk0 = base < n_act ? (MODE == MODE_STAGE ? md.elpk[sweep_idx(sp, base + le < n_act ? base + le : base, n_act)] : 0) : 0;
     pdl_wait();
     if (MODE == MODE_STAGE && sp.stage == sp.S && blockIdx.x == 0 && threadIdx.x == 0) {
         atomicAdd(md.evals, md.evals[2]);           // sum_r E_r N_C(r), set by the mesh pipeline
@@ -696,7 +725,7 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
     // packed entry (element | member | level) of this thread's slot in the group starting at b
     auto entry_at = [&](int b) {
         const int t = b + le;
-        const int tt = t < n_act ? t : b;
+        const int tt = sweep_idx(sp, t < n_act ? t : b, n_act);
         if (MODE == MODE_STAGE) return md.elpk[tt];
         return tt | ((int)md.mem[tt] << PK_EBITS) | ((int)md.lev[tt] << (PK_EBITS + 3));
     };

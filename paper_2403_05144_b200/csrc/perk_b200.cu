@@ -74,6 +74,7 @@ struct perk_ctx {
     uint8_t *amr_map[2] = {nullptr, nullptr};
     int *amr_flags = nullptr;                            // balance: iteration k changed a cell
     int vol_blocks = 0, vol_blocks_sc = 0, surf_blocks = 0, grad_blocks = 0;
+    int sweep = 1;               // alternate the list direction of consecutive stage kernels (PERK_SWEEP=0: off)
     unsigned kind_mask = ~0u;              // kernel kinds launch_step issues (perk_time_kernels)
     bool step1d = false;                   // small 1D mesh: whole step in one single-CTA launch
     StepTab1D *tb1d = nullptr;
@@ -557,14 +558,22 @@ static void launch_step(perk_ctx *c, cudaStream_t s, double *U, double dt, Prof 
         prof_mark(p, s, -1);
         return;
     }
+    // alternating sweep direction (StageParams::rev): every gradient / surface / volume launch of the step
+    // walks its lists opposite to the launch before it, so it starts where the L2 is still warm
+    // (graphs restricted to one kernel kind -- perk_time_kernels -- keep every launch forward: consecutive
+    // launches of one kind re-read the same arrays, and sweeping them back and forth would show a reuse
+    // the step does not have)
+    int k = 0;
+    const bool sweep = c->sweep && (c->kind_mask & 3u) == 3u;
+    auto dir = [&](StageParams sp) { sp.rev = sweep ? (k++ & 1) : 0; return sp; };
     for (int i = 1; i <= c->tab.S; ++i) {
         const StageParams sp = stage_params(c, i, dt, MODE_STAGE, 0u);
         if (c->sc) launch_sc(c, s, sp, U, nullptr, p);
-        if (c->ns) launch_br1(c, s, sp, U, nullptr, p);
+        if (c->ns) launch_br1(c, s, dir(sp), U, nullptr, p);
         prof_mark(p, s, 0);
-        if ((c->kind_mask >> 0) & 1u) launch_surface(c, s, sp, U, nullptr);
+        if ((c->kind_mask >> 0) & 1u) launch_surface(c, s, dir(sp), U, nullptr);
         prof_mark(p, s, 1);
-        if ((c->kind_mask >> 1) & 1u) launch_volume(c, s, sp, U, nullptr, nullptr);
+        if ((c->kind_mask >> 1) & 1u) launch_volume(c, s, dir(sp), U, nullptr, nullptr);
         prof_mark(p, s, -1);
     }
 }
@@ -851,6 +860,7 @@ extern "C" int perk_init_dd(perk_ctx **out, const perk_problem *prob, const uint
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occf, k_surf2d<MODE_STAGE, false>, 256, 0));
         c->surf_blocks = std::min(blocks_for(4ll * c->cap_faces, 256), SM_COUNT_B200 * std::max(occf, 1));
         c->surf_blocks = cap_env("PERK_SURF_BLOCKS", c->surf_blocks);
+        if (const char *e = std::getenv("PERK_SWEEP")) c->sweep = std::atoi(e) != 0;
         // re-mesh (transfer double buffer, old-mesh copy) and AMR scratch, allocated up front so that
         // no cudaMalloc / memset lands inside a timed re-mesh
         CU(dalloc(c, &c->Utmp, (size_t)c->cap * c->nv * c->npe));
