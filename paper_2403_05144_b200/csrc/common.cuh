@@ -330,6 +330,51 @@ __device__ __forceinline__ void cp_async16(void *dst, const void *src)
 {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+// L2 eviction hints for data that is dead once this launch has read it (face fluxes, the viscous volume
+// term, the viscous-flux traces; U_n and K_1, whose next reader is several launches away): with the
+// alternating sweep (StageParams::rev) what the next launch finds in the L2 is what its predecessor left
+// there, so dead lines are offered for eviction first.  L2_HINTS = 0: plain loads; 1: Fs and Dv; 2: also U_n and
+// K_1 (cfg 3, whose working set is about the size of the L2: 0.5407 / 0.5386 / 0.5243 ms per step; cfg 5:
+// 5.873 / 5.861 / 5.859; profiles/r02_ab_l2_hints2.json).
+#ifndef L2_HINTS
+#define L2_HINTS 2
+#endif
+__device__ __forceinline__ unsigned long long l2_evict_first_policy()
+{
+    unsigned long long p = 0;
+#if L2_HINTS
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+#endif
+    return p;
+}
+__device__ __forceinline__ void cp_async16_dead(void *dst, const void *src, unsigned long long pol)
+{
+#if L2_HINTS
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "l"(pol) : "memory");
+#else
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+#endif
+}
+__device__ __forceinline__ double2 ldg2_dead(const double2 *p, unsigned long long pol)
+{
+#if L2_HINTS
+    double2 r;
+    asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(pol));
+    return r;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ double ldg_dead(const double *p, unsigned long long pol)
+{
+#if L2_HINTS
+    double r;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+    return r;
+#else
+    return __ldg(p);
+#endif
+}
 __device__ __forceinline__ void cp_async8(void *dst, const void *src)
 {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");

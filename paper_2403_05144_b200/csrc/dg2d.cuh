@@ -266,6 +266,11 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
     const int nI = 4 * nif;
     int gt = blockIdx.x * blockDim.x + threadIdx.x;
     const int4 *__restrict__ IR = MODE == MODE_STAGE ? md.ifcs : md.ifc;
+#ifndef L2_HINTS_SURF
+#define L2_HINTS_SURF 0     // (the policy operand pushes the Navier-Stokes instantiation over its 80 registers)
+#endif
+    const unsigned long long pol_dead = NS && L2_HINTS_SURF ? l2_evict_first_policy() : 0ull;   // Vt is dead after this launch
+    auto ldg_vt = [&](const double *p) { return L2_HINTS_SURF ? ldg_dead(p, pol_dead) : __ldg(p); };
     pdl_wait();
     // two interface face nodes per iteration while both are interfaces: twice the loads in flight
     // per thread (the kernel is bound by the latency of the record -> trace gathers).  (Tried: the next
@@ -288,8 +293,8 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
         if (NS) {
 #pragma unroll
             for (int c = 0; c < GV; ++c) {
-                fa[1 + c] -= 0.5 * (__ldg(Vt + vidx2d(Ia.x, 2 * Ia.z, c, ka)) + __ldg(Vt + vidx2d(Ia.y, 2 * Ia.z + 1, c, ka)));
-                fb[1 + c] -= 0.5 * (__ldg(Vt + vidx2d(Ib.x, 2 * Ib.z, c, kb)) + __ldg(Vt + vidx2d(Ib.y, 2 * Ib.z + 1, c, kb)));
+                fa[1 + c] -= 0.5 * (ldg_vt(Vt + vidx2d(Ia.x, 2 * Ia.z, c, ka)) + ldg_vt(Vt + vidx2d(Ia.y, 2 * Ia.z + 1, c, ka)));
+                fb[1 + c] -= 0.5 * (ldg_vt(Vt + vidx2d(Ib.x, 2 * Ib.z, c, kb)) + ldg_vt(Vt + vidx2d(Ib.y, 2 * Ib.z + 1, c, kb)));
             }
         }
         store_face2d(Fs, Ia.x, 2 * Ia.z, ka, fa);
@@ -312,7 +317,7 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
             if (NS) {
 #pragma unroll
                 for (int c = 0; c < GV; ++c)
-                    fl[1 + c] -= 0.5 * (__ldg(Vt + vidx2d(I.x, 2 * o, c, k)) + __ldg(Vt + vidx2d(I.y, 2 * o + 1, c, k)));
+                    fl[1 + c] -= 0.5 * (ldg_vt(Vt + vidx2d(I.x, 2 * o, c, k)) + ldg_vt(Vt + vidx2d(I.y, 2 * o + 1, c, k)));
             }
             store_face2d(Fs, I.x, 2 * o, k, fl);
             store_face2d(Fs, I.y, 2 * o + 1, k, fl);
@@ -353,7 +358,7 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
             if (NS) {   // central viscous flux on each half: (P F^v_large + F^v_small) / 2
                 double vl[GV];
 #pragma unroll
-                for (int c = 0; c < GV; ++c) vl[c] = __ldg(Vt + vidx2d(M.x, lf, c, k));
+                for (int c = 0; c < GV; ++c) vl[c] = ldg_vt(Vt + vidx2d(M.x, lf, c, k));
 #pragma unroll
                 for (int c = 0; c < GV; ++c) {
                     double il = 0.0, ih = 0.0;
@@ -363,8 +368,8 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
                         il = fma(cB.Plo[k][j], vj, il);
                         ih = fma(cB.Pup[k][j], vj, ih);
                     }
-                    flo[1 + c] -= 0.5 * (il + __ldg(Vt + vidx2d(M.y, sf, c, k)));
-                    fhi[1 + c] -= 0.5 * (ih + __ldg(Vt + vidx2d(M.z, sf, c, k)));
+                    flo[1 + c] -= 0.5 * (il + ldg_vt(Vt + vidx2d(M.y, sf, c, k)));
+                    fhi[1 + c] -= 0.5 * (ih + ldg_vt(Vt + vidx2d(M.z, sf, c, k)));
                 }
             }
             store_face2d(Fs, M.y, sf, k, flo);
@@ -734,6 +739,17 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
 #pragma unroll
         for (int r = 0; r < 4; ++r) cp_async16(dst + 2 * (t8 + 8 * r), src + 2 * (t8 + 8 * r));
     };
+    const unsigned long long pol_dead = l2_evict_first_policy();   // Fs, Dv, U_n, K_1: not read again soon
+    auto copy_block_dead = [&](double *dst, const double *src) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) cp_async16_dead(dst + 2 * (t8 + 8 * r), src + 2 * (t8 + 8 * r), pol_dead);
+    };
+    // U_n and K_1 come back at the next stage (L2_HINTS = 2 marks them too)
+    auto copy_block_far = [&](double *dst, const double *src) {
+        if (L2_HINTS >= 2) copy_block_dead(dst, src);
+        else copy_block(dst, src);
+    };
+    auto ldg2_far = [&](const double2 *p) { return L2_HINTS >= 2 ? ldg2_dead(p, pol_dead) : __ldg(p); };
     auto issue_state = [&](int pkx) {
         const size_t off = (size_t)pk_elem(pkx) * 64;
         const int srce = state_src(sp, pk_member(pkx));
@@ -814,9 +830,9 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
             const bool need_k1 = MODE == MODE_STAGE && sp.stage > 1 && (sp.stage < sp.S || sp.fin_k1);
             if (FSF == 18) {   // padded face layout: chunk c of the 512 B block -> 2c + 2 (c / 8)
 #pragma unroll
-                for (int r = 0; r < 4; ++r) cp_async16(EP(EPI_FS) + 2 * (t8 + 8 * r) + 2 * r, Fs + eb + 2 * (t8 + 8 * r));
+                for (int r = 0; r < 4; ++r) cp_async16_dead(EP(EPI_FS) + 2 * (t8 + 8 * r) + 2 * r, Fs + eb + 2 * (t8 + 8 * r), pol_dead);
             } else {
-                copy_block(EP(EPI_FS), Fs + eb);
+                copy_block_dead(EP(EPI_FS), Fs + eb);
             }
             // stage S combines with W (P-ERK3) or U_n
             if (EM == 2) {
@@ -824,18 +840,18 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
                     const double *usrc = (Wb && sp.stage == sp.S) ? Wb : Un;
 #pragma unroll
                     for (int v = 0; v < 4; ++v) {
-                        if (need_un) pre_un[v] = __ldg(reinterpret_cast<const double2 *>(usrc + eb + v * 16 + q0));
-                        if (need_k1) pre_k1[v] = __ldg(reinterpret_cast<const double2 *>(K1 + eb + v * 16 + q0));
+                        if (need_un) pre_un[v] = ldg2_far(reinterpret_cast<const double2 *>(usrc + eb + v * 16 + q0));
+                        if (need_k1) pre_k1[v] = ldg2_far(reinterpret_cast<const double2 *>(K1 + eb + v * 16 + q0));
                     }
                 }
             } else {
-                if (need_un) copy_block(EP(EPI_UN), (Wb && sp.stage == sp.S ? Wb : Un) + eb);
-                if (need_k1) copy_block(EP(EPI_K1), K1 + eb);
+                if (need_un) copy_block_far(EP(EPI_UN), (Wb && sp.stage == sp.S ? Wb : Un) + eb);
+                if (need_k1) copy_block_far(EP(EPI_K1), K1 + eb);
             }
             if (NS) {   // the element's 48 BR1 central traces, or (BR1_DV) its viscous volume term (384 B = 24 chunks)
 #pragma unroll
                 for (int r = 0; r < 3; ++r)
-                    cp_async16(EP(EPI_GS) + 2 * (t8 + 8 * r), Gs + (size_t)e * 4 * GV * NP + 2 * (t8 + 8 * r));
+                    cp_async16_dead(EP(EPI_GS) + 2 * (t8 + 8 * r), Gs + (size_t)e * 4 * GV * NP + 2 * (t8 + 8 * r), pol_dead);
             }
             cp_async_commit();
         }
@@ -908,8 +924,8 @@ k_vol2d(MeshDev md, StageParams sp, double *__restrict__ Un,
             const double *usrc = (Wb && sp.stage == sp.S) ? Wb : Un;
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
-                if (need_un) pre_un[v] = __ldg(reinterpret_cast<const double2 *>(usrc + eb + v * 16 + q0));
-                if (need_k1) pre_k1[v] = __ldg(reinterpret_cast<const double2 *>(K1 + eb + v * 16 + q0));
+                if (need_un) pre_un[v] = ldg2_far(reinterpret_cast<const double2 *>(usrc + eb + v * 16 + q0));
+                if (need_k1) pre_k1[v] = ldg2_far(reinterpret_cast<const double2 *>(K1 + eb + v * 16 + q0));
             }
         }
         if (NS && !BR1_DV) {
