@@ -9,6 +9,8 @@ pool): results must not depend on the schedule.
   sleeps a pseudo-random 0..4 us at each warp barrier and asynchronous-copy wait, so the threads of a
   warp drift apart; a missing __syncwarp or cp.async wait would read stale shared memory.  Jittered
   == unjittered, bitwise.
+* the alternating sweep direction of consecutive stage kernels (StageParams::rev, DESIGN §5 item 4) is a
+  schedule change only: PERK_SWEEP=0 (every launch forward) must give the same bits.
 Each case runs in a subprocess (the grid caps are read at perk_init; the debug library is loaded
 instead of the release one there)."""
 import json
@@ -79,3 +81,10 @@ def test_jitter_debug_build(case):
         assert r["sha"] == ref["sha"], (case, seed)
     # the debug build computes the same numbers as the release build
     assert _run(case, {})["sha"] == ref["sha"]
+
+
+@pytest.mark.parametrize("case", ["euler", "ns", "sc"])
+def test_sweep_direction_independent(case):
+    """Every stage kernel walks its lists opposite to its predecessor (L2 reuse); items are independent,
+    so the all-forward schedule gives bitwise the same state."""
+    assert _run(case, {"PERK_SWEEP": "0"})["sha"] == _run(case, {})["sha"]
