@@ -233,7 +233,8 @@ def kernel_counts(cfg):
     except (OSError, ValueError):
         return None
     d["_path"] = os.path.relpath(path, ROOT)
-    d["_current_build"] = d.get("lib_sha16") == _lib_sha()
+    from paper_2403_05144_b200.build import source_sha16
+    d["_current_build"] = d.get("src_sha16") == source_sha16() or d.get("lib_sha16") == _lib_sha()
     return d
 
 

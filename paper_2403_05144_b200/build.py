@@ -18,6 +18,18 @@ def sources():
     return [os.path.join(d, f) for f in sorted(os.listdir(d))] + [os.path.join(ROOT, "include", "perk.h")]
 
 
+def source_sha16() -> str:
+    """sha256 prefix of the kernel sources (csrc/, include/perk.h): identifies the code a profile was taken on
+    (the .so itself is not bit-reproducible from build to build)."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in sources():
+        h.update(os.path.basename(f).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 TOOLS = [("fp64_peak.cu", "fp64_peak")]   # measured fp64 FMA peak (bench.py roofline denominator)
 
 

@@ -180,13 +180,6 @@ __host__ __device__ constexpr size_t grad2d_smem_bytes()
 #endif
 // 1 = only the x-line threads finalise Dv (half the shared-memory traffic of the x + y sum, idle y-line
 // threads): slower (1.99 vs 1.95 ms/step), off
-// 1 = the next group's gathers (neighbour traces, own nodes) are issued one iteration ahead, after the
-// gradients, into the registers the central traces have just released (needs GRAD2D_LAZYVOTE: a predicated
-// lazy-state FMA would wait for the loads on the spot; and GRAD2D_MINB 3 for the registers)
-#ifndef GRAD2D_PF
-#define GRAD2D_PF 0
-#endif
-static_assert(!GRAD2D_PF || (GRAD2D_LAZYVOTE && GRAD2D_STG == 0 && BR1_FUSED), "GRAD2D_PF needs the warp-voted lazy path, unstaged loads and the fused kernel");
 #ifndef GRAD2D_DVX
 #define GRAD2D_DVX 0
 #endif
@@ -257,80 +250,6 @@ __global__ void __launch_bounds__(128, MODE == MODE_RHS ? 3 : GRAD2D_MINB) k_gra
     issue_state(pk);
     if (!FUSED) issue_gs(pk);
     cp_async_commit();
-#if GRAD2D_LG
-    // the second small element of a large mortar side (rare: 1-2 % of the elements have such a face) is
-    // gathered inside the large-side branch below, not here: 16 registers less at the top
-    constexpr int NH = 1;
-#else
-    constexpr int NH = 2;
-#endif
-    double un[2][NH][4];   // the neighbours' conserved traces at this thread's two face nodes
-    double2 u[4];          // the element's own two nodes (GRAD2D_STG = 0)
-    // the gathers of group pkx (face entries fnx): issued at the top of its iteration, or (GRAD2D_PF) one
-    // iteration ahead, after the gradients of the group before, so that they fly during its viscous part
-    auto gather = [&](int pkx, const int2 fnx[2]) {
-        if (FUSED) {
-            int xe[2][NH], xs[2][NH];
-#pragma unroll
-            for (int f = 0; f < 2; ++f) {
-                const int p0 = fnx[f].x >= 0 ? fnx[f].x : pkx;
-                xe[f][0] = pk_elem(p0);
-                xs[f][0] = state_src(sp, pk_member(p0));
-                if (NH == 2) {
-                    const int p1 = fnx[f].y >= 0 ? fnx[f].y : p0;
-                    xe[f][NH - 1] = pk_elem(p1);
-                    xs[f][NH - 1] = state_src(sp, pk_member(p1));
-                }
-            }
-#pragma unroll
-            for (int f = 0; f < 2; ++f)
-#pragma unroll
-                for (int h = 0; h < NH; ++h) {
-                    if (h == 1 && fnx[f].y < 0) continue;
-                    const double *P = state_base(sb, xs[f][h]) + (size_t)xe[f][h] * 64 + face_node2d((2 * o + f) ^ 1, ln);
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) un[f][h][v] = __ldg(P + v * 16);
-                }
-            // lazily formed neighbour states: skipped by the whole warp when none of its lanes has one (the
-            // if-converted K_1 loads and FMAs were ~9 % of the kernel's issued instructions at the stages
-            // where no state is lazy); the warp is converged here
-            bool nlazy = false;
-#pragma unroll
-            for (int f = 0; f < 2; ++f)
-#pragma unroll
-                for (int h = 0; h < NH; ++h) nlazy |= !(h == 1 && fnx[f].y < 0) && xs[f][h] == SRC_LAZY;
-            if (!GRAD2D_LAZYVOTE || __any_sync(0xffffffffu, nlazy)) {
-#pragma unroll
-                for (int f = 0; f < 2; ++f)
-#pragma unroll
-                    for (int h = 0; h < NH; ++h) {
-                        if ((h == 1 && fnx[f].y < 0) || xs[f][h] != SRC_LAZY) continue;
-                        const double *P = K1 + (size_t)xe[f][h] * 64 + face_node2d((2 * o + f) ^ 1, ln);
-                        double kk[4];
-#pragma unroll
-                        for (int v = 0; v < 4; ++v) kk[v] = __ldg(P + v * 16);
-#pragma unroll
-                        for (int v = 0; v < 4; ++v) un[f][h][v] = fma(dtc, kk[v], un[f][h][v]);
-                    }
-            }
-        }
-        const int ex = pk_elem(pkx);
-        const int srcx = state_src(sp, pk_member(pkx));
-        const bool olazy_x = !GRAD2D_LAZYVOTE || __any_sync(0xffffffffu, srcx == SRC_LAZY);
-        if (GRAD2D_STG == 0) {   // the element's own two nodes, issued with the neighbour gathers
-            const double *Ps = state_base(sb, srcx) + (size_t)ex * 64 + q0;
-#pragma unroll
-            for (int v = 0; v < 4; ++v) u[v] = __ldg(reinterpret_cast<const double2 *>(Ps + v * 16));
-            if (olazy_x && srcx == SRC_LAZY) {
-                double2 k[4];
-#pragma unroll
-                for (int v = 0; v < 4; ++v) k[v] = __ldg(reinterpret_cast<const double2 *>(K1 + (size_t)ex * 64 + v * 16 + q0));
-#pragma unroll
-                for (int v = 0; v < 4; ++v) u[v] = make_double2(fma(dtc, k[v].x, u[v].x), fma(dtc, k[v].y, u[v].y));
-            }
-        }
-    };
-    if (GRAD2D_PF) gather(pk, fn);
     for (; base < n_act; base += stride) {
         const bool valid = base + le < n_act;
         const bool has_next = base + stride < n_act;
@@ -352,11 +271,78 @@ __global__ void __launch_bounds__(128, MODE == MODE_RHS ? 3 : GRAD2D_MINB) k_gra
         // entry -> face-table chain stalled every iteration and shared-memory conflicts doubled; the next
         // group's neighbour traces prefetched into L2 / L1 after the gradients, 2.42; 3 CTAs/SM, 2.19;
         // the next group's first-neighbour traces loaded into registers after this group's phase 1
-        // (entries three groups ahead, 3 CTAs/SM for the registers), 2.14 vs 2.07)
-        if (!GRAD2D_PF) gather(pk, fn);
+        // (entries three groups ahead, 3 CTAs/SM for the registers), 2.14 vs 2.07; again after the
+        // instruction diet, when these gathers had become the top stall: the next group's neighbour AND own
+        // loads issued after the gradients into the registers the central traces release, 168 registers at
+        // 3 CTAs/SM: 1.99 vs 1.77 at 4 CTAs/SM -- 3 CTAs/SM alone costs 1.97, profiles/r02_ab_grad_pf.json)
+#if GRAD2D_LG
+        // the second small element of a large mortar side (rare: 1-2 % of the elements have such a face) is
+        // gathered inside the large-side branch below, not here: 16 registers less at the top
+        double un[2][1][4];
+        constexpr int NH = 1;
+#else
+        double un[2][2][4];
+        constexpr int NH = 2;
+#endif
+        if (FUSED) {
+            int xe[2][NH], xs[2][NH];
+#pragma unroll
+            for (int f = 0; f < 2; ++f) {
+                const int p0 = fn[f].x >= 0 ? fn[f].x : pk;
+                xe[f][0] = pk_elem(p0);
+                xs[f][0] = state_src(sp, pk_member(p0));
+                if (NH == 2) {
+                    const int p1 = fn[f].y >= 0 ? fn[f].y : p0;
+                    xe[f][NH - 1] = pk_elem(p1);
+                    xs[f][NH - 1] = state_src(sp, pk_member(p1));
+                }
+            }
+#pragma unroll
+            for (int f = 0; f < 2; ++f)
+#pragma unroll
+                for (int h = 0; h < NH; ++h) {
+                    if (h == 1 && fn[f].y < 0) continue;
+                    const double *P = state_base(sb, xs[f][h]) + (size_t)xe[f][h] * 64 + face_node2d((2 * o + f) ^ 1, ln);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) un[f][h][v] = __ldg(P + v * 16);
+                }
+            // lazily formed neighbour states: skipped by the whole warp when none of its lanes has one (the
+            // if-converted K_1 loads and FMAs were ~9 % of the kernel's issued instructions at the stages
+            // where no state is lazy); the warp is converged here
+            bool nlazy = false;
+#pragma unroll
+            for (int f = 0; f < 2; ++f)
+#pragma unroll
+                for (int h = 0; h < NH; ++h) nlazy |= !(h == 1 && fn[f].y < 0) && xs[f][h] == SRC_LAZY;
+            if (!GRAD2D_LAZYVOTE || __any_sync(0xffffffffu, nlazy)) {
+#pragma unroll
+                for (int f = 0; f < 2; ++f)
+#pragma unroll
+                    for (int h = 0; h < NH; ++h) {
+                        if ((h == 1 && fn[f].y < 0) || xs[f][h] != SRC_LAZY) continue;
+                        const double *P = K1 + (size_t)xe[f][h] * 64 + face_node2d((2 * o + f) ^ 1, ln);
+                        double kk[4];
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) kk[v] = __ldg(P + v * 16);
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) un[f][h][v] = fma(dtc, kk[v], un[f][h][v]);
+                    }
+            }
+        }
+        double2 u[4];
         const bool olazy_any = !GRAD2D_LAZYVOTE || __any_sync(0xffffffffu, src == SRC_LAZY);
-        int2 fn_next[2] = {fn[0], fn[1]};
-        if (GRAD2D_PF && has_next) faces_of(pk_next, fn_next);   // used after the gradients, for the next group's gathers
+        if (GRAD2D_STG == 0) {   // the element's own two nodes, issued with the neighbour gathers
+            const double *Ps = state_base(sb, src) + (size_t)e * 64 + q0;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) u[v] = __ldg(reinterpret_cast<const double2 *>(Ps + v * 16));
+            if (olazy_any && src == SRC_LAZY) {
+                double2 k[4];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) k[v] = __ldg(reinterpret_cast<const double2 *>(K1 + (size_t)e * 64 + v * 16 + q0));
+#pragma unroll
+                for (int v = 0; v < 4; ++v) u[v] = make_double2(fma(dtc, k[v].x, u[v].x), fma(dtc, k[v].y, u[v].y));
+            }
+        }
         PERK_JITTER(11);
         cp_async_wait<0>();
         __syncwarp();
@@ -485,13 +471,7 @@ __global__ void __launch_bounds__(128, MODE == MODE_RHS ? 3 : GRAD2D_MINB) k_gra
         __syncwarp();
         if (!FUSED && has_next) issue_gs(pk_next);          // gst consumed
         cp_async_commit();
-        if (GRAD2D_PF) {
-            fn[0] = fn_next[0];
-            fn[1] = fn_next[1];
-            if (has_next) gather(pk_next, fn);              // un, u are consumed: refill them for the next group
-        } else if (FUSED && has_next) {
-            faces_of(pk_next, fn);                          // the next group's face entries (used at its top)
-        }
+        if (FUSED && has_next) faces_of(pk_next, fn);       // the next group's face entries (used at its top)
         if (BR1_DV) {
             // viscous flux in direction o at the line's 4 nodes: the end nodes' go to Vt (face traces),
             // all four into dv[i] = sum_a Dhat_ia F^v_o(node a); x + y lines summed through shared memory

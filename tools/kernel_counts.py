@@ -8,7 +8,8 @@ Here:
 writes profiles/r02_kernel_counts_cfg5.json: per kind the executed fp64 flops (2 DFMA + DMUL + DADD,
 thread-level SASS counts) and the cold-cache DRAM bytes (ncu flushes caches between replays) summed
 over the kind's launches and divided by the number of P-ERK steps the command ran (warmup + steps),
-plus the sha256 prefix of the library that produced them (bench.py marks counts of another build):
+plus the sha256 prefixes of the kernel sources (src_sha16: run this with the sources the GPU-side command
+was built from) and of the library that produced them (bench.py marks counts of another build):
 the file the GPU-side command wrote (sha256sum of the .so it ran), else the local library.
 """
 import collections
@@ -62,6 +63,12 @@ def summarise(path, steps):
     return out
 
 
+def source_sha16():
+    sys.path.insert(0, ROOT)
+    from paper_2403_05144_b200.build import source_sha16 as f
+    return f()
+
+
 def lib_sha():
     with open(os.path.join(ROOT, "paper_2403_05144_b200", "lib", "libperk_b200.so"), "rb") as f:
         return hashlib.sha256(f.read()).hexdigest()[:16]
@@ -70,7 +77,7 @@ def lib_sha():
 if __name__ == "__main__":
     src, cfg, steps = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
     sha = open(sys.argv[4]).read().split()[0][:16] if len(sys.argv) > 4 else lib_sha()
-    res = {"config": cfg, "source": os.path.basename(src), "steps_profiled": steps, "lib_sha16": sha,
+    res = {"config": cfg, "source": os.path.basename(src), "steps_profiled": steps, "lib_sha16": sha, "src_sha16": source_sha16(),
            "command": f"ncu --metrics {','.join(METRICS)} --clock-control none --csv "
                       f"python bench.py --profile-only --config {cfg} --steps 1 --warmup {steps - 1}",
            "kinds": summarise(src, steps)}
