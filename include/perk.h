@@ -155,7 +155,10 @@ int perk_pattern_mask(int32_t S, int32_t E, int32_t kind, const int32_t *stages_
  * stream: a cudaStream_t (NULL = legacy stream).
  * Ownership: unless out / prob / level_map_dev / tab is NULL (EINVAL, *out untouched), *out receives
  * the context on EVERY return, including errors: read perk_last_error(*out), then release it with
- * perk_destroy (it frees whatever was allocated before the failure). */
+ * perk_destroy (it frees whatever was allocated before the failure).
+ * Environment read here (schedule knobs; none changes a result bit): PERK_VOL_BLOCKS / PERK_GRAD_BLOCKS /
+ * PERK_SURF_BLOCKS cap the persistent grids (race tests); PERK_SWEEP=0 makes every 2D stage kernel walk
+ * its lists forward instead of alternating the direction from launch to launch (DESIGN.md §5 item 4). */
 int perk_init(perk_ctx **out, const perk_problem *prob, const uint8_t *level_map_dev, const perk_tableau *tab,
               void *stream);
 int perk_destroy(perk_ctx *ctx);
