@@ -180,6 +180,13 @@ __host__ __device__ constexpr size_t grad2d_smem_bytes()
 #endif
 // 1 = only the x-line threads finalise Dv (half the shared-memory traffic of the x + y sum, idle y-line
 // threads): slower (1.99 vs 1.95 ms/step), off
+// 1 = Dv is stored with the streaming policy (st.global.cs): its reader, the volume kernel, runs after the
+// surface kernel has streamed several hundred MB through the L2, so the lines are offered for eviction
+// first and the L2 keeps Vt and the stage state for the surface kernel (cfg 5 step 5.798 -> 5.755 ms
+// together with the streaming Vt loads of k_surf2d, profiles/r02_ab_cs.json)
+#ifndef GRAD2D_DVCS
+#define GRAD2D_DVCS 1
+#endif
 #ifndef GRAD2D_DVX
 #define GRAD2D_DVX 0
 #endif
@@ -554,7 +561,11 @@ __global__ void __launch_bounds__(128, MODE == MODE_RHS ? 3 : GRAD2D_MINB) k_gra
                     const double2 sx = *reinterpret_cast<const double2 *>(&sm[G_V1 + c][0][eox + q0]);
                     const double s0 = sx.x + sm[G_V1 + c][1][yo + eoy + 4 * i0 + j0];
                     const double s1 = sx.y + sm[G_V1 + c][1][yo + eoy + 4 * (i0 + 1) + j0];
+#if GRAD2D_DVCS
+                    __stcs(reinterpret_cast<double2 *>(Dv + (size_t)e * (GV * 16) + c * 16 + q0), make_double2(J * s0, J * s1));
+#else
                     *reinterpret_cast<double2 *>(Dv + (size_t)e * (GV * 16) + c * 16 + q0) = make_double2(J * s0, J * s1);
+#endif
                 }
             }
 #endif

@@ -267,10 +267,12 @@ __global__ void __launch_bounds__(256, SURF2D_MINB) k_surf2d(MeshDev md, StagePa
     int gt = blockIdx.x * blockDim.x + threadIdx.x;
     const int4 *__restrict__ IR = MODE == MODE_STAGE ? md.ifcs : md.ifc;
 #ifndef L2_HINTS_SURF
-#define L2_HINTS_SURF 0     // (the policy operand pushes the Navier-Stokes instantiation over its 80 registers)
+#define L2_HINTS_SURF 2     // Vt is dead once read: 2 = streaming loads (ld.global.cs, evict-first, no extra register;
+                            // cfg 5 surface 1.424 -> 1.411 ms/step); 1 = a cache-hint policy operand, which pushes the
+                            // Navier-Stokes instantiation over its 80 registers (spills, slower); 0 = plain loads
 #endif
-    const unsigned long long pol_dead = NS && L2_HINTS_SURF ? l2_evict_first_policy() : 0ull;   // Vt is dead after this launch
-    auto ldg_vt = [&](const double *p) { return L2_HINTS_SURF ? ldg_dead(p, pol_dead) : __ldg(p); };
+    const unsigned long long pol_dead = NS && L2_HINTS_SURF == 1 ? l2_evict_first_policy() : 0ull;   // Vt is dead after this launch
+    auto ldg_vt = [&](const double *p) { return L2_HINTS_SURF == 2 ? __ldcs(p) : (L2_HINTS_SURF ? ldg_dead(p, pol_dead) : __ldg(p)); };
     pdl_wait();
     // two interface face nodes per iteration while both are interfaces: twice the loads in flight
     // per thread (the kernel is bound by the latency of the record -> trace gathers).  (Tried: the next
